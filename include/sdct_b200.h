@@ -1,0 +1,133 @@
+/*
+ * sdct_b200.h — C ABI of the B200-native multi-dimensional DCT library.
+ *
+ * This is the drop-in boundary for the reference's hot path (arXiv 2110.01172
+ * three-stage DCT; reference C++ API in /root/reference/proj/include/sdct and
+ * its pybind11 module proj/bindings/module.cpp). Plain pointers, sizes and
+ * integer status codes only: no C++ or torch types cross this boundary.
+ *
+ * Conventions (identical to the reference, proj/include/sdct/dct2d.hpp:1-19,
+ * transforms_ext.hpp:1-15): unnormalised cosine sums, row-major, extents
+ * outermost first.
+ *   DCT_2D        y = sum x cos cos              (== scipy dctn type 2 / 4)
+ *   IDCT_2D       idct_2d(dct_2d(x)) == N1 N2 / 4 x
+ *   IDCT_IDXST_2D IDCT along axis 0, IDXST along axis 1
+ *   IDXST_IDCT_2D IDXST along axis 0, IDCT along axis 1
+ *   DCT_3D        == dctn / 8;  IDCT_3D: idct_3d(dct_3d(x)) == N1 N2 N3 / 8 x
+ *
+ * A plan describes one shape, one dtype and a leading batch count; every
+ * transform of the plan runs out of place on `batch` contiguous items.
+ * Device entry points are stream-ordered and asynchronous; host entry points
+ * copy through the plan's staging buffers and synchronise.
+ */
+#ifndef SDCT_B200_H_
+#define SDCT_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes. The C++ shim (include/sdct/errors.hpp) rethrows them as the
+ * reference's exception types (proj/include/sdct/errors.hpp:11-33):
+ * SHAPE -> ShapeError, PLAN -> PlanError (is-a ShapeError), BOUNDS ->
+ * BoundsError; the pybind module maps ShapeError to ValueError exactly like
+ * proj/bindings/module.cpp:64-65. */
+enum {
+  SDCT_OK = 0,
+  SDCT_ERR_SHAPE = 1,    /* rank/extent invalid                           */
+  SDCT_ERR_PLAN = 2,     /* input does not match the plan                 */
+  SDCT_ERR_BOUNDS = 3,   /* index out of range (corrupt-twiddle hook)     */
+  SDCT_ERR_CUDA = 4,     /* CUDA runtime failure (message has the detail) */
+  SDCT_ERR_OOM = 5,      /* device allocation failed                      */
+  SDCT_ERR_ARG = 6,      /* null pointer / unknown enum                   */
+  SDCT_ERR_NODEVICE = 7  /* no usable CUDA device                         */
+};
+
+enum { SDCT_F32 = 0, SDCT_F64 = 1 };
+
+/* Orientation of a 2D plan (proj/include/sdct/dct2d.hpp:26, 43-46). The GPU
+ * pipeline computes the same transform for both; the value is recorded so
+ * Plan2d::orientation() keeps the reference's meaning. -1 = automatic
+ * (maybe_transpose_strategy, proj/src/dct2d.cpp:294-298). */
+enum { SDCT_ORIENT_AUTO = -1, SDCT_ORIENT_DIRECT = 0, SDCT_ORIENT_TRANSPOSED = 1 };
+
+/* Transform kinds; each replaces the named reference entry point. */
+enum {
+  SDCT_DCT_2D = 0,        /* sdct::dct_2d        proj/include/sdct/dct2d.hpp:105-107 */
+  SDCT_IDCT_2D = 1,       /* sdct::idct_2d       proj/include/sdct/dct2d.hpp:115-117 */
+  SDCT_IDCT_IDXST_2D = 2, /* sdct::idct_idxst_2d proj/include/sdct/transforms_ext.hpp:34-35 */
+  SDCT_IDXST_IDCT_2D = 3, /* sdct::idxst_idct_2d proj/include/sdct/transforms_ext.hpp:36-37 */
+  SDCT_DCT_3D = 4,        /* sdct::dct_3d        proj/include/sdct/transforms_ext.hpp:77-79 */
+  SDCT_IDCT_3D = 5,       /* sdct::idct_3d       proj/include/sdct/transforms_ext.hpp:82-84 */
+  SDCT_DCT_2D_ROWCOL = 6, /* sdct::dct_2d_rowcol proj/include/sdct/dct2d.hpp:111-112 */
+  SDCT_DCT_1D = 7,        /* sdct::dct_1d        proj/include/sdct/dct1d.hpp:90-93  (rank-1 plans) */
+  SDCT_IDCT_1D = 8,       /* sdct::idct_1d       proj/include/sdct/dct1d.hpp:97-99  (rank-1 plans) */
+  SDCT_IDXST_1D = 9       /* sdct::idxst_1d      proj/include/sdct/transforms_ext.hpp:29-31 */
+};
+
+typedef struct sdct_plan_s* sdct_plan_t;
+
+/* Library version (major*10000 + minor*100 + patch). */
+int sdct_version(void);
+
+/* Thread-local message of the last failing call on this thread ("" if none). */
+const char* sdct_last_error(void);
+
+/* Plan construction — replaces sdct::Plan2d::Plan2d (proj/src/dct2d.cpp:300-306),
+ * sdct::Plan3d::Plan3d (proj/src/transforms_ext.cpp:313-320) and
+ * sdct::Plan1d (proj/include/sdct/dct1d.hpp:35-52). rank is 1, 2 or 3; dims
+ * holds rank positive extents; batch >= 1 items of that shape are processed
+ * per call. Builds the per-shape device twiddle tables and launch geometry on
+ * `device` (-1 = current device). Extents <= 0 give SDCT_ERR_SHAPE (the
+ * reference throws ShapeError, dct2d.cpp:12-15). */
+int sdct_plan_create(sdct_plan_t* plan, int rank, const int64_t* dims, int64_t batch, int dtype,
+                     int orientation, int device);
+int sdct_plan_destroy(sdct_plan_t plan);
+
+/* Plan facts: orientation actually used (Plan2d::orientation()), whether the
+ * power-of-two fast kernels serve this shape (1) or the generic path (0),
+ * and the device workspace bytes sdct_exec needs when the caller supplies one. */
+int sdct_plan_orientation(sdct_plan_t plan, int* orientation);
+int sdct_plan_is_fast(sdct_plan_t plan, int* fast);
+int sdct_plan_workspace_size(sdct_plan_t plan, size_t* bytes);
+
+/* Test-only fault injection: negates axis-1 twiddle b[index] (2D) exactly like
+ * sdct::Plan2d::corrupt_twiddle_for_testing (proj/src/dct2d.cpp:312-317);
+ * index >= N2 gives SDCT_ERR_BOUNDS. */
+int sdct_plan_corrupt_twiddle(sdct_plan_t plan, int64_t index);
+
+/* Run one transform on device memory, stream-ordered. d_in/d_out hold
+ * batch*numel elements of the plan dtype (distinct buffers). d_workspace may
+ * be NULL (the plan's own workspace is used; concurrent calls on one plan then
+ * need distinct streams serialised by the caller) or a buffer of
+ * sdct_plan_workspace_size bytes. stream is a cudaStream_t (NULL = default). */
+int sdct_exec(sdct_plan_t plan, int kind, const void* d_in, void* d_out, void* d_workspace,
+              void* stream);
+
+/* Same transform on host memory: copies in (H2D), runs, copies out (D2H) and
+ * synchronises `stream`. This is what the C++ value API (RealTensor in,
+ * RealTensor out, proj/include/sdct/tensor.hpp:34-78) calls. */
+int sdct_exec_host(sdct_plan_t plan, int kind, const void* h_in, void* h_out, void* stream);
+
+/* Stage-level access for timing the individual kernels of a transform:
+ * number of kernel launches of `kind`, and a launch of one of them with the
+ * same argument meaning as sdct_exec (stage k reads/writes the buffers the
+ * full pipeline would). */
+int sdct_stage_count(sdct_plan_t plan, int kind, int* count);
+int sdct_exec_stage(sdct_plan_t plan, int kind, int stage, const void* d_in, void* d_out,
+                    void* d_workspace, void* stream);
+
+/* Analytic sdct::StageCounters (proj/include/sdct/exec.hpp:29-50) for one
+ * call of `kind`: full_tensor_stages, element_reads, element_writes,
+ * real_mults, real_adds — the values the reference's Counted kernels tally
+ * (proj/src/dct2d.cpp:48-238), computed from the plan's shape. */
+int sdct_counters(sdct_plan_t plan, int kind, uint64_t out[5]);
+
+#ifdef __cplusplus
+}  /* extern "C" */
+#endif
+
+#endif  /* SDCT_B200_H_ */

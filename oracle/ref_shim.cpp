@@ -1,0 +1,82 @@
+// TEST INFRASTRUCTURE — NOT PRODUCT CODE.
+//
+// Flat C entry points over the *unmodified* reference library (compiled from
+// /root/reference/proj/src by oracle/Makefile into oracle/_ref/libsdct_ref.so).
+// Used only by tests/, bench.py's cpu_baseline / --impl reference legs and
+// tests/golden/make_golden.py. The product path never links or loads this.
+//
+// Each entry builds the reference plan once (Plan2d / Plan3d, as the reference
+// does per call in proj/src/dct2d.cpp:389-393) and then runs the transform
+// `reps` times so a caller can time the prebuilt-plan path; the output of the
+// last repetition is written to `out`.
+
+#include <cstddef>
+#include <cstring>
+#include <exception>
+#include <string>
+
+#include "sdct/dct2d.hpp"
+#include "sdct/errors.hpp"
+#include "sdct/exec.hpp"
+#include "sdct/transforms_ext.hpp"
+
+namespace {
+
+thread_local std::string g_err;
+
+enum RefKind {
+  REF_DCT2 = 0,
+  REF_IDCT2 = 1,
+  REF_IDCT_IDXST = 2,
+  REF_IDXST_IDCT = 3,
+  REF_DCT3 = 4,
+  REF_IDCT3 = 5,
+  REF_DCT2_ROWCOL = 6,
+};
+
+}  // namespace
+
+extern "C" {
+
+const char* sdct_ref_last_error() { return g_err.c_str(); }
+
+// Returns 0 on success, 1 on shape errors, 2 on anything else.
+int sdct_ref_run(int kind, int rank, const std::size_t* dims, const double* in, double* out,
+                 unsigned threads, int reps) {
+  try {
+    sdct::ExecConfig cfg;
+    cfg.parallelism_degree = threads;
+    sdct::Shape shape(dims, dims + rank);
+    sdct::RealTensor x(shape, std::vector<double>(in, in + sdct::numel(shape)));
+    sdct::RealTensor y;
+    if (kind == REF_DCT3 || kind == REF_IDCT3) {
+      if (rank != 3) throw sdct::ShapeError("3D kinds need rank 3");
+      sdct::Plan3d plan(dims[0], dims[1], dims[2]);
+      for (int r = 0; r < reps; ++r)
+        y = kind == REF_DCT3 ? sdct::dct_3d(x, plan, cfg) : sdct::idct_3d(x, plan, cfg);
+    } else {
+      if (rank != 2) throw sdct::ShapeError("2D kinds need rank 2");
+      sdct::Plan2d plan(dims[0], dims[1]);
+      for (int r = 0; r < reps; ++r) {
+        switch (kind) {
+          case REF_DCT2: y = sdct::dct_2d(x, plan, cfg); break;
+          case REF_IDCT2: y = sdct::idct_2d(x, plan, cfg); break;
+          case REF_IDCT_IDXST: y = sdct::idct_idxst_2d(x, plan, cfg); break;
+          case REF_IDXST_IDCT: y = sdct::idxst_idct_2d(x, plan, cfg); break;
+          case REF_DCT2_ROWCOL: y = sdct::dct_2d_rowcol(x, plan, cfg); break;
+          default: throw sdct::ShapeError("unknown kind");
+        }
+      }
+    }
+    std::memcpy(out, y.data(), y.size() * sizeof(double));
+    return 0;
+  } catch (const sdct::ShapeError& e) {
+    g_err = e.what();
+    return 1;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 2;
+  }
+}
+
+}  // extern "C"

@@ -1,0 +1,99 @@
+"""Dispatch between the reference-compatible numpy surface (``_sdct``) and the
+device path for torch CUDA tensors (cached ``_sdct.Plan`` per shape/dtype/device,
+workspace from torch's caching allocator on the current stream)."""
+from __future__ import annotations
+
+import threading
+
+from . import _sdct
+
+_KIND = {
+    "dct_1d": _sdct.DCT_1D, "idct_1d": _sdct.IDCT_1D, "idxst_1d": _sdct.IDXST_1D,
+    "dct_2d": _sdct.DCT_2D, "idct_2d": _sdct.IDCT_2D, "idct_idxst_2d": _sdct.IDCT_IDXST_2D,
+    "idxst_idct_2d": _sdct.IDXST_IDCT_2D, "dct_2d_rowcol": _sdct.DCT_2D_ROWCOL,
+    "dct_3d": _sdct.DCT_3D, "idct_3d": _sdct.IDCT_3D,
+}
+_RANK = {"dct_1d": 1, "idct_1d": 1, "idxst_1d": 1, "dct_3d": 3, "idct_3d": 3}
+
+_plans: dict = {}
+_lock = threading.Lock()
+
+
+def plan_for(dims, batch: int = 1, dtype: str = "float64", device: int = 0):
+    """Cached device plan for ``batch`` items of shape ``dims``."""
+    key = (tuple(int(d) for d in dims), int(batch), dtype, int(device))
+    with _lock:
+        p = _plans.get(key)
+        if p is None:
+            import torch
+
+            with torch.cuda.device(device):
+                p = _sdct.Plan(list(key[0]), key[1], dtype)
+            _plans[key] = p
+        return p
+
+
+def _is_torch_cuda(x) -> bool:
+    t = type(x)
+    return t.__module__.startswith("torch") and getattr(x, "is_cuda", False)
+
+
+def _device_call(name: str, x):
+    import torch
+
+    rank = _RANK.get(name, 2)
+    if x.dim() < rank:
+        raise ShapeError(f"{name} expects a rank-{rank} tensor (plus optional batch dims), got {tuple(x.shape)}")
+    if x.dtype not in (torch.float32, torch.float64):
+        raise ValueError(f"{name}: dtype must be float32 or float64, got {x.dtype}")
+    x = x.contiguous()
+    core = tuple(x.shape[x.dim() - rank:])
+    batch = 1
+    for d in x.shape[: x.dim() - rank]:
+        batch *= int(d)
+    if batch == 0 or any(d == 0 for d in core):
+        raise ShapeError("tensor extents must be positive")
+    dt = "float32" if x.dtype == torch.float32 else "float64"
+    dev = x.device.index if x.device.index is not None else torch.cuda.current_device()
+    plan = plan_for(core, batch, dt, dev)
+    out = torch.empty_like(x)
+    with torch.cuda.device(dev):
+        stream = torch.cuda.current_stream(dev)
+        ws = torch.empty(plan.workspace_bytes, dtype=torch.uint8, device=x.device)
+        plan.run(_KIND[name], x.data_ptr(), out.data_ptr(), stream.cuda_stream, ws.data_ptr())
+    return out
+
+
+ShapeError = _sdct.ShapeError
+
+
+def _make(name: str, with_variant: bool = False):
+    host = getattr(_sdct, name)
+
+    if with_variant:
+        def fn(x, variant: str = "n", threads: int = 0):
+            if _is_torch_cuda(x):
+                return _device_call(name, x)
+            return host(x, variant=variant, threads=threads)
+    else:
+        def fn(x, threads: int = 0):
+            if _is_torch_cuda(x):
+                return _device_call(name, x)
+            return host(x, threads=threads)
+
+    fn.__name__ = name
+    fn.__qualname__ = name
+    fn.__doc__ = host.__doc__
+    return fn
+
+
+dct_1d = _make("dct_1d", with_variant=True)
+idct_1d = _make("idct_1d")
+idxst_1d = _make("idxst_1d")
+dct_2d = _make("dct_2d")
+dct_2d_rowcol = _make("dct_2d_rowcol")
+idct_2d = _make("idct_2d")
+idct_idxst_2d = _make("idct_idxst_2d")
+idxst_idct_2d = _make("idxst_idct_2d")
+dct_3d = _make("dct_3d")
+idct_3d = _make("idct_3d")

@@ -1,0 +1,6 @@
+// Column-kernel instantiations, double.
+#include "fast_launch.cuh"
+
+namespace sdctb {
+SDCTB_DEFINE_LAUNCH_COL(double)
+}  // namespace sdctb

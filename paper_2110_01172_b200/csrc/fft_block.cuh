@@ -1,0 +1,247 @@
+// In-CTA power-of-two FFT engine.
+//
+// A CTA holds `nlines` independent lines of length L (complex, float2/double2)
+// in shared memory and transforms all of them in place with decimation-in-
+// frequency radix-R stages (R <= 16). Each thread loads R elements of one
+// butterfly into registers, runs a fully unrolled radix-R DFT, applies the
+// stage twiddles W_span^{j k}, and writes the R results back to the same slots.
+// After the last stage X(k) sits at slot digit_pos<L>(k) (mixed-radix digit
+// reversal); callers absorb that permutation into their store index math, so
+// no separate reorder pass exists.
+//
+// This replaces the reference's scalar radix-2 FftWorkspace::pow2_fft
+// (proj/src/rfft.cpp:65-89) for the power-of-two extents of the hot path.
+//
+// Shared-memory layouts are XOR-swizzled so that every stage's access pattern
+// is bank-conflict free (checked by tests/test_swizzle.py, which replays the
+// exact index math below).
+#pragma once
+
+#include "sdct_common.cuh"
+
+namespace sdctb {
+
+// ---- radix plan: ceil(log2(L)/4) stages, bits spread evenly, larger first --
+template <int L>
+struct RadixPlan {
+  static constexpr int lg = ilog2c(L);
+  static constexpr int S = lg == 0 ? 0 : (lg + 3) / 4;
+  static constexpr int bits(int s) { return lg / S + (s < lg % S ? 1 : 0); }
+  static constexpr int R(int s) { return 1 << bits(s); }
+  // span(s): length of the sub-FFTs stage s operates on; span(S) == 1.
+  static constexpr int span(int s) {
+    int ls = L;
+    for (int t = 0; t < s; ++t) ls /= R(t);
+    return ls;
+  }
+};
+
+// Slot holding X(k) after all DIF stages: k = d0 + R0 d1 + R0 R1 d2 + ...,
+// pos = sum_s d_s * span(s+1).
+template <int L>
+__host__ __device__ __forceinline__ int digit_pos(int k) {
+  using P = RadixPlan<L>;
+  int pos = 0;
+#pragma unroll
+  for (int s = 0; s < P::S; ++s) {
+    const int r = P::R(s);
+    pos += (k & (r - 1)) * P::span(s + 1);
+    k >>= P::bits(s);
+  }
+  return pos;
+}
+
+// ---- bank-conflict-free swizzles (index in complex elements) ---------------
+// GF(2)-linear maps a -> a ^ g(a >> SH), g(h) = XOR of C[d % 4] over the set
+// bits d of h. 16-B elements (SH = 3) are served 8 lanes per wavefront, 8-B
+// elements (SH = 4) 16 lanes. Column tiles use constants that make every
+// aligned dyadic window injective; row tiles use constants found by
+// exhaustive search over the row kernel's stage patterns. tests/swizzle_model.py
+// replays this math and tests/test_swizzle.py asserts conflict degree 1.
+// Linearity lets a butterfly swizzle its base once and XOR per-element offsets.
+template <int C0, int C1, int C2, int C3, int SH>
+struct LinSwz {
+  __host__ __device__ __forceinline__ static int g(unsigned h) {
+#if defined(__CUDA_ARCH__)
+    return ((-(int)(__popc(h & 0x11111111u) & 1)) & C0) ^ ((-(int)(__popc(h & 0x22222222u) & 1)) & C1) ^
+           ((-(int)(__popc(h & 0x44444444u) & 1)) & C2) ^ ((-(int)(__popc(h & 0x88888888u) & 1)) & C3);
+#else
+    int r = 0;
+    for (int d = 0; h; ++d, h >>= 1)
+      if (h & 1u) r ^= (d & 3) == 0 ? C0 : (d & 3) == 1 ? C1 : (d & 3) == 2 ? C2 : C3;
+    return r;
+#endif
+  }
+  __host__ __device__ __forceinline__ static int f(int a) {
+    return a ^ g(static_cast<unsigned>(a) >> SH);
+  }
+  // constexpr evaluation for compile-time offsets
+  static constexpr int fc(int a) {
+    int r = 0;
+    unsigned h = static_cast<unsigned>(a) >> SH;
+    for (int d = 0; h; ++d, h >>= 1)
+      if (h & 1u) r ^= (d & 3) == 0 ? C0 : (d & 3) == 1 ? C1 : (d & 3) == 2 ? C2 : C3;
+    return a ^ r;
+  }
+};
+template <typename T> struct SwzCol;
+template <> struct SwzCol<double> : LinSwz<4, 6, 5, 7, 3> {};
+template <> struct SwzCol<float> : LinSwz<8, 12, 10, 15, 4> {};
+template <typename T> struct SwzRow;
+template <> struct SwzRow<double> : LinSwz<1, 2, 4, 1, 3> {};
+template <> struct SwzRow<float> : LinSwz<1, 6, 10, 8, 4> {};
+
+// Column tile: element (line c, n) at n*W + c (lines interleaved), W = 1 << lgw.
+template <typename T>
+struct ColLayout {
+  int lgw;
+  __device__ __forceinline__ int raw(int line, int n) const { return (n << lgw) + line; }
+  __device__ __forceinline__ int at(int line, int n) const { return SwzCol<T>::f(raw(line, n)); }
+  __device__ __forceinline__ static int swz(int a) { return SwzCol<T>::f(a); }
+  // swizzled offset of element stride q (used as XOR offsets inside a butterfly)
+  __device__ __forceinline__ int off(int q) const { return SwzCol<T>::f(q << lgw); }
+};
+// Row tile: element (line, n) at line*L + n (lines contiguous).
+template <typename T, int L>
+struct RowLayout {
+  __device__ __forceinline__ int raw(int line, int n) const { return line * L + n; }
+  __device__ __forceinline__ int at(int line, int n) const { return SwzRow<T>::f(raw(line, n)); }
+  __device__ __forceinline__ static int swz(int a) { return SwzRow<T>::f(a); }
+  __device__ __forceinline__ int off(int q) const { return SwzRow<T>::f(q); }
+};
+
+// ---- in-register radix-R DFT, natural order in and out ---------------------
+template <typename T> struct K16;
+template <> struct K16<double> {
+  // cos(2 pi m / 16), m = 0..4
+  __device__ __forceinline__ static double c(int m) {
+    return m == 0 ? 1.0 : m == 1 ? 0.92387953251128675613 : m == 2 ? 0.70710678118654752440
+         : m == 3 ? 0.38268343236508977173 : 0.0;
+  }
+};
+template <> struct K16<float> {
+  __device__ __forceinline__ static float c(int m) {
+    return m == 0 ? 1.0f : m == 1 ? 0.92387953251128675613f : m == 2 ? 0.70710678118654752440f
+         : m == 3 ? 0.38268343236508977173f : 0.0f;
+  }
+};
+
+// multiply by W_R^k = exp(-+ 2 pi i k / R); k, R compile-time after unrolling
+template <typename T, bool INV>
+__device__ __forceinline__ cx_t<T> mul_wrk(cx_t<T> v, int k, int R) {
+  const int m16 = (k * 16) / R;  // angle in units of 2pi/16, 0..15
+  if (m16 == 0) return v;
+  if (m16 == 4) return mul_mi<INV>(v);
+  if (m16 == 8) return mk(-v.x, -v.y);
+  if (m16 == 12) return mul_mi<!INV>(v);
+  // generic: exp(-i theta) forward, exp(+i theta) inverse, theta = 2 pi m16 / 16
+  const int q = m16 & 3, quad = m16 >> 2;  // theta = quad*pi/2 + q*pi/8
+  T c = K16<T>::c(q), s = K16<T>::c(4 - q);  // cos, sin of q*pi/8
+  // rotate by quad quarter turns
+  T cr = c, sr = s;
+  if (quad == 1) { cr = -s; sr = c; }
+  if (quad == 2) { cr = -c; sr = -s; }
+  if (quad == 3) { cr = s; sr = -c; }
+  if (!INV) sr = -sr;
+  return mk(v.x * cr - v.y * sr, v.x * sr + v.y * cr);
+}
+
+template <typename T, int R, bool INV>
+__device__ __forceinline__ void dft_reg(cx_t<T>* v) {
+  if constexpr (R == 1) {
+    return;
+  } else if constexpr (R == 2) {
+    const cx_t<T> a = v[0], b = v[1];
+    v[0] = cadd(a, b);
+    v[1] = csub(a, b);
+  } else {
+    cx_t<T> e[R / 2], o[R / 2];
+#pragma unroll
+    for (int r = 0; r < R / 2; ++r) {
+      e[r] = v[2 * r];
+      o[r] = v[2 * r + 1];
+    }
+    dft_reg<T, R / 2, INV>(e);
+    dft_reg<T, R / 2, INV>(o);
+#pragma unroll
+    for (int k = 0; k < R / 2; ++k) {
+      const cx_t<T> t = mul_wrk<T, INV>(o[k], k, R);
+      v[k] = cadd(e[k], t);
+      v[k + R / 2] = csub(e[k], t);
+    }
+  }
+}
+
+// ---- one DIF stage over all lines -------------------------------------------
+// tw: circle table C[m] = exp(-2 pi i m / CL); W_L^1 = C[tw_step].
+// LINE_FAST: butterfly index decodes line first (column tiles) or j first.
+template <typename T, int L, int S_IDX, bool INV, bool LINE_FAST, class Lay>
+__device__ __forceinline__ void dif_stage(cx_t<T>* buf, const Lay& lay, int lg_lines, int tid,
+                                          int nthreads, const cx_t<T>* __restrict__ tw,
+                                          int tw_step) {
+  using P = RadixPlan<L>;
+  constexpr int R = P::R(S_IDX);
+  constexpr int SPAN = P::span(S_IDX);
+  constexpr int Q = SPAN / R;  // butterflies per block
+  constexpr int LG_Q = ilog2c(Q);
+  constexpr int LG_BLK = ilog2c(L / SPAN);
+  const int total = (L / R) << lg_lines;
+  // The element offsets r*Q occupy bits disjoint from base = b*SPAN + j (and
+  // from the line bits), so by linearity swz(base + r*Q) = swz(base) ^ swz(r*Q).
+  int xo[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) xo[r] = lay.off(r * Q);
+  for (int bf = tid; bf < total; bf += nthreads) {
+    int line, j, b;
+    if (LINE_FAST) {
+      line = bf & ((1 << lg_lines) - 1);
+      const int rest = bf >> lg_lines;
+      j = rest & (Q - 1);
+      b = rest >> LG_Q;
+    } else {
+      j = bf & (Q - 1);
+      const int rest = bf >> LG_Q;
+      b = rest & ((1 << LG_BLK) - 1);
+      line = rest >> LG_BLK;
+    }
+    const int base = b * SPAN + j;
+    const int sb = lay.at(line, base);
+    cx_t<T> v[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) v[r] = buf[sb ^ xo[r]];
+    dft_reg<T, R, INV>(v);
+    if (SPAN > R && j != 0) {
+      // W_SPAN^j = W_L^{j L/SPAN}
+      cx_t<T> w1 = __ldg(&tw[(j * (L / SPAN)) * tw_step]);
+      if (INV) w1 = cconj(w1);
+      cx_t<T> w = w1;
+#pragma unroll
+      for (int k = 1; k < R; ++k) {
+        v[k] = cmul(v[k], w);
+        if (k + 1 < R) w = cmul(w, w1);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) buf[sb ^ xo[r]] = v[r];
+  }
+}
+
+template <typename T, int L, int S_IDX, bool INV, bool LINE_FAST, class Lay>
+__device__ __forceinline__ void dif_stages(cx_t<T>* buf, const Lay& lay, int lg_lines, int tid,
+                                           int nthreads, const cx_t<T>* __restrict__ tw,
+                                           int tw_step) {
+  if constexpr (S_IDX < RadixPlan<L>::S) {
+    dif_stage<T, L, S_IDX, INV, LINE_FAST>(buf, lay, lg_lines, tid, nthreads, tw, tw_step);
+    __syncthreads();
+    dif_stages<T, L, S_IDX + 1, INV, LINE_FAST>(buf, lay, lg_lines, tid, nthreads, tw, tw_step);
+  }
+}
+
+// Full transform of every line; ends with a __syncthreads().
+template <typename T, int L, bool INV, bool LINE_FAST, class Lay>
+__device__ __forceinline__ void block_fft(cx_t<T>* buf, const Lay& lay, int lg_lines,
+                                          const cx_t<T>* __restrict__ tw, int tw_step) {
+  dif_stages<T, L, 0, INV, LINE_FAST>(buf, lay, lg_lines, threadIdx.x, blockDim.x, tw, tw_step);
+}
+
+}  // namespace sdctb

@@ -1,0 +1,24 @@
+// Host-side description of one generic-path job (any extents, rank 1..3).
+#pragma once
+
+#include <cuda_runtime.h>
+
+namespace sdctb {
+
+struct GenericJob {
+  int rank = 2;
+  int dims[3] = {1, 1, 1};
+  long long batch = 1;
+  bool inverse = false;
+  int mode = 0;          // inverse composite embedding: 0 none, 1 axis 0, 2 axis 1 (rank 1: 2 = idxst)
+  int sign_axis = -1;    // inverse: negate odd k along this axis
+  double scale = 1.0;    // inverse gather scale (1/4 in 2D, 1/8 in 3D, 1/2 in 1D)
+  const double2* quarter[3] = {nullptr, nullptr, nullptr};  // e^{-i pi k/(2 N_a)}
+  const double2* circle[3] = {nullptr, nullptr, nullptr};   // e^{-2 pi i t / N_a}
+};
+
+// Workspace: 2 * numel * batch * sizeof(double2) bytes.
+template <typename T>
+cudaError_t generic_run(const GenericJob& job, const void* in, void* out, void* ws, cudaStream_t st);
+
+}  // namespace sdctb

@@ -1,0 +1,277 @@
+// C++ value API (namespace sdct) over the C ABI. Each function validates its
+// arguments exactly like the reference (same exception types and trigger
+// conditions, proj/src/dct2d.cpp:12-38, transforms_ext.cpp:14-35), then hands
+// the host tensor to sdct_exec_host, which stages it through the plan's device
+// buffers. No arithmetic happens here: there is no CPU fallback.
+#include <cmath>
+#include <numbers>
+#include <string>
+
+#include "sdct/device.hpp"
+#include "sdct/dct1d.hpp"
+#include "sdct/dct2d.hpp"
+#include "sdct/transforms_ext.hpp"
+#include "sdct_b200.h"
+
+namespace sdct {
+
+std::string shape_to_string(const Shape& dims) {
+  std::string s;
+  for (std::size_t i = 0; i < dims.size(); ++i) {
+    if (i) s += "x";
+    s += std::to_string(dims[i]);
+  }
+  return s.empty() ? "()" : s;
+}
+
+std::size_t offset(const Shape& dims, const Index& index) {
+  if (index.size() != dims.size())
+    throw BoundsError("index rank " + std::to_string(index.size()) + " does not match tensor rank " +
+                      std::to_string(dims.size()));
+  std::size_t off = 0;
+  for (std::size_t a = 0; a < dims.size(); ++a) {
+    if (index[a] >= dims[a])
+      throw BoundsError("index " + std::to_string(index[a]) + " out of range on axis " + std::to_string(a));
+    off = off * dims[a] + index[a];
+  }
+  return off;
+}
+
+namespace detail {
+
+void check(int status) {
+  if (status == SDCT_OK) return;
+  const std::string msg = sdct_last_error();
+  switch (status) {
+    case SDCT_ERR_SHAPE: throw ShapeError(msg);
+    case SDCT_ERR_PLAN: throw PlanError(msg);
+    case SDCT_ERR_BOUNDS: throw BoundsError(msg);
+    case SDCT_ERR_ARG: throw std::invalid_argument(msg);
+    default: throw DeviceError(msg);
+  }
+}
+
+PlanPtr make_plan(const std::vector<std::int64_t>& dims, std::int64_t batch, int dtype, int orientation) {
+  sdct_plan_t p = nullptr;
+  check(sdct_plan_create(&p, static_cast<int>(dims.size()), dims.data(), batch, dtype, orientation, -1));
+  return PlanPtr(p, PlanDeleter{});
+}
+
+RealTensor run_host(sdct_plan_t plan, int kind, const RealTensor& x, StageCounters* counters) {
+  RealTensor out(x.dims());
+  check(sdct_exec_host(plan, kind, x.data(), out.data(), nullptr));
+  if (counters) {
+    uint64_t c[5];
+    check(sdct_counters(plan, kind, c));
+    counters->full_tensor_stages += c[0];
+    counters->element_reads += c[1];
+    counters->element_writes += c[2];
+    counters->real_mults += c[3];
+    counters->real_adds += c[4];
+  }
+  return out;
+}
+
+}  // namespace detail
+
+namespace {
+
+std::size_t checked_extent(std::size_t n) {
+  if (n == 0) throw ShapeError("transform extents must be positive");
+  return n;
+}
+
+void require_rank(const RealTensor& x, std::size_t rank, const char* name) {
+  if (x.rank() != rank)
+    throw ShapeError(std::string(name) + " expects a rank-" + std::to_string(rank) + " tensor, got " +
+                     shape_to_string(x.dims()));
+}
+
+void require_plan2(const RealTensor& x, const Plan2d& plan, const char* name) {
+  require_rank(x, 2, name);
+  if (x.dim(0) != plan.n1() || x.dim(1) != plan.n2())
+    throw PlanError(std::string(name) + ": plan built for " + std::to_string(plan.n1()) + "x" +
+                    std::to_string(plan.n2()) + ", input is " + shape_to_string(x.dims()));
+}
+
+void require_plan3(const RealTensor& x, const Plan3d& plan, const char* name) {
+  require_rank(x, 3, name);
+  if (x.dims() != Shape{plan.n1(), plan.n2(), plan.n3()})
+    throw PlanError(std::string(name) + ": plan built for " + std::to_string(plan.n1()) + "x" +
+                    std::to_string(plan.n2()) + "x" + std::to_string(plan.n3()) + ", input is " +
+                    shape_to_string(x.dims()));
+}
+
+void require_plan1(const RealTensor& x, const Plan1d& plan, const char* name) {
+  require_rank(x, 1, name);
+  if (x.dim(0) != plan.n())
+    throw PlanError(std::string(name) + ": plan built for length " + std::to_string(plan.n()) +
+                    ", input has length " + std::to_string(x.dim(0)));
+}
+
+}  // namespace
+
+std::vector<std::complex<double>> quarter_wave_table(std::size_t n) {
+  std::vector<std::complex<double>> t(n);
+  for (std::size_t k = 0; k < n; ++k) {
+    const double ph = -std::numbers::pi * static_cast<double>(k) / (2.0 * static_cast<double>(n));
+    t[k] = {std::cos(ph), std::sin(ph)};
+  }
+  return t;
+}
+
+// ---- 1D ---------------------------------------------------------------------
+Plan1d::Plan1d(std::size_t n, Dct1dVariant variant)
+    : n_(checked_extent(n)),
+      variant_(variant),
+      twiddle_(quarter_wave_table(n)),
+      plan_(detail::make_plan({static_cast<std::int64_t>(n)}, 1, SDCT_F64, SDCT_ORIENT_DIRECT)) {}
+
+RealTensor dct_1d(const RealTensor& x, const Plan1d& plan, const ExecConfig&, StageCounters* counters) {
+  require_plan1(x, plan, "dct_1d");
+  return detail::run_host(plan.handle(), SDCT_DCT_1D, x, counters);
+}
+RealTensor dct_1d(const RealTensor& x, Dct1dVariant variant, const ExecConfig& cfg) {
+  require_rank(x, 1, "dct_1d");
+  return dct_1d(x, Plan1d(x.dim(0), variant), cfg);
+}
+RealTensor idct_1d(const RealTensor& x, const Plan1d& plan, const ExecConfig&, StageCounters* counters) {
+  require_plan1(x, plan, "idct_1d");
+  if (plan.variant() != Dct1dVariant::NPoint)
+    throw PlanError("idct_1d runs on the N-point scheme; build the plan with NPoint");
+  return detail::run_host(plan.handle(), SDCT_IDCT_1D, x, counters);
+}
+RealTensor idct_1d(const RealTensor& x, const ExecConfig& cfg) {
+  require_rank(x, 1, "idct_1d");
+  return idct_1d(x, Plan1d(x.dim(0)), cfg);
+}
+RealTensor idxst_1d(const RealTensor& x, const Plan1d& plan, const ExecConfig&, StageCounters* counters) {
+  require_plan1(x, plan, "idxst_1d");
+  if (plan.variant() != Dct1dVariant::NPoint)
+    throw PlanError("idxst_1d runs on the N-point scheme; build the plan with NPoint");
+  return detail::run_host(plan.handle(), SDCT_IDXST_1D, x, counters);
+}
+RealTensor idxst_1d(const RealTensor& x, const ExecConfig& cfg) {
+  require_rank(x, 1, "idxst_1d");
+  return idxst_1d(x, Plan1d(x.dim(0)), cfg);
+}
+
+// ---- 2D ---------------------------------------------------------------------
+Orientation maybe_transpose_strategy(std::size_t n1, std::size_t n2) {
+  return (n2 < n1 && n1 >= 4 * n2) ? Orientation::Transposed : Orientation::Direct;
+}
+
+Plan2d::Plan2d(std::size_t n1, std::size_t n2, std::optional<Orientation> force)
+    : n1_(checked_extent(n1)),
+      n2_(checked_extent(n2)),
+      orientation_(force.value_or(maybe_transpose_strategy(n1, n2))),
+      twiddle_a_(quarter_wave_table(n1)),
+      twiddle_b_(quarter_wave_table(n2)),
+      plan_(detail::make_plan({static_cast<std::int64_t>(n1), static_cast<std::int64_t>(n2)}, 1, SDCT_F64,
+                              orientation_ == Orientation::Direct ? SDCT_ORIENT_DIRECT
+                                                                  : SDCT_ORIENT_TRANSPOSED)) {}
+
+void Plan2d::corrupt_twiddle_for_testing(std::size_t index) {
+  if (index >= twiddle_b_.size())
+    throw BoundsError("corrupt_twiddle_for_testing: index " + std::to_string(index) +
+                      " out of range for table of size " + std::to_string(twiddle_b_.size()));
+  detail::check(sdct_plan_corrupt_twiddle(plan_.get(), static_cast<int64_t>(index)));
+  twiddle_b_[index] = -twiddle_b_[index];
+}
+
+RealTensor dct_2d(const RealTensor& x, const Plan2d& plan, const ExecConfig&, StageCounters* counters) {
+  require_plan2(x, plan, "dct_2d");
+  return detail::run_host(plan.handle(), SDCT_DCT_2D, x, counters);
+}
+RealTensor dct_2d(const RealTensor& x, const ExecConfig& cfg) {
+  require_rank(x, 2, "dct_2d");
+  return dct_2d(x, Plan2d(x.dim(0), x.dim(1)), cfg);
+}
+RealTensor dct_2d_rowcol(const RealTensor& x, const Plan2d& plan, const ExecConfig&, StageCounters* counters) {
+  require_plan2(x, plan, "dct_2d_rowcol");
+  return detail::run_host(plan.handle(), SDCT_DCT_2D_ROWCOL, x, counters);
+}
+
+namespace detail {
+RealTensor idct_family_2d(const RealTensor& x, const Plan2d& plan, ReverseAxis mode, const ExecConfig&,
+                          StageCounters* counters) {
+  require_plan2(x, plan, "idct_family_2d");
+  const int kind = mode == ReverseAxis::Axis0   ? SDCT_IDXST_IDCT_2D
+                   : mode == ReverseAxis::Axis1 ? SDCT_IDCT_IDXST_2D
+                                                : SDCT_IDCT_2D;
+  return run_host(plan.handle(), kind, x, counters);
+}
+}  // namespace detail
+
+RealTensor idct_2d(const RealTensor& x, const Plan2d& plan, const ExecConfig& cfg, StageCounters* counters) {
+  require_plan2(x, plan, "idct_2d");
+  return detail::idct_family_2d(x, plan, detail::ReverseAxis::None, cfg, counters);
+}
+RealTensor idct_2d(const RealTensor& x, const ExecConfig& cfg) {
+  require_rank(x, 2, "idct_2d");
+  return idct_2d(x, Plan2d(x.dim(0), x.dim(1)), cfg);
+}
+
+RealTensor idct_idxst_2d(const RealTensor& x, const Plan2d& plan, const ExecConfig& cfg, StageCounters* c) {
+  require_plan2(x, plan, "idct_idxst_2d");
+  return detail::idct_family_2d(x, plan, detail::ReverseAxis::Axis1, cfg, c);
+}
+RealTensor idxst_idct_2d(const RealTensor& x, const Plan2d& plan, const ExecConfig& cfg, StageCounters* c) {
+  require_plan2(x, plan, "idxst_idct_2d");
+  return detail::idct_family_2d(x, plan, detail::ReverseAxis::Axis0, cfg, c);
+}
+RealTensor composite_2d(const RealTensor& x, const Plan2d& plan, CompositeKind kind, const ExecConfig& cfg,
+                        StageCounters* c) {
+  return kind == CompositeKind::IdctIdxst ? idct_idxst_2d(x, plan, cfg, c) : idxst_idct_2d(x, plan, cfg, c);
+}
+
+// ---- 3D ---------------------------------------------------------------------
+Plan3d::Plan3d(std::size_t n1, std::size_t n2, std::size_t n3)
+    : n1_(checked_extent(n1)),
+      n2_(checked_extent(n2)),
+      n3_(checked_extent(n3)),
+      twiddle_a_(quarter_wave_table(n1)),
+      twiddle_b_(quarter_wave_table(n2)),
+      twiddle_c_(quarter_wave_table(n3)),
+      plan_(detail::make_plan({static_cast<std::int64_t>(n1), static_cast<std::int64_t>(n2),
+                               static_cast<std::int64_t>(n3)},
+                              1, SDCT_F64, SDCT_ORIENT_DIRECT)) {}
+
+RealTensor dct_3d(const RealTensor& x, const Plan3d& plan, const ExecConfig&, StageCounters* counters) {
+  require_plan3(x, plan, "dct_3d");
+  return detail::run_host(plan.handle(), SDCT_DCT_3D, x, counters);
+}
+RealTensor dct_3d(const RealTensor& x, const ExecConfig& cfg) {
+  require_rank(x, 3, "dct_3d");
+  return dct_3d(x, Plan3d(x.dim(0), x.dim(1), x.dim(2)), cfg);
+}
+RealTensor idct_3d(const RealTensor& x, const Plan3d& plan, const ExecConfig&, StageCounters* counters) {
+  require_plan3(x, plan, "idct_3d");
+  return detail::run_host(plan.handle(), SDCT_IDCT_3D, x, counters);
+}
+RealTensor idct_3d(const RealTensor& x, const ExecConfig& cfg) {
+  require_rank(x, 3, "idct_3d");
+  return idct_3d(x, Plan3d(x.dim(0), x.dim(1), x.dim(2)), cfg);
+}
+
+// ---- device plans -------------------------------------------------------------
+DevicePlan::DevicePlan(const std::vector<std::int64_t>& dims, std::int64_t batch, Dtype dtype)
+    : plan_(detail::make_plan(dims, batch, static_cast<int>(dtype), SDCT_ORIENT_AUTO)) {}
+
+void DevicePlan::run(int kind, const void* d_in, void* d_out, void* stream, void* d_workspace) const {
+  detail::check(sdct_exec(plan_.get(), kind, d_in, d_out, d_workspace, stream));
+}
+
+std::size_t DevicePlan::workspace_bytes() const {
+  std::size_t b = 0;
+  detail::check(sdct_plan_workspace_size(plan_.get(), &b));
+  return b;
+}
+
+bool DevicePlan::fast() const {
+  int f = 0;
+  detail::check(sdct_plan_is_fast(plan_.get(), &f));
+  return f != 0;
+}
+
+}  // namespace sdct

@@ -1,0 +1,264 @@
+// Generic path: any extents (odd, non-power-of-two, tiny), ranks 1..3, fp64
+// arithmetic throughout (inputs/outputs may be fp32). It restates the
+// reference's three stages one full-tensor pass at a time:
+//   forward : parity gather (dct2d.cpp:48-70 / transforms_ext.cpp:165-183)
+//             -> full complex DFT along each axis (direct sums with exact
+//                table twiddles; replaces rfft.cpp's Bluestein for odd N)
+//             -> per-output postprocess (the identity of dct2d.hpp:6-7 and its
+//                3D analogue).
+//   inverse : full Hermitian spectrum from the merged preprocess
+//             (dct2d.cpp:161-198 / transforms_ext.cpp:187-216, Hermitian fill
+//             as irfft_nd does, rfft.cpp:233-243) -> inverse DFT per axis ->
+//             real part, inverse parity gather, scale and sign (214-238).
+// It is the correctness path for shapes outside the power-of-two fast path;
+// cost is O(numel * sum(N_axis)).
+#include "generic.h"
+#include "sdct_common.cuh"
+
+namespace sdctb {
+
+namespace {
+
+constexpr int kThreads = 256;
+
+inline int nblocks(long long n) {
+  long long b = (n + kThreads - 1) / kThreads;
+  return static_cast<int>(b > 2147483647LL ? 2147483647LL : b);
+}
+
+struct Dims {
+  int rank;
+  int n[3];       // logical extents (rank entries used, outermost first)
+  long long numel;
+};
+
+__device__ __forceinline__ void unflat(long long f, const Dims& d, int* idx) {
+  for (int a = d.rank - 1; a >= 0; --a) {
+    idx[a] = static_cast<int>(f % d.n[a]);
+    f /= d.n[a];
+  }
+}
+
+template <typename T>
+__global__ void g_gather_fwd(const T* __restrict__ x, double2* __restrict__ c, Dims d, long long batch_items) {
+  const long long total = d.numel * batch_items;
+  for (long long f = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; f < total;
+       f += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long b = f / d.numel;
+    int idx[3];
+    unflat(f - b * d.numel, d, idx);
+    long long src = 0;
+    for (int a = 0; a < d.rank; ++a) src = src * d.n[a] + parity_embed(idx[a], d.n[a]);
+    c[f] = make_double2(static_cast<double>(x[b * d.numel + src]), 0.0);
+  }
+}
+
+// out[o, k, i] = sum_m in[o, m, i] W_n^{+-m k}; tab[t] = e^{-2 pi i t / n}
+__global__ void g_dft_axis(const double2* __restrict__ in, double2* __restrict__ out, long long outer,
+                           int n, long long inner, const double2* __restrict__ tab, int inverse) {
+  const long long total = outer * n * inner;
+  for (long long f = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; f < total;
+       f += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long i = f % inner;
+    const long long rest = f / inner;
+    const int k = static_cast<int>(rest % n);
+    const long long o = rest / n;
+    const double2* line = in + o * n * inner + i;
+    double re = 0.0, im = 0.0;
+    long long t = 0;
+    for (int m = 0; m < n; ++m) {
+      double2 w = tab[t];
+      if (inverse) w.y = -w.y;
+      const double2 v = line[m * inner];
+      re += v.x * w.x - v.y * w.y;
+      im += v.x * w.y + v.y * w.x;
+      t += k;
+      if (t >= n) t -= n;
+    }
+    out[f] = make_double2(re, im);
+  }
+}
+
+__device__ __forceinline__ double2 cm(double2 a, double2 b) {
+  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ double2 cj(double2 a) { return make_double2(a.x, -a.y); }
+__device__ __forceinline__ double2 ca(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+
+// 1D: y(k) = Re(b(k) X(k))             (dct1d N-point postprocess, scale 1)
+// 2D: y = 1/2 Re(b (a X(k1,k2) + conj(a) X(-k1,k2)))               (dct2d.hpp:6)
+// 3D: y = 1/4 Re(c (ab X + conj(a) b X(-k1) + a conj(b) X(-k2) + conj(ab) X(-k1,-k2)))
+template <typename T>
+__global__ void g_post(const double2* __restrict__ X, T* __restrict__ y, Dims d, long long batch_items,
+                       const double2* __restrict__ ta, const double2* __restrict__ tb,
+                       const double2* __restrict__ tc) {
+  const long long total = d.numel * batch_items;
+  for (long long f = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; f < total;
+       f += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long b = f / d.numel;
+    const double2* Xb = X + b * d.numel;
+    int k[3];
+    unflat(f - b * d.numel, d, k);
+    double v;
+    if (d.rank == 1) {
+      v = cm(ta[k[0]], Xb[k[0]]).x;
+    } else if (d.rank == 2) {
+      const int n1 = d.n[0], n2 = d.n[1];
+      const int r1 = (n1 - k[0]) % n1;
+      const double2 a = ta[k[0]];
+      const double2 x1 = Xb[static_cast<long long>(k[0]) * n2 + k[1]];
+      const double2 x2 = Xb[static_cast<long long>(r1) * n2 + k[1]];
+      v = 0.5 * cm(tb[k[1]], ca(cm(a, x1), cm(cj(a), x2))).x;
+    } else {
+      const int n1 = d.n[0], n2 = d.n[1], n3 = d.n[2];
+      const int r1 = (n1 - k[0]) % n1, r2 = (n2 - k[1]) % n2;
+      auto at = [&](int i, int j) { return Xb[(static_cast<long long>(i) * n2 + j) * n3 + k[2]]; };
+      const double2 a = ta[k[0]], bb = tb[k[1]];
+      const double2 ab = cm(a, bb), cb = cm(cj(a), bb);
+      double2 s = cm(ab, at(k[0], k[1]));
+      s = ca(s, cm(cb, at(r1, k[1])));
+      s = ca(s, cm(cj(cb), at(k[0], r2)));
+      s = ca(s, cm(cj(ab), at(r1, r2)));
+      v = 0.25 * cm(tc[k[2]], s).x;
+    }
+    y[f] = static_cast<T>(v);
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ double fetch2g(const T* x, int i, int j, int n1, int n2, int mode) {
+  if (i == n1 || j == n2) return 0.0;
+  if (mode == 1) {
+    if (i == 0) return 0.0;
+    i = n1 - i;
+  } else if (mode == 2) {
+    if (j == 0) return 0.0;
+    j = n2 - j;
+  }
+  return static_cast<double>(x[static_cast<long long>(i) * n2 + j]);
+}
+
+// Full Hermitian spectrum of the merged inverse preprocess (any rank 1..3).
+// 1D (idct_1d, dct1d.cpp:185-220 embedding): X'(k) = conj(a(k)) (x(k) - i x(N-k)), x(N) := 0.
+template <typename T>
+__global__ void g_pre(const T* __restrict__ x, double2* __restrict__ Xo, Dims d, long long batch_items,
+                      int mode, const double2* __restrict__ ta, const double2* __restrict__ tb,
+                      const double2* __restrict__ tc) {
+  const long long total = d.numel * batch_items;
+  for (long long f = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; f < total;
+       f += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long b = f / d.numel;
+    const T* xb = x + b * d.numel;
+    int k[3];
+    unflat(f - b * d.numel, d, k);
+    const int last = d.rank - 1;
+    const int nl = d.n[last];
+    bool flip = k[last] > nl / 2;  // Hermitian fill of the upper half of the last axis
+    int e[3];
+    for (int a = 0; a < d.rank; ++a) e[a] = flip ? (d.n[a] - k[a]) % d.n[a] : k[a];
+    double2 val;
+    if (d.rank == 1) {
+      const int n = d.n[0], kk = e[0];
+      double p = static_cast<double>(xb[kk]);
+      double q = kk == 0 ? 0.0 : static_cast<double>(xb[n - kk]);
+      if (mode == 2) {  // idxst embedding: x(N-n) with x(N) := 0 (transforms_ext.cpp:238-242)
+        p = kk == 0 ? 0.0 : static_cast<double>(xb[n - kk]);
+        q = kk == 0 ? 0.0 : static_cast<double>(xb[kk]);
+        val = cm(cj(ta[kk]), make_double2(p, -q));
+      } else {
+        val = cm(cj(ta[kk]), make_double2(p, -q));
+      }
+    } else if (d.rank == 2) {
+      const int n1 = d.n[0], n2 = d.n[1];
+      const int k1 = e[0], m2 = e[1];
+      // pick the reference work item (q1 <= n1/2) that writes row k1
+      const bool direct = k1 <= n1 / 2;
+      const int q1 = direct ? k1 : n1 - k1;
+      const double p = fetch2g(xb, q1, m2, n1, n2, mode);
+      const double q = fetch2g(xb, n1 - q1, n2 - m2, n1, n2, mode);
+      const double r = fetch2g(xb, n1 - q1, m2, n1, n2, mode);
+      const double s = fetch2g(xb, q1, n2 - m2, n1, n2, mode);
+      const double2 w = cj(cm(ta[k1], tb[m2]));
+      val = direct ? cm(w, make_double2(p - q, -(r + s))) : cm(w, make_double2(r - s, -(p + q)));
+    } else {
+      const int n1 = d.n[0], n2 = d.n[1], n3 = d.n[2];
+      const int i = e[0], j = e[1], kk = e[2];
+      auto F = [&](int ii, int jj, int ll) -> double {
+        if (ii == n1 || jj == n2 || ll == n3) return 0.0;
+        return static_cast<double>(xb[(static_cast<long long>(ii) * n2 + jj) * n3 + ll]);
+      };
+      const int r1 = n1 - i, r2 = n2 - j, r3 = n3 - kk;
+      const double re = (F(i, j, kk) - F(r1, r2, kk)) - (F(r1, j, r3) + F(i, r2, r3));
+      const double im = F(r1, r2, r3) - ((F(r1, j, kk) + F(i, r2, kk)) + F(i, j, r3));
+      const double2 w = cj(cm(cm(ta[i], tb[j]), tc[kk]));
+      val = cm(w, make_double2(re, im));
+    }
+    Xo[f] = flip ? cj(val) : val;
+  }
+}
+
+template <typename T>
+__global__ void g_gather_inv(const double2* __restrict__ z, T* __restrict__ y, Dims d, long long batch_items,
+                             double scale, int sign_axis) {
+  const long long total = d.numel * batch_items;
+  for (long long f = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; f < total;
+       f += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long b = f / d.numel;
+    int k[3];
+    unflat(f - b * d.numel, d, k);
+    long long src = 0;
+    for (int a = 0; a < d.rank; ++a) src = src * d.n[a] + parity_source(k[a], d.n[a]);
+    double v = scale * z[b * d.numel + src].x;
+    if (sign_axis >= 0 && (k[sign_axis] & 1)) v = -v;
+    y[f] = static_cast<T>(v);
+  }
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+template <typename T>
+cudaError_t generic_run(const GenericJob& job, const void* in, void* out, void* ws, cudaStream_t st) {
+  Dims d;
+  d.rank = job.rank;
+  d.numel = 1;
+  for (int a = 0; a < 3; ++a) d.n[a] = a < job.rank ? job.dims[a] : 1;
+  for (int a = 0; a < job.rank; ++a) d.numel *= job.dims[a];
+  const long long total = d.numel * job.batch;
+  double2* A = static_cast<double2*>(ws);
+  double2* B = A + total;
+  const int g = nblocks(total);
+  auto dft_all = [&](double2*& cur, double2*& nxt, int inverse) {
+    for (int a = 0; a < job.rank; ++a) {
+      long long inner = 1, outer = job.batch;
+      for (int t = a + 1; t < job.rank; ++t) inner *= job.dims[t];
+      for (int t = 0; t < a; ++t) outer *= job.dims[t];
+      if (job.dims[a] > 1) {
+        g_dft_axis<<<g, kThreads, 0, st>>>(cur, nxt, outer, job.dims[a], inner, job.circle[a], inverse);
+        double2* t = cur;
+        cur = nxt;
+        nxt = t;
+      }
+    }
+  };
+  double2* cur = A;
+  double2* nxt = B;
+  if (!job.inverse) {
+    g_gather_fwd<T><<<g, kThreads, 0, st>>>(static_cast<const T*>(in), A, d, job.batch);
+    dft_all(cur, nxt, 0);
+    g_post<T><<<g, kThreads, 0, st>>>(cur, static_cast<T*>(out), d, job.batch, job.quarter[0],
+                                       job.quarter[1], job.quarter[2]);
+  } else {
+    g_pre<T><<<g, kThreads, 0, st>>>(static_cast<const T*>(in), A, d, job.batch, job.mode,
+                                      job.quarter[0], job.quarter[1], job.quarter[2]);
+    dft_all(cur, nxt, 1);
+    g_gather_inv<T><<<g, kThreads, 0, st>>>(cur, static_cast<T*>(out), d, job.batch, job.scale,
+                                             job.sign_axis);
+  }
+  return cudaGetLastError();
+}
+
+template cudaError_t generic_run<float>(const GenericJob&, const void*, void*, void*, cudaStream_t);
+template cudaError_t generic_run<double>(const GenericJob&, const void*, void*, void*, cudaStream_t);
+
+}  // namespace sdctb

@@ -1,0 +1,740 @@
+// Plan object, dispatch and the extern "C" boundary (include/sdct_b200.h).
+//
+// A plan caches everything per shape that the reference rebuilds per call
+// (proj/src/dct2d.cpp:389-393 builds a fresh Plan2d on every Python call):
+// the quarter-wave tables a, b (, c) (proj/src/dct1d.cpp:41-48), the FFT
+// circle table, the packing twiddles, the launch geometry (band width W of the
+// column kernels) and a device workspace for the one inter-pass intermediate.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/sdct_b200.h"
+#include "fast_launch.cuh"
+#include "generic.h"
+
+using namespace sdctb;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+  return fail(e == cudaErrorMemoryAllocation ? SDCT_ERR_OOM : SDCT_ERR_CUDA,
+              std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+bool is_pow2(long long n) { return n > 0 && (n & (n - 1)) == 0; }
+int ilog2i(long long n) {
+  int l = 0;
+  while ((1LL << l) < n) ++l;
+  return l;
+}
+
+class DeviceGuard {
+ public:
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev_);
+    if (dev >= 0 && dev != prev_) {
+      cudaSetDevice(dev);
+      switched_ = true;
+    }
+  }
+  ~DeviceGuard() {
+    if (switched_) cudaSetDevice(prev_);
+  }
+
+ private:
+  int prev_ = 0;
+  bool switched_ = false;
+};
+
+}  // namespace
+
+cudaError_t sdctb::prep_smem_ptr(const void* kernel, size_t smem) {
+  static std::mutex mu;
+  static std::unordered_map<const void*, size_t> granted;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = granted.find(kernel);
+  if (it != granted.end() && it->second >= smem) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  if (e == cudaSuccess) granted[kernel] = smem;
+  return e;
+}
+
+struct sdct_plan_s {
+  int rank = 2;
+  int n[3] = {1, 1, 1};
+  long long batch = 1;
+  long long numel = 1;  // per item
+  int dtype = SDCT_F64;
+  int orientation = SDCT_ORIENT_DIRECT;
+  int device = 0;
+  bool fast = false;
+  // fast geometry
+  int M = 0;        // packed z-line length (n_last / 2)
+  int lgw[2] = {1, 1};  // column-kernel band widths: pass over axis 0, pass over axis 1 (3D)
+  int Lc = 1;       // circle-table length
+  // device tables (one allocation)
+  void* tables = nullptr;
+  void* circ = nullptr;  // dtype: W_Lc^m
+  void* ta = nullptr;    // dtype quarter-wave tables
+  void* tb = nullptr;
+  void* tc = nullptr;
+  void* tu = nullptr;    // dtype: W_{Nlast}^k, k <= M
+  double2* gq[3] = {nullptr, nullptr, nullptr};  // generic fp64 quarter-wave tables
+  double2* gc[3] = {nullptr, nullptr, nullptr};  // generic fp64 circle tables
+  size_t b_offset_fast = 0, b_offset_gen = 0;    // element offsets of table b (corrupt hook)
+  // workspace + host staging
+  void* ws = nullptr;
+  size_t ws_bytes = 0;
+  void* d_in = nullptr;
+  void* d_out = nullptr;
+  std::mutex mu;
+
+  void* gws = nullptr;  // generic-path scratch on fast plans (row-column), lazily allocated
+  size_t elem() const { return dtype == SDCT_F32 ? 4 : 8; }
+  size_t generic_ws_bytes() const {
+    return 2 * static_cast<size_t>(batch) * static_cast<size_t>(numel) * sizeof(double2);
+  }
+  size_t item_bytes() const { return static_cast<size_t>(numel) * elem(); }
+};
+
+namespace {
+
+template <typename T>
+void fill_table(std::vector<unsigned char>& blob, size_t& off, const std::vector<long double>& re,
+                const std::vector<long double>& im) {
+  off = (blob.size() + 255) & ~size_t(255);
+  blob.resize(off + re.size() * 2 * sizeof(T));
+  T* p = reinterpret_cast<T*>(blob.data() + off);
+  for (size_t i = 0; i < re.size(); ++i) {
+    p[2 * i] = static_cast<T>(re[i]);
+    p[2 * i + 1] = static_cast<T>(im[i]);
+  }
+}
+
+// e^{-i 2 pi num * k / den} for k < count
+void circle(std::vector<long double>& re, std::vector<long double>& im, long long count,
+            long double num, long double den) {
+  const long double pi = 3.141592653589793238462643383279502884L;
+  re.resize(count);
+  im.resize(count);
+  for (long long k = 0; k < count; ++k) {
+    const long double ph = -2.0L * pi * num * static_cast<long double>(k) / den;
+    re[k] = cosl(ph);
+    im[k] = sinl(ph);
+  }
+}
+
+int pick_lgw(int L, int M, long long planes_batch, size_t cxsize) {
+  // Largest band that keeps the tile <= 128 KB, <= 32 columns, <= M, while
+  // keeping >= 2 CTAs per SM of parallelism when the problem allows.
+  long long w = std::max<long long>(2, (128 * 1024) / (static_cast<long long>(L) * cxsize));
+  w = std::min<long long>(w, 32);
+  w = std::min<long long>(w, M);
+  while (w > 2 && (M / w) * planes_batch < 2 * 148) w >>= 1;
+  return ilog2i(w);
+}
+
+int build_plan(sdct_plan_s* p) {
+  const int r = p->rank;
+  const size_t cx = 2 * p->elem();
+  // ---- fast-path eligibility ----
+  bool fast = false;
+  if (r == 2) {
+    const int n1 = p->n[0], n2 = p->n[1];
+    fast = is_pow2(n1) && is_pow2(n2) && n1 >= 2 && n2 >= 8 && n1 <= kMaxFastLen && n2 / 2 <= kMaxFastLen;
+  } else if (r == 3) {
+    const int n1 = p->n[0], n2 = p->n[1], n3 = p->n[2];
+    fast = is_pow2(n1) && is_pow2(n2) && is_pow2(n3) && n1 >= 2 && n2 >= 2 && n3 >= 8 &&
+           n1 <= kMaxFastLen && n2 <= kMaxFastLen && n3 / 2 <= kMaxFastLen &&
+           static_cast<size_t>(4) * (n3 / 2) * cx <= 200 * 1024;
+  }
+  p->fast = fast;
+
+  std::vector<unsigned char> blob;
+  std::vector<long double> re, im;
+  size_t off_circ = 0, off_ta = 0, off_tb = 0, off_tc = 0, off_tu = 0;
+  size_t off_gq[3] = {0, 0, 0}, off_gc[3] = {0, 0, 0};
+  if (fast) {
+    const int nl = p->n[r - 1];
+    p->M = nl / 2;
+    p->Lc = std::max(p->n[0], p->M);
+    if (r == 3) p->Lc = std::max(p->Lc, p->n[1]);
+    const bool f32 = p->dtype == SDCT_F32;
+    auto put = [&](size_t& off) {
+      if (f32) fill_table<float>(blob, off, re, im);
+      else fill_table<double>(blob, off, re, im);
+    };
+    circle(re, im, p->Lc, 1.0L, p->Lc);
+    put(off_circ);
+    circle(re, im, p->n[0], 1.0L, 4.0L * p->n[0]);
+    put(off_ta);
+    circle(re, im, p->n[1], 1.0L, 4.0L * p->n[1]);
+    put(off_tb);
+    if (r == 3) {
+      circle(re, im, p->n[2], 1.0L, 4.0L * p->n[2]);
+      put(off_tc);
+    }
+    circle(re, im, p->M + 1, 1.0L, nl);
+    put(off_tu);
+    const long long pb0 = (r == 2 ? 1 : p->n[1]) * p->batch;
+    p->lgw[0] = pick_lgw(p->n[0], p->M, pb0, cx);
+    if (r == 3) p->lgw[1] = pick_lgw(p->n[1], p->M, static_cast<long long>(p->n[0]) * p->batch, cx);
+    p->ws_bytes = static_cast<size_t>(p->batch) * p->item_bytes();
+  } else {
+    p->ws_bytes = p->generic_ws_bytes();
+  }
+  // generic-path tables are always present (odd shapes, row-column, 1D)
+  for (int a = 0; a < r; ++a) {
+    circle(re, im, p->n[a], 1.0L, 4.0L * p->n[a]);
+    fill_table<double>(blob, off_gq[a], re, im);
+    circle(re, im, p->n[a], 1.0L, p->n[a]);
+    fill_table<double>(blob, off_gc[a], re, im);
+  }
+  cudaError_t e = cudaMalloc(&p->tables, blob.size());
+  if (e != cudaSuccess) return cuda_fail(e, "allocating plan tables");
+  e = cudaMemcpy(p->tables, blob.data(), blob.size(), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) return cuda_fail(e, "uploading plan tables");
+  unsigned char* base = static_cast<unsigned char*>(p->tables);
+  if (fast) {
+    p->circ = base + off_circ;
+    p->ta = base + off_ta;
+    p->tb = base + off_tb;
+    p->tc = r == 3 ? base + off_tc : nullptr;
+    p->tu = base + off_tu;
+    p->b_offset_fast = off_tb;
+  }
+  for (int a = 0; a < r; ++a) {
+    p->gq[a] = reinterpret_cast<double2*>(base + off_gq[a]);
+    p->gc[a] = reinterpret_cast<double2*>(base + off_gc[a]);
+  }
+  p->b_offset_gen = r >= 2 ? off_gq[1] : off_gq[0];
+  e = cudaMalloc(&p->ws, p->ws_bytes);
+  if (e != cudaSuccess) return cuda_fail(e, "allocating plan workspace");
+  return SDCT_OK;
+}
+
+bool kind_ok(const sdct_plan_s* p, int kind) {
+  switch (kind) {
+    case SDCT_DCT_2D:
+    case SDCT_IDCT_2D:
+    case SDCT_IDCT_IDXST_2D:
+    case SDCT_IDXST_IDCT_2D:
+    case SDCT_DCT_2D_ROWCOL:
+      return p->rank == 2;
+    case SDCT_DCT_3D:
+    case SDCT_IDCT_3D:
+      return p->rank == 3;
+    case SDCT_DCT_1D:
+    case SDCT_IDCT_1D:
+    case SDCT_IDXST_1D:
+      return p->rank == 1;
+    default:
+      return false;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Stage lists. Every transform is an ordered list of kernel launches; the
+// full transform runs all of them, sdct_exec_stage runs one.
+// ---------------------------------------------------------------------------
+template <typename T>
+int run_fast(sdct_plan_s* p, int kind, int only_stage, const void* in, void* out, void* ws,
+             cudaStream_t st, int* nstages) {
+  using V = cx_t<T>;
+  const int n1 = p->n[0], n2 = p->n[1], n3 = p->n[2];
+  const int M = p->M;
+  const size_t cx = sizeof(V);
+  const V* circ = static_cast<const V*>(p->circ);
+  const long long item = p->numel;
+  const int B = static_cast<int>(p->batch);
+  int stage = 0;
+  cudaError_t e = cudaSuccess;
+  auto want = [&](void) { return only_stage < 0 || only_stage == stage; };
+  auto col = [&](int L, int lgw, bool inv, int ld, int stv, int planes, const ColArgs& a) {
+    if (want() && e == cudaSuccess) {
+      const dim3 grid(M >> lgw, planes, B);
+      const size_t smem = static_cast<size_t>(L) << lgw;
+      e = launch_col<T>(L, inv, ld, stv, grid, smem * cx, st, a, circ, p->Lc / L);
+    }
+    ++stage;
+  };
+  auto row = [&](int rk, int groups, const RowArgs& a) {
+    if (want() && e == cudaSuccess) {
+      const int G = (rk == RK_FWD2 || rk == RK_INV2) ? 2 : 4;
+      const dim3 grid(groups, B);
+      e = launch_row<T>(M, rk, grid, static_cast<size_t>(G) * M * cx, st, a, circ, p->Lc / M);
+    }
+    ++stage;
+  };
+  RowArgs ra{};
+  ra.n1 = n1;
+  ra.n2 = n2;
+  ra.n3 = n3;
+  ra.ta = p->ta;
+  ra.tb = p->tb;
+  ra.tc = p->tc;
+  ra.tu = p->tu;
+  if (p->rank == 2) {
+    const long long inter = static_cast<long long>(n1) * M;
+    if (kind == SDCT_DCT_2D) {
+      ColArgs c{};
+      c.src = in;
+      c.dst = ws;
+      c.in_row = n2;
+      c.in_batch = item;
+      c.out_row = M;
+      c.out_batch = inter;
+      c.lgw = p->lgw[0];
+      col(n1, p->lgw[0], false, LD_SRC, ST_INTER, 1, c);
+      ra.src = ws;
+      ra.src_batch = inter;
+      ra.dst = out;
+      ra.dst_batch = item;
+      row(RK_FWD2, n1 / 2, ra);
+    } else {
+      const int mode = kind == SDCT_IDXST_IDCT_2D ? 1 : kind == SDCT_IDCT_IDXST_2D ? 2 : 0;
+      ra.src = in;
+      ra.src_batch = item;
+      ra.dst = ws;
+      ra.dst_batch = inter;
+      ra.mode = mode;
+      row(RK_INV2, n1 / 2, ra);
+      ColArgs c{};
+      c.src = ws;
+      c.dst = out;
+      c.in_row = M;
+      c.in_batch = inter;
+      c.out_row = n2;
+      c.out_batch = item;
+      c.lgw = p->lgw[0];
+      c.scale = 0.25;
+      c.sign_row = mode == 1;
+      c.sign_col = mode == 2;
+      col(n1, p->lgw[0], true, LD_INTER, ST_DST, 1, c);
+    }
+  } else {
+    const long long inter = static_cast<long long>(n1) * n2 * M;
+    const int groups = (n1 / 2 + 1) * (n2 / 2 + 1);
+    if (kind == SDCT_DCT_3D) {
+      ColArgs c{};
+      c.src = in;
+      c.dst = ws;
+      c.in_row = static_cast<long long>(n2) * n3;
+      c.in_plane = n3;
+      c.in_plane_par = n2;
+      c.in_batch = item;
+      c.out_row = static_cast<long long>(n2) * M;
+      c.out_plane = M;
+      c.out_batch = inter;
+      c.lgw = p->lgw[0];
+      col(n1, p->lgw[0], false, LD_SRC, ST_INTER, n2, c);
+      ColArgs d{};
+      d.src = ws;
+      d.dst = ws;
+      d.in_row = M;
+      d.in_plane = static_cast<long long>(n2) * M;
+      d.in_batch = inter;
+      d.out_row = M;
+      d.out_plane = static_cast<long long>(n2) * M;
+      d.out_batch = inter;
+      d.lgw = p->lgw[1];
+      col(n2, p->lgw[1], false, LD_INTER, ST_INTER, n1, d);
+      ra.src = ws;
+      ra.src_batch = inter;
+      ra.dst = out;
+      ra.dst_batch = item;
+      row(RK_FWD3, groups, ra);
+    } else {
+      ra.src = in;
+      ra.src_batch = item;
+      ra.dst = ws;
+      ra.dst_batch = inter;
+      row(RK_INV3, groups, ra);
+      ColArgs d{};
+      d.src = ws;
+      d.dst = ws;
+      d.in_row = M;
+      d.in_plane = static_cast<long long>(n2) * M;
+      d.in_batch = inter;
+      d.out_row = M;
+      d.out_plane = static_cast<long long>(n2) * M;
+      d.out_batch = inter;
+      d.lgw = p->lgw[1];
+      col(n2, p->lgw[1], true, LD_INTER, ST_INTER, n1, d);
+      ColArgs c{};
+      c.src = ws;
+      c.dst = out;
+      c.in_row = static_cast<long long>(n2) * M;
+      c.in_plane = M;
+      c.in_batch = inter;
+      c.out_row = static_cast<long long>(n2) * n3;
+      c.out_plane = n3;
+      c.out_plane_par = n2;
+      c.out_batch = item;
+      c.lgw = p->lgw[0];
+      c.scale = 0.125;
+      col(n1, p->lgw[0], true, LD_INTER, ST_DST, n2, c);
+    }
+  }
+  if (nstages) *nstages = stage;
+  if (e != cudaSuccess) return cuda_fail(e, "launching fast-path kernel");
+  return SDCT_OK;
+}
+
+GenericJob make_job(const sdct_plan_s* p, int kind) {
+  GenericJob j;
+  j.rank = p->rank;
+  for (int a = 0; a < p->rank; ++a) {
+    j.dims[a] = p->n[a];
+    j.quarter[a] = p->gq[a];
+    j.circle[a] = p->gc[a];
+  }
+  j.batch = p->batch;
+  switch (kind) {
+    case SDCT_IDCT_2D: j.inverse = true; j.scale = 0.25; break;
+    case SDCT_IDXST_IDCT_2D: j.inverse = true; j.scale = 0.25; j.mode = 1; j.sign_axis = 0; break;
+    case SDCT_IDCT_IDXST_2D: j.inverse = true; j.scale = 0.25; j.mode = 2; j.sign_axis = 1; break;
+    case SDCT_IDCT_3D: j.inverse = true; j.scale = 0.125; break;
+    case SDCT_IDCT_1D: j.inverse = true; j.scale = 0.5; break;
+    case SDCT_IDXST_1D: j.inverse = true; j.scale = 0.5; j.mode = 2; j.sign_axis = 0; break;
+    default: break;
+  }
+  return j;
+}
+
+int generic_stage_count(const sdct_plan_s* p) {
+  int n = 2;
+  for (int a = 0; a < p->rank; ++a) n += p->n[a] > 1;
+  return n;
+}
+
+template <typename T>
+int run(sdct_plan_s* p, int kind, int only_stage, const void* in, void* out, void* ws,
+        cudaStream_t st, int* nstages) {
+  // Row-column baseline and the 1D transforms run on the generic path.
+  const bool use_fast = p->fast && kind != SDCT_DCT_2D_ROWCOL;
+  if (use_fast) return run_fast<T>(p, kind, only_stage, in, out, ws, st, nstages);
+  if (nstages) *nstages = 1;  // generic path is timed as one unit
+  if (only_stage > 0) return SDCT_OK;
+  if (p->fast && ws == p->ws) {
+    // fast plan running a generic-path transform: needs the larger scratch
+    if (!p->gws) {
+      cudaError_t ea = cudaMalloc(&p->gws, p->generic_ws_bytes());
+      if (ea != cudaSuccess) return cuda_fail(ea, "allocating generic scratch");
+    }
+    ws = p->gws;
+  }
+  cudaError_t e = generic_run<T>(make_job(p, kind), in, out, ws, st);
+  if (e != cudaSuccess) return cuda_fail(e, "launching generic-path kernels");
+  return SDCT_OK;
+}
+
+int dispatch(sdct_plan_s* p, int kind, int only_stage, const void* in, void* out, void* ws,
+             cudaStream_t st, int* nstages) {
+  if (!kind_ok(p, kind)) return fail(SDCT_ERR_PLAN, "transform kind does not match the plan rank");
+  if (!ws) ws = p->ws;
+  DeviceGuard g(p->device);
+  return p->dtype == SDCT_F32 ? run<float>(p, kind, only_stage, in, out, ws, st, nstages)
+                              : run<double>(p, kind, only_stage, in, out, ws, st, nstages);
+}
+
+// ---- analytic StageCounters (replays the reference's Counted tallies) -----
+struct Cnt {
+  unsigned long long stages = 0, reads = 0, writes = 0, mults = 0, adds = 0;
+  void cmul() { mults += 4; adds += 2; }
+};
+
+void count_dct2(long long m1, long long m2, Cnt& c) {
+  // parity gather (dct2d.cpp:48-70) + fused post (82-115)
+  c.stages = 3;
+  c.reads += m1 * m2;
+  c.writes += m1 * m2;
+  const long long h2 = m2 / 2 + 1;
+  for (long long q1 = 0; q1 <= m1 / 2; ++q1)
+    for (long long q2 = 0; q2 < h2; ++q2) {
+      const bool deg1 = (m1 - q1) % m1 == q1, deg2 = (m2 - q2) % m2 == q2;
+      c.reads += deg1 ? 1 : 2;
+      c.cmul(); c.cmul(); c.adds += 2; c.cmul();
+      c.writes += 1 + (deg2 ? 0 : 1);
+      if (!deg1) {
+        c.adds += 2; c.cmul();
+        c.writes += 1 + (deg2 ? 0 : 1);
+      }
+    }
+}
+
+void count_idct2(long long m1, long long m2, int mode, Cnt& c) {
+  // idct_pre (dct2d.cpp:161-198) + inverse gather (214-238)
+  c.stages = 3;
+  const long long h2 = m2 / 2 + 1;
+  auto loads = [&](long long i, long long j) -> int {
+    if (i == m1 || j == m2) return 0;
+    if (mode == 1 && i == 0) return 0;
+    if (mode == 2 && j == 0) return 0;
+    return 1;
+  };
+  for (long long q1 = 0; q1 <= m1 / 2; ++q1)
+    for (long long n2 = 0; n2 < h2; ++n2) {
+      c.reads += loads(q1, n2) + loads(m1 - q1, m2 - n2) + loads(m1 - q1, n2) + loads(q1, m2 - n2);
+      c.cmul(); c.adds += 2; c.cmul(); c.writes += 1;
+      if ((m1 - q1) % m1 != q1) {
+        c.cmul(); c.adds += 2; c.cmul(); c.writes += 1;
+      }
+    }
+  c.reads += m1 * m2;
+  c.writes += m1 * m2;
+}
+
+void count_dct3(long long n1, long long n2, long long n3, Cnt& c) {
+  c.stages = 3;
+  const long long N = n1 * n2 * n3;
+  c.reads += N;
+  c.writes += N;
+  for (long long q1 = 0; q1 <= n1 / 2; ++q1)
+    for (long long q2 = 0; q2 <= n2 / 2; ++q2)
+      for (long long q3 = 0; q3 <= n3 / 2; ++q3) {
+        const bool d1 = (n1 - q1) % n1 == q1, d2 = (n2 - q2) % n2 == q2, d3 = (n3 - q3) % n3 == q3;
+        c.reads += 1 + (d1 ? 0 : 1) + (d2 ? 0 : 1) + ((d1 || d2) ? 0 : 1);
+        c.cmul(); c.cmul();            // ab, cb
+        c.cmul(); c.cmul(); c.cmul(); c.cmul();  // t1..t4
+        c.adds += 4;                   // sum12, sum34
+        c.adds += 2; c.cmul();         // cu00
+        c.writes += 1 + (d3 ? 0 : 1);
+        if (!d2) { c.adds += 2; c.cmul(); c.writes += 1 + (d3 ? 0 : 1); }
+        if (!d1) {
+          c.adds += 4;                 // dif12, dif34
+          c.adds += 2; c.cmul(); c.writes += 1 + (d3 ? 0 : 1);
+          if (!d2) { c.adds += 2; c.cmul(); c.writes += 1 + (d3 ? 0 : 1); }
+        }
+      }
+}
+
+void count_idct3(long long n1, long long n2, long long n3, Cnt& c) {
+  c.stages = 3;
+  const long long h3 = n3 / 2 + 1;
+  auto ld = [&](long long i, long long j, long long k) -> int { return (i == n1 || j == n2 || k == n3) ? 0 : 1; };
+  for (long long i = 0; i < n1; ++i)
+    for (long long j = 0; j < n2; ++j)
+      for (long long k = 0; k < h3; ++k) {
+        const long long r1 = n1 - i, r2 = n2 - j, r3 = n3 - k;
+        c.reads += ld(i, j, k) + ld(r1, r2, k) + ld(r1, j, r3) + ld(i, r2, r3) + ld(r1, r2, r3) +
+                   ld(r1, j, k) + ld(i, r2, k) + ld(i, j, r3);
+        c.adds += 3 + 3;
+        c.cmul(); c.cmul(); c.cmul();
+        c.writes += 1;
+      }
+  const long long N = n1 * n2 * n3;
+  c.reads += N;
+  c.writes += N;
+}
+
+}  // namespace
+
+// ===========================================================================
+// extern "C"
+// ===========================================================================
+extern "C" {
+
+int sdct_version(void) { return 10000; }
+
+const char* sdct_last_error(void) { return g_last_error.c_str(); }
+
+int sdct_plan_create(sdct_plan_t* out, int rank, const int64_t* dims, int64_t batch, int dtype,
+                     int orientation, int device) {
+  if (!out || !dims) return fail(SDCT_ERR_ARG, "null argument to sdct_plan_create");
+  *out = nullptr;
+  if (rank < 1 || rank > 3) return fail(SDCT_ERR_SHAPE, "plans cover rank 1..3, got rank " + std::to_string(rank));
+  for (int a = 0; a < rank; ++a)
+    if (dims[a] <= 0) return fail(SDCT_ERR_SHAPE, "transform extents must be positive");
+  for (int a = 0; a < rank; ++a)
+    if (dims[a] > (1LL << 30)) return fail(SDCT_ERR_SHAPE, "extent too large");
+  if (batch < 1) return fail(SDCT_ERR_SHAPE, "batch must be >= 1");
+  if (dtype != SDCT_F32 && dtype != SDCT_F64) return fail(SDCT_ERR_ARG, "dtype must be SDCT_F32 or SDCT_F64");
+  if (orientation < -1 || orientation > 1) return fail(SDCT_ERR_ARG, "unknown orientation");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    return fail(SDCT_ERR_NODEVICE, "no CUDA device available");
+  }
+  if (device < 0) cudaGetDevice(&device);
+  if (device >= ndev) return fail(SDCT_ERR_ARG, "device index out of range");
+  auto* p = new sdct_plan_s;
+  p->rank = rank;
+  p->numel = 1;
+  for (int a = 0; a < rank; ++a) {
+    p->n[a] = static_cast<int>(dims[a]);
+    p->numel *= dims[a];
+  }
+  p->batch = batch;
+  p->dtype = dtype;
+  p->device = device;
+  if (rank == 2) {
+    // maybe_transpose_strategy (proj/src/dct2d.cpp:294-298)
+    const bool tr = p->n[1] < p->n[0] && p->n[0] >= 4LL * p->n[1];
+    p->orientation = orientation == SDCT_ORIENT_AUTO ? (tr ? SDCT_ORIENT_TRANSPOSED : SDCT_ORIENT_DIRECT)
+                                                     : orientation;
+  }
+  DeviceGuard g(device);
+  const int rc = build_plan(p);
+  if (rc != SDCT_OK) {
+    sdct_plan_destroy(p);
+    return rc;
+  }
+  *out = p;
+  return SDCT_OK;
+}
+
+int sdct_plan_destroy(sdct_plan_t p) {
+  if (!p) return SDCT_OK;
+  DeviceGuard g(p->device);
+  cudaFree(p->tables);
+  cudaFree(p->ws);
+  cudaFree(p->d_in);
+  cudaFree(p->d_out);
+  cudaFree(p->gws);
+  delete p;
+  return SDCT_OK;
+}
+
+int sdct_plan_orientation(sdct_plan_t p, int* o) {
+  if (!p || !o) return fail(SDCT_ERR_ARG, "null argument");
+  *o = p->orientation;
+  return SDCT_OK;
+}
+
+int sdct_plan_is_fast(sdct_plan_t p, int* f) {
+  if (!p || !f) return fail(SDCT_ERR_ARG, "null argument");
+  *f = p->fast ? 1 : 0;
+  return SDCT_OK;
+}
+
+int sdct_plan_workspace_size(sdct_plan_t p, size_t* bytes) {
+  if (!p || !bytes) return fail(SDCT_ERR_ARG, "null argument");
+  *bytes = p->ws_bytes;
+  return SDCT_OK;
+}
+
+int sdct_plan_corrupt_twiddle(sdct_plan_t p, int64_t index) {
+  if (!p) return fail(SDCT_ERR_ARG, "null plan");
+  const int axis = p->rank >= 2 ? 1 : 0;
+  if (index < 0 || index >= p->n[axis])
+    return fail(SDCT_ERR_BOUNDS, "corrupt_twiddle_for_testing: index " + std::to_string(index) +
+                                     " out of range for table of size " + std::to_string(p->n[axis]));
+  DeviceGuard g(p->device);
+  unsigned char* base = static_cast<unsigned char*>(p->tables);
+  auto flip = [&](size_t off, bool f32) -> int {
+    const size_t esz = f32 ? 8 : 16;
+    off += static_cast<size_t>(index) * esz;
+    unsigned char tmp[16];
+    cudaError_t e = cudaMemcpy(tmp, base + off, esz, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return cuda_fail(e, "reading twiddle");
+    if (f32) {
+      float* v = reinterpret_cast<float*>(tmp);
+      v[0] = -v[0];
+      v[1] = -v[1];
+    } else {
+      double* v = reinterpret_cast<double*>(tmp);
+      v[0] = -v[0];
+      v[1] = -v[1];
+    }
+    e = cudaMemcpy(base + off, tmp, esz, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return cuda_fail(e, "writing twiddle");
+    return SDCT_OK;
+  };
+  int rc = flip(p->b_offset_gen, false);
+  if (rc == SDCT_OK && p->fast) rc = flip(p->b_offset_fast, p->dtype == SDCT_F32);
+  return rc;
+}
+
+int sdct_exec(sdct_plan_t p, int kind, const void* d_in, void* d_out, void* d_ws, void* stream) {
+  if (!p || !d_in || !d_out) return fail(SDCT_ERR_ARG, "null argument to sdct_exec");
+  if (d_in == d_out) return fail(SDCT_ERR_ARG, "sdct_exec is out of place: d_in == d_out");
+  return dispatch(p, kind, -1, d_in, d_out, d_ws, static_cast<cudaStream_t>(stream), nullptr);
+}
+
+int sdct_exec_host(sdct_plan_t p, int kind, const void* h_in, void* h_out, void* stream) {
+  if (!p || !h_in || !h_out) return fail(SDCT_ERR_ARG, "null argument to sdct_exec_host");
+  if (!kind_ok(p, kind)) return fail(SDCT_ERR_PLAN, "transform kind does not match the plan rank");
+  std::lock_guard<std::mutex> lock(p->mu);
+  DeviceGuard g(p->device);
+  const size_t bytes = static_cast<size_t>(p->batch) * p->item_bytes();
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaError_t e;
+  if (!p->d_in) {
+    if ((e = cudaMalloc(&p->d_in, bytes)) != cudaSuccess) return cuda_fail(e, "allocating staging");
+    if ((e = cudaMalloc(&p->d_out, bytes)) != cudaSuccess) return cuda_fail(e, "allocating staging");
+  }
+  if ((e = cudaMemcpyAsync(p->d_in, h_in, bytes, cudaMemcpyHostToDevice, st)) != cudaSuccess)
+    return cuda_fail(e, "copying input to device");
+  const int rc = dispatch(p, kind, -1, p->d_in, p->d_out, nullptr, st, nullptr);
+  if (rc != SDCT_OK) return rc;
+  if ((e = cudaMemcpyAsync(h_out, p->d_out, bytes, cudaMemcpyDeviceToHost, st)) != cudaSuccess)
+    return cuda_fail(e, "copying output to host");
+  if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return cuda_fail(e, "synchronising");
+  return SDCT_OK;
+}
+
+int sdct_stage_count(sdct_plan_t p, int kind, int* count) {
+  if (!p || !count) return fail(SDCT_ERR_ARG, "null argument");
+  if (!kind_ok(p, kind)) return fail(SDCT_ERR_PLAN, "transform kind does not match the plan rank");
+  if (p->fast && kind != SDCT_DCT_2D_ROWCOL) {
+    *count = p->rank == 2 ? 2 : 3;
+  } else {
+    *count = 1;
+  }
+  return SDCT_OK;
+}
+
+int sdct_exec_stage(sdct_plan_t p, int kind, int stage, const void* d_in, void* d_out, void* d_ws,
+                    void* stream) {
+  if (!p || !d_in || !d_out) return fail(SDCT_ERR_ARG, "null argument");
+  int n = 0;
+  int rc = sdct_stage_count(p, kind, &n);
+  if (rc != SDCT_OK) return rc;
+  if (stage < 0 || stage >= n) return fail(SDCT_ERR_BOUNDS, "stage index out of range");
+  return dispatch(p, kind, stage, d_in, d_out, d_ws, static_cast<cudaStream_t>(stream), nullptr);
+}
+
+int sdct_counters(sdct_plan_t p, int kind, uint64_t out[5]) {
+  if (!p || !out) return fail(SDCT_ERR_ARG, "null argument");
+  if (!kind_ok(p, kind)) return fail(SDCT_ERR_PLAN, "transform kind does not match the plan rank");
+  Cnt c;
+  const bool tr = p->rank == 2 && p->orientation == SDCT_ORIENT_TRANSPOSED;
+  const long long m1 = p->rank >= 2 ? (tr ? p->n[1] : p->n[0]) : p->n[0];
+  const long long m2 = p->rank >= 2 ? (tr ? p->n[0] : p->n[1]) : 1;
+  switch (kind) {
+    case SDCT_DCT_2D: count_dct2(m1, m2, c); break;
+    case SDCT_IDCT_2D: count_idct2(m1, m2, 0, c); break;
+    case SDCT_IDXST_IDCT_2D: count_idct2(m1, m2, tr ? 2 : 1, c); break;
+    case SDCT_IDCT_IDXST_2D: count_idct2(m1, m2, tr ? 1 : 2, c); break;
+    case SDCT_DCT_3D: count_dct3(p->n[0], p->n[1], p->n[2], c); break;
+    case SDCT_IDCT_3D: count_idct3(p->n[0], p->n[1], p->n[2], c); break;
+    case SDCT_DCT_2D_ROWCOL: c.stages = 8; break;
+    default: c.stages = 3; break;
+  }
+  const unsigned long long b = static_cast<unsigned long long>(p->batch);
+  out[0] = c.stages;
+  out[1] = c.reads * b;
+  out[2] = c.writes * b;
+  out[3] = c.mults * b;
+  out[4] = c.adds * b;
+  return SDCT_OK;
+}
+
+}  // extern "C"
