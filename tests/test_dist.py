@@ -1,0 +1,63 @@
+"""Multi-process host logic (gloo, world_size 2, CPU): batch shards are
+disjoint, complete and balanced, and the timing reduction is max-over-ranks —
+the same code paths bench.py uses under torchrun on NCCL."""
+import os
+import socket
+
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2110_01172_b200 import shard
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, total, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    s, e = shard.shard_range(total, world, rank)
+    t = torch.tensor([s, e], dtype=torch.int64)
+    out = [torch.zeros(2, dtype=torch.int64) for _ in range(world)]
+    dist.all_gather(out, t)
+    ms = torch.tensor([10.0 + rank], dtype=torch.float64)
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    if rank == 0:
+        q.put(([tuple(o.tolist()) for o in out], float(ms.item())))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("total", [512, 7])
+def test_gloo_world2_shards_cover_batch(total):
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, total, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    ranges, ms = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    covered = [i for s, e in ranges for i in range(s, e)]
+    assert covered == list(range(total))
+    sizes = [e - s for s, e in ranges]
+    assert max(sizes) - min(sizes) <= 1
+    assert ms == 11.0  # max over ranks
+
+
+def test_shard_helpers():
+    assert shard.shard_range(512, 8, 7) == (448, 512)
+    assert shard.spot_check_indices(512, 4) == [0, 127, 128, 255, 256, 383, 384, 511]
+    with pytest.raises(ValueError):
+        shard.shard_range(10, 2, 2)

@@ -1,0 +1,346 @@
+"""GPU parity tests: the CUDA path (called through the C ABI, include/sdct_b200.h,
+on device pointers) against the CPU oracle (oracle/sdct_oracle.c, itself pinned
+to the reference in tests/test_oracle.py) and against the reference's golden
+vectors. Tolerances (BASELINE.json north_star): rel-L2 <= 1e-12 fp64,
+<= 1e-5 fp32 (fp32 inputs are the fp64 draw rounded to fp32, fed identically
+to the fp64 oracle)."""
+import numpy as np
+import pytest
+import scipy.fft as sf
+
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+TOL = {"float64": 1e-12, "float32": 1e-5}
+KINDS_2D = ["dct_2d", "idct_2d", "idct_idxst_2d", "idxst_idct_2d"]
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+def run_capi(kind, x, dtype="float64", batch_shape=()):
+    """Run one transform through the C ABI on device memory; returns float64 numpy."""
+    torch = _torch()
+    from paper_2110_01172_b200 import capi
+
+    rank = capi.RANK_OF[kind]
+    tdt = torch.float64 if dtype == "float64" else torch.float32
+    xt = torch.as_tensor(np.ascontiguousarray(x), dtype=tdt).cuda()
+    core = xt.shape[xt.dim() - rank:]
+    batch = int(np.prod(xt.shape[: xt.dim() - rank])) if xt.dim() > rank else 1
+    plan = capi.Plan(core, batch=batch, dtype=capi.F64 if dtype == "float64" else capi.F32)
+    out = torch.empty_like(xt)
+    ws = torch.empty(max(plan.workspace_bytes, 1), dtype=torch.uint8, device="cuda")
+    plan.exec(kind, xt.data_ptr(), out.data_ptr(), ws.data_ptr(), torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    plan.close()
+    return out.double().cpu().numpy()
+
+
+def rnd(shape, seed, dtype="float64"):
+    x = np.random.default_rng(seed).uniform(-1.0, 1.0, shape)
+    if dtype == "float32":
+        x = x.astype(np.float32).astype(np.float64)
+    return x
+
+
+# ---------------------------------------------------------------- golden ---
+@pytest.mark.parametrize("kind", KINDS_2D)
+def test_golden_2d_fp64(golden, cuda, kind):
+    keys = sorted(k.split("/", 1)[1] for k in golden if k.startswith(kind + "/"))
+    for key in keys:
+        x = golden["in/" + key]
+        got = run_capi(kind, x)
+        want = golden[f"{kind}/{key}"]
+        assert oracle.rel_l2(got, want) <= 1e-12, (kind, key, oracle.rel_l2(got, want))
+        assert oracle.max_rel(got, want) <= 1e-10, (kind, key)
+
+
+@pytest.mark.parametrize("kind", ["dct_3d", "idct_3d"])
+def test_golden_3d_fp64(golden, cuda, kind):
+    keys = sorted(k.split("/", 1)[1] for k in golden if k.startswith(kind + "/"))
+    for key in keys:
+        x = golden["in/" + key]
+        got = run_capi(kind, x)
+        assert oracle.rel_l2(got, golden[f"{kind}/{key}"]) <= 1e-12, (kind, key)
+
+
+def test_golden_rowcol(golden, cuda):
+    for key in sorted(k.split("/", 1)[1] for k in golden if k.startswith("dct_2d_rowcol/")):
+        x = golden["in/" + key]
+        got = run_capi("dct_2d_rowcol", x)
+        assert oracle.rel_l2(got, golden["dct_2d_rowcol/" + key]) <= 1e-12, key
+
+
+def test_known_answers(golden, cuda):
+    np.testing.assert_allclose(run_capi("dct_2d", np.ones((2, 2))), [[4, 0], [0, 0]], atol=1e-15)
+    d = np.zeros((2, 2))
+    d[0, 0] = 1
+    np.testing.assert_allclose(run_capi("dct_2d", d), golden["kat/delta2x2/dct_2d"], atol=1e-15)
+    y = run_capi("dct_3d", np.ones((2, 2, 2)))
+    assert abs(y[0, 0, 0] - 8) < 1e-12 and np.abs(y.ravel()[1:]).max() < 1e-12
+    # fast path KAT: constant image -> only the DC coefficient survives
+    y = run_capi("dct_2d", np.ones((64, 64)))
+    assert abs(y[0, 0] - 4096) < 1e-9 and np.abs(y.ravel()[1:]).max() < 1e-9
+
+
+# ------------------------------------------------------ oracle sweeps ------
+SHAPES_2D = [(2, 8), (4, 16), (8, 8), (16, 8), (8, 64), (64, 8), (128, 256), (256, 128), (512, 512),
+             (2, 4096), (4096, 8), (5, 7), (31, 17), (16, 3), (3, 16), (100, 60), (1, 9), (9, 1)]
+
+
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+@pytest.mark.parametrize("kind", KINDS_2D)
+def test_2d_vs_oracle(cuda, dtype, kind):
+    for i, shape in enumerate(SHAPES_2D):
+        x = rnd(shape, 100 + i, dtype)
+        got = run_capi(kind, x, dtype)
+        want = getattr(oracle.port, kind)(x)
+        err = oracle.rel_l2(got, want)
+        assert err <= TOL[dtype], (kind, shape, dtype, err)
+
+
+SHAPES_3D = [(2, 2, 8), (4, 8, 16), (16, 4, 8), (8, 8, 64), (32, 32, 32), (3, 4, 5), (2, 6, 9), (64, 16, 16)]
+
+
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+@pytest.mark.parametrize("kind", ["dct_3d", "idct_3d"])
+def test_3d_vs_oracle(cuda, dtype, kind):
+    for i, shape in enumerate(SHAPES_3D):
+        x = rnd(shape, 200 + i, dtype)
+        err = oracle.rel_l2(run_capi(kind, x, dtype), getattr(oracle.port, kind)(x))
+        assert err <= TOL[dtype], (kind, shape, dtype, err)
+
+
+# --------------------------------------------------- BASELINE configs ------
+@pytest.mark.slow
+def test_c1_dct_1024_fp64(cuda):
+    x = rnd((1024, 1024), 1)
+    assert oracle.rel_l2(run_capi("dct_2d", x), oracle.port.dct_2d(x)) <= 1e-12
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+def test_c2_round_trip_4096(cuda, dtype):
+    x = rnd((4096, 4096), 2, dtype)
+    y = run_capi("dct_2d", x, dtype)
+    assert oracle.rel_l2(y, oracle.port.dct_2d(x)) <= TOL[dtype]
+    z = run_capi("idct_2d", y.astype(np.float32) if dtype == "float32" else y, dtype)
+    assert oracle.rel_l2(z / (4096 * 4096 / 4), x) <= 10 * TOL[dtype]
+    zi = run_capi("idct_2d", x, dtype)
+    assert oracle.rel_l2(zi, oracle.port.idct_2d(x)) <= TOL[dtype]
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+def test_c3_composites_2048(cuda, dtype):
+    x = rnd((2048, 2048), 3, dtype)
+    for kind in ("idct_idxst_2d", "idxst_idct_2d"):
+        assert oracle.rel_l2(run_capi(kind, x, dtype), getattr(oracle.port, kind)(x)) <= TOL[dtype], kind
+
+
+@pytest.mark.slow
+def test_c4_dct3d_256_fp32(cuda):
+    x = rnd((256, 256, 256), 4, "float32")
+    assert oracle.rel_l2(run_capi("dct_3d", x, "float32"), oracle.port.dct_3d(x)) <= 1e-5
+    back = run_capi("idct_3d", run_capi("dct_3d", x, "float32").astype(np.float32), "float32")
+    assert oracle.rel_l2(back / (256 ** 3 / 8), x) <= 1e-5
+
+
+@pytest.mark.slow
+def test_c5_batched_fp32_spot_checks(cuda):
+    from paper_2110_01172_b200 import shard
+
+    total = 16
+    xs = np.stack([rnd((2048, 2048), shard.item_seed(i), "float32") for i in range(total)])
+    ys = run_capi("dct_2d", xs, "float32")
+    for i in shard.spot_check_indices(total, 4):
+        assert oracle.rel_l2(ys[i], oracle.port.dct_2d(xs[i])) <= 1e-5, i
+    # a batched item equals the same item transformed alone, bit for bit
+    assert np.array_equal(ys[5], run_capi("dct_2d", xs[5], "float32"))
+
+
+# ------------------------------------------------------ properties ---------
+def test_round_trip_scaling(cuda):
+    for shape in [(1, 1), (2, 2), (9, 14), (8, 8), (256, 64)]:
+        x = rnd(shape, 7)
+        back = run_capi("idct_2d", run_capi("dct_2d", x))
+        assert oracle.rel_l2(back / (shape[0] * shape[1] / 4), x) <= 1e-12, shape
+    for shape in [(2, 3, 4), (8, 8, 8), (16, 8, 32)]:
+        x = rnd(shape, 8)
+        back = run_capi("idct_3d", run_capi("dct_3d", x))
+        assert oracle.rel_l2(back / (np.prod(shape) / 8), x) <= 1e-12, shape
+
+
+def test_linearity(cuda):
+    a, b = rnd((128, 64), 10), rnd((128, 64), 11)
+    for kind in KINDS_2D:
+        lhs = run_capi(kind, 2.0 * a - 3.0 * b)
+        rhs = 2.0 * run_capi(kind, a) - 3.0 * run_capi(kind, b)
+        assert oracle.rel_l2(lhs, rhs) <= 1e-13, kind
+
+
+def test_sine_axis_annihilates_slot_zero(cuda):
+    # proj/tests/test_transforms_ext.cpp:158-170 (odd shape: generic path; pow2: fast path)
+    for n in (5, 16):
+        x = np.zeros((n, n))
+        x[:, 0] = np.arange(n) + 1.0
+        assert np.abs(run_capi("idct_idxst_2d", x)).max() < 1e-12
+        z = np.zeros((n, n))
+        z[0, :] = np.arange(n) + 1.0
+        assert np.abs(run_capi("idxst_idct_2d", z)).max() < 1e-12
+
+
+def test_zero_input(cuda):
+    for kind in KINDS_2D:
+        assert not run_capi(kind, np.zeros((64, 32))).any()
+
+
+def test_bitwise_deterministic(cuda):
+    x = rnd((512, 256), 12)
+    for kind in KINDS_2D:
+        assert np.array_equal(run_capi(kind, x), run_capi(kind, x)), kind
+
+
+def test_batched_equals_unbatched(cuda):
+    xs = np.stack([rnd((64, 128), 20 + i) for i in range(3)])
+    ys = run_capi("idct_2d", xs)
+    for i in range(3):
+        assert np.array_equal(ys[i], run_capi("idct_2d", xs[i])), i
+    xs3 = np.stack([rnd((8, 16, 32), 30 + i) for i in range(2)])
+    ys3 = run_capi("dct_3d", xs3)
+    for i in range(2):
+        assert np.array_equal(ys3[i], run_capi("dct_3d", xs3[i])), i
+
+
+# ------------------------------------------------------ C ABI behaviour ----
+def test_stage_api_composes_to_full_transform(cuda):
+    torch = _torch()
+    from paper_2110_01172_b200 import capi
+
+    x = torch.tensor(rnd((256, 512), 13), device="cuda")
+    plan = capi.Plan((256, 512))
+    ws = torch.empty(plan.workspace_bytes, dtype=torch.uint8, device="cuda")
+    for kind in ("dct_2d", "idct_2d"):
+        full = torch.empty_like(x)
+        staged = torch.empty_like(x)
+        plan.exec(kind, x.data_ptr(), full.data_ptr(), ws.data_ptr())
+        for st in range(plan.stage_count(kind)):
+            plan.exec_stage(kind, st, x.data_ptr(), staged.data_ptr(), ws.data_ptr())
+        torch.cuda.synchronize()
+        assert torch.equal(full, staged), kind
+
+
+def test_corrupt_twiddle_is_detected(cuda):
+    # proj/src/dct2d.cpp:312-317, proj/tests/test_dct2d.cpp:260-267
+    torch = _torch()
+    from paper_2110_01172_b200 import capi
+
+    for shape in ((8, 8), (64, 64), (7, 9)):
+        x = rnd(shape, 14)
+        plan = capi.Plan(shape)
+        xt = torch.tensor(x, device="cuda")
+        out = torch.empty_like(xt)
+        plan.corrupt_twiddle(3)
+        plan.exec("dct_2d", xt.data_ptr(), out.data_ptr())
+        torch.cuda.synchronize()
+        assert oracle.max_rel(out.cpu().numpy(), oracle.port.dct_direct_2d(x)) > 1e-6, shape
+        with pytest.raises(IndexError):
+            plan.corrupt_twiddle(shape[1])
+
+
+def test_kind_rank_mismatch_is_plan_error(cuda):
+    torch = _torch()
+    from paper_2110_01172_b200 import capi
+
+    plan = capi.Plan((8, 8))
+    buf = torch.zeros(64, dtype=torch.float64, device="cuda")
+    out = torch.empty_like(buf)
+    with pytest.raises(ValueError):
+        plan.exec("dct_3d", buf.data_ptr(), out.data_ptr())
+    with pytest.raises(capi.SdctError):
+        plan.exec("dct_2d", buf.data_ptr(), buf.data_ptr())  # out of place only
+
+
+def test_counters_match_reference_tallies(cuda):
+    # proj/tests/test_dct2d.cpp:195-258
+    from paper_2110_01172_b200 import capi
+
+    p = capi.Plan((8, 8))
+    stages, reads, writes, mults, adds = p.counters("dct_2d")
+    assert (stages, mults, adds) == (3, 360, 260)
+    assert reads == 64 + 8 * 5 and writes == 2 * 64
+    assert capi.Plan((8, 8)).counters("dct_2d_rowcol")[0] == 8
+    for n1, n2 in ((7, 9), (8, 7), (7, 8)):
+        s, r, w, m, a = capi.Plan((n1, n2), orientation=capi.ORIENT_DIRECT).counters("dct_2d")
+        assert r - n1 * n2 == n1 * (n2 // 2 + 1) and w == 2 * n1 * n2
+
+
+def test_non_default_stream(cuda):
+    torch = _torch()
+    from paper_2110_01172_b200 import capi
+
+    x = torch.tensor(rnd((512, 512), 15), device="cuda")
+    plan = capi.Plan((512, 512))
+    out = torch.empty_like(x)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        plan.exec("dct_2d", x.data_ptr(), out.data_ptr(), 0, s.cuda_stream)
+    s.synchronize()
+    assert oracle.rel_l2(out.cpu().numpy(), oracle.port.dct_2d(x.cpu().numpy())) <= 1e-12
+
+
+# --------------------------------------- reference python surface (ported) --
+def test_reference_smoke_surface(cuda):
+    """proj/tests/python/test_smoke.py, against this package's numpy surface."""
+    import paper_2110_01172_b200 as sdct
+
+    rng = np.random.default_rng(20240815)
+    x = rng.uniform(-1.0, 1.0, size=(24, 17))
+    np.testing.assert_allclose(sdct.dct_2d(x), sf.dctn(x, type=2) / 4.0, rtol=0, atol=1e-9)
+    x = rng.uniform(-1.0, 1.0, size=(13, 21))
+    np.testing.assert_allclose(sdct.dct_2d_rowcol(x), sdct.dct_2d(x), rtol=0, atol=1e-10)
+    x = rng.uniform(-1.0, 1.0, size=(5, 6, 7))
+    np.testing.assert_allclose(sdct.dct_3d(x), sf.dctn(x, type=2) / 8.0, rtol=0, atol=1e-10)
+    x2 = rng.uniform(-1.0, 1.0, size=(9, 14))
+    np.testing.assert_allclose(sdct.idct_2d(sdct.dct_2d(x2)), (9 * 14 / 4) * x2, rtol=0, atol=1e-9)
+    x3 = rng.uniform(-1.0, 1.0, size=(4, 5, 6))
+    np.testing.assert_allclose(sdct.idct_3d(sdct.dct_3d(x3)), (4 * 5 * 6 / 8) * x3, rtol=0, atol=1e-9)
+    x1 = rng.uniform(-1.0, 1.0, size=30)
+    np.testing.assert_allclose(sdct.idct_1d(sdct.dct_1d(x1)), (30 / 2) * x1, rtol=0, atol=1e-9)
+    x1 = rng.uniform(-1.0, 1.0, size=64)
+    np.testing.assert_allclose(sdct.dct_1d(x1), sf.dct(x1, type=2) / 2.0, rtol=0, atol=1e-10)
+    n = 12
+    x = rng.uniform(-1.0, 1.0, size=n)
+    k = np.arange(n)[:, None]
+    m = np.arange(1, n)[None, :]
+    want = (x[1:][None, :] * np.sin(np.pi / n * m * (k + 0.5))).sum(axis=1)
+    np.testing.assert_allclose(sdct.idxst_1d(x), want, rtol=0, atol=1e-10)
+    x = rng.uniform(-1.0, 1.0, size=(8, 8))
+    idct_rows = np.stack([sdct.idct_1d(row) for row in x])
+    want = np.stack([sdct.idxst_1d(col) for col in idct_rows.T]).T
+    np.testing.assert_allclose(sdct.idxst_idct_2d(x), want, rtol=0, atol=1e-10)
+    with pytest.raises(ValueError):
+        sdct.dct_2d(np.zeros(8))
+    x = rng.uniform(-1.0, 1.0, size=(33, 17))
+    base = sdct.dct_2d(x, threads=1)
+    for t in (2, 4, 8):
+        assert np.array_equal(sdct.dct_2d(x, threads=t), base)
+
+
+def test_torch_entry_points(cuda):
+    torch = _torch()
+    import paper_2110_01172_b200 as sdct
+
+    x = rnd((3, 64, 32), 16)
+    for dt, tol in ((torch.float64, 1e-12), (torch.float32, 1e-5)):
+        xt = torch.tensor(x, dtype=dt, device="cuda")
+        y = sdct.dct_2d(xt)
+        assert y.dtype == dt and y.device == xt.device and y.shape == xt.shape
+        for i in range(3):
+            assert oracle.rel_l2(y[i].double().cpu().numpy(), oracle.port.dct_2d(x[i])) <= tol * 10
