@@ -1,0 +1,10 @@
+// Column-kernel instantiations: float, variant 0 (see ColVariant).
+#include "fast_launch.cuh"
+
+namespace sdctb {
+template <>
+cudaError_t launch_col_variant<float, 0>(int L, int nl, dim3 grid, cudaStream_t st, const CUtensorMap& map,
+                                         const ColArgs& a, const TwSet& tw) {
+  return launch_col_var<float, 0>(L, nl, grid, st, map, a, tw);
+}
+}  // namespace sdctb

@@ -1,7 +1,8 @@
-// Runtime -> compile-time dispatch for the fast-path kernels. Each dtype's
-// column and row kernels are instantiated in their own translation unit
-// (fast_col_f32.cu, fast_col_f64.cu, fast_row_f32.cu, fast_row_f64.cu) so the
-// build compiles them in parallel.
+// Runtime -> compile-time dispatch for the fast-path kernels. The column
+// kernel band width NL is a compile-time parameter with two choices per
+// (dtype, L): nl_default (tile <= 128 KB) and 2 (small / low-parallelism
+// problems). Each (dtype, variant) is instantiated in its own translation
+// unit (fast_*.cu) so the build compiles them in parallel.
 #pragma once
 
 #include "kernels_fast.cuh"
@@ -10,14 +11,15 @@ namespace sdctb {
 
 constexpr int kMaxFastLen = 4096;  // largest FFT length with a fast kernel
 
-template <typename T>
-cudaError_t launch_col(int L, bool inv, int load, int store, dim3 grid, size_t smem, cudaStream_t st,
-                       const ColArgs& a, const cx_t<T>* tw, int tw_step);
-template <typename T>
-cudaError_t launch_row(int M, int kind, dim3 grid, size_t smem, cudaStream_t st, const RowArgs& a,
-                       const cx_t<T>* tw, int tw_step);
+// column-kernel variants
+enum ColVariant { CV_FWD_SRC = 0, CV_FWD_INTER = 1, CV_INV_INTER = 2, CV_INV_DST = 3 };
 
-inline int col_threads_rt(int L) { return L >= 1024 ? 512 : 256; }
+__host__ __device__ constexpr int nl_default(int esize, int L) {
+  // complex element = 2*esize bytes; tile L*NL*2*esize <= 128 KB, 2 <= NL <= 32
+  return (128 * 1024) / (L * 2 * esize) >= 32 ? 32
+         : (128 * 1024) / (L * 2 * esize) <= 2 ? 2
+                                                : (128 * 1024) / (L * 2 * esize);
+}
 
 // Opt each kernel instantiation in to > 48 KB dynamic shared memory (once).
 cudaError_t prep_smem_ptr(const void* kernel, size_t smem);
@@ -27,108 +29,102 @@ inline cudaError_t prep_smem(K kernel, size_t smem) {
   return prep_smem_ptr(reinterpret_cast<const void*>(kernel), smem);
 }
 
-#define SDCTB_COL_CASE(T, LL)                                                                   \
-  case LL: {                                                                                    \
-    if (!inv && load == LD_SRC && store == ST_INTER) {                                         \
-      auto k = col_kernel<T, LL, false, LD_SRC, ST_INTER>;                                     \
-      if ((e = prep_smem(k, smem)) != cudaSuccess) return e;                                   \
-      k<<<grid, col_threads<LL>(), smem, st>>>(a, tw, tw_step);                                \
-    } else if (!inv && load == LD_INTER && store == ST_INTER) {                                \
-      auto k = col_kernel<T, LL, false, LD_INTER, ST_INTER>;                                   \
-      if ((e = prep_smem(k, smem)) != cudaSuccess) return e;                                   \
-      k<<<grid, col_threads<LL>(), smem, st>>>(a, tw, tw_step);                                \
-    } else if (inv && load == LD_INTER && store == ST_INTER) {                                 \
-      auto k = col_kernel<T, LL, true, LD_INTER, ST_INTER>;                                    \
-      if ((e = prep_smem(k, smem)) != cudaSuccess) return e;                                   \
-      k<<<grid, col_threads<LL>(), smem, st>>>(a, tw, tw_step);                                \
-    } else if (inv && load == LD_INTER && store == ST_DST) {                                   \
-      auto k = col_kernel<T, LL, true, LD_INTER, ST_DST>;                                      \
-      if ((e = prep_smem(k, smem)) != cudaSuccess) return e;                                   \
-      k<<<grid, col_threads<LL>(), smem, st>>>(a, tw, tw_step);                                \
-    } else {                                                                                    \
-      return cudaErrorInvalidValue;                                                             \
-    }                                                                                           \
-    break;                                                                                      \
-  }
+template <typename T>
+cudaError_t launch_col(int variant, int L, int nl, dim3 grid, cudaStream_t st, const CUtensorMap& map,
+                       const ColArgs& a, const TwSet& tw);
+template <typename T>
+cudaError_t launch_row(int M, int kind, dim3 grid, cudaStream_t st, const RowArgs& a, const TwSet& tw);
 
-#define SDCTB_DEFINE_LAUNCH_COL(T)                                                              \
-  template <>                                                                                   \
-  cudaError_t launch_col<T>(int L, bool inv, int load, int store, dim3 grid, size_t smem,       \
-                            cudaStream_t st, const ColArgs& a, const cx_t<T>* tw, int tw_step) { \
-    cudaError_t e = cudaSuccess;                                                                \
-    switch (L) {                                                                                \
-      SDCTB_COL_CASE(T, 2)                                                                      \
-      SDCTB_COL_CASE(T, 4)                                                                      \
-      SDCTB_COL_CASE(T, 8)                                                                      \
-      SDCTB_COL_CASE(T, 16)                                                                     \
-      SDCTB_COL_CASE(T, 32)                                                                     \
-      SDCTB_COL_CASE(T, 64)                                                                     \
-      SDCTB_COL_CASE(T, 128)                                                                    \
-      SDCTB_COL_CASE(T, 256)                                                                    \
-      SDCTB_COL_CASE(T, 512)                                                                    \
-      SDCTB_COL_CASE(T, 1024)                                                                   \
-      SDCTB_COL_CASE(T, 2048)                                                                   \
-      SDCTB_COL_CASE(T, 4096)                                                                   \
-      default:                                                                                  \
-        return cudaErrorInvalidValue;                                                           \
-    }                                                                                           \
-    return cudaGetLastError();                                                                  \
-  }
+// threads per CTA (host side, must match the kernels' compile-time geometry)
+inline int tile_threads(int L, int nl) {
+  int lg = 0;
+  while ((1 << lg) < L) ++lg;
+  const int S = lg == 0 ? 0 : (lg + 3) / 4;
+  const int r0 = S == 0 ? 1 : 1 << (lg / S + (0 < lg % S ? 1 : 0));
+  const int nt0 = L * nl / r0;
+  return nt0 > 512 ? 512 : nt0;
+}
 
-#define SDCTB_ROW_CASE(T, MM)                                                                   \
-  case MM: {                                                                                    \
-    switch (kind) {                                                                             \
-      case RK_FWD2: {                                                                           \
-        auto k = row_kernel<T, MM, RK_FWD2>;                                                   \
-        if ((e = prep_smem(k, smem)) != cudaSuccess) return e;                                 \
-        k<<<grid, kRowThreads, smem, st>>>(a, tw, tw_step);                                    \
-        break;                                                                                  \
-      }                                                                                         \
-      case RK_INV2: {                                                                           \
-        auto k = row_kernel<T, MM, RK_INV2>;                                                   \
-        if ((e = prep_smem(k, smem)) != cudaSuccess) return e;                                 \
-        k<<<grid, kRowThreads, smem, st>>>(a, tw, tw_step);                                    \
-        break;                                                                                  \
-      }                                                                                         \
-      case RK_FWD3: {                                                                           \
-        auto k = row_kernel<T, MM, RK_FWD3>;                                                   \
-        if ((e = prep_smem(k, smem)) != cudaSuccess) return e;                                 \
-        k<<<grid, kRowThreads, smem, st>>>(a, tw, tw_step);                                    \
-        break;                                                                                  \
-      }                                                                                         \
-      case RK_INV3: {                                                                           \
-        auto k = row_kernel<T, MM, RK_INV3>;                                                   \
-        if ((e = prep_smem(k, smem)) != cudaSuccess) return e;                                 \
-        k<<<grid, kRowThreads, smem, st>>>(a, tw, tw_step);                                    \
-        break;                                                                                  \
-      }                                                                                         \
-      default:                                                                                  \
-        return cudaErrorInvalidValue;                                                           \
-    }                                                                                           \
-    break;                                                                                      \
-  }
+// ---- per-variant implementation (included by the fast_col_*.cu units) -------
+template <typename T, int L, int NL, int VAR>
+cudaError_t launch_col_one(dim3 grid, cudaStream_t st, const CUtensorMap& map, const ColArgs& a,
+                           const TwSet& tw) {
+  constexpr bool INV = VAR == CV_INV_INTER || VAR == CV_INV_DST;
+  constexpr int LD = VAR == CV_FWD_SRC ? LD_SRC : LD_INTER;
+  constexpr int STO = VAR == CV_INV_DST ? ST_DST : ST_INTER;
+  auto k = col_kernel<T, L, NL, INV, LD, STO>;
+  const size_t smem = static_cast<size_t>(L) * NL * sizeof(cx_t<T>) + 16;  // + mbarrier
+  cudaError_t e = prep_smem(k, smem);
+  if (e != cudaSuccess) return e;
+  k<<<grid, Tile<T, L, NL, true>::NT, smem, st>>>(map, a, tw);
+  return cudaGetLastError();
+}
 
-#define SDCTB_DEFINE_LAUNCH_ROW(T)                                                              \
-  template <>                                                                                   \
-  cudaError_t launch_row<T>(int M, int kind, dim3 grid, size_t smem, cudaStream_t st,           \
-                            const RowArgs& a, const cx_t<T>* tw, int tw_step) {                 \
-    cudaError_t e = cudaSuccess;                                                                \
-    switch (M) {                                                                                \
-      SDCTB_ROW_CASE(T, 4)                                                                      \
-      SDCTB_ROW_CASE(T, 8)                                                                      \
-      SDCTB_ROW_CASE(T, 16)                                                                     \
-      SDCTB_ROW_CASE(T, 32)                                                                     \
-      SDCTB_ROW_CASE(T, 64)                                                                     \
-      SDCTB_ROW_CASE(T, 128)                                                                    \
-      SDCTB_ROW_CASE(T, 256)                                                                    \
-      SDCTB_ROW_CASE(T, 512)                                                                    \
-      SDCTB_ROW_CASE(T, 1024)                                                                   \
-      SDCTB_ROW_CASE(T, 2048)                                                                   \
-      SDCTB_ROW_CASE(T, 4096)                                                                   \
-      default:                                                                                  \
-        return cudaErrorInvalidValue;                                                           \
-    }                                                                                           \
-    return cudaGetLastError();                                                                  \
+template <typename T, int L, int VAR>
+cudaError_t launch_col_L(int nl, dim3 grid, cudaStream_t st, const CUtensorMap& map, const ColArgs& a,
+                         const TwSet& tw) {
+  constexpr int NLD = nl_default(sizeof(T), L);
+  if (nl == NLD) return launch_col_one<T, L, NLD, VAR>(grid, st, map, a, tw);
+  if constexpr (NLD != 2) {
+    if (nl == 2) return launch_col_one<T, L, 2, VAR>(grid, st, map, a, tw);
   }
+  return cudaErrorInvalidValue;
+}
+
+template <typename T, int VAR>
+cudaError_t launch_col_var(int L, int nl, dim3 grid, cudaStream_t st, const CUtensorMap& map, const ColArgs& a,
+                           const TwSet& tw) {
+  switch (L) {
+    case 2: return launch_col_L<T, 2, VAR>(nl, grid, st, map, a, tw);
+    case 4: return launch_col_L<T, 4, VAR>(nl, grid, st, map, a, tw);
+    case 8: return launch_col_L<T, 8, VAR>(nl, grid, st, map, a, tw);
+    case 16: return launch_col_L<T, 16, VAR>(nl, grid, st, map, a, tw);
+    case 32: return launch_col_L<T, 32, VAR>(nl, grid, st, map, a, tw);
+    case 64: return launch_col_L<T, 64, VAR>(nl, grid, st, map, a, tw);
+    case 128: return launch_col_L<T, 128, VAR>(nl, grid, st, map, a, tw);
+    case 256: return launch_col_L<T, 256, VAR>(nl, grid, st, map, a, tw);
+    case 512: return launch_col_L<T, 512, VAR>(nl, grid, st, map, a, tw);
+    case 1024: return launch_col_L<T, 1024, VAR>(nl, grid, st, map, a, tw);
+    case 2048: return launch_col_L<T, 2048, VAR>(nl, grid, st, map, a, tw);
+    case 4096: return launch_col_L<T, 4096, VAR>(nl, grid, st, map, a, tw);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+template <typename T, int VAR>
+cudaError_t launch_col_variant(int L, int nl, dim3 grid, cudaStream_t st, const CUtensorMap& map,
+                               const ColArgs& a, const TwSet& tw);
+
+template <typename T, int M, int KIND>
+cudaError_t launch_row_one(dim3 grid, cudaStream_t st, const RowArgs& a, const TwSet& tw) {
+  constexpr int G = (KIND == RK_FWD2 || KIND == RK_INV2) ? 2 : 4;
+  auto k = row_kernel<T, M, KIND>;
+  const size_t smem = static_cast<size_t>(G) * M * sizeof(cx_t<T>) + 16;  // + mbarrier
+  cudaError_t e = prep_smem(k, smem);
+  if (e != cudaSuccess) return e;
+  k<<<grid, row_threads<T, M, KIND>(), smem, st>>>(a, tw);
+  return cudaGetLastError();
+}
+
+template <typename T, int KIND>
+cudaError_t launch_row_kind(int M, dim3 grid, cudaStream_t st, const RowArgs& a, const TwSet& tw) {
+  switch (M) {
+    case 4: return launch_row_one<T, 4, KIND>(grid, st, a, tw);
+    case 8: return launch_row_one<T, 8, KIND>(grid, st, a, tw);
+    case 16: return launch_row_one<T, 16, KIND>(grid, st, a, tw);
+    case 32: return launch_row_one<T, 32, KIND>(grid, st, a, tw);
+    case 64: return launch_row_one<T, 64, KIND>(grid, st, a, tw);
+    case 128: return launch_row_one<T, 128, KIND>(grid, st, a, tw);
+    case 256: return launch_row_one<T, 256, KIND>(grid, st, a, tw);
+    case 512: return launch_row_one<T, 512, KIND>(grid, st, a, tw);
+    case 1024: return launch_row_one<T, 1024, KIND>(grid, st, a, tw);
+    case 2048: return launch_row_one<T, 2048, KIND>(grid, st, a, tw);
+    case 4096: return launch_row_one<T, 4096, KIND>(grid, st, a, tw);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+template <typename T, int KIND>
+cudaError_t launch_row_kind_ext(int M, dim3 grid, cudaStream_t st, const RowArgs& a, const TwSet& tw);
 
 }  // namespace sdctb

@@ -51,6 +51,50 @@ __host__ __device__ __forceinline__ int digit_pos(int k) {
   return pos;
 }
 
+// Inverse of digit_pos: frequency index held at slot n.
+template <int L>
+__host__ __device__ __forceinline__ int digit_rev(int n) {
+  using P = RadixPlan<L>;
+  int k = 0, shift = 0;
+#pragma unroll
+  for (int s = 0; s < P::S; ++s) {
+    k |= ((n / P::span(s + 1)) & (P::R(s) - 1)) << shift;
+    shift += P::bits(s);
+  }
+  return k;
+}
+
+// Runtime versions for extents only known at run time (row selection of the
+// intermediate, 3D plane mapping). Same radix plan as RadixPlan<L>.
+__host__ __device__ inline int rt_digit_pos(int k, int L) {
+  int lg = 0;
+  while ((1 << lg) < L) ++lg;
+  if (lg == 0) return 0;
+  const int S = (lg + 3) / 4;
+  int span = L, pos = 0;
+  for (int s = 0; s < S; ++s) {
+    const int b = lg / S + (s < lg % S ? 1 : 0);
+    span >>= b;
+    pos += (k & ((1 << b) - 1)) * span;
+    k >>= b;
+  }
+  return pos;
+}
+__host__ __device__ inline int rt_digit_rev(int n, int L) {
+  int lg = 0;
+  while ((1 << lg) < L) ++lg;
+  if (lg == 0) return 0;
+  const int S = (lg + 3) / 4;
+  int span = L, k = 0, shift = 0;
+  for (int s = 0; s < S; ++s) {
+    const int b = lg / S + (s < lg % S ? 1 : 0);
+    span >>= b;
+    k |= ((n / span) & ((1 << b) - 1)) << shift;
+    shift += b;
+  }
+  return k;
+}
+
 // ---- bank-conflict-free swizzles (index in complex elements) ---------------
 // GF(2)-linear maps a -> a ^ g(a >> SH), g(h) = XOR of C[d % 4] over the set
 // bits d of h. 16-B elements (SH = 3) are served 8 lanes per wavefront, 8-B

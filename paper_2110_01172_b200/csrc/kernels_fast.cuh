@@ -3,11 +3,22 @@
 // parity reorder, MD real FFT, twiddle/Hermitian postprocess), with the
 // reorder fused into the FFT's load and the postprocess into its store.
 //
-//   col_kernel : FFT along a strided axis for a band of W complex columns
-//                (all L rows of the band live in one CTA's shared memory).
+//   col_kernel : FFT along a strided axis for a band of NL complex columns
+//                (all L rows of the band live in one CTA).
 //   row_kernel : FFT along the contiguous axis for a group of G rows that the
 //                Hermitian/postprocess math couples (G = 2 in 2D: rows k1 and
 //                N1-k1; G = 4 in 3D: rows (+-k1, +-k2)).
+//
+// Register-resident engine (v2): every tile geometry is compile time. Each
+// thread owns E = L*NL/NT elements; in stage s it runs E/R_s radix-R_s DIF
+// butterflies whose shared-memory slots are a per-thread swizzled base XOR
+// compile-time offsets (the swizzle is GF(2)-linear and the offset bits are
+// disjoint from the base bits). Stage-0 operands are loaded from global memory
+// straight into registers (column kernels, forward row kernels) and the last
+// stage leaves its results in registers (column kernels store them straight
+// to global memory), so an S-stage FFT makes S-1 shared-memory round trips.
+// Twiddles come from per-stage tables W_span^{jk} laid out [k-1][j] (one
+// coalesced, L1-resident load per factor) instead of a recurrence.
 //
 // Real-to-complex packing (shared by every pipeline): the reordered real line
 // x' of even length N is read as the complex line z(m) = x'(2m) + i x'(2m+1),
@@ -15,7 +26,9 @@
 // z(M-1-u)) comes exactly from the contiguous source quad x(4u..4u+3):
 //   z(u) = (x0, x2),  z(M-1-u) = (x3, x1).
 // Intermediates store z-columns "pair-interleaved": column s = 2u holds z(u),
-// s = 2u+1 holds z(M-1-u); row kernels undo that with a shared-memory scatter.
+// s = 2u+1 holds z(M-1-u). Forward intermediates keep the column-FFT output
+// rows in slot (digit-reversed) order; row kernels select rows through
+// rt_digit_pos, so no reorder pass exists anywhere.
 //
 // Reference stages replaced (Direct orientation):
 //   dct_2d           proj/src/dct2d.cpp:367-387 (+ parity_gather 48-70,
@@ -26,6 +39,7 @@
 #pragma once
 
 #include "fft_block.cuh"
+#include "tma.cuh"
 
 namespace sdctb {
 
@@ -33,16 +47,22 @@ enum ColLoad { LD_SRC = 0, LD_INTER = 1 };
 enum ColStore { ST_INTER = 0, ST_DST = 1 };
 enum RowKind { RK_FWD2 = 0, RK_INV2 = 1, RK_FWD3 = 2, RK_INV3 = 3 };
 
+// Per-stage twiddle tables of one FFT length: st[s][(k-1)*Q + j] = W_span^{j k}.
+struct TwSet {
+  const void* st[4];
+};
+
 struct ColArgs {
   const void* src;
   void* dst;
   long long in_row, in_plane, in_batch;     // element strides (T for real src, cx for complex)
   long long out_row, out_plane, out_batch;  // element strides (T for real dst, cx for complex)
   int in_plane_par;                         // >0: source plane = parity_embed(plane, n)
-  int out_plane_par;                        // >0: dest plane   = parity_embed(plane, n)
-  int lgw;                                  // log2(W), W complex columns per CTA
+  int out_plane_map;                        // ST_DST: 0 plane, 1 pe(plane), 2 pe(digit_rev(plane))
+  int out_plane_n;                          // extent used by out_plane_map
   int sign_row, sign_col;                   // final gather: negate odd k along axis
   double scale;                             // final gather scale
+  int tma_plane_par;                        // TMA plane coordinate = parity_embed(plane, n) when > 0
 };
 
 struct RowArgs {
@@ -57,12 +77,7 @@ struct RowArgs {
   const void* tu;                  // W_{Nlast}^k, k <= Nlast/2 (packing twiddles)
 };
 
-template <int L>
-constexpr int col_threads() { return L >= 1024 ? 512 : 256; }
-constexpr int kRowThreads = 256;
-
 // ---- small helpers ----------------------------------------------------------
-// z-column index of intermediate column s (pair-interleaved storage)
 __device__ __forceinline__ int s_to_m(int s, int M) { return (s & 1) ? M - 1 - (s >> 1) : (s >> 1); }
 
 // Hermitian unpack of the packed 2-real FFT: Z(k) = E + iO with
@@ -82,147 +97,328 @@ __device__ __forceinline__ V pack(V X, V Xhi, V w) {
   return mk(s.x - t.y, s.y + t.x);     // s + i t
 }
 
-template <typename T> struct Vec16;
-template <> struct Vec16<float> { using type = float4; };
-template <> struct Vec16<double> { using type = double2; };
+template <typename T> struct Vec2;
+template <> struct Vec2<float> { using type = float2; };
+template <> struct Vec2<double> { using type = double2; };
+
+// ============================================================================
+// Register-resident tile engine
+// ============================================================================
+template <typename T>
+constexpr int tile_max_threads() { return 512; }
+
+template <typename T, int L_, int NL_, bool LF>
+struct Tile {
+  static constexpr int L = L_;
+  static constexpr int NL = NL_;
+  using P = RadixPlan<L>;
+  using V = cx_t<T>;
+  using Real = T;
+  static constexpr int S = P::S;
+  static constexpr int R0 = P::R(0);
+  static constexpr int LGNL = ilog2c(NL);
+  static constexpr int TOT = L * NL;
+  static constexpr int NT0 = TOT / R0;
+  static constexpr int NT = NT0 > tile_max_threads<T>() ? tile_max_threads<T>() : NT0;
+  static constexpr int E = TOT / NT;
+  static constexpr unsigned MASK = NT >= 32 ? 0xffffffffu : ((1u << NT) - 1u);
+
+  // unswizzled address of element (line, n)
+  __host__ __device__ static constexpr int raw(int line, int n) { return LF ? (n << LGNL) + line : line * L + n; }
+  __device__ __forceinline__ static int swz(int a) { return LF ? SwzCol<T>::f(a) : SwzRow<T>::f(a); }
+  static constexpr int swzc(int a) { return LF ? SwzCol<T>::fc(a) : SwzRow<T>::fc(a); }
+  // compile-time swizzled offset of element stride q at slot multiple r
+  template <int s>
+  static constexpr int off(int r) {
+    return swzc(LF ? ((r * (P::span(s) / P::R(s))) << LGNL) : r * (P::span(s) / P::R(s)));
+  }
+
+  // butterfly bf of stage s -> (line, j, b)
+  template <int s>
+  __device__ __forceinline__ static void decode(int bf, int& line, int& j, int& b) {
+    constexpr int Q = P::span(s) / P::R(s);
+    constexpr int NB = L / P::span(s);
+    if (LF) {
+      line = bf & (NL - 1);
+      const int rest = bf >> LGNL;
+      j = rest & (Q - 1);
+      b = rest >> ilog2c(Q);
+    } else {
+      j = bf & (Q - 1);
+      const int rest = bf >> ilog2c(Q);
+      b = rest & (NB - 1);
+      line = rest >> ilog2c(NB);
+    }
+  }
+  template <int s>
+  __device__ __forceinline__ static int base(int bf) {
+    int line, j, b;
+    decode<s>(bf, line, j, b);
+    return swz(raw(line, b * P::span(s) + j));
+  }
+};
+
+// Twiddles of one stage for the thread's butterflies. A few powers W^{jk}
+// (k in LOADK) are loaded ahead of the data they multiply (they depend only
+// on the thread's fixed j), the rest are products of two loaded powers, so
+// every factor stays within ~2 ulp and no recurrence chain exists.
+template <int R>
+struct TwPlan;
+template <>
+struct TwPlan<2> {
+  static constexpr int NLD = 1;
+  static constexpr int k(int i) { return 1; }
+};
+template <>
+struct TwPlan<4> {
+  static constexpr int NLD = 3;
+  static constexpr int k(int i) { return i + 1; }
+};
+template <>
+struct TwPlan<8> {
+  static constexpr int NLD = 4;
+  static constexpr int k(int i) { return i + 1; }  // 1,2,3,4
+};
+template <>
+struct TwPlan<16> {
+  static constexpr int NLD = 6;
+  static constexpr int k(int i) { return i < 4 ? i + 1 : (i == 4 ? 8 : 12); }  // 1,2,3,4,8,12
+};
+
+template <class TL, int s>
+struct StageTw {
+  using P = typename TL::P;
+  using V = typename TL::V;
+  static constexpr int R = P::R(s), SPAN = P::span(s), Q = SPAN / R;
+  static constexpr int NBF = TL::E / R;
+  static constexpr bool ACTIVE = SPAN > R;
+  static constexpr int NLD = ACTIVE ? TwPlan<R>::NLD : 1;
+  V w[NBF][NLD];
+
+  __device__ __forceinline__ void load(const void* twt, int t) {
+    if constexpr (ACTIVE) {
+      const V* tw = static_cast<const V*>(twt);
+#pragma unroll
+      for (int i = 0; i < NBF; ++i) {
+        int line, j, b;
+        TL::template decode<s>(t + i * TL::NT, line, j, b);
+#pragma unroll
+        for (int l = 0; l < NLD; ++l) w[i][l] = __ldg(tw + (TwPlan<R>::k(l) - 1) * Q + j);
+      }
+    }
+  }
+  // W^{jk} for butterfly i
+  __device__ __forceinline__ V get(int i, int k) const {
+    if constexpr (R == 16) {
+      if (k <= 4) return w[i][k - 1];
+      if (k == 8) return w[i][4];
+      if (k == 12) return w[i][5];
+      const int hi = k & 12, lo = k & 3;  // k = hi + lo, lo in 1..3
+      const V wh = hi == 4 ? w[i][3] : hi == 8 ? w[i][4] : w[i][5];
+      return cmul(wh, w[i][lo - 1]);
+    } else if constexpr (R == 8) {
+      if (k <= 4) return w[i][k - 1];
+      return cmul(w[i][3], w[i][k - 5]);
+    } else {
+      return w[i][k - 1];
+    }
+  }
+};
+
+template <class TL, int s, bool INV>
+__device__ __forceinline__ void stage_compute(typename TL::V* v, const StageTw<TL, s>& tw) {
+  using P = typename TL::P;
+  constexpr int R = P::R(s), SPAN = P::span(s);
+  constexpr int NBF = TL::E / R;
+#pragma unroll
+  for (int i = 0; i < NBF; ++i) {
+    dft_reg<typename TL::Real, R, INV>(v + i * R);
+    if constexpr (SPAN > R) {
+#pragma unroll
+      for (int k = 1; k < R; ++k) {
+        const auto w = tw.get(i, k);
+        v[i * R + k] = INV ? cmulc(v[i * R + k], w) : cmul(v[i * R + k], w);
+      }
+    }
+  }
+}
+
+template <class TL, int s>
+__device__ __forceinline__ void to_smem(const typename TL::V* v, typename TL::V* sm, int t) {
+  using P = typename TL::P;
+  constexpr int R = P::R(s), NBF = TL::E / R;
+#pragma unroll
+  for (int i = 0; i < NBF; ++i) {
+    const int sb = TL::template base<s>(t + i * TL::NT);
+#pragma unroll
+    for (int r = 0; r < R; ++r) sm[sb ^ TL::template off<s>(r)] = v[i * R + r];
+  }
+}
+
+template <class TL, int s>
+__device__ __forceinline__ void from_smem(typename TL::V* v, const typename TL::V* sm, int t) {
+  using P = typename TL::P;
+  constexpr int R = P::R(s), NBF = TL::E / R;
+#pragma unroll
+  for (int i = 0; i < NBF; ++i) {
+    const int sb = TL::template base<s>(t + i * TL::NT);
+#pragma unroll
+    for (int r = 0; r < R; ++r) v[i * R + r] = sm[sb ^ TL::template off<s>(r)];
+  }
+}
+
+template <class TL, bool INV, int s>
+__device__ __forceinline__ void later_stages(typename TL::V* v, typename TL::V* sm, const TwSet& tw, int t) {
+  if constexpr (s < TL::S) {
+    StageTw<TL, s> w;
+    w.load(tw.st[s], t);  // issued before the smem reads it overlaps
+    from_smem<TL, s>(v, sm, t);
+    stage_compute<TL, s, INV>(v, w);
+    if constexpr (s + 1 < TL::S) {
+      to_smem<TL, s>(v, sm, t);
+      __syncthreads();
+    }
+    later_stages<TL, INV, s + 1>(v, sm, tw, t);
+  }
+}
+
+// Full FFT of a tile whose stage-0 operands are already in v and whose
+// stage-0 twiddles were prefetched into w0. On return v holds the last
+// stage's outputs (slot n = b*R_last + r of the thread's last-stage butterflies).
+template <class TL, bool INV>
+__device__ __forceinline__ void fft_regs(typename TL::V* v, typename TL::V* sm, const TwSet& tw,
+                                         const StageTw<TL, 0>& w0, int t) {
+  stage_compute<TL, 0, INV>(v, w0);
+  if constexpr (TL::S > 1) {
+    to_smem<TL, 0>(v, sm, t);
+    __syncthreads();
+    later_stages<TL, INV, 1>(v, sm, tw, t);
+  }
+}
+
+// Last-stage butterfly i of thread t -> (line, slot base b*R_last)
+template <class TL>
+__device__ __forceinline__ void last_decode(int bf, int& line, int& b) {
+  int j;
+  TL::template decode<TL::S - 1>(bf, line, j, b);
+}
 
 // ============================================================================
 // Column kernel
 // ============================================================================
-template <typename T, int L, bool INV, int LOAD, int STORE>
-__global__ void __launch_bounds__(col_threads<L>())
-    col_kernel(ColArgs a, const cx_t<T>* __restrict__ tw, int tw_step) {
+template <typename T, int L, int NL, bool INV, int LOAD, int STORE>
+__global__ void __launch_bounds__(Tile<T, L, NL, true>::NT)
+    col_kernel(const __grid_constant__ CUtensorMap tmap, ColArgs a, TwSet tw) {
+  using TL = Tile<T, L, NL, true>;
+  using P = typename TL::P;
   using V = cx_t<T>;
-  using V4 = typename Vec16<T>::type;
-  constexpr int NT = col_threads<L>();
-  constexpr int VEC = 16 / sizeof(T);   // reals per 16-B vector
-  constexpr int CPV = 16 / sizeof(V);   // complex per 16-B vector
-  constexpr int U = 4;                  // loads in flight per thread per batch
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  V* buf = reinterpret_cast<V*>(smem_raw);
-  const int lgw = a.lgw;
-  const int W = 1 << lgw;
-  const ColLayout<T> lay{lgw};
-  const int tid = threadIdx.x;
+  using V2 = typename Vec2<T>::type;
+  constexpr int R0 = TL::R0, Q0 = L / R0, NBF0 = TL::E / R0;
+  constexpr int SL = TL::S - 1, RL = P::R(SL), NBFL = TL::E / RL;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  V* sm = reinterpret_cast<V*>(smem_raw);
+  const int t = threadIdx.x;
   const int band = blockIdx.x, plane = blockIdx.y, batch = blockIdx.z;
+  V v[TL::E];
 
-  // ---------------------------------------------------------------- load ---
+  // ------------------------------------------------- stage-0 operands ------
+  // The band tile (L rows x 2*NL reals) lands in shared memory through TMA
+  // (4D map: inner reals, FFT rows, planes, batch), then each thread reads its
+  // stage-0 operands; the same shared memory then serves as the exchange
+  // buffer.
+  StageTw<TL, 0> w0;
+  w0.load(tw.st[0], t);  // latency hidden under the tile load
+  {
+    constexpr int BOXR = L < 256 ? L : 256;
+    constexpr uint32_t TILE_BYTES = static_cast<uint32_t>(L) * 2 * NL * sizeof(T);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw + TILE_BYTES);  // after the tile
+    if (t == 0) {
+      prefetch_tmap(&tmap);
+      mbar_init(bar, 1);
+    }
+    __syncthreads();
+    if (t == 0) {
+      const int pc = a.tma_plane_par ? parity_embed(plane, a.tma_plane_par) : plane;
+      mbar_expect_tx(bar, TILE_BYTES);
+#pragma unroll 1
+      for (int r0 = 0; r0 < L; r0 += BOXR)
+        tma_load_4d(reinterpret_cast<T*>(smem_raw) + static_cast<size_t>(r0) * 2 * NL, &tmap, band * 2 * NL, r0,
+                    pc, batch, bar);
+    }
+    mbar_wait(bar, 0);
+  }
   if constexpr (LOAD == LD_SRC) {
-    // real source, parity reorder along the FFT axis (rows) and the packed
-    // contiguous axis; a band is 2W contiguous reals per row.
-    const int pl = a.in_plane_par ? parity_embed(plane, a.in_plane_par) : plane;
-    const T* src = static_cast<const T*>(a.src) + batch * a.in_batch + pl * a.in_plane +
-                   static_cast<long long>(band) * (2 * W);
-    const int lg_vpr = lgw + 1 - ilog2c(VEC);  // vectors per row = 2W / VEC
-    const int nvec = L << lg_vpr;
-    for (int v0 = 0; v0 < nvec; v0 += NT * U) {
-      V4 t[U];
+    // real source; slot n of the FFT reads source row pe(n) (parity reorder
+    // along the FFT axis); line 2g+h of the band is z(u) (h=0) or z(M-1-u)
+    // (h=1) of source quad g: lanes h=0/1 read the two halves and swap one real.
+    const V2* raw = reinterpret_cast<const V2*>(smem_raw);
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int v = v0 + u * NT + tid;
-        if (v < nvec) {
-          const int r = v >> lg_vpr, vi = v & ((1 << lg_vpr) - 1);
-          t[u] = __ldg(reinterpret_cast<const V4*>(src + r * a.in_row + vi * VEC));
-        }
-      }
+    for (int i = 0; i < NBF0; ++i) {
+      const int bf = t + i * TL::NT;
+      const int line = bf & (NL - 1), j = bf >> TL::LGNL;
+      const int h = line & 1;
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int v = v0 + u * NT + tid;
-        if constexpr (sizeof(T) == 4) {
-          if (v < nvec) {
-            const int r = v >> lg_vpr, g = v & ((1 << lg_vpr) - 1);
-            const int slot = parity_source(r, L);
-            const float4 x = reinterpret_cast<const float4&>(t[u]);
-            buf[lay.at(2 * g, slot)] = mk(x.x, x.z);
-            buf[lay.at(2 * g + 1, slot)] = mk(x.w, x.y);
-          }
-        } else {
-          // fp64: a source quad spans two lanes; swap the middle reals.
-          if (v0 + u * NT < nvec) {  // warp-uniform (nvec is a multiple of 2)
-            const int r = v >> lg_vpr, vi = v & ((1 << lg_vpr) - 1);
-            const int g = vi >> 1, h = vi & 1;
-            const double2 x = reinterpret_cast<const double2&>(t[u]);
-            const double send = h ? x.x : x.y;
-            const double recv = __shfl_xor_sync(0xffffffffu, send, 1);
-            if (v < nvec) {
-              const int slot = parity_source(r, L);
-              buf[lay.at(2 * g + h, slot)] = h ? mk(x.y, recv) : mk(x.x, recv);
-            }
-          }
-        }
+      for (int r = 0; r < R0; ++r) {
+        const int n = j + r * Q0;
+        const int row = (r < R0 / 2) ? 2 * n : 2 * L - 1 - 2 * n;
+        const V2 x = raw[row * NL + line];
+        const T send = h ? x.x : x.y;
+        const T recv = __shfl_xor_sync(TL::MASK, send, 1);
+        v[i * R0 + r] = h ? mk(x.y, recv) : mk(x.x, recv);
       }
     }
   } else {
-    const V* src = static_cast<const V*>(a.src) + batch * a.in_batch + plane * a.in_plane +
-                   static_cast<long long>(band) * W;
-    const int lg_vpr = lgw - ilog2c(CPV);
-    const int nvec = L << lg_vpr;
-    for (int v0 = 0; v0 < nvec; v0 += NT * U) {
-      V4 t[U];
+    const V* raw = reinterpret_cast<const V*>(smem_raw);
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int v = v0 + u * NT + tid;
-        if (v < nvec) {
-          const int r = v >> lg_vpr, ci = v & ((1 << lg_vpr) - 1);
-          t[u] = __ldg(reinterpret_cast<const V4*>(src + r * a.in_row + ci * CPV));
-        }
-      }
+    for (int i = 0; i < NBF0; ++i) {
+      const int bf = t + i * TL::NT;
+      const int line = bf & (NL - 1), j = bf >> TL::LGNL;
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int v = v0 + u * NT + tid;
-        if (v < nvec) {
-          const int r = v >> lg_vpr, ci = v & ((1 << lg_vpr) - 1);
-          const V* e = reinterpret_cast<const V*>(&t[u]);
-#pragma unroll
-          for (int k = 0; k < CPV; ++k) buf[lay.at(ci * CPV + k, r)] = e[k];
-        }
-      }
+      for (int r = 0; r < R0; ++r) v[i * R0 + r] = raw[(j + r * Q0) * NL + line];
     }
   }
-  __syncthreads();
+  __syncthreads();  // raw tile consumed; smem becomes the exchange buffer
 
-  // ----------------------------------------------------------------- FFT ---
-  block_fft<T, L, INV, true>(buf, lay, lgw, tw, tw_step);
+  fft_regs<TL, INV>(v, sm, tw, w0, t);
+  if constexpr (TL::S == 1) __syncthreads();  // in-place passes: all loads before any store
 
-  // --------------------------------------------------------------- store ---
+  // --------------------------------------------------------- store ---------
   if constexpr (STORE == ST_INTER) {
+    // rows in slot order (the consumer selects rows through digit_pos)
     V* dst = static_cast<V*>(a.dst) + batch * a.out_batch + plane * a.out_plane +
-             static_cast<long long>(band) * W;
-    const int lg_vpr = lgw - ilog2c(CPV);
-    const int nvec = L << lg_vpr;
-    for (int v = tid; v < nvec; v += NT) {
-      const int r = v >> lg_vpr, ci = v & ((1 << lg_vpr) - 1);
-      const int slot = digit_pos<L>(r);
-      V4 o;
-      V* e = reinterpret_cast<V*>(&o);
+             static_cast<long long>(band) * NL;
 #pragma unroll
-      for (int k = 0; k < CPV; ++k) e[k] = buf[lay.at(ci * CPV + k, slot)];
-      *reinterpret_cast<V4*>(dst + r * a.out_row + ci * CPV) = o;
+    for (int i = 0; i < NBFL; ++i) {
+      int line, b;
+      last_decode<TL>(t + i * TL::NT, line, b);
+#pragma unroll
+      for (int r = 0; r < RL; ++r) dst[(b * RL + r) * a.out_row + line] = v[i * RL + r];
     }
   } else {
-    // final inverse gather: y(k1, 4u+c) from z(ps(k1)), scale and signs
-    const int pl = a.out_plane_par ? parity_embed(plane, a.out_plane_par) : plane;
+    // final inverse gather: y(k1, 4u + c) = scale * z(ps(k1)) components
+    int pl = plane;
+    if (a.out_plane_map == 1) pl = parity_embed(plane, a.out_plane_n);
+    else if (a.out_plane_map == 2) pl = parity_embed(rt_digit_rev(plane, a.out_plane_n), a.out_plane_n);
     T* dst = static_cast<T*>(a.dst) + batch * a.out_batch + pl * a.out_plane +
-             static_cast<long long>(band) * (2 * W);
+             static_cast<long long>(band) * (2 * NL);
     const T sc = static_cast<T>(a.scale);
-    const int lg_vpr = lgw + 1 - ilog2c(VEC);
-    const int nvec = L << lg_vpr;
-    for (int v = tid; v < nvec; v += NT) {
-      const int k1 = v >> lg_vpr, vi = v & ((1 << lg_vpr) - 1);
-      const int slot = digit_pos<L>(parity_source(k1, L));
-      const T srow = (a.sign_row && (k1 & 1)) ? -sc : sc;
-      const T scol = a.sign_col ? -srow : srow;
-      if constexpr (sizeof(T) == 4) {
-        const int g = vi;
-        const V zg = buf[lay.at(2 * g, slot)], zm = buf[lay.at(2 * g + 1, slot)];
-        *reinterpret_cast<float4*>(dst + k1 * a.out_row + 4 * g) =
-            make_float4(zg.x * srow, zm.y * scol, zg.y * srow, zm.x * scol);
-      } else {
-        const int g = vi >> 1, h = vi & 1;
-        const V zg = buf[lay.at(2 * g, slot)], zm = buf[lay.at(2 * g + 1, slot)];
-        const double2 o = h ? make_double2(zg.y * srow, zm.x * scol)
-                            : make_double2(zg.x * srow, zm.y * scol);
-        *reinterpret_cast<double2*>(dst + k1 * a.out_row + 4 * g + 2 * h) = o;
+#pragma unroll
+    for (int i = 0; i < NBFL; ++i) {
+      int line, b;
+      last_decode<TL>(t + i * TL::NT, line, b);
+      const int h = line & 1;
+      const int kb = digit_rev<L>(b * RL);  // spatial index of slot b*RL
+#pragma unroll
+      for (int r = 0; r < RL; ++r) {
+        const int ii = kb + r * (L / RL);
+        const int k1 = (r < RL / 2) ? 2 * ii : 2 * L - 1 - 2 * ii;  // pe(ii)
+        const V z = v[i * RL + r];
+        const T recv = __shfl_xor_sync(TL::MASK, z.y, 1);
+        const T s0 = (a.sign_row && (k1 & 1)) ? -sc : sc;
+        const T s1 = a.sign_col ? -s0 : s0;
+        // lane h=0: (Re z(u), Im z(M-1-u)) = y(4u, 4u+1); h=1: (Im z(u), Re z(M-1-u)) = y(4u+2, 4u+3)
+        const V2 o = h ? V2{recv * s0, z.x * s1} : V2{z.x * s0, recv * s1};
+        *reinterpret_cast<V2*>(dst + k1 * a.out_row + 2 * line) = o;
       }
     }
   }
@@ -289,31 +485,65 @@ __device__ __forceinline__ cx_t<T> pre3_entry(const T* x, int i, int j, int k, c
   return cmul(w, mk(re, im));
 }
 
+template <typename T, int M, int G>
+using RowTile = Tile<T, M, G, false>;
+
 template <typename T, int M, int KIND>
-__global__ void __launch_bounds__(kRowThreads)
-    row_kernel(RowArgs a, const cx_t<T>* __restrict__ tw, int tw_step) {
+constexpr int row_threads() {
+  return RowTile<T, M, (KIND == RK_FWD2 || KIND == RK_INV2) ? 2 : 4>::NT;
+}
+
+// Natural-order smem index of (line, m) in a row tile.
+template <typename T, int M>
+__device__ __forceinline__ int row_nat(int line, int m) {
+  return SwzRow<T>::f(line * M + m);
+}
+
+// Writes the last stage's results (in registers) at natural (frequency/
+// spatial) order: slot n = b*R + r holds index digit_rev(n) = kb + r*(M/R).
+template <class TL>
+__device__ __forceinline__ void last_to_natural(const typename TL::V* v, typename TL::V* sm, int t) {
+  using P = typename TL::P;
+  constexpr int RL = P::R(TL::S - 1), NBFL = TL::E / RL, M = TL::L;
+#pragma unroll
+  for (int i = 0; i < NBFL; ++i) {
+    int line, b;
+    last_decode<TL>(t + i * TL::NT, line, b);
+    const int sb = TL::swz(line * M + digit_rev<M>(b * RL));
+#pragma unroll
+    for (int r = 0; r < RL; ++r) sm[sb ^ TL::swzc(r * (M / RL))] = v[i * RL + r];
+  }
+}
+
+template <typename T, int M, int KIND>
+__global__ void __launch_bounds__(row_threads<T, M, KIND>())
+    row_kernel(RowArgs a, TwSet tw) {
   using V = cx_t<T>;
-  using V4 = typename Vec16<T>::type;
+  using V4 = typename Cx<T>::vec4;
   constexpr int G = (KIND == RK_FWD2 || KIND == RK_INV2) ? 2 : 4;
   constexpr bool INV = (KIND == RK_INV2 || KIND == RK_INV3);
+  using TL = RowTile<T, M, G>;
+  constexpr int NT = TL::NT;
+  constexpr int R0 = TL::R0, Q0 = M / R0, NBF0 = TL::E / R0;
   constexpr int CPV = 16 / sizeof(V);
-  constexpr int NT = kRowThreads;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  V* buf = reinterpret_cast<V*>(smem_raw);
-  const RowLayout<T, M> lay;
-  const int tid = threadIdx.x;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  V* sm = reinterpret_cast<V*>(smem_raw);
+  const int t = threadIdx.x;
   const int P = blockIdx.x, batch = blockIdx.y;
   const int n1 = a.n1, n2 = a.n2;
 
-  // rows of this group and their degeneracy
-  int rows[G];
+  // frequency rows of this group, their slot-order rows in the forward
+  // intermediate, and degeneracy
+  int rows[G], irow[G];
   bool deg1 = false, deg2 = false;
   int q1 = 0, q2 = 0, m1 = 0, m2 = 0;
   if constexpr (G == 2) {
-    q1 = P == 0 ? 0 : P;
+    q1 = P;
     m1 = P == 0 ? n1 / 2 : n1 - P;
     rows[0] = q1;
     rows[1] = m1;
+    irow[0] = rt_digit_pos(q1, n1);
+    irow[1] = rt_digit_pos(m1, n1);
   } else {
     const int h2 = n2 / 2 + 1;
     q1 = P / h2;
@@ -326,124 +556,167 @@ __global__ void __launch_bounds__(kRowThreads)
     rows[1] = m1 * n2 + q2;
     rows[2] = q1 * n2 + m2;
     rows[3] = m1 * n2 + m2;
+    const int p1q = rt_digit_pos(q1, n1), p1m = rt_digit_pos(m1, n1);
+    const int p2q = rt_digit_pos(q2, n2), p2m = rt_digit_pos(m2, n2);
+    irow[0] = p1q * n2 + p2q;
+    irow[1] = p1m * n2 + p2q;
+    irow[2] = p1q * n2 + p2m;
+    irow[3] = p1m * n2 + p2m;
   }
 
-  // ---------------------------------------------------------------- load ---
+  V v[TL::E];
   if constexpr (!INV) {
-    const V* src = static_cast<const V*>(a.src) + batch * a.src_batch;
-    constexpr int VPR = M / CPV;
-    for (int v = tid; v < G * VPR; v += NT) {
-      const int line = v / VPR, ci = v - line * VPR;
-      const V4 t = __ldg(reinterpret_cast<const V4*>(src + static_cast<long long>(rows[line]) * M + ci * CPV));
-      const V* e = reinterpret_cast<const V*>(&t);
+    // ---- forward: the G rows land in smem by 1D bulk copies ----------------
+    StageTw<TL, 0> w0;
+    w0.load(tw.st[0], t);
+    {
+      uint64_t* bar = reinterpret_cast<uint64_t*>(sm + G * M);  // after the tile
+      if (t == 0) mbar_init(bar, 1);
+      __syncthreads();
+      if (t == 0) {
+        const V* src = static_cast<const V*>(a.src) + batch * a.src_batch;
+        mbar_expect_tx(bar, static_cast<uint32_t>(G * M * sizeof(V)));
 #pragma unroll
-      for (int k = 0; k < CPV; ++k) buf[lay.at(line, s_to_m(ci * CPV + k, M))] = e[k];
+        for (int l = 0; l < G; ++l)
+          bulk_load(sm + l * M, src + static_cast<long long>(irow[l]) * M, static_cast<uint32_t>(M * sizeof(V)), bar);
+      }
+      mbar_wait(bar, 0);
     }
-  } else if constexpr (KIND == RK_INV2) {
+#pragma unroll
+    for (int i = 0; i < NBF0; ++i) {
+      int line, j, b;
+      TL::template decode<0>(t + i * NT, line, j, b);
+#pragma unroll
+      for (int r = 0; r < R0; ++r) {
+        const int n = j + r * Q0;
+        const int s = (r < R0 / 2) ? 2 * n : 2 * M - 1 - 2 * n;  // pair-interleaved column of z(n)
+        v[i * R0 + r] = sm[line * M + s];
+      }
+    }
+    __syncthreads();  // raw rows consumed; smem becomes the exchange buffer
+    fft_regs<TL, false>(v, sm, tw, w0, t);
+    __syncthreads();  // last-stage smem reads done before natural-order writes
+    last_to_natural<TL>(v, sm, t);
+    __syncthreads();
+  } else {
+    // ---- inverse: merged preprocess + packing into smem (natural order) ----
     const T* x = static_cast<const T*>(a.src) + batch * a.src_batch;
     const V* tu = static_cast<const V*>(a.tu);
-    for (int k = tid; k <= M / 2; k += NT) {
-      V A0, A1, B0, B1;  // X'(line, k), X'(line, M-k)
-      if (P != 0) {
-        pre2_item(x, q1, k, a, A0, A1);
-        pre2_item(x, q1, M - k, a, B0, B1);
-      } else {
-        V d0, d1;
-        pre2_item(x, 0, k, a, A0, d0);
-        pre2_item(x, n1 / 2, k, a, A1, d1);
-        pre2_item(x, 0, M - k, a, B0, d0);
-        pre2_item(x, n1 / 2, M - k, a, B1, d1);
+    if constexpr (KIND == RK_INV2) {
+      for (int k = t; k <= M / 2; k += NT) {
+        V A0, A1, B0, B1;  // X'(line, k), X'(line, M-k)
+        if (P != 0) {
+          pre2_item(x, q1, k, a, A0, A1);
+          pre2_item(x, q1, M - k, a, B0, B1);
+        } else {
+          V d0, d1;
+          pre2_item(x, 0, k, a, A0, d0);
+          pre2_item(x, n1 / 2, k, a, A1, d1);
+          pre2_item(x, 0, M - k, a, B0, d0);
+          pre2_item(x, n1 / 2, M - k, a, B1, d1);
+        }
+        // partner line of each row (-k1): swap for pairs, self for P == 0
+        const V pA0 = P != 0 ? A1 : A0, pA1 = P != 0 ? A0 : A1;
+        const V pB0 = P != 0 ? B1 : B0, pB1 = P != 0 ? B0 : B1;
+        const V wk = __ldg(tu + k);
+        sm[row_nat<T, M>(0, k & (M - 1))] = pack(A0, k == 0 ? B0 : cconj(pB0), wk);
+        sm[row_nat<T, M>(1, k & (M - 1))] = pack(A1, k == 0 ? B1 : cconj(pB1), wk);
+        if (k != 0 && 2 * k != M) {
+          const V wmk = __ldg(tu + (M - k));
+          sm[row_nat<T, M>(0, M - k)] = pack(B0, cconj(pA0), wmk);
+          sm[row_nat<T, M>(1, M - k)] = pack(B1, cconj(pA1), wmk);
+        }
       }
-      // partner line of each row (-k1): swap for pairs, self for P == 0
-      const V pA0 = P != 0 ? A1 : A0, pA1 = P != 0 ? A0 : A1;
-      const V pB0 = P != 0 ? B1 : B0, pB1 = P != 0 ? B0 : B1;
-      const V wk = __ldg(tu + k);
-      buf[lay.at(0, k)] = pack(A0, k == 0 ? B0 : cconj(pB0), wk);
-      buf[lay.at(1, k)] = pack(A1, k == 0 ? B1 : cconj(pB1), wk);
-      if (k != 0 && 2 * k != M) {
-        const V wmk = __ldg(tu + (M - k));
-        buf[lay.at(0, M - k)] = pack(B0, cconj(pA0), wmk);
-        buf[lay.at(1, M - k)] = pack(B1, cconj(pA1), wmk);
+    } else {  // RK_INV3
+      const int li[4] = {q1, m1, q1, m1}, lj[4] = {q2, q2, m2, m2};
+      for (int k = t; k <= M / 2; k += NT) {
+        V A[4], B[4];
+#pragma unroll
+        for (int l = 0; l < 4; ++l) {
+          A[l] = pre3_entry(x, li[l], lj[l], k, a);
+          B[l] = pre3_entry(x, li[l], lj[l], M - k, a);
+        }
+        const V wk = __ldg(tu + k);
+#pragma unroll
+        for (int l = 0; l < 4; ++l)
+          sm[row_nat<T, M>(l, k & (M - 1))] = pack(A[l], k == 0 ? B[l] : cconj(B[3 - l]), wk);
+        if (k != 0 && 2 * k != M) {
+          const V wmk = __ldg(tu + (M - k));
+#pragma unroll
+          for (int l = 0; l < 4; ++l) sm[row_nat<T, M>(l, M - k)] = pack(B[l], cconj(A[3 - l]), wmk);
+        }
       }
     }
-  } else {  // RK_INV3
-    const T* x = static_cast<const T*>(a.src) + batch * a.src_batch;
-    const V* tu = static_cast<const V*>(a.tu);
-    const int li[4] = {q1, m1, q1, m1}, lj[4] = {q2, q2, m2, m2};
-    for (int k = tid; k <= M / 2; k += NT) {
-      V A[4], B[4];
-#pragma unroll
-      for (int l = 0; l < 4; ++l) {
-        A[l] = pre3_entry(x, li[l], lj[l], k, a);
-        B[l] = pre3_entry(x, li[l], lj[l], M - k, a);
-      }
-      const V wk = __ldg(tu + k);
-#pragma unroll
-      for (int l = 0; l < 4; ++l) buf[lay.at(l, k)] = pack(A[l], k == 0 ? B[l] : cconj(B[3 - l]), wk);
-      if (k != 0 && 2 * k != M) {
-        const V wmk = __ldg(tu + (M - k));
-#pragma unroll
-        for (int l = 0; l < 4; ++l) buf[lay.at(l, M - k)] = pack(B[l], cconj(A[3 - l]), wmk);
-      }
-    }
-  }
-  __syncthreads();
-
-  // ----------------------------------------------------------------- FFT ---
-  block_fft<T, M, INV, false>(buf, lay, ilog2c(G), tw, tw_step);
-
-  // --------------------------------------------------------------- store ---
-  if constexpr (INV) {
+    StageTw<TL, 0> w0;
+    w0.load(tw.st[0], t);
+    __syncthreads();
+    from_smem<TL, 0>(v, sm, t);
+    fft_regs<TL, true>(v, sm, tw, w0, t);
+    __syncthreads();
+    last_to_natural<TL>(v, sm, t);
+    __syncthreads();
+    // ---- store rows (natural row order) in pair-interleaved column order ---
     V* dst = static_cast<V*>(a.dst) + batch * a.dst_batch;
     constexpr int VPR = M / CPV;
-    for (int v = tid; v < G * VPR; v += NT) {
-      const int line = v / VPR, ci = v - line * VPR;
+    for (int w = t; w < G * VPR; w += NT) {
+      const int line = w / VPR, ci = w - line * VPR;
       if (G == 4 && ((line == 1 && deg1) || (line == 2 && deg2) || (line == 3 && (deg1 || deg2))))
         continue;
       V4 o;
       V* e = reinterpret_cast<V*>(&o);
 #pragma unroll
-      for (int k = 0; k < CPV; ++k) e[k] = buf[lay.at(line, digit_pos<M>(s_to_m(ci * CPV + k, M)))];
+      for (int k = 0; k < CPV; ++k) e[k] = sm[row_nat<T, M>(line, s_to_m(ci * CPV + k, M))];
       *reinterpret_cast<V4*>(dst + static_cast<long long>(rows[line]) * M + ci * CPV) = o;
     }
-  } else if constexpr (KIND == RK_FWD2) {
-    // merged DCT postprocess (proj/src/dct2d.cpp:93-113) on the unpacked rows
+    return;
+  }
+
+  // ---- forward postprocess from natural-order smem -------------------------
+  if constexpr (KIND == RK_FWD2) {
+    // merged DCT postprocess (proj/src/dct2d.cpp:93-113) on the unpacked
+    // rows. Items q2 and M-q2 read the same four spectrum values, so one
+    // thread handles the pair: 4 smem reads -> up to 8 outputs.
     T* y = static_cast<T*>(a.dst) + batch * a.dst_batch;
     const V* ta = static_cast<const V*>(a.ta);
     const V* tb = static_cast<const V*>(a.tb);
     const V* tu = static_cast<const V*>(a.tu);
-    for (int k2 = tid; k2 <= M; k2 += NT) {
-      const int ka = digit_pos<M>(k2 & (M - 1)), kb = digit_pos<M>((M - k2) & (M - 1));
-      const V w = __ldg(tu + k2), b = __ldg(tb + k2);
-      const bool deg2k = (k2 == 0) || (k2 == M);
-      const V Z0a = buf[lay.at(0, ka)], Z0b = buf[lay.at(0, kb)];
-      const V Z1a = buf[lay.at(1, ka)], Z1b = buf[lay.at(1, kb)];
+    T* r0 = y + static_cast<long long>(q1) * n2;
+    T* r1 = y + static_cast<long long>(m1) * n2;
+    const V av0 = __ldg(ta + q1), av1 = __ldg(ta + m1);
+    auto item = [&](int q, V Z0a, V Z0b, V Z1a, V Z1b) {
+      // Z0a = Z(k1, q), Z0b = Z(k1, -q), Z1a = Z(k1', q), Z1b = Z(k1', -q)
+      const V w = __ldg(tu + q), b = __ldg(tb + q);
+      const bool deg2k = (q == 0) || (q == M);
       if (P != 0) {
         const V X1 = unpack(Z0a, cconj(Z1b), w);
         const V X2 = unpack(Z1a, cconj(Z0b), w);
-        const V av = __ldg(ta + q1);
-        const V ax1 = cmul(av, X1), ax2 = cmulc(X2, av);
-        const V s = cmul(b, cadd(ax1, ax2)), t = cmul(b, csub(ax1, ax2));
-        T* r0 = y + static_cast<long long>(q1) * n2;
-        T* r1 = y + static_cast<long long>(m1) * n2;
-        r0[k2] = T(0.5) * s.x;
-        r1[k2] = T(-0.5) * t.y;
+        const V ax1 = cmul(av0, X1), ax2 = cmulc(X2, av0);
+        const V sv = cmul(b, cadd(ax1, ax2)), tv = cmul(b, csub(ax1, ax2));
+        r0[q] = T(0.5) * sv.x;
+        r1[q] = T(-0.5) * tv.y;
         if (!deg2k) {
-          r0[n2 - k2] = T(-0.5) * s.y;
-          r1[n2 - k2] = T(-0.5) * t.x;
+          r0[n2 - q] = T(-0.5) * sv.y;
+          r1[n2 - q] = T(-0.5) * tv.x;
         }
       } else {
-#pragma unroll
-        for (int l = 0; l < 2; ++l) {
-          const int row = l == 0 ? 0 : n1 / 2;
-          const V X1 = l == 0 ? unpack(Z0a, cconj(Z0b), w) : unpack(Z1a, cconj(Z1b), w);
-          const V av = __ldg(ta + row);
-          const V s = cmul(b, cadd(cmul(av, X1), cmulc(X1, av)));
-          T* r0 = y + static_cast<long long>(row) * n2;
-          r0[k2] = T(0.5) * s.x;
-          if (!deg2k) r0[n2 - k2] = T(-0.5) * s.y;
+        const V X0 = unpack(Z0a, cconj(Z0b), w);
+        const V X1 = unpack(Z1a, cconj(Z1b), w);
+        const V s0 = cmul(b, cadd(cmul(av0, X0), cmulc(X0, av0)));
+        const V s1 = cmul(b, cadd(cmul(av1, X1), cmulc(X1, av1)));
+        r0[q] = T(0.5) * s0.x;
+        r1[q] = T(0.5) * s1.x;
+        if (!deg2k) {
+          r0[n2 - q] = T(-0.5) * s0.y;
+          r1[n2 - q] = T(-0.5) * s1.y;
         }
       }
+    };
+    for (int k2 = t; k2 <= M / 2; k2 += NT) {
+      const int kb = (M - k2) & (M - 1);
+      const V Z0a = sm[row_nat<T, M>(0, k2)], Z0b = sm[row_nat<T, M>(0, kb)];
+      const V Z1a = sm[row_nat<T, M>(1, k2)], Z1b = sm[row_nat<T, M>(1, kb)];
+      item(k2, Z0a, Z0b, Z1a, Z1b);
+      if (2 * k2 != M) item(M - k2, Z0b, Z0a, Z1b, Z1a);
     }
   } else {  // RK_FWD3: merged 3D postprocess (proj/src/transforms_ext.cpp:117-157)
     T* y = static_cast<T*>(a.dst) + batch * a.dst_batch;
@@ -452,13 +725,13 @@ __global__ void __launch_bounds__(kRowThreads)
     const V av = __ldg(static_cast<const V*>(a.ta) + q1);
     const V bv = __ldg(static_cast<const V*>(a.tb) + q2);
     const V ab = cmul(av, bv), cb = cmulc(bv, av);  // a b, conj(a) b
-    auto put = [&](int i, int j, int k, T v) { y[(static_cast<long long>(i) * n2 + j) * n3 + k] = v; };
-    for (int k3 = tid; k3 <= M; k3 += NT) {
-      const int ka = digit_pos<M>(k3 & (M - 1)), kb = digit_pos<M>((M - k3) & (M - 1));
+    auto put = [&](int i, int j, int k, T val) { y[(static_cast<long long>(i) * n2 + j) * n3 + k] = val; };
+    auto item = [&](int k3, const V* Za, const V* Zb) {
+      // Za[l] = Z(line l, k3), Zb[l] = Z(line l, -k3)
       const V w = __ldg(tu + k3);
       V X[4];
 #pragma unroll
-      for (int l = 0; l < 4; ++l) X[l] = unpack(buf[lay.at(l, ka)], cconj(buf[lay.at(3 - l, kb)]), w);
+      for (int l = 0; l < 4; ++l) X[l] = unpack(Za[l], cconj(Zb[3 - l]), w);
       const bool deg3 = (k3 == 0) || (k3 == M);
       const int m3 = n3 - k3;
       const V f1 = X[0];
@@ -487,6 +760,17 @@ __global__ void __launch_bounds__(kRowThreads)
           if (!deg3) put(m1, m2, m3, T(0.25) * u11.y);
         }
       }
+    };
+    for (int k3 = t; k3 <= M / 2; k3 += NT) {
+      const int kb = (M - k3) & (M - 1);
+      V Za[4], Zb[4];
+#pragma unroll
+      for (int l = 0; l < 4; ++l) {
+        Za[l] = sm[row_nat<T, M>(l, k3)];
+        Zb[l] = sm[row_nat<T, M>(l, kb)];
+      }
+      item(k3, Za, Zb);
+      if (2 * k3 != M) item(M - k3, Zb, Za);
     }
   }
 }

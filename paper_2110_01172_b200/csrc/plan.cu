@@ -5,12 +5,15 @@
 // the quarter-wave tables a, b (, c) (proj/src/dct1d.cpp:41-48), the FFT
 // circle table, the packing twiddles, the launch geometry (band width W of the
 // column kernels) and a device workspace for the one inter-pass intermediate.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <cstdint>
 #include <mutex>
 #include <string>
 #include <unordered_map>
@@ -85,12 +88,12 @@ struct sdct_plan_s {
   int device = 0;
   bool fast = false;
   // fast geometry
-  int M = 0;        // packed z-line length (n_last / 2)
-  int lgw[2] = {1, 1};  // column-kernel band widths: pass over axis 0, pass over axis 1 (3D)
-  int Lc = 1;       // circle-table length
+  int M = 0;            // packed z-line length (n_last / 2)
+  int nl[2] = {2, 2};   // column-kernel band widths: pass over axis 0, pass over axis 1 (3D)
+  TwSet tw_col[2] = {};  // per-stage twiddle tables: axis-0 / axis-1 column FFTs
+  TwSet tw_row = {};     // row FFT (length M)
   // device tables (one allocation)
   void* tables = nullptr;
-  void* circ = nullptr;  // dtype: W_Lc^m
   void* ta = nullptr;    // dtype quarter-wave tables
   void* tb = nullptr;
   void* tc = nullptr;
@@ -140,14 +143,39 @@ void circle(std::vector<long double>& re, std::vector<long double>& im, long lon
   }
 }
 
-int pick_lgw(int L, int M, long long planes_batch, size_t cxsize) {
-  // Largest band that keeps the tile <= 128 KB, <= 32 columns, <= M, while
-  // keeping >= 2 CTAs per SM of parallelism when the problem allows.
-  long long w = std::max<long long>(2, (128 * 1024) / (static_cast<long long>(L) * cxsize));
-  w = std::min<long long>(w, 32);
-  w = std::min<long long>(w, M);
-  while (w > 2 && (M / w) * planes_batch < 2 * 148) w >>= 1;
-  return ilog2i(w);
+int pick_nl(int esize, int L, int M, long long planes_batch) {
+  // nl_default keeps the tile <= 128 KB; fall back to 2 columns when the
+  // problem is too narrow or offers < 2 CTAs per SM at the default width.
+  const int nld = nl_default(esize, L);
+  if (nld <= M && (M / nld) * planes_batch >= 2 * 148) return nld;
+  return 2;
+}
+
+// Per-stage DIF twiddle tables of one FFT length (same radix plan as
+// RadixPlan<L>): stage s with span > R stores W_span^{j k} at (k-1)*Q + j.
+template <typename T>
+void stage_tables(std::vector<unsigned char>& blob, int L, size_t offs[4]) {
+  int lg = 0;
+  while ((1 << lg) < L) ++lg;
+  const int S = lg == 0 ? 0 : (lg + 3) / 4;
+  const long double pi = 3.141592653589793238462643383279502884L;
+  int span = L;
+  for (int s = 0; s < 4; ++s) offs[s] = SIZE_MAX;
+  for (int s = 0; s < S; ++s) {
+    const int R = 1 << (lg / S + (s < lg % S ? 1 : 0));
+    const int Q = span / R;
+    if (span > R) {
+      std::vector<long double> re(static_cast<size_t>(R - 1) * Q), im(re.size());
+      for (int k = 1; k < R; ++k)
+        for (int j = 0; j < Q; ++j) {
+          const long double ph = -2.0L * pi * static_cast<long double>(j * k) / span;
+          re[(k - 1) * Q + j] = cosl(ph);
+          im[(k - 1) * Q + j] = sinl(ph);
+        }
+      fill_table<T>(blob, offs[s], re, im);
+    }
+    span = Q;
+  }
 }
 
 int build_plan(sdct_plan_s* p) {
@@ -168,20 +196,24 @@ int build_plan(sdct_plan_s* p) {
 
   std::vector<unsigned char> blob;
   std::vector<long double> re, im;
-  size_t off_circ = 0, off_ta = 0, off_tb = 0, off_tc = 0, off_tu = 0;
+  size_t off_ta = 0, off_tb = 0, off_tc = 0, off_tu = 0;
   size_t off_gq[3] = {0, 0, 0}, off_gc[3] = {0, 0, 0};
+  size_t st_c0[4], st_c1[4], st_r[4];
   if (fast) {
-    const int nl = p->n[r - 1];
-    p->M = nl / 2;
-    p->Lc = std::max(p->n[0], p->M);
-    if (r == 3) p->Lc = std::max(p->Lc, p->n[1]);
+    const int nlast = p->n[r - 1];
+    p->M = nlast / 2;
     const bool f32 = p->dtype == SDCT_F32;
     auto put = [&](size_t& off) {
       if (f32) fill_table<float>(blob, off, re, im);
       else fill_table<double>(blob, off, re, im);
     };
-    circle(re, im, p->Lc, 1.0L, p->Lc);
-    put(off_circ);
+    auto stages = [&](int L, size_t* o) {
+      if (f32) stage_tables<float>(blob, L, o);
+      else stage_tables<double>(blob, L, o);
+    };
+    stages(p->n[0], st_c0);
+    if (r == 3) stages(p->n[1], st_c1);
+    stages(p->M, st_r);
     circle(re, im, p->n[0], 1.0L, 4.0L * p->n[0]);
     put(off_ta);
     circle(re, im, p->n[1], 1.0L, 4.0L * p->n[1]);
@@ -190,11 +222,11 @@ int build_plan(sdct_plan_s* p) {
       circle(re, im, p->n[2], 1.0L, 4.0L * p->n[2]);
       put(off_tc);
     }
-    circle(re, im, p->M + 1, 1.0L, nl);
+    circle(re, im, p->M + 1, 1.0L, nlast);
     put(off_tu);
     const long long pb0 = (r == 2 ? 1 : p->n[1]) * p->batch;
-    p->lgw[0] = pick_lgw(p->n[0], p->M, pb0, cx);
-    if (r == 3) p->lgw[1] = pick_lgw(p->n[1], p->M, static_cast<long long>(p->n[0]) * p->batch, cx);
+    p->nl[0] = pick_nl(static_cast<int>(p->elem()), p->n[0], p->M, pb0);
+    if (r == 3) p->nl[1] = pick_nl(static_cast<int>(p->elem()), p->n[1], p->M, static_cast<long long>(p->n[0]) * p->batch);
     p->ws_bytes = static_cast<size_t>(p->batch) * p->item_bytes();
   } else {
     p->ws_bytes = p->generic_ws_bytes();
@@ -212,7 +244,12 @@ int build_plan(sdct_plan_s* p) {
   if (e != cudaSuccess) return cuda_fail(e, "uploading plan tables");
   unsigned char* base = static_cast<unsigned char*>(p->tables);
   if (fast) {
-    p->circ = base + off_circ;
+    auto tws = [&](const size_t* o, TwSet& t) {
+      for (int k = 0; k < 4; ++k) t.st[k] = o[k] == SIZE_MAX ? nullptr : base + o[k];
+    };
+    tws(st_c0, p->tw_col[0]);
+    if (r == 3) tws(st_c1, p->tw_col[1]);
+    tws(st_r, p->tw_row);
     p->ta = base + off_ta;
     p->tb = base + off_tb;
     p->tc = r == 3 ? base + off_tc : nullptr;
@@ -253,33 +290,67 @@ bool kind_ok(const sdct_plan_s* p, int kind) {
 // Stage lists. Every transform is an ordered list of kernel launches; the
 // full transform runs all of them, sdct_exec_stage runs one.
 // ---------------------------------------------------------------------------
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no link
+// against libcuda needed).
+PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* f = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  });
+  return fn;
+}
+
+// 4D map over a column pass input: dims (innermost first) {inner reals, FFT
+// rows, planes, batch} with byte strides for dims 1..3; box {2*nl, min(L,256), 1, 1}.
+bool make_col_map(CUtensorMap* map, bool f32, const void* base, long long inner, long long rows,
+                  long long row_stride_b, long long planes, long long plane_stride_b, long long batch,
+                  long long batch_stride_b, int nl, int L) {
+  auto enc = tmap_encoder();
+  if (!enc) return false;
+  const cuuint64_t dims[4] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(rows),
+                              static_cast<cuuint64_t>(planes), static_cast<cuuint64_t>(batch)};
+  const cuuint64_t strides[3] = {static_cast<cuuint64_t>(row_stride_b), static_cast<cuuint64_t>(plane_stride_b),
+                                 static_cast<cuuint64_t>(batch_stride_b)};
+  const cuuint32_t box[4] = {static_cast<cuuint32_t>(2 * nl), static_cast<cuuint32_t>(L < 256 ? L : 256), 1, 1};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  const CUresult r = enc(map, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4,
+                         const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                         CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 template <typename T>
 int run_fast(sdct_plan_s* p, int kind, int only_stage, const void* in, void* out, void* ws,
              cudaStream_t st, int* nstages) {
-  using V = cx_t<T>;
   const int n1 = p->n[0], n2 = p->n[1], n3 = p->n[2];
   const int M = p->M;
-  const size_t cx = sizeof(V);
-  const V* circ = static_cast<const V*>(p->circ);
   const long long item = p->numel;
   const int B = static_cast<int>(p->batch);
   int stage = 0;
   cudaError_t e = cudaSuccess;
   auto want = [&](void) { return only_stage < 0 || only_stage == stage; };
-  auto col = [&](int L, int lgw, bool inv, int ld, int stv, int planes, const ColArgs& a) {
-    if (want() && e == cudaSuccess) {
-      const dim3 grid(M >> lgw, planes, B);
-      const size_t smem = static_cast<size_t>(L) << lgw;
-      e = launch_col<T>(L, inv, ld, stv, grid, smem * cx, st, a, circ, p->Lc / L);
+  const bool f32 = sizeof(T) == 4;
+  const long long es = sizeof(T);
+  bool map_ok = true;
+  // column pass over an axis of length L with band width nl; the TMA map
+  // describes its input (see make_col_map)
+  auto col = [&](int variant, int L, int nl, int planes, const ColArgs& a, const TwSet& tw, long long inner,
+                 long long rows, long long rs, long long np, long long ps, long long bs) {
+    if (want() && e == cudaSuccess && map_ok) {
+      CUtensorMap map;
+      map_ok = make_col_map(&map, f32, a.src, inner, rows, rs * es, np, ps * es, B, bs * es, nl, L);
+      if (map_ok) e = launch_col<T>(variant, L, nl, dim3(M / nl, planes, B), st, map, a, tw);
     }
     ++stage;
   };
   auto row = [&](int rk, int groups, const RowArgs& a) {
-    if (want() && e == cudaSuccess) {
-      const int G = (rk == RK_FWD2 || rk == RK_INV2) ? 2 : 4;
-      const dim3 grid(groups, B);
-      e = launch_row<T>(M, rk, grid, static_cast<size_t>(G) * M * cx, st, a, circ, p->Lc / M);
-    }
+    if (want() && e == cudaSuccess) e = launch_row<T>(M, rk, dim3(groups, B), st, a, p->tw_row);
     ++stage;
   };
   RowArgs ra{};
@@ -300,8 +371,7 @@ int run_fast(sdct_plan_s* p, int kind, int only_stage, const void* in, void* out
       c.in_batch = item;
       c.out_row = M;
       c.out_batch = inter;
-      c.lgw = p->lgw[0];
-      col(n1, p->lgw[0], false, LD_SRC, ST_INTER, 1, c);
+      col(CV_FWD_SRC, n1, p->nl[0], 1, c, p->tw_col[0], n2, n1, n2, 1, item, item);
       ra.src = ws;
       ra.src_batch = inter;
       ra.dst = out;
@@ -322,16 +392,16 @@ int run_fast(sdct_plan_s* p, int kind, int only_stage, const void* in, void* out
       c.in_batch = inter;
       c.out_row = n2;
       c.out_batch = item;
-      c.lgw = p->lgw[0];
       c.scale = 0.25;
       c.sign_row = mode == 1;
       c.sign_col = mode == 2;
-      col(n1, p->lgw[0], true, LD_INTER, ST_DST, 1, c);
+      col(CV_INV_DST, n1, p->nl[0], 1, c, p->tw_col[0], 2LL * M, n1, 2LL * M, 1, 2 * inter, 2 * inter);
     }
   } else {
     const long long inter = static_cast<long long>(n1) * n2 * M;
     const int groups = (n1 / 2 + 1) * (n2 / 2 + 1);
     if (kind == SDCT_DCT_3D) {
+      // axis 0 (rows i, source plane pe(j)) -> intermediate [i_slot][j][s]
       ColArgs c{};
       c.src = in;
       c.dst = ws;
@@ -342,8 +412,9 @@ int run_fast(sdct_plan_s* p, int kind, int only_stage, const void* in, void* out
       c.out_row = static_cast<long long>(n2) * M;
       c.out_plane = M;
       c.out_batch = inter;
-      c.lgw = p->lgw[0];
-      col(n1, p->lgw[0], false, LD_SRC, ST_INTER, n2, c);
+      c.tma_plane_par = n2;
+      col(CV_FWD_SRC, n1, p->nl[0], n2, c, p->tw_col[0], n3, n1, static_cast<long long>(n2) * n3, n2, n3, item);
+      // axis 1 (rows j, planes i_slot), in place -> [i_slot][j_slot][s]
       ColArgs d{};
       d.src = ws;
       d.dst = ws;
@@ -353,8 +424,7 @@ int run_fast(sdct_plan_s* p, int kind, int only_stage, const void* in, void* out
       d.out_row = M;
       d.out_plane = static_cast<long long>(n2) * M;
       d.out_batch = inter;
-      d.lgw = p->lgw[1];
-      col(n2, p->lgw[1], false, LD_INTER, ST_INTER, n1, d);
+      col(CV_FWD_INTER, n2, p->nl[1], n1, d, p->tw_col[1], 2LL * M, n2, 2LL * M, n1, 2LL * n2 * M, 2 * inter);
       ra.src = ws;
       ra.src_batch = inter;
       ra.dst = out;
@@ -365,7 +435,7 @@ int run_fast(sdct_plan_s* p, int kind, int only_stage, const void* in, void* out
       ra.src_batch = item;
       ra.dst = ws;
       ra.dst_batch = inter;
-      row(RK_INV3, groups, ra);
+      row(RK_INV3, groups, ra);  // -> [k1][k2][s]
       ColArgs d{};
       d.src = ws;
       d.dst = ws;
@@ -375,8 +445,8 @@ int run_fast(sdct_plan_s* p, int kind, int only_stage, const void* in, void* out
       d.out_row = M;
       d.out_plane = static_cast<long long>(n2) * M;
       d.out_batch = inter;
-      d.lgw = p->lgw[1];
-      col(n2, p->lgw[1], true, LD_INTER, ST_INTER, n1, d);
+      col(CV_INV_INTER, n2, p->nl[1], n1, d, p->tw_col[1], 2LL * M, n2, 2LL * M, n1, 2LL * n2 * M,
+          2 * inter);  // -> [k1][j_slot][s]
       ColArgs c{};
       c.src = ws;
       c.dst = out;
@@ -385,14 +455,15 @@ int run_fast(sdct_plan_s* p, int kind, int only_stage, const void* in, void* out
       c.in_batch = inter;
       c.out_row = static_cast<long long>(n2) * n3;
       c.out_plane = n3;
-      c.out_plane_par = n2;
+      c.out_plane_map = 2;  // plane j_slot -> y plane pe(digit_rev(j_slot))
+      c.out_plane_n = n2;
       c.out_batch = item;
-      c.lgw = p->lgw[0];
       c.scale = 0.125;
-      col(n1, p->lgw[0], true, LD_INTER, ST_DST, n2, c);
+      col(CV_INV_DST, n1, p->nl[0], n2, c, p->tw_col[0], 2LL * M, n1, 2LL * n2 * M, n2, 2LL * M, 2 * inter);
     }
   }
   if (nstages) *nstages = stage;
+  if (!map_ok) return fail(SDCT_ERR_CUDA, "cuTensorMapEncodeTiled failed (driver entry point or tile geometry)");
   if (e != cudaSuccess) return cuda_fail(e, "launching fast-path kernel");
   return SDCT_OK;
 }
@@ -418,11 +489,6 @@ GenericJob make_job(const sdct_plan_s* p, int kind) {
   return j;
 }
 
-int generic_stage_count(const sdct_plan_s* p) {
-  int n = 2;
-  for (int a = 0; a < p->rank; ++a) n += p->n[a] > 1;
-  return n;
-}
 
 template <typename T>
 int run(sdct_plan_s* p, int kind, int only_stage, const void* in, void* out, void* ws,

@@ -122,3 +122,42 @@ if __name__ == "__main__":
                     continue
                 print("col", esize, L, nl, stage_degrees(L, nl, 256, esize, True),
                       "row", stage_degrees(L, nl, 256, esize, False))
+
+
+def digit_rev(L: int, n: int) -> int:
+    """Inverse of digit_pos: the frequency index held at slot n."""
+    S, bits, R, span = radix_plan(L)
+    k = 0
+    shift = 0
+    for s in range(S):
+        d = (n // span[s + 1]) % R[s]
+        k |= d << shift
+        shift += bits[s]
+    return k
+
+
+def row_extra_degrees(L, G, esize, nthreads):
+    """v2 row-kernel patterns beyond the DIF stages: (a) last stage writes its
+    outputs at natural-frequency addresses, (b) natural-order reads by
+    consecutive threads, (c) pair-interleaved (s-order) reads."""
+    S, bits, R, span = radix_plan(L)
+    r_ = R[S - 1]
+    nbf = L * G // r_
+    worst = {"kwrite": 1, "natural": 1, "sorder": 1}
+    for it in range(0, nbf, nthreads):
+        for w0 in range(0, min(nthreads, nbf - it), 32):
+            for r in range(r_):
+                addrs = []
+                for bf in range(it + w0, min(it + w0 + 32, nbf)):
+                    b = bf % (L // r_)
+                    line = bf // (L // r_)
+                    n = b * r_ + r
+                    addrs.append(row_at(line, digit_rev(L, n), L, esize))
+                worst["kwrite"] = max(worst["kwrite"], conflict_degree(addrs, esize))
+    for line in range(G):
+        for base in range(0, L, 32):
+            addrs = [row_at(line, (base + t) % L, L, esize) for t in range(32)]
+            worst["natural"] = max(worst["natural"], conflict_degree(addrs, esize))
+            m = [(s >> 1) if s % 2 == 0 else L - 1 - (s >> 1) for s in range(base, base + 32)]
+            worst["sorder"] = max(worst["sorder"], conflict_degree([row_at(line, x % L, L, esize) for x in m], esize))
+    return worst
