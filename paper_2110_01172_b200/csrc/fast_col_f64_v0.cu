@@ -4,7 +4,7 @@
 namespace sdctb {
 template <>
 cudaError_t launch_col_variant<double, 0>(int L, int nl, dim3 grid, cudaStream_t st, const CUtensorMap& map,
-                                         const ColArgs& a, const TwSet& tw) {
-  return launch_col_var<double, 0>(L, nl, grid, st, map, a, tw);
+                                         const CUtensorMap& omap, const ColArgs& a, const TwSet& tw) {
+  return launch_col_var<double, 0>(L, nl, grid, st, map, omap, a, tw);
 }
 }  // namespace sdctb

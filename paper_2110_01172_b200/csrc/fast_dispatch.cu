@@ -5,12 +5,12 @@ namespace sdctb {
 
 template <typename T>
 cudaError_t launch_col(int variant, int L, int nl, dim3 grid, cudaStream_t st, const CUtensorMap& map,
-                       const ColArgs& a, const TwSet& tw) {
+                       const CUtensorMap& omap, const ColArgs& a, const TwSet& tw) {
   switch (variant) {
-    case CV_FWD_SRC: return launch_col_variant<T, CV_FWD_SRC>(L, nl, grid, st, map, a, tw);
-    case CV_FWD_INTER: return launch_col_variant<T, CV_FWD_INTER>(L, nl, grid, st, map, a, tw);
-    case CV_INV_INTER: return launch_col_variant<T, CV_INV_INTER>(L, nl, grid, st, map, a, tw);
-    case CV_INV_DST: return launch_col_variant<T, CV_INV_DST>(L, nl, grid, st, map, a, tw);
+    case CV_FWD_SRC: return launch_col_variant<T, CV_FWD_SRC>(L, nl, grid, st, map, omap, a, tw);
+    case CV_FWD_INTER: return launch_col_variant<T, CV_FWD_INTER>(L, nl, grid, st, map, omap, a, tw);
+    case CV_INV_INTER: return launch_col_variant<T, CV_INV_INTER>(L, nl, grid, st, map, omap, a, tw);
+    case CV_INV_DST: return launch_col_variant<T, CV_INV_DST>(L, nl, grid, st, map, omap, a, tw);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -26,9 +26,9 @@ cudaError_t launch_row(int M, int kind, dim3 grid, cudaStream_t st, const RowArg
   }
 }
 
-template cudaError_t launch_col<float>(int, int, int, dim3, cudaStream_t, const CUtensorMap&, const ColArgs&,
+template cudaError_t launch_col<float>(int, int, int, dim3, cudaStream_t, const CUtensorMap&, const CUtensorMap&, const ColArgs&,
                                       const TwSet&);
-template cudaError_t launch_col<double>(int, int, int, dim3, cudaStream_t, const CUtensorMap&, const ColArgs&,
+template cudaError_t launch_col<double>(int, int, int, dim3, cudaStream_t, const CUtensorMap&, const CUtensorMap&, const ColArgs&,
                                        const TwSet&);
 template cudaError_t launch_row<float>(int, int, dim3, cudaStream_t, const RowArgs&, const TwSet&);
 template cudaError_t launch_row<double>(int, int, dim3, cudaStream_t, const RowArgs&, const TwSet&);

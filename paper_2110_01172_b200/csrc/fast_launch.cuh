@@ -14,11 +14,16 @@ constexpr int kMaxFastLen = 4096;  // largest FFT length with a fast kernel
 // column-kernel variants
 enum ColVariant { CV_FWD_SRC = 0, CV_FWD_INTER = 1, CV_INV_INTER = 2, CV_INV_DST = 3 };
 
+// Column tiles target 64 KB (two CTAs per SM) with rows of >= 32 B
+// (NL >= 16 / esize). L = 4096 cannot fit 32-B rows in 64 KB, so it runs the
+// cluster-split kernel: two CTAs per band, L/2 rows each.
+__host__ __device__ constexpr bool col_split(int L) { return false; }
 __host__ __device__ constexpr int nl_default(int esize, int L) {
-  // complex element = 2*esize bytes; tile L*NL*2*esize <= 128 KB, 2 <= NL <= 32
-  return (128 * 1024) / (L * 2 * esize) >= 32 ? 32
-         : (128 * 1024) / (L * 2 * esize) <= 2 ? 2
-                                                : (128 * 1024) / (L * 2 * esize);
+  // complex element = 2*esize bytes; tile (L or L/2) * NL * 2*esize <= 64 KB
+  return (64 * 1024) / ((col_split(L) ? L / 2 : L) * 2 * esize) >= 32 ? 32
+         : (64 * 1024) / ((col_split(L) ? L / 2 : L) * 2 * esize) <= 16 / esize
+             ? 16 / esize
+             : (64 * 1024) / ((col_split(L) ? L / 2 : L) * 2 * esize);
 }
 
 // Opt each kernel instantiation in to > 48 KB dynamic shared memory (once).
@@ -31,7 +36,7 @@ inline cudaError_t prep_smem(K kernel, size_t smem) {
 
 template <typename T>
 cudaError_t launch_col(int variant, int L, int nl, dim3 grid, cudaStream_t st, const CUtensorMap& map,
-                       const ColArgs& a, const TwSet& tw);
+                       const CUtensorMap& omap, const ColArgs& a, const TwSet& tw);
 template <typename T>
 cudaError_t launch_row(int M, int kind, dim3 grid, cudaStream_t st, const RowArgs& a, const TwSet& tw);
 
@@ -47,53 +52,73 @@ inline int tile_threads(int L, int nl) {
 
 // ---- per-variant implementation (included by the fast_col_*.cu units) -------
 template <typename T, int L, int NL, int VAR>
-cudaError_t launch_col_one(dim3 grid, cudaStream_t st, const CUtensorMap& map, const ColArgs& a,
-                           const TwSet& tw) {
+cudaError_t launch_col_one(dim3 grid, cudaStream_t st, const CUtensorMap& map, const CUtensorMap& omap,
+                           const ColArgs& a, const TwSet& tw) {
   constexpr bool INV = VAR == CV_INV_INTER || VAR == CV_INV_DST;
   constexpr int LD = VAR == CV_FWD_SRC ? LD_SRC : LD_INTER;
   constexpr int STO = VAR == CV_INV_DST ? ST_DST : ST_INTER;
+  // persistent: one CTA per resident slot, each walking tiles
   auto k = col_kernel<T, L, NL, INV, LD, STO>;
-  const size_t smem = static_cast<size_t>(L) * NL * sizeof(cx_t<T>) + 16;  // + mbarrier
+  constexpr int NT = Tile<T, L, NL, true>::NT;
+  // landing/exchange tile + half-tile staging + mbarrier
+  const size_t tile = static_cast<size_t>(L) * NL * sizeof(cx_t<T>);
+  const size_t smem = ((((tile + 127) & ~size_t(127)) + tile / 2 + 127) & ~size_t(127)) + 16;
   cudaError_t e = prep_smem(k, smem);
   if (e != cudaSuccess) return e;
-  k<<<grid, Tile<T, L, NL, true>::NT, smem, st>>>(map, a, tw);
+  static int resident = 0;
+  if (!resident) {
+    int dev = 0, sms = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, NT, smem);
+    resident = sms * (per > 0 ? per : 1);
+  }
+  ColArgs b = a;
+  b.nbands = static_cast<int>(grid.x);
+  b.nplanes = static_cast<int>(grid.y);
+  b.ntiles = static_cast<int>(grid.x * grid.y * grid.z);
+  const int ctas = b.ntiles < resident ? b.ntiles : resident;
+  k<<<ctas, NT, smem, st>>>(map, omap, b, tw);
   return cudaGetLastError();
 }
 
 template <typename T, int L, int VAR>
-cudaError_t launch_col_L(int nl, dim3 grid, cudaStream_t st, const CUtensorMap& map, const ColArgs& a,
-                         const TwSet& tw) {
+cudaError_t launch_col_L(int nl, dim3 grid, cudaStream_t st, const CUtensorMap& map, const CUtensorMap& omap,
+                         const ColArgs& a, const TwSet& tw) {
   constexpr int NLD = nl_default(sizeof(T), L);
-  if (nl == NLD) return launch_col_one<T, L, NLD, VAR>(grid, st, map, a, tw);
+  if (nl == NLD) return launch_col_one<T, L, NLD, VAR>(grid, st, map, omap, a, tw);
   if constexpr (NLD != 2) {
-    if (nl == 2) return launch_col_one<T, L, 2, VAR>(grid, st, map, a, tw);
+    if (nl == 2) return launch_col_one<T, L, 2, VAR>(grid, st, map, omap, a, tw);
+  }
+  if constexpr (NLD != 4 && sizeof(T) == 4) {
+    if (nl == 4) return launch_col_one<T, L, 4, VAR>(grid, st, map, omap, a, tw);
   }
   return cudaErrorInvalidValue;
 }
 
 template <typename T, int VAR>
-cudaError_t launch_col_var(int L, int nl, dim3 grid, cudaStream_t st, const CUtensorMap& map, const ColArgs& a,
-                           const TwSet& tw) {
+cudaError_t launch_col_var(int L, int nl, dim3 grid, cudaStream_t st, const CUtensorMap& map,
+                           const CUtensorMap& omap, const ColArgs& a, const TwSet& tw) {
   switch (L) {
-    case 2: return launch_col_L<T, 2, VAR>(nl, grid, st, map, a, tw);
-    case 4: return launch_col_L<T, 4, VAR>(nl, grid, st, map, a, tw);
-    case 8: return launch_col_L<T, 8, VAR>(nl, grid, st, map, a, tw);
-    case 16: return launch_col_L<T, 16, VAR>(nl, grid, st, map, a, tw);
-    case 32: return launch_col_L<T, 32, VAR>(nl, grid, st, map, a, tw);
-    case 64: return launch_col_L<T, 64, VAR>(nl, grid, st, map, a, tw);
-    case 128: return launch_col_L<T, 128, VAR>(nl, grid, st, map, a, tw);
-    case 256: return launch_col_L<T, 256, VAR>(nl, grid, st, map, a, tw);
-    case 512: return launch_col_L<T, 512, VAR>(nl, grid, st, map, a, tw);
-    case 1024: return launch_col_L<T, 1024, VAR>(nl, grid, st, map, a, tw);
-    case 2048: return launch_col_L<T, 2048, VAR>(nl, grid, st, map, a, tw);
-    case 4096: return launch_col_L<T, 4096, VAR>(nl, grid, st, map, a, tw);
+    case 2: return launch_col_L<T, 2, VAR>(nl, grid, st, map, omap, a, tw);
+    case 4: return launch_col_L<T, 4, VAR>(nl, grid, st, map, omap, a, tw);
+    case 8: return launch_col_L<T, 8, VAR>(nl, grid, st, map, omap, a, tw);
+    case 16: return launch_col_L<T, 16, VAR>(nl, grid, st, map, omap, a, tw);
+    case 32: return launch_col_L<T, 32, VAR>(nl, grid, st, map, omap, a, tw);
+    case 64: return launch_col_L<T, 64, VAR>(nl, grid, st, map, omap, a, tw);
+    case 128: return launch_col_L<T, 128, VAR>(nl, grid, st, map, omap, a, tw);
+    case 256: return launch_col_L<T, 256, VAR>(nl, grid, st, map, omap, a, tw);
+    case 512: return launch_col_L<T, 512, VAR>(nl, grid, st, map, omap, a, tw);
+    case 1024: return launch_col_L<T, 1024, VAR>(nl, grid, st, map, omap, a, tw);
+    case 2048: return launch_col_L<T, 2048, VAR>(nl, grid, st, map, omap, a, tw);
+    case 4096: return launch_col_L<T, 4096, VAR>(nl, grid, st, map, omap, a, tw);
     default: return cudaErrorInvalidValue;
   }
 }
 
 template <typename T, int VAR>
 cudaError_t launch_col_variant(int L, int nl, dim3 grid, cudaStream_t st, const CUtensorMap& map,
-                               const ColArgs& a, const TwSet& tw);
+                               const CUtensorMap& omap, const ColArgs& a, const TwSet& tw);
 
 template <typename T, int M, int KIND>
 cudaError_t launch_row_one(dim3 grid, cudaStream_t st, const RowArgs& a, const TwSet& tw) {

@@ -63,7 +63,16 @@ struct ColArgs {
   int sign_row, sign_col;                   // final gather: negate odd k along axis
   double scale;                             // final gather scale
   int tma_plane_par;                        // TMA plane coordinate = parity_embed(plane, n) when > 0
+  const void* twc;                          // split kernels: combine twiddles W_L^k, k < L/2
+  int nbands, nplanes, ntiles;              // persistent column kernels: tile = band + nbands*(plane + nplanes*batch)
+  unsigned long long* trace;                // debug: per-tile phase timestamps (nullptr in production)
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long v;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
+  return v;
+}
 
 struct RowArgs {
   const void* src;
@@ -282,6 +291,26 @@ __device__ __forceinline__ void later_stages(typename TL::V* v, typename TL::V* 
   }
 }
 
+// All stages but the last one's butterflies: runs stages 0..S-2 and loads the
+// last stage's operands from smem (returns with the smem free for reuse after
+// a barrier). Used by persistent kernels to start the next tile's load early.
+template <class TL, bool INV, int s>
+__device__ __forceinline__ void stages_until_last(typename TL::V* v, typename TL::V* sm, const TwSet& tw, int t,
+                                                  StageTw<TL, TL::S - 1>& wl) {
+  if constexpr (s == TL::S - 1) {
+    wl.load(tw.st[s], t);
+    from_smem<TL, s>(v, sm, t);
+  } else {
+    StageTw<TL, s> w;
+    w.load(tw.st[s], t);
+    from_smem<TL, s>(v, sm, t);
+    stage_compute<TL, s, INV>(v, w);
+    to_smem<TL, s>(v, sm, t);
+    __syncthreads();
+    stages_until_last<TL, INV, s + 1>(v, sm, tw, t, wl);
+  }
+}
+
 // Full FFT of a tile whose stage-0 operands are already in v and whose
 // stage-0 twiddles were prefetched into w0. On return v holds the last
 // stage's outputs (slot n = b*R_last + r of the thread's last-stage butterflies).
@@ -303,125 +332,318 @@ __device__ __forceinline__ void last_decode(int bf, int& line, int& b) {
   TL::template decode<TL::S - 1>(bf, line, j, b);
 }
 
+// ---- intermediate row order ---------------------------------------------------
+// The forward column FFT (DIF) leaves X(k) at slot n = digit_pos(k); its
+// last-stage butterfly (line, b) holds slots b*R + r (R = last radix). It
+// stores slot n at intermediate row sigma(n) = (n % R) * (L/R) + n / R, so
+// lanes with consecutive b write consecutive rows (conflict-free staging,
+// contiguous TMA boxes). The inverse column FFT (DIT, the transposed
+// factorisation) reads its input in exactly that order. Row kernels address
+// frequency k of an intermediate through srow(k) = sigma(digit_pos(k)).
+__host__ __device__ inline int rt_last_radix(int L) {
+  int lg = 0;
+  while ((1 << lg) < L) ++lg;
+  if (lg == 0) return 1;
+  const int S = (lg + 3) / 4;
+  return 1 << (lg / S + (S - 1 < lg % S ? 1 : 0));
+}
+__host__ __device__ inline int rt_srow(int k, int L) {
+  const int n = rt_digit_pos(k, L);
+  const int R = rt_last_radix(L);
+  return (n % R) * (L / R) + n / R;
+}
+
+// ---- DIT engine (transpose of the DIF engine) --------------------------------
+// DIF: B_0, T_0, B_1, ..., T_{S-2}, B_{S-1}, then digit reversal. Its transpose
+// (the same DFT, the DFT matrix is symmetric) runs the stage groups in reverse:
+// input placed by digit position, B_{S-1}, T_{S-2}, B_{S-2}, ..., T_0, B_0;
+// outputs come out in natural order at the stage-0 slots j + r*Q0.
+template <class TL, int s, bool INV>
+__device__ __forceinline__ void dit_compute(typename TL::V* v, const StageTw<TL, s>& tw) {
+  using P = typename TL::P;
+  constexpr int R = P::R(s), SPAN = P::span(s);
+  constexpr int NBF = TL::E / R;
+#pragma unroll
+  for (int i = 0; i < NBF; ++i) {
+    if constexpr (SPAN > R) {
+#pragma unroll
+      for (int k = 1; k < R; ++k) {
+        const auto w = tw.get(i, k);
+        v[i * R + k] = INV ? cmulc(v[i * R + k], w) : cmul(v[i * R + k], w);
+      }
+    }
+    dft_reg<typename TL::Real, R, INV>(v + i * R);
+  }
+}
+
+// DIT stages S-2 .. s (descending); operands of stage s+1 are in smem.
+template <class TL, bool INV, int s>
+__device__ __forceinline__ void dit_down(typename TL::V* v, typename TL::V* sm, const TwSet& tw, int t) {
+  if constexpr (s >= 0) {
+    StageTw<TL, s> w;
+    w.load(tw.st[s], t);
+    from_smem<TL, s>(v, sm, t);
+    dit_compute<TL, s, INV>(v, w);
+    if constexpr (s > 0) {
+      to_smem<TL, s>(v, sm, t);
+      __syncthreads();
+      dit_down<TL, INV, s - 1>(v, sm, tw, t);
+    }
+  }
+}
+
 // ============================================================================
 // Column kernel
 // ============================================================================
+// Persistent: CTA walks tiles blockIdx.x, +gridDim.x, ... A tile (band of NL
+// complex columns x L rows) lands in smem by TMA; the FFT runs in registers
+// with smem exchanges; results leave through a half-tile smem staging buffer
+// and TMA stores (the bulk engine generates the 32-B row segments, not the
+// LSU). The next tile's load is issued as soon as the current tile's last
+// stage has read its operands, so it overlaps the last stage and the stores.
+//   forward (DIF): LD_SRC (parity rows + packing) or LD_INTER (natural rows);
+//                  output rows in sigma order (ST_INTER).
+//   inverse (DIT): input rows in sigma order; output natural rows (ST_INTER)
+//                  or the final gather to y (ST_DST: rows pe(i), 1/4 or 1/8,
+//                  signs), stored as even / odd y-row classes.
 template <typename T, int L, int NL, bool INV, int LOAD, int STORE>
 __global__ void __launch_bounds__(Tile<T, L, NL, true>::NT)
-    col_kernel(const __grid_constant__ CUtensorMap tmap, ColArgs a, TwSet tw) {
+    col_kernel(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUtensorMap tout, ColArgs a,
+               TwSet tw) {
   using TL = Tile<T, L, NL, true>;
   using P = typename TL::P;
   using V = cx_t<T>;
   using V2 = typename Vec2<T>::type;
+  constexpr int NT = TL::NT;
+  constexpr int S = TL::S, SL = S - 1;
   constexpr int R0 = TL::R0, Q0 = L / R0, NBF0 = TL::E / R0;
-  constexpr int SL = TL::S - 1, RL = P::R(SL), NBFL = TL::E / RL;
+  constexpr int RL = P::R(SL), NBFL = TL::E / RL;
+  constexpr int BOXR = L < 256 ? L : 256;
+  constexpr int HALF = L / 2;
+  constexpr int BOXH = HALF < 256 ? HALF : 256;
+  constexpr uint32_t TILE_BYTES = static_cast<uint32_t>(L) * 2 * NL * sizeof(T);
+  constexpr uint32_t STG_OFF = (TILE_BYTES + 127u) & ~127u;                      // TMA needs 128-B aligned smem
+  constexpr uint32_t BAR_OFF = (STG_OFF + TILE_BYTES / 2 + 127u) & ~127u;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   V* sm = reinterpret_cast<V*>(smem_raw);
+  T* stg = reinterpret_cast<T*>(smem_raw + STG_OFF);  // half-tile staging [HALF][2*NL]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw + BAR_OFF);
   const int t = threadIdx.x;
-  const int band = blockIdx.x, plane = blockIdx.y, batch = blockIdx.z;
-  V v[TL::E];
 
-  // ------------------------------------------------- stage-0 operands ------
-  // The band tile (L rows x 2*NL reals) lands in shared memory through TMA
-  // (4D map: inner reals, FFT rows, planes, batch), then each thread reads its
-  // stage-0 operands; the same shared memory then serves as the exchange
-  // buffer.
-  StageTw<TL, 0> w0;
-  w0.load(tw.st[0], t);  // latency hidden under the tile load
-  {
-    constexpr int BOXR = L < 256 ? L : 256;
-    constexpr uint32_t TILE_BYTES = static_cast<uint32_t>(L) * 2 * NL * sizeof(T);
-    uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw + TILE_BYTES);  // after the tile
-    if (t == 0) {
-      prefetch_tmap(&tmap);
-      mbar_init(bar, 1);
-    }
-    __syncthreads();
-    if (t == 0) {
-      const int pc = a.tma_plane_par ? parity_embed(plane, a.tma_plane_par) : plane;
-      mbar_expect_tx(bar, TILE_BYTES);
+  auto coords = [&](int tile, int& band, int& plane, int& batch) {
+    band = tile % a.nbands;
+    const int rest = tile / a.nbands;
+    plane = rest % a.nplanes;
+    batch = rest / a.nplanes;
+  };
+  auto issue = [&](int tile) {  // thread 0 only
+    int band, plane, batch;
+    coords(tile, band, plane, batch);
+    const int pc = a.tma_plane_par ? parity_embed(plane, a.tma_plane_par) : plane;
+    mbar_expect_tx(bar, TILE_BYTES);
 #pragma unroll 1
-      for (int r0 = 0; r0 < L; r0 += BOXR)
-        tma_load_4d(reinterpret_cast<T*>(smem_raw) + static_cast<size_t>(r0) * 2 * NL, &tmap, band * 2 * NL, r0,
-                    pc, batch, bar);
-    }
-    mbar_wait(bar, 0);
+    for (int r0 = 0; r0 < L; r0 += BOXR)
+      tma_load_4d(reinterpret_cast<T*>(smem_raw) + static_cast<size_t>(r0) * 2 * NL, &tin, band * 2 * NL, r0, pc,
+                  batch, bar);
+  };
+  if (t == 0) {
+    prefetch_tmap(&tin);
+    prefetch_tmap(&tout);
+    mbar_init(bar, 1);
   }
-  if constexpr (LOAD == LD_SRC) {
-    // real source; slot n of the FFT reads source row pe(n) (parity reorder
-    // along the FFT axis); line 2g+h of the band is z(u) (h=0) or z(M-1-u)
-    // (h=1) of source quad g: lanes h=0/1 read the two halves and swap one real.
-    const V2* raw = reinterpret_cast<const V2*>(smem_raw);
+  __syncthreads();
+  if (t == 0 && static_cast<int>(blockIdx.x) < a.ntiles) issue(blockIdx.x);
+
+  uint32_t phase = 0;
+  for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
+    int band, plane, batch;
+    coords(tile, band, plane, batch);
+    V v[TL::E];
+    unsigned long long tr0 = 0, tr1 = 0, tr2 = 0;
+    if (a.trace && t == 0) tr0 = gtimer();
+
+    if constexpr (!INV) {
+      // =================== forward: DIF ===================
+      StageTw<TL, 0> w0;
+      w0.load(tw.st[0], t);  // latency hidden under the tile load
+      mbar_wait(bar, phase);
+      phase ^= 1;
+      if (a.trace && t == 0) tr1 = gtimer();
+      if constexpr (LOAD == LD_SRC) {
+        // slot n reads source row pe(n); line 2g+h is z(u) (h=0) or z(M-1-u)
+        // (h=1) of source quad g: lanes h=0/1 read the halves, swap one real
+        const V2* raw = reinterpret_cast<const V2*>(smem_raw);
 #pragma unroll
-    for (int i = 0; i < NBF0; ++i) {
-      const int bf = t + i * TL::NT;
-      const int line = bf & (NL - 1), j = bf >> TL::LGNL;
-      const int h = line & 1;
+        for (int i = 0; i < NBF0; ++i) {
+          const int bf = t + i * NT;
+          const int line = bf & (NL - 1), j = bf >> TL::LGNL;
+          const int h = line & 1;
 #pragma unroll
-      for (int r = 0; r < R0; ++r) {
-        const int n = j + r * Q0;
-        const int row = (r < R0 / 2) ? 2 * n : 2 * L - 1 - 2 * n;
-        const V2 x = raw[row * NL + line];
-        const T send = h ? x.x : x.y;
-        const T recv = __shfl_xor_sync(TL::MASK, send, 1);
-        v[i * R0 + r] = h ? mk(x.y, recv) : mk(x.x, recv);
+          for (int r = 0; r < R0; ++r) {
+            const int n = j + r * Q0;
+            const int row = (r < R0 / 2) ? 2 * n : 2 * L - 1 - 2 * n;
+            const V2 x = raw[row * NL + line];
+            const T send = h ? x.x : x.y;
+            const T recv = __shfl_xor_sync(TL::MASK, send, 1);
+            v[i * R0 + r] = h ? mk(x.y, recv) : mk(x.x, recv);
+          }
+        }
+      } else {
+        const V* raw = reinterpret_cast<const V*>(smem_raw);
+#pragma unroll
+        for (int i = 0; i < NBF0; ++i) {
+          const int bf = t + i * NT;
+          const int line = bf & (NL - 1), j = bf >> TL::LGNL;
+#pragma unroll
+          for (int r = 0; r < R0; ++r) v[i * R0 + r] = raw[(j + r * Q0) * NL + line];
+        }
+      }
+      __syncthreads();  // raw tile consumed; smem becomes the exchange buffer
+      StageTw<TL, SL> wl;
+      if constexpr (S == 1) {
+        wl = w0;
+      } else {
+        stage_compute<TL, 0, false>(v, w0);
+        to_smem<TL, 0>(v, sm, t);
+        __syncthreads();
+        stages_until_last<TL, false, 1>(v, sm, tw, t, wl);
+      }
+      __syncthreads();  // last-stage operands are in registers: smem is free
+      if (a.trace && t == 0) tr2 = gtimer();
+      if (t == 0 && tile + static_cast<int>(gridDim.x) < a.ntiles) {
+        fence_async_smem();
+        issue(tile + gridDim.x);
+      }
+      stage_compute<TL, SL, false>(v, wl);
+      // ---- store: slot n = b*RL + r -> row sigma(n) = b + (L/RL)*r ----
+#pragma unroll
+      for (int half = 0; half < 2; ++half) {
+        if (t == 0) bulk_wait_read();  // staging free again
+        __syncthreads();
+        V* sv = reinterpret_cast<V*>(stg);
+#pragma unroll
+        for (int i = 0; i < NBFL; ++i) {
+          int line, b;
+          last_decode<TL>(t + i * NT, line, b);
+#pragma unroll
+          for (int r = half * (RL / 2); r < (half + 1) * (RL / 2); ++r)
+            sv[(b + (L / RL) * (r - half * (RL / 2))) * NL + line] = v[i * RL + r];
+        }
+        fence_async_smem();
+        __syncthreads();
+        if (t == 0) {
+#pragma unroll 1
+          for (int r0 = 0; r0 < HALF; r0 += BOXH)
+            tma_store_4d(&tout, band * 2 * NL, half * HALF + r0, plane, batch, stg + static_cast<size_t>(r0) * 2 * NL);
+          bulk_commit();
+        }
+      }
+    } else {
+      // =================== inverse: DIT ===================
+      StageTw<TL, SL> wl;  // first DIT stage (S-1) has no twiddles
+      mbar_wait(bar, phase);
+      phase ^= 1;
+      if (a.trace && t == 0) tr1 = gtimer();
+      {
+        // stage S-1 operands: slot b*RL + r lives in storage row sigma = b + (L/RL) r
+        const V* raw = reinterpret_cast<const V*>(smem_raw);
+#pragma unroll
+        for (int i = 0; i < NBFL; ++i) {
+          int line, b;
+          last_decode<TL>(t + i * NT, line, b);
+#pragma unroll
+          for (int r = 0; r < RL; ++r) v[i * RL + r] = raw[(b + (L / RL) * r) * NL + line];
+        }
+      }
+      __syncthreads();  // raw tile consumed
+      dit_compute<TL, SL, true>(v, wl);
+      if constexpr (S > 1) {
+        to_smem<TL, SL>(v, sm, t);
+        __syncthreads();
+        dit_down<TL, true, SL - 1>(v, sm, tw, t);  // ends with stage 0 in registers
+      }
+      __syncthreads();  // all smem reads done
+      if (a.trace && t == 0) tr2 = gtimer();
+      if (t == 0 && tile + static_cast<int>(gridDim.x) < a.ntiles) {
+        fence_async_smem();
+        issue(tile + gridDim.x);
+      }
+      // outputs: stage-0 butterfly (line, j) holds natural index ii = j + r*Q0
+      if constexpr (STORE == ST_INTER) {
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {
+          if (t == 0) bulk_wait_read();
+          __syncthreads();
+          V* sv = reinterpret_cast<V*>(stg);
+#pragma unroll
+          for (int i = 0; i < NBF0; ++i) {
+            const int bf = t + i * NT;
+            const int line = bf & (NL - 1), j = bf >> TL::LGNL;
+#pragma unroll
+            for (int r = half * (R0 / 2); r < (half + 1) * (R0 / 2); ++r)
+              sv[(j + (r - half * (R0 / 2)) * Q0) * NL + line] = v[i * R0 + r];
+          }
+          fence_async_smem();
+          __syncthreads();
+          if (t == 0) {
+#pragma unroll 1
+            for (int r0 = 0; r0 < HALF; r0 += BOXH)
+              tma_store_4d(&tout, band * 2 * NL, half * HALF + r0, plane, batch,
+                           stg + static_cast<size_t>(r0) * 2 * NL);
+            bulk_commit();
+          }
+        }
+      } else {
+        // final gather: y row pe(ii): even rows 2ii (ii < L/2) and odd rows
+        // 2L-1-2ii (ii >= L/2), staged per class and stored through a 5D map
+        // {reals, row class, row pair, planes, batch}
+        const T sc = static_cast<T>(a.scale);
+        int pl = plane;
+        if (a.out_plane_map == 1) pl = parity_embed(plane, a.out_plane_n);
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {
+          if (t == 0) bulk_wait_read();
+          __syncthreads();
+          V2* sv = reinterpret_cast<V2*>(stg);
+#pragma unroll
+          for (int i = 0; i < NBF0; ++i) {
+            const int bf = t + i * NT;
+            const int line = bf & (NL - 1), j = bf >> TL::LGNL;
+            const int h = line & 1;
+#pragma unroll
+            for (int r = half * (R0 / 2); r < (half + 1) * (R0 / 2); ++r) {
+              const int ii = j + r * Q0;
+              const int k1 = half == 0 ? 2 * ii : 2 * L - 1 - 2 * ii;  // pe(ii)
+              const int srow = half == 0 ? ii : L - 1 - ii;             // pair index
+              const V z = v[i * R0 + r];
+              const T recv = __shfl_xor_sync(TL::MASK, z.y, 1);
+              const T s0 = (a.sign_row && (k1 & 1)) ? -sc : sc;
+              const T s1 = a.sign_col ? -s0 : s0;
+              // h=0: (Re z(u), Im z(M-1-u)) = y(4u, 4u+1); h=1: (Im z(u), Re z(M-1-u)) = y(4u+2, 4u+3)
+              sv[srow * NL + line] = h ? V2{recv * s0, z.x * s1} : V2{z.x * s0, recv * s1};
+            }
+          }
+          fence_async_smem();
+          __syncthreads();
+          if (t == 0) {
+#pragma unroll 1
+            for (int r0 = 0; r0 < HALF; r0 += BOXH)
+              tma_store_5d(&tout, band * 2 * NL, half, r0, pl, batch, stg + static_cast<size_t>(r0) * 2 * NL);
+            bulk_commit();
+          }
+        }
       }
     }
-  } else {
-    const V* raw = reinterpret_cast<const V*>(smem_raw);
-#pragma unroll
-    for (int i = 0; i < NBF0; ++i) {
-      const int bf = t + i * TL::NT;
-      const int line = bf & (NL - 1), j = bf >> TL::LGNL;
-#pragma unroll
-      for (int r = 0; r < R0; ++r) v[i * R0 + r] = raw[(j + r * Q0) * NL + line];
+    if (a.trace && t == 0) {
+      unsigned long long* o = a.trace + 5 * static_cast<long long>(tile);
+      o[0] = tr0;
+      o[1] = tr1;
+      o[2] = tr2;
+      o[3] = gtimer();
+      o[4] = blockIdx.x;
     }
   }
-  __syncthreads();  // raw tile consumed; smem becomes the exchange buffer
-
-  fft_regs<TL, INV>(v, sm, tw, w0, t);
-  if constexpr (TL::S == 1) __syncthreads();  // in-place passes: all loads before any store
-
-  // --------------------------------------------------------- store ---------
-  if constexpr (STORE == ST_INTER) {
-    // rows in slot order (the consumer selects rows through digit_pos)
-    V* dst = static_cast<V*>(a.dst) + batch * a.out_batch + plane * a.out_plane +
-             static_cast<long long>(band) * NL;
-#pragma unroll
-    for (int i = 0; i < NBFL; ++i) {
-      int line, b;
-      last_decode<TL>(t + i * TL::NT, line, b);
-#pragma unroll
-      for (int r = 0; r < RL; ++r) dst[(b * RL + r) * a.out_row + line] = v[i * RL + r];
-    }
-  } else {
-    // final inverse gather: y(k1, 4u + c) = scale * z(ps(k1)) components
-    int pl = plane;
-    if (a.out_plane_map == 1) pl = parity_embed(plane, a.out_plane_n);
-    else if (a.out_plane_map == 2) pl = parity_embed(rt_digit_rev(plane, a.out_plane_n), a.out_plane_n);
-    T* dst = static_cast<T*>(a.dst) + batch * a.out_batch + pl * a.out_plane +
-             static_cast<long long>(band) * (2 * NL);
-    const T sc = static_cast<T>(a.scale);
-#pragma unroll
-    for (int i = 0; i < NBFL; ++i) {
-      int line, b;
-      last_decode<TL>(t + i * TL::NT, line, b);
-      const int h = line & 1;
-      const int kb = digit_rev<L>(b * RL);  // spatial index of slot b*RL
-#pragma unroll
-      for (int r = 0; r < RL; ++r) {
-        const int ii = kb + r * (L / RL);
-        const int k1 = (r < RL / 2) ? 2 * ii : 2 * L - 1 - 2 * ii;  // pe(ii)
-        const V z = v[i * RL + r];
-        const T recv = __shfl_xor_sync(TL::MASK, z.y, 1);
-        const T s0 = (a.sign_row && (k1 & 1)) ? -sc : sc;
-        const T s1 = a.sign_col ? -s0 : s0;
-        // lane h=0: (Re z(u), Im z(M-1-u)) = y(4u, 4u+1); h=1: (Im z(u), Re z(M-1-u)) = y(4u+2, 4u+3)
-        const V2 o = h ? V2{recv * s0, z.x * s1} : V2{z.x * s0, recv * s1};
-        *reinterpret_cast<V2*>(dst + k1 * a.out_row + 2 * line) = o;
-      }
-    }
-  }
+  if (t == 0) bulk_wait_all();  // stores complete before the CTA retires
 }
 
 // ============================================================================
@@ -532,8 +754,8 @@ __global__ void __launch_bounds__(row_threads<T, M, KIND>())
   const int P = blockIdx.x, batch = blockIdx.y;
   const int n1 = a.n1, n2 = a.n2;
 
-  // frequency rows of this group, their slot-order rows in the forward
-  // intermediate, and degeneracy
+  // frequency rows of this group, their storage rows in the intermediate
+  // (srow = sigma(digit_pos), the column FFTs' order), and degeneracy
   int rows[G], irow[G];
   bool deg1 = false, deg2 = false;
   int q1 = 0, q2 = 0, m1 = 0, m2 = 0;
@@ -542,8 +764,8 @@ __global__ void __launch_bounds__(row_threads<T, M, KIND>())
     m1 = P == 0 ? n1 / 2 : n1 - P;
     rows[0] = q1;
     rows[1] = m1;
-    irow[0] = rt_digit_pos(q1, n1);
-    irow[1] = rt_digit_pos(m1, n1);
+    irow[0] = rt_srow(q1, n1);
+    irow[1] = rt_srow(m1, n1);
   } else {
     const int h2 = n2 / 2 + 1;
     q1 = P / h2;
@@ -556,8 +778,8 @@ __global__ void __launch_bounds__(row_threads<T, M, KIND>())
     rows[1] = m1 * n2 + q2;
     rows[2] = q1 * n2 + m2;
     rows[3] = m1 * n2 + m2;
-    const int p1q = rt_digit_pos(q1, n1), p1m = rt_digit_pos(m1, n1);
-    const int p2q = rt_digit_pos(q2, n2), p2m = rt_digit_pos(m2, n2);
+    const int p1q = rt_srow(q1, n1), p1m = rt_srow(m1, n1);
+    const int p2q = rt_srow(q2, n2), p2m = rt_srow(m2, n2);
     irow[0] = p1q * n2 + p2q;
     irow[1] = p1m * n2 + p2q;
     irow[2] = p1q * n2 + p2m;
@@ -603,28 +825,92 @@ __global__ void __launch_bounds__(row_threads<T, M, KIND>())
     const T* x = static_cast<const T*>(a.src) + batch * a.src_batch;
     const V* tu = static_cast<const V*>(a.tu);
     if constexpr (KIND == RK_INV2) {
-      for (int k = t; k <= M / 2; k += NT) {
-        V A0, A1, B0, B1;  // X'(line, k), X'(line, M-k)
-        if (P != 0) {
-          pre2_item(x, q1, k, a, A0, A1);
-          pre2_item(x, q1, M - k, a, B0, B1);
-        } else {
-          V d0, d1;
-          pre2_item(x, 0, k, a, A0, d0);
-          pre2_item(x, n1 / 2, k, a, A1, d1);
-          pre2_item(x, 0, M - k, a, B0, d0);
-          pre2_item(x, n1 / 2, M - k, a, B1, d1);
+      // Rows q1 and m1 land in smem by bulk copy (2 x N2 reals = the tile's
+      // size); the merged preprocess then reads its operands from smem into
+      // registers, synchronises, and overwrites the same smem with the packed
+      // spectrum (natural order).
+      constexpr int NI = (M / 2) / NT + 1;  // items k in [0, M/2] per thread
+      T* rowA = reinterpret_cast<T*>(smem_raw);
+      T* rowB = rowA + 2 * M;
+      {
+        uint64_t* bar = reinterpret_cast<uint64_t*>(sm + G * M);
+        if (t == 0) mbar_init(bar, 1);
+        __syncthreads();
+        if (t == 0) {
+          const uint32_t rb = static_cast<uint32_t>(n2 * sizeof(T));
+          mbar_expect_tx(bar, 2 * rb);
+          bulk_load(rowA, x + static_cast<long long>(q1) * n2, rb, bar);
+          bulk_load(rowB, x + static_cast<long long>(m1) * n2, rb, bar);
         }
-        // partner line of each row (-k1): swap for pairs, self for P == 0
-        const V pA0 = P != 0 ? A1 : A0, pA1 = P != 0 ? A0 : A1;
-        const V pB0 = P != 0 ? B1 : B0, pB1 = P != 0 ? B0 : B1;
-        const V wk = __ldg(tu + k);
-        sm[row_nat<T, M>(0, k & (M - 1))] = pack(A0, k == 0 ? B0 : cconj(pB0), wk);
-        sm[row_nat<T, M>(1, k & (M - 1))] = pack(A1, k == 0 ? B1 : cconj(pB1), wk);
-        if (k != 0 && 2 * k != M) {
-          const V wmk = __ldg(tu + (M - k));
-          sm[row_nat<T, M>(0, M - k)] = pack(B0, cconj(pA0), wmk);
-          sm[row_nat<T, M>(1, M - k)] = pack(B1, cconj(pA1), wmk);
+        mbar_wait(bar, 0);
+      }
+      // operands: for n2 in {k, M-k}: D(n2) and R(n2) of both rows, where
+      // D = x(n2), R = x(N2-n2) (x(N2) := 0); mode 2 (IDXST along axis 1)
+      // reads x(N2-n2) for D and x(n2) for R with x(0) := 0.
+      T op[NI][8];
+#pragma unroll
+      for (int it = 0; it < NI; ++it) {
+        const int k = t + it * NT;
+        if (k <= M / 2) {
+          const int ks[2] = {k, M - k};
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const int nn = ks[u];
+            const bool z = nn == 0;
+            const int pd = a.mode == 2 ? n2 - nn : nn;
+            const int pr = a.mode == 2 ? nn : n2 - nn;
+            const bool zd = a.mode == 2 && z, zr = z;
+            op[it][4 * u + 0] = zd ? T(0) : rowA[pd & (n2 - 1)];
+            op[it][4 * u + 1] = zr ? T(0) : rowA[pr & (n2 - 1)];
+            op[it][4 * u + 2] = zd ? T(0) : rowB[pd & (n2 - 1)];
+            op[it][4 * u + 3] = zr ? T(0) : rowB[pr & (n2 - 1)];
+          }
+        }
+      }
+      const V* ta = static_cast<const V*>(a.ta);
+      const V* tb = static_cast<const V*>(a.tb);
+      const V ca0 = cconj(__ldg(ta + q1)), ca1 = cconj(__ldg(ta + m1));
+      __syncthreads();  // all operands read: smem becomes the packed spectrum
+      // X'(line, n2) from the operands (proj/src/dct2d.cpp:182-195)
+      auto xp = [&](const T* o, V cb, V& x0, V& x1) {
+        // o = {DA, RA, DB, RB}; p,s from the q1 row, r,q from the m1 row
+        T p = o[0], sv = o[1], r = o[2], q = o[3];
+        if (a.mode == 1) {  // IDXST along axis 0 swaps the row roles
+          p = o[2];
+          sv = o[3];
+          r = o[0];
+          q = o[1];
+        }
+        if (P == 0) {
+          // rows 0 and N1/2, each its own mirror: row 0 pairs with the zero
+          // row N1; mode 1 zeroes row 0 entirely
+          const T pa = a.mode == 1 ? T(0) : o[0], sa = a.mode == 1 ? T(0) : o[1];
+          x0 = cmul(cmul(ca0, cb), mk(pa, -sa));                 // p = pa, q = r = 0, s = sa
+          x1 = cmul(cmul(ca1, cb), mk(o[2] - o[3], -(o[2] + o[3])));  // p = r = DB, q = s = RB
+          return;
+        }
+        x0 = cmul(cmul(ca0, cb), mk(p - q, -(r + sv)));
+        x1 = cmul(cmul(ca1, cb), mk(r - sv, -(p + q)));
+      };
+#pragma unroll
+      for (int it = 0; it < NI; ++it) {
+        const int k = t + it * NT;
+        if (k <= M / 2) {
+          const V bk = __ldg(tb + k), bm = __ldg(tb + (M - k));
+          V A0, A1, B0, B1;  // X'(line, k), X'(line, M-k)
+          xp(&op[it][0], cconj(bk), A0, A1);
+          xp(&op[it][4], cconj(bm), B0, B1);
+          // partner line of each row (-k1): swap for pairs, self for P == 0
+          const V pA0 = P != 0 ? A1 : A0, pA1 = P != 0 ? A0 : A1;
+          const V pB0 = P != 0 ? B1 : B0, pB1 = P != 0 ? B0 : B1;
+          const V bk2 = cmul(bk, bk), bm2 = cmul(bm, bm);
+          const V wk = cmul(bk2, bk2), wmk = cmul(bm2, bm2);  // W_N2^k = b(k)^4
+          sm[row_nat<T, M>(0, k & (M - 1))] = pack(A0, k == 0 ? B0 : cconj(pB0), wk);
+          sm[row_nat<T, M>(1, k & (M - 1))] = pack(A1, k == 0 ? B1 : cconj(pB1), wk);
+          if (k != 0 && 2 * k != M) {
+            sm[row_nat<T, M>(0, M - k)] = pack(B0, cconj(pA0), wmk);
+            sm[row_nat<T, M>(1, M - k)] = pack(B1, cconj(pA1), wmk);
+          }
         }
       }
     } else {  // RK_INV3
@@ -666,7 +952,7 @@ __global__ void __launch_bounds__(row_threads<T, M, KIND>())
       V* e = reinterpret_cast<V*>(&o);
 #pragma unroll
       for (int k = 0; k < CPV; ++k) e[k] = sm[row_nat<T, M>(line, s_to_m(ci * CPV + k, M))];
-      *reinterpret_cast<V4*>(dst + static_cast<long long>(rows[line]) * M + ci * CPV) = o;
+      *reinterpret_cast<V4*>(dst + static_cast<long long>(irow[line]) * M + ci * CPV) = o;
     }
     return;
   }

@@ -12,6 +12,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <cstdint>
 #include <mutex>
@@ -28,6 +29,7 @@ using namespace sdctb;
 namespace {
 
 thread_local std::string g_last_error;
+unsigned long long* g_trace = nullptr;  // debug: column-kernel phase timestamps (sdct_debug_set_trace)
 
 int fail(int code, const std::string& msg) {
   g_last_error = msg;
@@ -92,6 +94,7 @@ struct sdct_plan_s {
   int nl[2] = {2, 2};   // column-kernel band widths: pass over axis 0, pass over axis 1 (3D)
   TwSet tw_col[2] = {};  // per-stage twiddle tables: axis-0 / axis-1 column FFTs
   TwSet tw_row = {};     // row FFT (length M)
+  void* tw_comb[2] = {nullptr, nullptr};  // split column passes: W_L^k, k < L/2
   // device tables (one allocation)
   void* tables = nullptr;
   void* ta = nullptr;    // dtype quarter-wave tables
@@ -144,10 +147,17 @@ void circle(std::vector<long double>& re, std::vector<long double>& im, long lon
 }
 
 int pick_nl(int esize, int L, int M, long long planes_batch) {
-  // nl_default keeps the tile <= 128 KB; fall back to 2 columns when the
-  // problem is too narrow or offers < 2 CTAs per SM at the default width.
+  if (const char* f = getenv("SDCT_FORCE_NL")) {  // developer override (tools/)
+    const int v = atoi(f);
+    if (v >= 2 && v <= M) return v;
+  }
+  // nl_default: 64 KB tiles with >= 32-B rows (cluster-split for L = 4096).
+  // Narrower bands when the problem is too narrow or offers < 2 CTAs per SM.
+  const int per_band = col_split(L) ? 2 : 1;
   const int nld = nl_default(esize, L);
-  if (nld <= M && (M / nld) * planes_batch >= 2 * 148) return nld;
+  if (nld <= M && (M / nld) * planes_batch * per_band >= 2 * 148) return nld;
+  const int nmin = 16 / esize;  // 32-B rows
+  if (nmin < nld && nmin <= M && (M / nmin) * planes_batch * per_band >= 148) return nmin;
   return 2;
 }
 
@@ -199,6 +209,7 @@ int build_plan(sdct_plan_s* p) {
   size_t off_ta = 0, off_tb = 0, off_tc = 0, off_tu = 0;
   size_t off_gq[3] = {0, 0, 0}, off_gc[3] = {0, 0, 0};
   size_t st_c0[4], st_c1[4], st_r[4];
+  size_t off_comb[2] = {SIZE_MAX, SIZE_MAX};
   if (fast) {
     const int nlast = p->n[r - 1];
     p->M = nlast / 2;
@@ -211,9 +222,16 @@ int build_plan(sdct_plan_s* p) {
       if (f32) stage_tables<float>(blob, L, o);
       else stage_tables<double>(blob, L, o);
     };
-    stages(p->n[0], st_c0);
-    if (r == 3) stages(p->n[1], st_c1);
+    // column FFTs of length L >= 4096 run cluster-split: local tables for L/2
+    stages(col_split(p->n[0]) ? p->n[0] / 2 : p->n[0], st_c0);
+    if (r == 3) stages(col_split(p->n[1]) ? p->n[1] / 2 : p->n[1], st_c1);
     stages(p->M, st_r);
+    for (int ax = 0; ax < (r == 3 ? 2 : 1); ++ax) {
+      if (col_split(p->n[ax])) {
+        circle(re, im, p->n[ax] / 2, 1.0L, p->n[ax]);
+        put(off_comb[ax]);
+      }
+    }
     circle(re, im, p->n[0], 1.0L, 4.0L * p->n[0]);
     put(off_ta);
     circle(re, im, p->n[1], 1.0L, 4.0L * p->n[1]);
@@ -250,6 +268,7 @@ int build_plan(sdct_plan_s* p) {
     tws(st_c0, p->tw_col[0]);
     if (r == 3) tws(st_c1, p->tw_col[1]);
     tws(st_r, p->tw_row);
+    for (int ax = 0; ax < 2; ++ax) p->tw_comb[ax] = off_comb[ax] == SIZE_MAX ? nullptr : base + off_comb[ax];
     p->ta = base + off_ta;
     p->tb = base + off_tb;
     p->tc = r == 3 ? base + off_tc : nullptr;
@@ -316,7 +335,7 @@ bool make_col_map(CUtensorMap* map, bool f32, const void* base, long long inner,
                               static_cast<cuuint64_t>(planes), static_cast<cuuint64_t>(batch)};
   const cuuint64_t strides[3] = {static_cast<cuuint64_t>(row_stride_b), static_cast<cuuint64_t>(plane_stride_b),
                                  static_cast<cuuint64_t>(batch_stride_b)};
-  const cuuint32_t box[4] = {static_cast<cuuint32_t>(2 * nl), static_cast<cuuint32_t>(L < 256 ? L : 256), 1, 1};
+  const cuuint32_t box[4] = {static_cast<cuuint32_t>(2 * nl), static_cast<cuuint32_t>(L < 256 ? L : 256), 1, 1};  // L = rows per box cap
   const cuuint32_t estr[4] = {1, 1, 1, 1};
   const CUresult r = enc(map, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4,
                          const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -324,6 +343,35 @@ bool make_col_map(CUtensorMap* map, bool f32, const void* base, long long inner,
                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
+
+// 5D map over y for the inverse final gather: {inner reals, row class (2,
+// stride = row stride), row pair (rows/2, stride = 2 rows), planes, batch};
+// box {2*nl, 1, min(rows/2, 256), 1, 1}. Even y rows 2p hold pe-images of the
+// first half of the spatial indices, odd rows 2p+1 the second half.
+bool make_class_map(CUtensorMap* map, bool f32, const void* base, long long inner, long long rows,
+                    long long row_stride_b, long long planes, long long plane_stride_b, long long batch,
+                    long long batch_stride_b, int nl) {
+  auto enc = tmap_encoder();
+  if (!enc) return false;
+  const long long pairs = rows / 2;
+  const cuuint64_t dims[5] = {static_cast<cuuint64_t>(inner), 2, static_cast<cuuint64_t>(pairs),
+                              static_cast<cuuint64_t>(planes), static_cast<cuuint64_t>(batch)};
+  const cuuint64_t strides[4] = {static_cast<cuuint64_t>(row_stride_b), static_cast<cuuint64_t>(2 * row_stride_b),
+                                 static_cast<cuuint64_t>(plane_stride_b), static_cast<cuuint64_t>(batch_stride_b)};
+  const cuuint32_t box[5] = {static_cast<cuuint32_t>(2 * nl), 1, static_cast<cuuint32_t>(pairs < 256 ? pairs : 256), 1,
+                             1};
+  const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+  const CUresult r = enc(map, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5,
+                         const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                         CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+// Geometry of one side (input or output) of a column pass, in reals.
+struct Side {
+  long long inner, rows, row_stride, planes, plane_stride, batch_stride;
+};
 
 template <typename T>
 int run_fast(sdct_plan_s* p, int kind, int only_stage, const void* in, void* out, void* ws,
@@ -340,12 +388,24 @@ int run_fast(sdct_plan_s* p, int kind, int only_stage, const void* in, void* out
   bool map_ok = true;
   // column pass over an axis of length L with band width nl; the TMA map
   // describes its input (see make_col_map)
-  auto col = [&](int variant, int L, int nl, int planes, const ColArgs& a, const TwSet& tw, long long inner,
-                 long long rows, long long rs, long long np, long long ps, long long bs) {
+  // column pass over an axis of length L with band width nl; TMA maps for its
+  // input (4D) and output (4D intermediate, or the 5D even/odd-row map of y)
+  auto col = [&](int variant, int L, int nl, int planes, ColArgs a, const TwSet& tw, const Side& in,
+                 const Side& o) {
+    a.trace = g_trace;
     if (want() && e == cudaSuccess && map_ok) {
-      CUtensorMap map;
-      map_ok = make_col_map(&map, f32, a.src, inner, rows, rs * es, np, ps * es, B, bs * es, nl, L);
-      if (map_ok) e = launch_col<T>(variant, L, nl, dim3(M / nl, planes, B), st, map, a, tw);
+      CUtensorMap mi, mo;
+      map_ok = make_col_map(&mi, f32, a.src, in.inner, in.rows, in.row_stride * es, in.planes,
+                            in.plane_stride * es, B, in.batch_stride * es, nl, L);
+      if (map_ok) {
+        if (variant == CV_INV_DST)
+          map_ok = make_class_map(&mo, f32, a.dst, o.inner, o.rows, o.row_stride * es, o.planes, o.plane_stride * es,
+                                  B, o.batch_stride * es, nl);
+        else
+          map_ok = make_col_map(&mo, f32, a.dst, o.inner, o.rows, o.row_stride * es, o.planes, o.plane_stride * es,
+                                B, o.batch_stride * es, nl, L / 2);
+      }
+      if (map_ok) e = launch_col<T>(variant, L, nl, dim3(M / nl, planes, B), st, mi, mo, a, tw);
     }
     ++stage;
   };
@@ -371,7 +431,8 @@ int run_fast(sdct_plan_s* p, int kind, int only_stage, const void* in, void* out
       c.in_batch = item;
       c.out_row = M;
       c.out_batch = inter;
-      col(CV_FWD_SRC, n1, p->nl[0], 1, c, p->tw_col[0], n2, n1, n2, 1, item, item);
+      col(CV_FWD_SRC, n1, p->nl[0], 1, c, p->tw_col[0], Side{n2, n1, n2, 1, item, item},
+          Side{2LL * M, n1, 2LL * M, 1, 2 * inter, 2 * inter});
       ra.src = ws;
       ra.src_batch = inter;
       ra.dst = out;
@@ -395,7 +456,8 @@ int run_fast(sdct_plan_s* p, int kind, int only_stage, const void* in, void* out
       c.scale = 0.25;
       c.sign_row = mode == 1;
       c.sign_col = mode == 2;
-      col(CV_INV_DST, n1, p->nl[0], 1, c, p->tw_col[0], 2LL * M, n1, 2LL * M, 1, 2 * inter, 2 * inter);
+      col(CV_INV_DST, n1, p->nl[0], 1, c, p->tw_col[0], Side{2LL * M, n1, 2LL * M, 1, 2 * inter, 2 * inter},
+          Side{n2, n1, n2, 1, item, item});
     }
   } else {
     const long long inter = static_cast<long long>(n1) * n2 * M;
@@ -413,7 +475,8 @@ int run_fast(sdct_plan_s* p, int kind, int only_stage, const void* in, void* out
       c.out_plane = M;
       c.out_batch = inter;
       c.tma_plane_par = n2;
-      col(CV_FWD_SRC, n1, p->nl[0], n2, c, p->tw_col[0], n3, n1, static_cast<long long>(n2) * n3, n2, n3, item);
+      col(CV_FWD_SRC, n1, p->nl[0], n2, c, p->tw_col[0], Side{n3, n1, static_cast<long long>(n2) * n3, n2, n3, item},
+          Side{2LL * M, n1, 2LL * n2 * M, n2, 2LL * M, 2 * inter});
       // axis 1 (rows j, planes i_slot), in place -> [i_slot][j_slot][s]
       ColArgs d{};
       d.src = ws;
@@ -424,7 +487,8 @@ int run_fast(sdct_plan_s* p, int kind, int only_stage, const void* in, void* out
       d.out_row = M;
       d.out_plane = static_cast<long long>(n2) * M;
       d.out_batch = inter;
-      col(CV_FWD_INTER, n2, p->nl[1], n1, d, p->tw_col[1], 2LL * M, n2, 2LL * M, n1, 2LL * n2 * M, 2 * inter);
+      col(CV_FWD_INTER, n2, p->nl[1], n1, d, p->tw_col[1], Side{2LL * M, n2, 2LL * M, n1, 2LL * n2 * M, 2 * inter},
+          Side{2LL * M, n2, 2LL * M, n1, 2LL * n2 * M, 2 * inter});
       ra.src = ws;
       ra.src_batch = inter;
       ra.dst = out;
@@ -445,8 +509,8 @@ int run_fast(sdct_plan_s* p, int kind, int only_stage, const void* in, void* out
       d.out_row = M;
       d.out_plane = static_cast<long long>(n2) * M;
       d.out_batch = inter;
-      col(CV_INV_INTER, n2, p->nl[1], n1, d, p->tw_col[1], 2LL * M, n2, 2LL * M, n1, 2LL * n2 * M,
-          2 * inter);  // -> [k1][j_slot][s]
+      col(CV_INV_INTER, n2, p->nl[1], n1, d, p->tw_col[1], Side{2LL * M, n2, 2LL * M, n1, 2LL * n2 * M, 2 * inter},
+          Side{2LL * M, n2, 2LL * M, n1, 2LL * n2 * M, 2 * inter});  // -> [k1 srow][j][s]
       ColArgs c{};
       c.src = ws;
       c.dst = out;
@@ -455,11 +519,12 @@ int run_fast(sdct_plan_s* p, int kind, int only_stage, const void* in, void* out
       c.in_batch = inter;
       c.out_row = static_cast<long long>(n2) * n3;
       c.out_plane = n3;
-      c.out_plane_map = 2;  // plane j_slot -> y plane pe(digit_rev(j_slot))
+      c.out_plane_map = 1;  // plane j (natural after the DIT axis-1 pass) -> y plane pe(j)
       c.out_plane_n = n2;
       c.out_batch = item;
       c.scale = 0.125;
-      col(CV_INV_DST, n1, p->nl[0], n2, c, p->tw_col[0], 2LL * M, n1, 2LL * n2 * M, n2, 2LL * M, 2 * inter);
+      col(CV_INV_DST, n1, p->nl[0], n2, c, p->tw_col[0], Side{2LL * M, n1, 2LL * n2 * M, n2, 2LL * M, 2 * inter},
+          Side{n3, n1, static_cast<long long>(n2) * n3, n2, n3, item});
     }
   }
   if (nstages) *nstages = stage;
@@ -618,6 +683,13 @@ void count_idct3(long long n1, long long n2, long long n3, Cnt& c) {
 extern "C" {
 
 int sdct_version(void) { return 10000; }
+
+// Debug hook (not part of the public header): device buffer of 5 u64 per
+// column tile, or NULL to disable. Used by tools/trace_col.py.
+int sdct_debug_set_trace(void* dev_buf) {
+  g_trace = static_cast<unsigned long long*>(dev_buf);
+  return SDCT_OK;
+}
 
 const char* sdct_last_error(void) { return g_last_error.c_str(); }
 

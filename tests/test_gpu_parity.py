@@ -90,7 +90,7 @@ def test_known_answers(golden, cuda):
 
 # ------------------------------------------------------ oracle sweeps ------
 SHAPES_2D = [(2, 8), (4, 16), (8, 8), (16, 8), (8, 64), (64, 8), (128, 256), (256, 128), (512, 512),
-             (2, 4096), (4096, 8), (5, 7), (31, 17), (16, 3), (3, 16), (100, 60), (1, 9), (9, 1)]
+             (2, 4096), (4096, 8), (4096, 16), (4096, 64), (8, 8192), (5, 7), (31, 17), (16, 3), (3, 16), (100, 60), (1, 9), (9, 1)]
 
 
 @pytest.mark.parametrize("dtype", ["float64", "float32"])
@@ -104,7 +104,8 @@ def test_2d_vs_oracle(cuda, dtype, kind):
         assert err <= TOL[dtype], (kind, shape, dtype, err)
 
 
-SHAPES_3D = [(2, 2, 8), (4, 8, 16), (16, 4, 8), (8, 8, 64), (32, 32, 32), (3, 4, 5), (2, 6, 9), (64, 16, 16)]
+SHAPES_3D = [(2, 2, 8), (4, 8, 16), (16, 4, 8), (8, 8, 64), (32, 32, 32), (3, 4, 5), (2, 6, 9), (64, 16, 16),
+             (4096, 2, 8), (2, 4096, 8), (4, 4, 8192)]
 
 
 @pytest.mark.parametrize("dtype", ["float64", "float32"])
