@@ -5,7 +5,10 @@
 // unit (fast_*.cu) so the build compiles them in parallel.
 #pragma once
 
+#include <cstdlib>
+
 #include "kernels_fast.cuh"
+#include "kernels_row2.cuh"
 
 namespace sdctb {
 
@@ -120,15 +123,51 @@ template <typename T, int VAR>
 cudaError_t launch_col_variant(int L, int nl, dim3 grid, cudaStream_t st, const CUtensorMap& map,
                                const CUtensorMap& omap, const ColArgs& a, const TwSet& tw);
 
+template <typename T, int M, bool INV, int MODE>
+cudaError_t launch_row2(dim3 grid, cudaStream_t st, const RowArgs& a, const TwSet& tw) {
+  auto k = row2_kernel<T, M, INV, MODE>;
+  using Geo = Row2Geom<T, M, MODE>;
+  cudaError_t e = prep_smem(k, Geo::SMEM);
+  if (e != cudaSuccess) return e;
+  static int resident = 0;
+  if (!resident) {
+    int dev = 0, sms = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, Geo::CTA, Geo::SMEM);
+    resident = sms * (per > 0 ? per : 1);
+  }
+  const int nitems = static_cast<int>(grid.x * grid.y);
+  // MODE 0: persistent, at most one CTA per two items so both groups work
+  const int want = MODE == 1 ? nitems : (nitems + 1) / 2;
+  const int ctas = want < resident || MODE == 1 ? want : resident;
+  k<<<ctas, Geo::CTA, Geo::SMEM, st>>>(a, tw, nitems);
+  return cudaGetLastError();
+}
+
 template <typename T, int M, int KIND>
 cudaError_t launch_row_one(dim3 grid, cudaStream_t st, const RowArgs& a, const TwSet& tw) {
-  constexpr int G = (KIND == RK_FWD2 || KIND == RK_INV2) ? 2 : 4;
-  auto k = row_kernel<T, M, KIND>;
-  const size_t smem = static_cast<size_t>(G) * M * sizeof(cx_t<T>) + 16;  // + mbarrier
-  cudaError_t e = prep_smem(k, smem);
-  if (e != cudaSuccess) return e;
-  k<<<grid, row_threads<T, M, KIND>(), smem, st>>>(a, tw);
-  return cudaGetLastError();
+  if constexpr (KIND == RK_FWD2 || KIND == RK_INV2) {
+    // measured on B200 at 4096^2 (tools/stage_time.py): the forward kernel
+    // gains from the persistent grouped ring, the inverse (heavier register
+    // use in its preprocess) runs best as one item per CTA
+    static const int forced = [] {
+      const char* f = getenv("SDCT_ROW2_MODE");  // developer override: 0 / 1
+      return f ? atoi(f) : -1;
+    }();
+    const bool one = forced >= 0 ? forced == 1 : KIND == RK_INV2;
+    if (one || row2_mode<T, M>() == 1) return launch_row2<T, M, KIND == RK_INV2, 1>(grid, st, a, tw);
+    if constexpr (row2_mode<T, M>() == 0) return launch_row2<T, M, KIND == RK_INV2, 0>(grid, st, a, tw);
+    return cudaErrorInvalidValue;
+  } else {
+    constexpr int G = 4;
+    auto k = row_kernel<T, M, KIND>;
+    const size_t smem = static_cast<size_t>(G) * M * sizeof(cx_t<T>) + 16;  // + mbarrier
+    cudaError_t e = prep_smem(k, smem);
+    if (e != cudaSuccess) return e;
+    k<<<grid, row_threads<T, M, KIND>(), smem, st>>>(a, tw);
+    return cudaGetLastError();
+  }
 }
 
 template <typename T, int KIND>

@@ -105,10 +105,22 @@ __host__ __device__ inline int rt_digit_rev(int n, int L) {
 // Linearity lets a butterfly swizzle its base once and XOR per-element offsets.
 template <int C0, int C1, int C2, int C3, int SH>
 struct LinSwz {
+  // g as a 16-entry nibble table indexed by the 4 class parities (p0..p3)
+  static constexpr unsigned long long nib_table() {
+    unsigned long long t = 0;
+    for (int p = 0; p < 16; ++p) {
+      const int v = ((p & 1) ? C0 : 0) ^ ((p & 2) ? C1 : 0) ^ ((p & 4) ? C2 : 0) ^ ((p & 8) ? C3 : 0);
+      t |= static_cast<unsigned long long>(v & 15) << (4 * p);
+    }
+    return t;
+  }
   __host__ __device__ __forceinline__ static int g(unsigned h) {
 #if defined(__CUDA_ARCH__)
-    return ((-(int)(__popc(h & 0x11111111u) & 1)) & C0) ^ ((-(int)(__popc(h & 0x22222222u) & 1)) & C1) ^
-           ((-(int)(__popc(h & 0x44444444u) & 1)) & C2) ^ ((-(int)(__popc(h & 0x88888888u) & 1)) & C3);
+    // fold the parities of the bit classes d % 4 into bits 0..3 (smem
+    // indices are < 2^16 elements, so h < 2^16), then one table lookup
+    h ^= h >> 8;
+    h ^= h >> 4;
+    return static_cast<int>((nib_table() >> ((h & 15u) * 4u)) & 15u);
 #else
     int r = 0;
     for (int d = 0; h; ++d, h >>= 1)

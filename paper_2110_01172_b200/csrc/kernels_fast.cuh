@@ -84,6 +84,13 @@ struct RowArgs {
   const void* tb;                  // e^{-i pi k/(2 N2)}, k < N2
   const void* tc;                  // e^{-i pi k/(2 N3)}, k < N3 (3D)
   const void* tu;                  // W_{Nlast}^k, k <= Nlast/2 (packing twiddles)
+  const int* s0;                   // storage row of frequency k1 in the intermediate: rt_srow(k1, n1)
+  const int* s1;                   // 3D: rt_srow(k2, n2)
+  const void* fb;                  // factor tables of tb / tu: e^{-i theta q} = hi[q >> fs] lo[q & (2^fs-1)]
+  const void* fu;
+  int fs;
+  int bad_q;                       // corrupt_twiddle_for_testing: b(bad_q) negated (-1: none)
+  int dev;                         // developer flags (0 in production): bit 0 skips the row FFT math
 };
 
 // ---- small helpers ----------------------------------------------------------
@@ -131,6 +138,10 @@ struct Tile {
   static constexpr int NT = NT0 > tile_max_threads<T>() ? tile_max_threads<T>() : NT0;
   static constexpr int E = TOT / NT;
   static constexpr unsigned MASK = NT >= 32 ? 0xffffffffu : ((1u << NT) - 1u);
+  static constexpr bool TWF = false;  // true: load all R-1 stage twiddles (no derived products)
+  // barrier over the threads sharing this tile (whole CTA here; thread
+  // groups with named barriers in the grouped row kernel)
+  __device__ __forceinline__ static void sync() { __syncthreads(); }
 
   // unswizzled address of element (line, n)
   __host__ __device__ static constexpr int raw(int line, int n) { return LF ? (n << LGNL) + line : line * L + n; }
@@ -201,7 +212,8 @@ struct StageTw {
   static constexpr int R = P::R(s), SPAN = P::span(s), Q = SPAN / R;
   static constexpr int NBF = TL::E / R;
   static constexpr bool ACTIVE = SPAN > R;
-  static constexpr int NLD = ACTIVE ? TwPlan<R>::NLD : 1;
+  static constexpr bool FULL = TL::TWF;
+  static constexpr int NLD = ACTIVE ? (FULL ? R - 1 : TwPlan<R>::NLD) : 1;
   V w[NBF][NLD];
 
   __device__ __forceinline__ void load(const void* twt, int t) {
@@ -212,13 +224,15 @@ struct StageTw {
         int line, j, b;
         TL::template decode<s>(t + i * TL::NT, line, j, b);
 #pragma unroll
-        for (int l = 0; l < NLD; ++l) w[i][l] = __ldg(tw + (TwPlan<R>::k(l) - 1) * Q + j);
+        for (int l = 0; l < NLD; ++l) w[i][l] = __ldg(tw + ((FULL ? l + 1 : TwPlan<R>::k(l)) - 1) * Q + j);
       }
     }
   }
   // W^{jk} for butterfly i
   __device__ __forceinline__ V get(int i, int k) const {
-    if constexpr (R == 16) {
+    if constexpr (FULL) {
+      return w[i][k - 1];
+    } else if constexpr (R == 16) {
       if (k <= 4) return w[i][k - 1];
       if (k == 8) return w[i][4];
       if (k == 12) return w[i][5];
@@ -285,7 +299,7 @@ __device__ __forceinline__ void later_stages(typename TL::V* v, typename TL::V* 
     stage_compute<TL, s, INV>(v, w);
     if constexpr (s + 1 < TL::S) {
       to_smem<TL, s>(v, sm, t);
-      __syncthreads();
+      TL::sync();
     }
     later_stages<TL, INV, s + 1>(v, sm, tw, t);
   }
@@ -306,7 +320,7 @@ __device__ __forceinline__ void stages_until_last(typename TL::V* v, typename TL
     from_smem<TL, s>(v, sm, t);
     stage_compute<TL, s, INV>(v, w);
     to_smem<TL, s>(v, sm, t);
-    __syncthreads();
+    TL::sync();
     stages_until_last<TL, INV, s + 1>(v, sm, tw, t, wl);
   }
 }
@@ -320,7 +334,7 @@ __device__ __forceinline__ void fft_regs(typename TL::V* v, typename TL::V* sm, 
   stage_compute<TL, 0, INV>(v, w0);
   if constexpr (TL::S > 1) {
     to_smem<TL, 0>(v, sm, t);
-    __syncthreads();
+    TL::sync();
     later_stages<TL, INV, 1>(v, sm, tw, t);
   }
 }
@@ -386,7 +400,7 @@ __device__ __forceinline__ void dit_down(typename TL::V* v, typename TL::V* sm, 
     dit_compute<TL, s, INV>(v, w);
     if constexpr (s > 0) {
       to_smem<TL, s>(v, sm, t);
-      __syncthreads();
+      TL::sync();
       dit_down<TL, INV, s - 1>(v, sm, tw, t);
     }
   }
@@ -764,8 +778,8 @@ __global__ void __launch_bounds__(row_threads<T, M, KIND>())
     m1 = P == 0 ? n1 / 2 : n1 - P;
     rows[0] = q1;
     rows[1] = m1;
-    irow[0] = rt_srow(q1, n1);
-    irow[1] = rt_srow(m1, n1);
+    irow[0] = __ldg(a.s0 + q1);
+    irow[1] = __ldg(a.s0 + m1);
   } else {
     const int h2 = n2 / 2 + 1;
     q1 = P / h2;
@@ -778,8 +792,8 @@ __global__ void __launch_bounds__(row_threads<T, M, KIND>())
     rows[1] = m1 * n2 + q2;
     rows[2] = q1 * n2 + m2;
     rows[3] = m1 * n2 + m2;
-    const int p1q = rt_srow(q1, n1), p1m = rt_srow(m1, n1);
-    const int p2q = rt_srow(q2, n2), p2m = rt_srow(m2, n2);
+    const int p1q = __ldg(a.s0 + q1), p1m = __ldg(a.s0 + m1);
+    const int p2q = __ldg(a.s1 + q2), p2m = __ldg(a.s1 + m2);
     irow[0] = p1q * n2 + p2q;
     irow[1] = p1m * n2 + p2q;
     irow[2] = p1q * n2 + p2m;

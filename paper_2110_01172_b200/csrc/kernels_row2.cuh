@@ -1,0 +1,361 @@
+// Persistent row-pair kernel of the 2D pipelines (forward DCT-II and the
+// inverse / IDXST-composite family).
+//
+// Work item = one row pair (k1, N1-k1) of one batch image (k1 = 0 pairs rows
+// 0 and N1/2, each its own mirror). That is the unit the reference's merged
+// postprocess (proj/src/dct2d.cpp:82-115) and merged inverse preprocess
+// (proj/src/dct2d.cpp:161-198) couple, so the row FFT and both of those
+// stages fuse into one pass over the rows.
+//
+// Pipeline (MODE 0, large rows): one persistent CTA per SM with two consumer
+// groups of NT threads (named barriers) and a ring of NBUF shared-memory
+// buffers. The CTA's k-th item (blockIdx.x + k*gridDim.x) is computed by
+// group k % 2 in buffer k % NBUF. A buffer receives its item by two 1D bulk
+// copies (one per row; completion on the buffer's `full` mbarrier), then is
+// that item's FFT exchange buffer; when the item is done the group's leader
+// arrives on the buffer's `empty` mbarrier and refills it with item k+NBUF.
+// So loads run NBUF-1 items ahead, two items' math interleaves on the SM
+// (16 warps), and no grid-wide phase alignment of load/compute/store forms.
+// A consumer waits `empty` (release of item k-NBUF) before `full`, which
+// keeps every mbarrier waiter at most one phase behind (parity-safe).
+// MODE 1 (small rows): one item per CTA, many CTAs per SM.
+//
+//   forward (RK_FWD2): rows srow(k1), srow(N1-k1) of the column pass's
+//     intermediate Z (pair-interleaved complex) -> row FFT -> Hermitian
+//     unpack + merged DCT postprocess -> rows k1, N1-k1 of y.
+//   inverse (RK_INV2): rows k1, N1-k1 of x (real) -> merged inverse
+//     preprocess + inverse packing -> inverse row FFT -> intermediate rows
+//     srow(k1), srow(N1-k1) (natural order, pair-interleaved columns).
+#pragma once
+
+#include "kernels_fast.cuh"
+
+namespace sdctb {
+
+// Row tile of the pair kernel. GROUPS > 1: the tile's threads are one of
+// several groups in the CTA; exchanges synchronise on the group's named
+// barrier (id 1 + group).
+template <typename T, int M, bool FULLTW, int GROUPS>
+struct Row2Tile : Tile<T, M, 2, false> {
+  using Base = Tile<T, M, 2, false>;
+  static constexpr bool TWF = FULLTW;
+  __device__ __forceinline__ static void sync() {
+    if constexpr (GROUPS == 1) {
+      __syncthreads();
+    } else {
+      named_sync(1 + static_cast<int>(threadIdx.x) / Base::NT, Base::NT);
+    }
+  }
+};
+
+// e^{-i theta q} = hi[q >> s] * lo[q & (2^s - 1)]; table = lo (2^s) then hi
+template <typename V>
+__device__ __forceinline__ V fac_lookup(const V* tab, int q, int s) {
+  return cmul(__ldg(tab + (1 << s) + (q >> s)), __ldg(tab + (q & ((1 << s) - 1))));
+}
+// b(M - q) = e^{-i pi/4} conj b(q) for b(q) = e^{-i pi q / (2 N2)}, M = N2 / 2
+template <typename V>
+__device__ __forceinline__ V mirror_b(V b) {
+  using T = decltype(b.x);
+  const T h = T(0.70710678118654752440);  // (h, -h) * (b.x, -b.y)
+  return mk(h * (b.x - b.y), -h * (b.x + b.y));
+}
+
+template <typename T, int M>
+constexpr int row2_mode() {
+  // two groups need two resident buffers
+  return Tile<T, M, 2, false>::NT >= 128 && 2u * (2u * M * sizeof(cx_t<T>)) <= 200u * 1024u ? 0 : 1;
+}
+
+template <typename T, int M, int MODE>
+struct Row2Geom {
+  static constexpr unsigned BUF = 2u * M * sizeof(cx_t<T>);  // one pair: 2 complex rows == 2 real rows of 2M
+  static constexpr int GROUPS = MODE == 0 ? 2 : 1;
+  static constexpr int NBUF = MODE == 1 ? 1
+                              : (200u * 1024u) / BUF >= 4 ? 4
+                              : ((200u * 1024u) / BUF < 2 ? 2 : static_cast<int>((200u * 1024u) / BUF));
+  using TL = Row2Tile<T, M, false, GROUPS>;
+  static constexpr int NT = TL::NT;  // threads per group
+  static constexpr int CTA = NT * GROUPS;
+  static constexpr int MINB = MODE == 1 ? 2 : 1;
+  static constexpr size_t SMEM = static_cast<size_t>(NBUF) * BUF + 16 * NBUF + 16;  // + full/empty mbarriers
+};
+
+template <typename T, int M, bool INV, int MODE>
+__global__ void __launch_bounds__(Row2Geom<T, M, MODE>::CTA, Row2Geom<T, M, MODE>::MINB)
+    row2_kernel(RowArgs a, TwSet tw, int nitems) {
+  using G = Row2Geom<T, M, MODE>;
+  using TL = typename G::TL;
+  using V = cx_t<T>;
+  using V4 = typename Cx<T>::vec4;
+  constexpr int NT = G::NT, NBUF = G::NBUF, GROUPS = G::GROUPS;
+  constexpr int R0 = TL::R0, Q0 = M / R0, NBF0 = TL::E / R0;
+  constexpr int NI = (M / 2) / NT + 1;  // postprocess / preprocess items k in [0, M/2] per thread
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + NBUF * G::BUF);
+  uint64_t* empty = full + NBUF;
+  const int grp = GROUPS == 1 ? 0 : static_cast<int>(threadIdx.x) / NT;
+  const int t = static_cast<int>(threadIdx.x) - grp * NT;  // thread index within the group
+  const int n1 = a.n1, n2 = a.n2, half = n1 / 2;
+
+  auto rows_of = [&](int P, int& q1, int& m1) {
+    q1 = P;
+    m1 = P == 0 ? half : n1 - P;
+  };
+  // thread 0: land item `it` in buffer b
+  auto issue = [&](int it, int b) {
+    const int P = it % half, batch = it / half;
+    int q1, m1;
+    rows_of(P, q1, m1);
+    unsigned char* dst = smem_raw + b * G::BUF;
+    uint64_t* bar = full + b;
+    mbar_expect_tx(bar, G::BUF);
+    if constexpr (!INV) {
+      const V* src = static_cast<const V*>(a.src) + batch * a.src_batch;
+      bulk_load(dst, src + static_cast<long long>(__ldg(a.s0 + q1)) * M, G::BUF / 2, bar);
+      bulk_load(dst + G::BUF / 2, src + static_cast<long long>(__ldg(a.s0 + m1)) * M, G::BUF / 2, bar);
+    } else {
+      const T* src = static_cast<const T*>(a.src) + batch * a.src_batch;
+      bulk_load(dst, src + static_cast<long long>(q1) * n2, G::BUF / 2, bar);
+      bulk_load(dst + G::BUF / 2, src + static_cast<long long>(m1) * n2, G::BUF / 2, bar);
+    }
+  };
+
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int b = 0; b < NBUF; ++b) {
+      mbar_init(full + b, 1);
+      mbar_init(empty + b, 1);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+#pragma unroll 1
+    for (int b = 0; b < NBUF; ++b) {
+      const int it = blockIdx.x + b * gridDim.x;
+      if (it < nitems) issue(it, b);
+    }
+  }
+
+  // hoisted swizzles of the natural-order row layout (linearity: the
+  // per-iteration parts are compile-time XOR offsets)
+  const int sw_t = TL::swz(t);
+  const int sw_nt = TL::swz((NT - t) & (NT - 1));
+
+#pragma unroll 1
+  for (int k = grp;; k += GROUPS) {
+    const int it = static_cast<int>(blockIdx.x) + k * static_cast<int>(gridDim.x);
+    if (it >= nitems) break;
+    const int b = k % NBUF;
+    const uint32_t ph = static_cast<uint32_t>(k / NBUF) & 1u;
+    if (k >= NBUF) mbar_wait(empty + b, ph ^ 1u);  // item k-NBUF released the buffer
+    V* sm = reinterpret_cast<V*>(smem_raw + b * G::BUF);
+    const int P = it % half, batch = it / half;
+    int q1, m1;
+    rows_of(P, q1, m1);
+    V v[TL::E];
+
+    if constexpr (!INV) {
+      // ================= forward: FFT + unpack + merged postprocess ==========
+      StageTw<TL, 0> w0;
+      w0.load(tw.st[0], t);
+      mbar_wait(full + b, ph);
+#pragma unroll
+      for (int i = 0; i < NBF0; ++i) {
+        int line, j, bb;
+        TL::template decode<0>(t + i * NT, line, j, bb);
+#pragma unroll
+        for (int r = 0; r < R0; ++r) {
+          const int n = j + r * Q0;
+          const int s = (r < R0 / 2) ? 2 * n : 2 * M - 1 - 2 * n;  // pair-interleaved column of z(n)
+          v[i * R0 + r] = sm[line * M + s];
+        }
+      }
+      TL::sync();  // landing rows consumed: the buffer becomes the exchange buffer
+      if (!(a.dev & 1)) fft_regs<TL, false>(v, sm, tw, w0, t);
+      TL::sync();
+      last_to_natural<TL>(v, sm, t);
+      TL::sync();
+
+      // merged postprocess (proj/src/dct2d.cpp:93-113) with the Hermitian
+      // unpack folded in: 2X = (A + B) + (-i W^q)(A - B), A = Z(k1, q),
+      // B = conj Z(-k1, -q); the factors 1/2 (unpack) and 1/2 (postprocess)
+      // ride on a(k1)/4.
+      T* y = static_cast<T*>(a.dst) + batch * a.dst_batch;
+      T* r0 = y + static_cast<long long>(q1) * n2;
+      T* r1 = y + static_cast<long long>(m1) * n2;
+      const V* fb = static_cast<const V*>(a.fb);
+      const V* fu = static_cast<const V*>(a.fu);
+      const V av0 = __ldg(static_cast<const V*>(a.ta) + q1), av1 = __ldg(static_cast<const V*>(a.ta) + m1);
+      const V a40 = mk(av0.x * T(0.25), av0.y * T(0.25)), a41 = mk(av1.x * T(0.25), av1.y * T(0.25));
+      // X' = S + w' D with S = A + B, D = A - B, w' = -i w
+      auto unpack2 = [](V A, V Bc, V w) {  // Bc = conj(B) as stored: B = (Bc.x, -Bc.y)
+        const T sx = A.x + Bc.x, sy = A.y - Bc.y;
+        const T dx = A.x - Bc.x, dy = A.y + Bc.y;
+        // w' = (w.y, -w.x): w' D = (w.y dx + w.x dy, w.y dy - w.x dx)
+        return mk(fma(w.y, dx, fma(w.x, dy, sx)), fma(w.y, dy, fma(-w.x, dx, sy)));
+      };
+      auto item = [&](int q, V Z0a, V Z0b, V Z1a, V Z1b, V bq, V w) {
+        // Z0a = Z(k1, q), Z0b = Z(k1, -q), Z1a = Z(k1', q), Z1b = Z(k1', -q);
+        // bq = b(q), w = W_N2^q
+        const bool deg2k = (q == 0) || (q == M);
+        if (P != 0) {
+          const V X1 = unpack2(Z0a, Z1b, w);  // 2 X(k1, q)
+          const V X2 = unpack2(Z1a, Z0b, w);  // 2 X(-k1, q)
+          const V ax1 = cmul(a40, X1), ax2 = cmulc(X2, a40);
+          const V sp = cadd(ax1, ax2), tp = csub(ax1, ax2);
+          // sv = b sp, tv = b tp; outputs sv.x, -tv.y, -sv.y, -tv.x
+          r0[q] = fma(bq.x, sp.x, -bq.y * sp.y);
+          r1[q] = -fma(bq.x, tp.y, bq.y * tp.x);
+          if (!deg2k) {
+            r0[n2 - q] = -fma(bq.x, sp.y, bq.y * sp.x);
+            r1[n2 - q] = fma(-bq.x, tp.x, bq.y * tp.y);
+          }
+        } else {
+          // rows 0 and N1/2 are their own mirrors (deg1: X2 = X1), so
+          // s = b (a + conj a) X = 2 Re(a4) b X'
+          const V X0 = unpack2(Z0a, Z0b, w);
+          const V X1 = unpack2(Z1a, Z1b, w);
+          const T c0 = T(2) * a40.x, c1 = T(2) * a41.x;
+          const V bx0 = cmul(bq, X0), bx1 = cmul(bq, X1);
+          r0[q] = c0 * bx0.x;
+          r1[q] = c1 * bx1.x;
+          if (!deg2k) {
+            r0[n2 - q] = -c0 * bx0.y;
+            r1[n2 - q] = -c1 * bx1.y;
+          }
+        }
+      };
+#pragma unroll
+      for (int i = 0; i < NI; ++i) {
+        const int k2 = t + i * NT;
+        if (k2 <= M / 2) {
+          // natural-order slots of k2 and kb = (M - k2) mod M in both lines
+          const int sa = sw_t ^ TL::swzc(i * NT);
+          const int sb = t ? (sw_nt ^ TL::swzc(M - (i + 1) * NT)) : TL::swzc((M - i * NT) & (M - 1));
+          const V Z0a = sm[sa], Z0b = sm[sb];
+          const V Z1a = sm[sa ^ TL::swzc(M)], Z1b = sm[sb ^ TL::swzc(M)];
+          // b(q), W^q from two small factor tables; the mirror q' = M - q
+          // needs none: b(M-q) = e^{-i pi/4} conj b(q), W^{M-q} = -conj W^q
+          const V bq = fac_lookup(fb, k2, a.fs), w = fac_lookup(fu, k2, a.fs);
+          const V bm = mirror_b(bq);
+          item(k2, Z0a, Z0b, Z1a, Z1b, k2 == a.bad_q ? mk(-bq.x, -bq.y) : bq, w);
+          if (2 * k2 != M) item(M - k2, Z0b, Z0a, Z1b, Z1a, M - k2 == a.bad_q ? mk(-bm.x, -bm.y) : bm, mk(-w.x, w.y));
+        }
+      }
+    } else {
+      // ============ inverse: merged preprocess + packing + inverse FFT =======
+      // buffer = rows q1 (A) and m1 (B) of x, 2M reals each
+      const T* rowA = reinterpret_cast<const T*>(sm);
+      const T* rowB = rowA + 2 * M;
+      mbar_wait(full + b, ph);
+      // operands for n2 in {k, M-k}: D = x(n2), R = x(N2-n2) (x(N2) := 0) of
+      // both rows; mode 2 (IDXST along axis 1) reads x(N2-n2) for D and x(n2)
+      // for R with x(0) := 0 (proj/src/dct2d.cpp:169-180)
+      T op[NI][8];
+#pragma unroll
+      for (int i = 0; i < NI; ++i) {
+        const int kk = t + i * NT;
+        if (kk <= M / 2) {
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const int nn = u ? M - kk : kk;
+            const bool z = nn == 0;
+            const int pd = a.mode == 2 ? n2 - nn : nn;
+            const int pr = a.mode == 2 ? nn : n2 - nn;
+            const bool zd = a.mode == 2 && z;
+            op[i][4 * u + 0] = zd ? T(0) : rowA[pd & (n2 - 1)];
+            op[i][4 * u + 1] = z ? T(0) : rowA[pr & (n2 - 1)];
+            op[i][4 * u + 2] = zd ? T(0) : rowB[pd & (n2 - 1)];
+            op[i][4 * u + 3] = z ? T(0) : rowB[pr & (n2 - 1)];
+          }
+        }
+      }
+      const V* ta = static_cast<const V*>(a.ta);
+      const V* fb = static_cast<const V*>(a.fb);
+      const V* fu = static_cast<const V*>(a.fu);
+      const V ca0 = cconj(__ldg(ta + q1)), ca1 = cconj(__ldg(ta + m1));
+      TL::sync();  // operands read: the buffer becomes the packed spectrum
+      // X'(line, n2) from o = {DA, RA, DB, RB} (proj/src/dct2d.cpp:182-195)
+      auto xp = [&](const T* o, V cb, V& x0, V& x1) {
+        const V c0 = cmul(ca0, cb), c1 = cmul(ca1, cb);
+        if (P == 0) {
+          // rows 0 and N1/2, each its own mirror: row 0 pairs with the zero
+          // row N1; mode 1 zeroes row 0 entirely
+          const T pa = a.mode == 1 ? T(0) : o[0], sa = a.mode == 1 ? T(0) : o[1];
+          x0 = cmul(c0, mk(pa, -sa));
+          x1 = cmul(c1, mk(o[2] - o[3], -(o[2] + o[3])));
+          return;
+        }
+        T p = o[0], sv = o[1], r = o[2], q = o[3];
+        if (a.mode == 1) {  // IDXST along axis 0 swaps the row roles
+          p = o[2];
+          sv = o[3];
+          r = o[0];
+          q = o[1];
+        }
+        x0 = cmul(c0, mk(p - q, -(r + sv)));
+        x1 = cmul(c1, mk(r - sv, -(p + q)));
+      };
+      const int sw0 = sw_t;
+#pragma unroll
+      for (int i = 0; i < NI; ++i) {
+        const int kk = t + i * NT;
+        if (kk <= M / 2) {
+          V A0, A1, B0, B1;  // X'(line, k), X'(line, M-k)
+          V bk = fac_lookup(fb, kk, a.fs), bm = mirror_b(bk);
+          if (kk == a.bad_q) bk = mk(-bk.x, -bk.y);
+          if (M - kk == a.bad_q) bm = mk(-bm.x, -bm.y);
+          xp(&op[i][0], cconj(bk), A0, A1);
+          xp(&op[i][4], cconj(bm), B0, B1);
+          // partner line of each row (-k1): swap for pairs, self for P == 0
+          const V pA0 = P != 0 ? A1 : A0, pA1 = P != 0 ? A0 : A1;
+          const V pB0 = P != 0 ? B1 : B0, pB1 = P != 0 ? B0 : B1;
+          const V wk = fac_lookup(fu, kk, a.fs), wmk = mk(-wk.x, wk.y);  // W_N2^k, W_N2^{M-k}
+          const int sa = sw0 ^ TL::swzc(i * NT);  // natural slot of k (mod M) in line 0
+          const int sa_ = kk == 0 ? 0 : sa;        // k == 0 -> slot 0 (kk = 0 only at t = 0, i = 0)
+          sm[sa_] = pack(A0, kk == 0 ? B0 : cconj(pB0), wk);
+          sm[sa_ ^ TL::swzc(M)] = pack(A1, kk == 0 ? B1 : cconj(pB1), wk);
+          if (kk != 0 && 2 * kk != M) {
+            const int sb = t ? (sw_nt ^ TL::swzc(M - (i + 1) * NT)) : TL::swzc((M - i * NT) & (M - 1));  // slot of M - k
+            sm[sb] = pack(B0, cconj(pA0), wmk);
+            sm[sb ^ TL::swzc(M)] = pack(B1, cconj(pA1), wmk);
+          }
+        }
+      }
+      StageTw<TL, 0> w0;
+      w0.load(tw.st[0], t);
+      TL::sync();
+      from_smem<TL, 0>(v, sm, t);
+      if (!(a.dev & 1)) fft_regs<TL, true>(v, sm, tw, w0, t);
+      TL::sync();
+      last_to_natural<TL>(v, sm, t);
+      TL::sync();
+      // store rows (natural row order) in pair-interleaved column order
+      V* dst = static_cast<V*>(a.dst) + batch * a.dst_batch;
+      constexpr int CPV = 16 / sizeof(V);
+      constexpr int VPR = M / CPV;
+      const int irow[2] = {__ldg(a.s0 + q1), __ldg(a.s0 + m1)};
+#pragma unroll 4
+      for (int w = t; w < 2 * VPR; w += NT) {
+        const int line = w / VPR, ci = w - line * VPR;
+        V4 o;
+        V* e = reinterpret_cast<V*>(&o);
+#pragma unroll
+        for (int c = 0; c < CPV; ++c) e[c] = sm[row_nat<T, M>(line, s_to_m(ci * CPV + c, M))];
+        *reinterpret_cast<V4*>(dst + static_cast<long long>(irow[line]) * M + ci * CPV) = o;
+      }
+    }
+    TL::sync();  // every read of buffer b by this group is done
+    if (t == 0) {
+      mbar_arrive(empty + b);
+      const int nxt = it + NBUF * static_cast<int>(gridDim.x);
+      if (nxt < nitems) {
+        fence_async_smem();  // generic-proxy smem accesses before the async refill
+        issue(nxt, b);
+      }
+    }
+  }
+}
+
+}  // namespace sdctb

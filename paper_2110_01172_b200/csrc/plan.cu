@@ -101,6 +101,11 @@ struct sdct_plan_s {
   void* tb = nullptr;
   void* tc = nullptr;
   void* tu = nullptr;    // dtype: W_{Nlast}^k, k <= M
+  int* srow[2] = {nullptr, nullptr};
+  void* fb = nullptr;    // dtype factor tables of tb and tu over q <= M (see RowArgs::fb)
+  void* fu = nullptr;
+  int fs = 0;
+  int bad_q = -1;        // corrupt_twiddle_for_testing index (row kernels), -1 = none  // intermediate storage row of frequency k: axis 0, axis 1 (3D)
   double2* gq[3] = {nullptr, nullptr, nullptr};  // generic fp64 quarter-wave tables
   double2* gc[3] = {nullptr, nullptr, nullptr};  // generic fp64 circle tables
   size_t b_offset_fast = 0, b_offset_gen = 0;    // element offsets of table b (corrupt hook)
@@ -210,6 +215,8 @@ int build_plan(sdct_plan_s* p) {
   size_t off_gq[3] = {0, 0, 0}, off_gc[3] = {0, 0, 0};
   size_t st_c0[4], st_c1[4], st_r[4];
   size_t off_comb[2] = {SIZE_MAX, SIZE_MAX};
+  size_t off_srow[2] = {SIZE_MAX, SIZE_MAX};
+  size_t off_fb = 0, off_fu = 0;
   if (fast) {
     const int nlast = p->n[r - 1];
     p->M = nlast / 2;
@@ -242,6 +249,35 @@ int build_plan(sdct_plan_s* p) {
     }
     circle(re, im, p->M + 1, 1.0L, nlast);
     put(off_tu);
+    {
+      // factor tables over q in [0, M]: lo = e^{-i th l}, l < 2^fs; hi = e^{-i th 2^fs h}
+      int lgq = 0;
+      while ((1 << lgq) <= p->M) ++lgq;  // q < 2^lgq
+      p->fs = (lgq + 1) / 2;
+      const int nlo = 1 << p->fs, nhi = (p->M >> p->fs) + 1;
+      const long double pi = 3.141592653589793238462643383279502884L;
+      for (int which = 0; which < 2; ++which) {
+        // b: theta = pi / (2 N2); u: theta = 2 pi / N2 (N2 = the last extent)
+        const long double th = which == 0 ? pi / (2.0L * nlast) : 2.0L * pi / nlast;
+        re.resize(nlo + nhi);
+        im.resize(nlo + nhi);
+        for (int l = 0; l < nlo; ++l) {
+          re[l] = cosl(-th * l);
+          im[l] = sinl(-th * l);
+        }
+        for (int h = 0; h < nhi; ++h) {
+          re[nlo + h] = cosl(-th * static_cast<long double>(h << p->fs));
+          im[nlo + h] = sinl(-th * static_cast<long double>(h << p->fs));
+        }
+        put(which == 0 ? off_fb : off_fu);
+      }
+    }
+    for (int ax = 0; ax < (r == 3 ? 2 : 1); ++ax) {
+      off_srow[ax] = (blob.size() + 255) & ~size_t(255);
+      blob.resize(off_srow[ax] + p->n[ax] * sizeof(int));
+      int* q = reinterpret_cast<int*>(blob.data() + off_srow[ax]);
+      for (int k = 0; k < p->n[ax]; ++k) q[k] = rt_srow(k, p->n[ax]);
+    }
     const long long pb0 = (r == 2 ? 1 : p->n[1]) * p->batch;
     p->nl[0] = pick_nl(static_cast<int>(p->elem()), p->n[0], p->M, pb0);
     if (r == 3) p->nl[1] = pick_nl(static_cast<int>(p->elem()), p->n[1], p->M, static_cast<long long>(p->n[0]) * p->batch);
@@ -273,6 +309,10 @@ int build_plan(sdct_plan_s* p) {
     p->tb = base + off_tb;
     p->tc = r == 3 ? base + off_tc : nullptr;
     p->tu = base + off_tu;
+    p->fb = base + off_fb;
+    p->fu = base + off_fu;
+    for (int ax = 0; ax < 2; ++ax)
+      p->srow[ax] = off_srow[ax] == SIZE_MAX ? nullptr : reinterpret_cast<int*>(base + off_srow[ax]);
     p->b_offset_fast = off_tb;
   }
   for (int a = 0; a < r; ++a) {
@@ -421,6 +461,19 @@ int run_fast(sdct_plan_s* p, int kind, int only_stage, const void* in, void* out
   ra.tb = p->tb;
   ra.tc = p->tc;
   ra.tu = p->tu;
+  ra.s0 = p->srow[0];
+  ra.s1 = p->srow[1];
+  ra.fb = p->fb;
+  ra.fu = p->fu;
+  ra.fs = p->fs;
+  ra.bad_q = p->bad_q;
+  {
+    static const int dev = [] {
+      const char* f = getenv("SDCT_DEV_FLAGS");  // developer experiments only (tools/)
+      return f ? atoi(f) : 0;
+    }();
+    ra.dev = dev;
+  }
   if (p->rank == 2) {
     const long long inter = static_cast<long long>(n1) * M;
     if (kind == SDCT_DCT_2D) {
@@ -797,6 +850,9 @@ int sdct_plan_corrupt_twiddle(sdct_plan_t p, int64_t index) {
   };
   int rc = flip(p->b_offset_gen, false);
   if (rc == SDCT_OK && p->fast) rc = flip(p->b_offset_fast, p->dtype == SDCT_F32);
+  // the 2D row kernels form b(q) from factor tables: they negate b at the
+  // corrupted index instead (same effect as the negated table entry)
+  if (rc == SDCT_OK) p->bad_q = p->bad_q < 0 ? static_cast<int>(index) : p->bad_q;
   return rc;
 }
 
