@@ -1,23 +1,30 @@
 #!/usr/bin/env python
-"""Benchmark of the hot path: 2D DCT -> IDCT round trip at 4096^2 fp64
-(BASELINE.json configs[1], the configuration the headline metric is quoted on).
+"""Benchmark of the hot path (BASELINE.json metric: 2D DCT/IDCT ms and
+effective GB/s vs the HBM roofline, with the reference CPU path alongside).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--size 4096] [--dtype float64|float32]
+                    [--workload c2|c1|c3|c4|c5] [--dtype float64|float32]
 
-One step = dct_2d then idct_2d of one 4096x4096 fp64 image (inputs resident
-in HBM for `value`). Algorithmic bytes per transform = 2 * numel * sizeof(T)
-(read the input once, write the output once), so a step moves
-4 * numel * sizeof(T) algorithmic bytes. Working set per step (input, DCT
-output, IDCT output, workspace = 4 x 134 MB) is > 4x the 126 MB L2, so no step
-re-reads the previous step's data from L2.
+Default workload c2 = BASELINE configs[1], the configuration the headline is
+quoted on: one step = dct_2d then idct_2d of one 4096x4096 fp64 image. The
+other BASELINE configs are selectable (c1 1024^2 fp64 DCT, c3 2048^2 IDXST/IDCT
+composites, c4 256^3 fp32 3D DCT, c5 batched 512 x 2048^2 fp32 DCT sharded
+over the ranks).
 
-N > 1 (torchrun): every rank transforms its own image (independent objects,
-no data-path collective) -> weak scaling; value = all ranks' bytes / max-over-
-ranks time. Rank 0 prints one JSON line.
+Algorithmic bytes per transform = 2 * numel * sizeof(T) (read the input once,
+write the output once). `value` = those bytes for all ranks /
+max-over-ranks device time, inputs resident in HBM. Workloads whose working
+set fits in the 126 MB L2 rotate over enough input/output sets that no step
+re-reads L2-resident data (said in config.l2).
+
+N > 1 (torchrun): c1-c4 = every rank transforms its own images (independent
+objects, no data-path collective, weak scaling); c5 = the fixed 512-image
+batch is split into contiguous shards (strong scaling). Rank 0 prints one JSON
+line.
 
 --impl reference: the unmodified reference CPU library (oracle/_ref, built from
-/root/reference by oracle/Makefile) on this host's cores, same metric/unit.
+/root/reference by oracle/Makefile; the C restatement when absent) on this
+host's cores, same workload, metric and unit (fp64: the reference is fp64-only).
 """
 from __future__ import annotations
 
@@ -114,41 +121,94 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
-def cpu_reference_rate(n: int, budget_s: float, max_steps: int | None = None):
-    """Round trips of the reference (oracle/_ref, all host threads) on an n x n
-    fp64 image; returns (GB/s, seconds per round trip, round trips timed, kind)."""
+# Workloads (BASELINE.json configs). mode "chain": kinds applied in sequence
+# to the step's input; "fan": each kind applied to the same input.
+WORKLOADS = {
+    "c2": dict(dims=(4096, 4096), kinds=["dct_2d", "idct_2d"], mode="chain", dtype="float64", batch=1,
+               desc="2D DCT-II -> IDCT round trip 4096x4096 {dt} per rank (BASELINE configs[1])"),
+    "c1": dict(dims=(1024, 1024), kinds=["dct_2d"], mode="chain", dtype="float64", batch=1,
+               desc="2D DCT-II 1024x1024 {dt} per rank (BASELINE configs[0])"),
+    "c3": dict(dims=(2048, 2048), kinds=["idct_idxst_2d", "idxst_idct_2d"], mode="fan", dtype="float64", batch=1,
+               desc="IDCT/IDXST + IDXST/IDCT composites 2048x2048 {dt} per rank (BASELINE configs[2])"),
+    "c4": dict(dims=(256, 256, 256), kinds=["dct_3d"], mode="chain", dtype="float32", batch=1,
+               desc="3D DCT-II 256^3 {dt} per rank (BASELINE configs[3])"),
+    "c5": dict(dims=(2048, 2048), kinds=["dct_2d"], mode="chain", dtype="float32", batch=512, sharded=True,
+               desc="batched DCT-II 512 x 2048x2048 {dt}, batch sharded over ranks (BASELINE configs[4])"),
+}
+L2_BYTES = 126 * 1024 * 1024
+
+
+def _numel(dims):
+    n = 1
+    for d in dims:
+        n *= d
+    return n
+
+
+def _shard(w, world, rank):
+    """Contiguous batch shard of this rank (c5) or the per-rank batch."""
+    if not w.get("sharded"):
+        return 0, w["batch"]
+    from paper_2110_01172_b200.shard import shard_range
+
+    lo, hi = shard_range(w["batch"], world, rank)
+    return lo, hi - lo
+
+
+# ---------------------------------------------------------------------------
+def cpu_reference_rate(w, budget_s: float, max_steps: int | None = None):
+    """The reference CPU path (oracle/_ref, all host threads; the C
+    restatement when the reference is not built) on a bounded sample of the
+    workload: whole steps, or for batched c5 a few images. Returns (GB/s of
+    the workload's algorithmic bytes, seconds per sampled unit, units timed,
+    kind, sample description)."""
     import numpy as np
 
     import oracle
 
-    x = np.random.default_rng(2).uniform(-1.0, 1.0, size=(n, n))
+    dims, kinds = w["dims"], w["kinds"]
+    x = np.random.default_rng(2).uniform(-1.0, 1.0, size=dims)
     if oracle.ref_available():
         kind = "reference"
-        fwd = lambda a: oracle.ref.run("dct_2d", a, threads=0)  # noqa: E731
-        inv = lambda a: oracle.ref.run("idct_2d", a, threads=0)  # noqa: E731
+        fns = [lambda a, k=k: oracle.ref.run(k, a, threads=0) for k in kinds]  # noqa: E731
     else:
         kind = "port"
-        fwd, inv = oracle.port.dct_2d, oracle.port.idct_2d
+        fns = [getattr(oracle.port, k) for k in kinds]
+
+    def unit():
+        if w["mode"] == "chain":
+            y = x
+            for f in fns:
+                y = f(y)
+        else:
+            for f in fns:
+                f(x)
+
     t0 = time.perf_counter()
-    inv(fwd(x))  # warm-up round trip (also sizes the sample)
-    t_rt = time.perf_counter() - t0
-    steps = max(1, int(budget_s / max(t_rt, 1e-3)))
+    unit()  # warm-up (also sizes the sample)
+    t_u = time.perf_counter() - t0
+    n = max(1, int(budget_s / max(t_u, 1e-3)))
     if max_steps is not None:
-        steps = min(steps, max_steps)
+        n = min(n, max_steps)
     t0 = time.perf_counter()
-    for _ in range(steps):
-        inv(fwd(x))
-    dt = (time.perf_counter() - t0) / steps
-    bytes_rt = 4.0 * n * n * 8
-    return bytes_rt / dt / 1e9, dt, steps, kind
+    for _ in range(n):
+        unit()
+    dt = (time.perf_counter() - t0) / n
+    bytes_unit = 2.0 * _numel(dims) * 8 * len(kinds)
+    what = " then ".join(kinds) if w["mode"] == "chain" else " + ".join(kinds)
+    sample = (f"{n} x ({what}) of one {'x'.join(map(str, dims))} fp64 image on the host, prebuilt plans, "
+              f"threads=0 ({dt * 1e3:.1f} ms each)")
+    if w.get("sharded"):
+        sample += f"; the {w['batch']}-image batch is {w['batch']} such units (rate is per byte, batch-independent)"
+    return bytes_unit / dt / 1e9, dt, n, kind, sample
 
 
 # ---------------------------------------------------------------------------
-def cufft_times(x, n, stream, reps):
-    """cuFFT R2C and C2R (D2Z / Z2D for fp64) of the same n x n shape, called
-    directly through libcufft (ctypes) so no framework copies or plan-cache
-    effects are timed. Library baseline only (north_star: 'cuFFT R2C on the
-    same shape ... reported alongside'). Returns (r2c_ms, c2r_ms)."""
+def cufft_times(x, dims, batch, stream, reps):
+    """cuFFT R2C and C2R (D2Z / Z2D for fp64) of the same shape and batch,
+    called directly through libcufft (ctypes; cufftPlanMany) so no framework
+    copies or plan-cache effects are timed. Library baseline only (north_star:
+    'cuFFT R2C on the same shape ... reported alongside'). Returns ms."""
     import ctypes
 
     import torch
@@ -164,26 +224,29 @@ def cufft_times(x, n, stream, reps):
         raise RuntimeError("libcufft not loadable")
     f64 = x.dtype == torch.float64
     fwd_type, inv_type = (0x6A, 0x6C) if f64 else (0x2A, 0x2C)
-    spec = torch.empty((n, n // 2 + 1), dtype=torch.complex128 if f64 else torch.complex64, device=x.device)
+    half = list(dims[:-1]) + [dims[-1] // 2 + 1]
+    spec = torch.empty([batch] + half, dtype=torch.complex128 if f64 else torch.complex64, device=x.device)
     out = torch.empty_like(x)
+    nn = (ctypes.c_int * len(dims))(*dims)
     pf, pi = ctypes.c_int(0), ctypes.c_int(0)
-    assert lib.cufftPlan2d(ctypes.byref(pf), n, n, fwd_type) == 0
-    assert lib.cufftPlan2d(ctypes.byref(pi), n, n, inv_type) == 0
-    sp = ctypes.c_void_p(stream.cuda_stream)
-    lib.cufftSetStream(pf, sp)
-    lib.cufftSetStream(pi, sp)
+    for pl, ty in ((pf, fwd_type), (pi, inv_type)):
+        rc = lib.cufftPlanMany(ctypes.byref(pl), len(dims), nn, None, 1, 0, None, 1, 0, ty, batch)
+        if rc != 0:
+            raise RuntimeError(f"cufftPlanMany failed ({rc})")
+        lib.cufftSetStream(pl, ctypes.c_void_p(stream.cuda_stream))
     exf = lib.cufftExecD2Z if f64 else lib.cufftExecR2C
     exi = lib.cufftExecZ2D if f64 else lib.cufftExecC2R
     xi, so, oo = ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(spec.data_ptr()), ctypes.c_void_p(out.data_ptr())
     res = []
-    for ex, a_, b_ in ((exf, xi, so), (exi, so, oo)):
+    for ex, pl, a_, b_ in ((exf, pf, xi, so), (exi, pi, so, oo)):
         for _ in range(3):
-            assert ex(pf if ex is exf else pi, a_, b_) == 0
+            if ex(pl, a_, b_) != 0:
+                raise RuntimeError("cufftExec failed")
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for _ in range(reps):
-            ex(pf if ex is exf else pi, a_, b_)
+            ex(pl, a_, b_)
         e1.record(stream)
         torch.cuda.synchronize()
         res.append(e0.elapsed_time(e1) / reps)
@@ -192,24 +255,23 @@ def cufft_times(x, n, stream, reps):
     return res[0], res[1]
 
 
-
-def run_reference(args, rank: int):
+# ---------------------------------------------------------------------------
+def run_reference(args, rank: int, world: int):
     if rank != 0:
         return
-    n = args.size
+    w = WORKLOADS[args.workload]
     # bound the whole --steps K --warmup W run to a few minutes of CPU time
-    rate, dt, steps, kind = cpu_reference_rate(n, budget_s=150.0, max_steps=args.steps)
+    rate, dt, steps, kind, sample = cpu_reference_rate(w, budget_s=150.0, max_steps=args.steps)
     cores, quota = _cores()
     line = {
         "impl": "reference", "metric": METRIC, "value": round(rate, 4), "unit": UNIT,
         "n_gpus": args.gpus, "steps": steps, "warmup": 1, "ms_per_step": round(dt * 1e3, 3),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic uniform(-1,1)",
-        "config": {"workload": f"2D DCT-II -> IDCT round trip {n}x{n} fp64 (BASELINE configs[1])",
+        "higher_is_better": True, "scaling": "strong" if w.get("sharded") else "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic uniform(-1,1)",
+        "config": {"workload": w["desc"].format(dt="fp64 (reference is fp64-only)"),
                    "requested_steps": args.steps, "requested_warmup": args.warmup},
         "cpu_baseline": {"value": round(rate, 4), "unit": UNIT, "cores": cores, "kind": kind,
-                         "cgroup_cpu_quota": quota,
-                         "sample": f"{steps} round trips of dct_2d+idct_2d {n}x{n} fp64, prebuilt plans, threads=0"},
+                         "cgroup_cpu_quota": quota, "sample": sample},
         "e2e": {"value": round(rate, 4), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -223,47 +285,82 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     import paper_2110_01172_b200 as sd
     from paper_2110_01172_b200 import _sdct
 
+    w = WORKLOADS[args.workload]
+    dtype = args.dtype or w["dtype"]
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    n = args.size
-    dt = torch.float64 if args.dtype == "float64" else torch.float32
+    dims = tuple(w["dims"])
+    dt = torch.float64 if dtype == "float64" else torch.float32
     esz = 8 if dt == torch.float64 else 4
-    numel = n * n
-    bytes_transform = 2.0 * numel * esz
-    bytes_step = 2 * bytes_transform
+    lo, B = _shard(w, world, rank)
+    numel = _numel(dims)
+    item_bytes = numel * esz
+    kinds = [getattr(_sdct, k.upper()) for k in w["kinds"]]
+    bytes_transform = 2.0 * numel * esz * B  # one kind over this rank's batch
+    bytes_step = bytes_transform * len(kinds)  # this rank
+    # whole-job bytes per step: every rank's own images, or the one sharded batch
+    job_bytes_step = world * bytes_step if not w.get("sharded") else 2.0 * numel * esz * w["batch"] * len(kinds)
 
+    # rotation sets so that no step reads L2-resident inputs of the previous one
+    set_bytes = item_bytes * B * (2 if w["mode"] == "fan" else len(kinds) + 1)
+    rot = 1 if set_bytes >= 2 * L2_BYTES else -(-2 * L2_BYTES // set_bytes) + 1
     g = torch.Generator(device="cpu").manual_seed(2 + rank)
-    x_host = (torch.rand((n, n), generator=g, dtype=torch.float64) * 2 - 1).to(dt)
-    x = x_host.to(dev)
+    x_host = (torch.rand((B,) + dims, generator=g, dtype=torch.float64) * 2 - 1).to(dt) if B <= 4 else None
+    xs = []
+    for r in range(rot):
+        if x_host is not None:
+            xs.append((x_host if r == 0 else torch.roll(x_host, r, dims=-1)).to(dev))
+        else:  # large batches: generate on the device (no multi-GB host copy)
+            gd = torch.Generator(device=dev).manual_seed(5 + rank + 1000 * r)
+            xs.append((torch.rand((B,) + dims, generator=gd, dtype=torch.float64, device=dev) * 2 - 1).to(dt))
+    nbuf = len(kinds) if w["mode"] == "chain" else len(kinds)
+    outs = [[torch.empty_like(xs[0]) for _ in range(nbuf)] for _ in range(rot)]
     stream = torch.cuda.current_stream(dev)
-
-    plan = sd.plan_for((n, n), 1, args.dtype, local_rank)
-    ws = torch.empty(plan.workspace_bytes, dtype=torch.uint8, device=dev)
-    y = torch.empty_like(x)
-    z = torch.empty_like(x)
     s = stream.cuda_stream
+    plan = sd.plan_for(dims, B, dtype, local_rank)
+    ws = torch.empty(plan.workspace_bytes, dtype=torch.uint8, device=dev)
 
-    def step():
-        plan.run(_sdct.DCT_2D, x.data_ptr(), y.data_ptr(), s, ws.data_ptr())
-        plan.run(_sdct.IDCT_2D, y.data_ptr(), z.data_ptr(), s, ws.data_ptr())
+    def step(i):
+        r = i % rot
+        src = xs[r]
+        for j, k in enumerate(kinds):
+            dst = outs[r][j]
+            plan.run(k, src.data_ptr(), dst.data_ptr(), s, ws.data_ptr())
+            if w["mode"] == "chain":
+                src = dst
 
     def barrier():
         if world > 1:
             dist.barrier()
 
-    # parity spot check of this rank's own data (round trip = N1 N2 / 4 x)
-    step()
+    # parity spot check of this rank's own data
+    step(0)
     torch.cuda.synchronize()
-    rt_err = float(((z / (numel / 4.0) - x).norm() / x.norm()).item())
+    parity = {}
+    if w["kinds"] == ["dct_2d", "idct_2d"]:
+        scale = numel / 4.0
+        parity["round_trip_rel_l2"] = float(((outs[0][1] / scale - xs[0]).norm() / xs[0].norm()).item())
+    elif rank == 0:
+        import numpy as np
+
+        import oracle
+
+        for j, k in enumerate(w["kinds"]):
+            if w["mode"] == "chain" and j > 0:
+                break
+            x0 = xs[0][0].double().cpu().numpy()
+            ref = getattr(oracle.port, k)(x0) if numel <= 1 << 22 else None
+            if ref is not None:
+                parity[f"{k}_rel_l2_vs_oracle"] = float(oracle.rel_l2(outs[0][j][0].double().cpu().numpy(), ref))
 
     clocks = ClockSampler(local_rank)
     clocks.start()
     t_w = time.perf_counter()
     i = 0
     while i < args.warmup or time.perf_counter() - t_w < 1.0:  # >= W steps and >= 1 s soak
-        step()
+        step(i)
         i += 1
-        if i % 50 == 0:
+        if i % 20 == 0:
             torch.cuda.synchronize()
     warm_done = i
     barrier()
@@ -271,8 +368,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    for _ in range(args.steps):
-        step()
+    for j in range(args.steps):
+        step(j)
     e1.record(stream)
     torch.cuda.synchronize()
     barrier()
@@ -283,89 +380,91 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     ms_per_step = ms / args.steps
-    value = world * bytes_step * args.steps / (ms / 1e3) / 1e9
+    value = job_bytes_step * args.steps / (ms / 1e3) / 1e9
 
     # ---- per-kernel timing (roofline of the dominant kernel) ----------------
     peak, peak_kind = _peaks()
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
     kernels = []
-    for kind_name, kind, src, dst in (("dct_2d", _sdct.DCT_2D, x, y), ("idct_2d", _sdct.IDCT_2D, y, z)):
-        for st in range(plan.stage_count(kind)):
+    src = xs[0]
+    for kn, k in zip(w["kinds"], kinds):
+        dst = outs[0][0]
+        for st in range(plan.stage_count(k)):
             times = []
             for _ in range(10):
                 flush.fill_(1)  # evict L2 (256 MB > 126 MB) outside the timed launch
                 a = torch.cuda.Event(enable_timing=True)
                 b = torch.cuda.Event(enable_timing=True)
                 a.record(stream)
-                plan.run_stage(kind, st, src.data_ptr(), dst.data_ptr(), s, ws.data_ptr())
+                plan.run_stage(k, st, src.data_ptr(), dst.data_ptr(), s, ws.data_ptr())
                 b.record(stream)
                 torch.cuda.synchronize()
                 times.append(a.elapsed_time(b))
             avg = sum(times[2:]) / len(times[2:])
-            kernels.append({"kernel": f"{kind_name}.stage{st}", "ms": avg,
-                            "gbs": bytes_transform / (avg / 1e3) / 1e9})
-        # re-run the full transform so dst holds valid data for the next kind
-        plan.run(kind, src.data_ptr(), dst.data_ptr(), s, ws.data_ptr())
+            kernels.append({"kernel": f"{kn}.stage{st}", "ms": avg, "gbs": bytes_transform / (avg / 1e3) / 1e9})
+        plan.run(k, src.data_ptr(), dst.data_ptr(), s, ws.data_ptr())  # dst valid for the next kind
+        if w["mode"] == "chain":
+            src = dst.clone()
     torch.cuda.synchronize()
-    dom = max(kernels, key=lambda k: k["ms"])
+    dom = max(kernels, key=lambda k_: k_["ms"])
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-            traffic = json.load(f).get(dom["kernel"])
+            traffic = json.load(f).get(f"{args.workload}:{dtype}:{dom['kernel']}")
     except Exception:
         pass
     roofline = {"bound": "hbm", "achieved": round(dom["gbs"], 2), "peak": peak, "unit": "GB/s",
                 "frac": round(dom["gbs"] / peak, 4), "traffic": traffic, "kernel": dom["kernel"],
-                "peak_kind": peak_kind,
-                "per_launch_bytes": bytes_transform,
-                "all_kernels": [{k2: (round(v, 4) if isinstance(v, float) else v) for k2, v in k.items()}
-                                for k in kernels],
+                "peak_kind": peak_kind, "per_launch_bytes": bytes_transform,
+                "all_kernels": [{k2: (round(v, 4) if isinstance(v, float) else v) for k2, v in k_.items()}
+                                for k_ in kernels],
                 "step_frac": round(value / world / peak, 4),
                 "step_frac_2pass_normalised": round(2 * value / world / peak, 4)}
 
     # ---- cuFFT on the same shape (library baseline, reported alongside) -----
     cufft = {}
     try:
-        reps = 20
+        reps = 10 if B > 1 else 20
+        r2c, c2r = cufft_times(xs[0], list(dims), B, stream, reps)
         a = torch.cuda.Event(enable_timing=True)
         b = torch.cuda.Event(enable_timing=True)
-        r2c, c2r = cufft_times(x, n, stream, reps)
         ours = {}
-        for kn, kind, src, dst in (("dct", _sdct.DCT_2D, x, y), ("idct", _sdct.IDCT_2D, y, z)):
+        src = xs[0]
+        for kn, k in zip(w["kinds"], kinds):
             a.record(stream)
             for _ in range(reps):
-                plan.run(kind, src.data_ptr(), dst.data_ptr(), s, ws.data_ptr())
+                plan.run(k, src.data_ptr(), outs[0][0].data_ptr(), s, ws.data_ptr())
             b.record(stream)
             torch.cuda.synchronize()
             ours[kn] = a.elapsed_time(b) / reps
-        cufft = {"api": "libcufft cufftPlan2d + cufftExec{D2Z,Z2D|R2C,C2R}, plan built outside timing",
-                 "r2c_ms": round(r2c, 4), "c2r_ms": round(c2r, 4), "dct_ms": round(ours["dct"], 4),
-                 "idct_ms": round(ours["idct"], 4), "dct_over_r2c": round(ours["dct"] / r2c, 3),
-                 "idct_over_c2r": round(ours["idct"] / c2r, 3)}
+        cufft = {"api": "libcufft cufftPlanMany + cufftExec{D2Z,Z2D|R2C,C2R}, plan built outside timing",
+                 "r2c_ms": round(r2c, 4), "c2r_ms": round(c2r, 4)}
+        for kn, v in ours.items():
+            cufft[f"{kn}_ms"] = round(v, 4)
+            base = r2c if kn.startswith("dct") else c2r
+            cufft[f"{kn}_over_{'r2c' if kn.startswith('dct') else 'c2r'}"] = round(v / base, 3)
     except Exception as e:  # pragma: no cover - reported, not fatal
         cufft = {"error": str(e)}
 
     # ---- end to end through the public API with host buffers ---------------
-    x_pin = x_host.pin_memory()
+    # sd.stream_host: per step, every item of the step goes pinned host -> H2D
+    # -> the workload's transforms -> D2H -> pinned host; consecutive items
+    # are software-pipelined over three streams (copies overlap the kernels
+    # and each other: PCIe is full duplex). Timed with CUDA events on the
+    # caller's stream, which the pipeline forks from and joins back into.
+    x_pin = xs[0][:1].cpu().pin_memory()
     out_pin = torch.empty_like(x_pin).pin_memory()
-    xd = torch.empty_like(x)
-
-    def e2e_step():
-        xd.copy_(x_pin, non_blocking=True)
-        yy = sd.dct_2d(xd)
-        zz = sd.idct_2d(yy)
-        out_pin.copy_(zz, non_blocking=True)
-
-    for _ in range(3):
-        e2e_step()
+    chains = [w["kinds"]] if w["mode"] == "chain" else [[k] for k in w["kinds"]]
+    for ch in chains:
+        sd.stream_host(ch, x_pin, out_pin, count=3, device=local_rank)  # warm-up (lane buffers)
     torch.cuda.synchronize()
     barrier()
-    e_steps = max(5, min(args.steps, 50))
+    e_steps = 1 if B > 16 else max(5, min(args.steps, 50))
     a = torch.cuda.Event(enable_timing=True)
     b = torch.cuda.Event(enable_timing=True)
     a.record(stream)
-    for _ in range(e_steps):
-        e2e_step()
+    for ch in chains:
+        sd.stream_host(ch, x_pin, out_pin, count=e_steps * B, device=local_rank, sync=False)
     b.record(stream)
     torch.cuda.synchronize()
     e_ms = a.elapsed_time(b)
@@ -373,41 +472,45 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         t = torch.tensor([e_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e_ms = float(t.item())
-    e2e_val = world * bytes_step * e_steps / (e_ms / 1e3) / 1e9
-    e2e_err = float(((out_pin.to(torch.float64) / (numel / 4.0) - x_host.to(torch.float64)).norm()
-                     / x_host.to(torch.float64).norm()).item())
+    e2e_val = job_bytes_step * e_steps / (e_ms / 1e3) / 1e9
+    if w["kinds"] == ["dct_2d", "idct_2d"]:
+        x0 = x_pin[0].to(torch.float64)
+        parity["e2e_round_trip_rel_l2"] = float(((out_pin[0].to(torch.float64) / (numel / 4.0) - x0).norm()
+                                                 / x0.norm()).item())
 
     # ---- CPU baseline (rank 0, N = 1 only) -----------------------------------
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        rate, dtr, steps, kind = cpu_reference_rate(n, budget_s=args.cpu_budget)
+        rate, dtr, n_units, kind, sample = cpu_reference_rate(w, budget_s=args.cpu_budget)
         cores, quota = _cores()
-        cpu = {"value": round(rate, 4), "unit": UNIT, "cores": cores, "kind": kind,
-               "cgroup_cpu_quota": quota,
-               "sample": f"{steps} round trips of dct_2d+idct_2d {n}x{n} fp64 on the host, prebuilt plans, "
-                         f"threads=0 ({dtr * 1e3:.1f} ms each)"}
+        cpu = {"value": round(rate, 4), "unit": UNIT, "cores": cores, "kind": kind, "cgroup_cpu_quota": quota,
+               "sample": sample}
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": warm_done, "ms_per_step": round(ms_per_step, 5),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "higher_is_better": True, "scaling": "strong" if w.get("sharded") else "weak", "vs_baseline": None,
             "dtype": "f64" if dt == torch.float64 else "f32",
             "data": "synthetic uniform(-1,1), device-resident",
-            "config": {"workload": f"2D DCT-II -> IDCT round trip {n}x{n} {args.dtype} per GPU (BASELINE configs[1])",
-                       "global_batch": world, "parallelism": f"replicas x{world} (independent images, no collective)",
-                       "l2": "working set 4x134 MB per step > 126 MB L2 (no flush needed)",
+            "config": {"workload": w["desc"].format(dt=dtype), "name": args.workload,
+                       "global_batch": w["batch"] if w.get("sharded") else world * B,
+                       "parallelism": (f"batch sharded x{world} (contiguous shards, no collective)" if w.get("sharded")
+                                       else f"replicas x{world} (independent images, no collective)"),
+                       "l2": ("working set per step > 2x the 126 MB L2 (no flush needed)" if rot == 1 else
+                              f"inputs/outputs rotate over {rot} sets ({rot * set_bytes / 2**20:.0f} MB > 2x L2)"),
                        "bytes_per_step_per_gpu": bytes_step},
             "roofline": roofline,
             "cpu_baseline": cpu,
-            "e2e": {"value": round(e2e_val, 3), "unit": UNIT, "h2d_bytes_per_step": numel * esz,
-                    "d2h_bytes_per_step": numel * esz, "steps": e_steps,
+            "e2e": {"value": round(e2e_val, 3), "unit": UNIT, "h2d_bytes_per_step": item_bytes * B * len(chains),
+                    "d2h_bytes_per_step": item_bytes * B * len(chains), "steps": e_steps,
                     "ms_per_step": round(e_ms / e_steps, 4),
-                    "path": "pinned host -> paper_2110_01172_b200.dct_2d/idct_2d (torch CUDA) -> pinned host"},
-            "gpu_launches": args.steps * (plan.stage_count(_sdct.DCT_2D) + plan.stage_count(_sdct.IDCT_2D)),
+                    "path": f"pinned host -> paper_2110_01172_b200.stream_host({w['kinds']}) "
+                            "(sdct_exec_host_pipelined, 3 overlapped lanes) -> pinned host"},
+            "gpu_launches": args.steps * sum(plan.stage_count(k) for k in kinds),
             "clocks": clk,
             "cufft": cufft,
-            "parity": {"round_trip_rel_l2": rt_err, "e2e_round_trip_rel_l2": e2e_err},
+            "parity": parity,
         }
         print(json.dumps(line), flush=True)
 
@@ -418,8 +521,9 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--size", type=int, default=4096)
-    ap.add_argument("--dtype", choices=["float64", "float32"], default="float64")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c2")
+    ap.add_argument("--dtype", choices=["float64", "float32"], default=None,
+                    help="override the workload's dtype (c2 runs fp64 by default)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     ap.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of CPU baseline sampling")
     args = ap.parse_args()
@@ -429,7 +533,7 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
-        run_reference(args, rank)
+        run_reference(args, rank, world)
         return
     if world > 1:
         import torch

@@ -112,6 +112,20 @@ int sdct_exec(sdct_plan_t plan, int kind, const void* d_in, void* d_out, void* d
  * RealTensor out, proj/include/sdct/tensor.hpp:34-78) calls. */
 int sdct_exec_host(sdct_plan_t plan, int kind, const void* h_in, void* h_out, void* stream);
 
+/* Host streaming: `count` independent items (each one plan-sized batch) go
+ * host -> device -> kinds[0] -> ... -> kinds[nkinds-1] -> host. Item i's input
+ * is at h_in + i*in_stride bytes and its result is written to
+ * h_out + i*out_stride (stride 0 reuses one buffer). The items are software
+ * pipelined over three internal streams with their own device buffers, so
+ * item i+1's H2D, item i's kernels and item i-1's D2H overlap (PCIe is full
+ * duplex). Stream-ordered on `stream` (fork/join through events): the call
+ * returns once everything is queued; results are in h_out when `stream`
+ * reaches that point. Host buffers must be pinned for the copies to overlap.
+ * The batched-host counterpart of calling dct_2d (proj/src/dct2d.cpp:389-393)
+ * once per image. */
+int sdct_exec_host_pipelined(sdct_plan_t plan, const int* kinds, int nkinds, const void* h_in, int64_t in_stride,
+                             void* h_out, int64_t out_stride, int64_t count, void* stream);
+
 /* Stage-level access for timing the individual kernels of a transform:
  * number of kernel launches of `kind`, and a launch of one of them with the
  * same argument meaning as sdct_exec (stage k reads/writes the buffers the

@@ -29,13 +29,14 @@ from .api import (
     idxst_1d,
     idxst_idct_2d,
     plan_for,
+    stream_host,
 )
 
 __all__ = [
     "ShapeError", "FormatError", "DeviceError", "amdahl_speedup",
     "dct_1d", "idct_1d", "idxst_1d",
     "dct_2d", "dct_2d_rowcol", "idct_2d", "idct_idxst_2d", "idxst_idct_2d",
-    "dct_3d", "idct_3d", "plan_for",
+    "dct_3d", "idct_3d", "plan_for", "stream_host",
 ]
 
 __version__ = "0.1.0"

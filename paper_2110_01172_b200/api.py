@@ -97,3 +97,45 @@ idct_idxst_2d = _make("idct_idxst_2d")
 idxst_idct_2d = _make("idxst_idct_2d")
 dct_3d = _make("dct_3d")
 idct_3d = _make("idct_3d")
+
+
+def stream_host(kinds, x, out=None, count=None, device: int = 0, sync: bool = True):
+    """Host-resident items through a chain of transforms on the GPU, with the
+    copies overlapped: item i+1's host->device copy, item i's kernels and item
+    i-1's device->host copy run concurrently (sdct_exec_host_pipelined).
+
+    kinds: transform names applied in order, e.g. ["dct_2d", "idct_2d"].
+    x:     CPU torch tensor (pin_memory() for overlap) of shape (items, *dims);
+           a leading extent of 1 with count > 1 re-sends the same item.
+    out:   CPU tensor for the results (same item shape); allocated pinned if
+           None; a leading extent of 1 keeps only the last result.
+    sync:  wait for completion (False: stream-ordered on the current stream).
+    """
+    import torch
+
+    names = [kinds] if isinstance(kinds, str) else list(kinds)
+    rank = _RANK.get(names[0], 2)
+    if any(_RANK.get(n, 2) != rank for n in names):
+        raise ShapeError("stream_host: every transform in the chain must have the same rank")
+    if x.is_cuda or x.dim() != rank + 1:
+        raise ShapeError(f"stream_host expects a CPU tensor of shape (items, *dims) with {rank} dims per item")
+    if x.dtype not in (torch.float32, torch.float64):
+        raise ValueError(f"stream_host: dtype must be float32 or float64, got {x.dtype}")
+    x = x.contiguous()
+    n = int(count) if count is not None else int(x.shape[0])
+    if out is None:
+        out = torch.empty((1 if x.shape[0] == 1 and n > 1 else n, *x.shape[1:]), dtype=x.dtype).pin_memory()
+    if out.dtype != x.dtype or tuple(out.shape[1:]) != tuple(x.shape[1:]) or not out.is_contiguous():
+        raise ShapeError("stream_host: out must be a contiguous tensor with the input's item shape and dtype")
+    if (x.shape[0] not in (1, n)) or (out.shape[0] not in (1, n)):
+        raise ShapeError("stream_host: leading extents must be 1 or the item count")
+    item = x[0].numel() * x.element_size()
+    dt = "float32" if x.dtype == torch.float32 else "float64"
+    plan = plan_for(tuple(x.shape[1:]), 1, dt, device)
+    with torch.cuda.device(device):
+        stream = torch.cuda.current_stream(device)
+        plan.run_host_pipelined([_KIND[k] for k in names], x.data_ptr(), 0 if x.shape[0] == 1 else item,
+                                out.data_ptr(), 0 if out.shape[0] == 1 else item, n, stream.cuda_stream)
+        if sync:
+            stream.synchronize()
+    return out

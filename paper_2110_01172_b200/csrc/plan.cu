@@ -114,6 +114,13 @@ struct sdct_plan_s {
   size_t ws_bytes = 0;
   void* d_in = nullptr;
   void* d_out = nullptr;
+  // host-streaming pipeline (sdct_exec_host_pipelined): per lane a stream,
+  // two item buffers and a workspace, created on first use
+  static constexpr int kLanes = 3;
+  cudaStream_t lane_st[kLanes] = {};
+  cudaEvent_t lane_ev[kLanes] = {};
+  cudaEvent_t fork_ev = nullptr;
+  void* lane_buf[kLanes][3] = {};
   std::mutex mu;
 
   void* gws = nullptr;  // generic-path scratch on fast plans (row-column), lazily allocated
@@ -799,6 +806,12 @@ int sdct_plan_destroy(sdct_plan_t p) {
   cudaFree(p->d_in);
   cudaFree(p->d_out);
   cudaFree(p->gws);
+  for (int l = 0; l < sdct_plan_s::kLanes; ++l) {
+    for (void* b : p->lane_buf[l]) cudaFree(b);
+    if (p->lane_st[l]) cudaStreamDestroy(p->lane_st[l]);
+    if (p->lane_ev[l]) cudaEventDestroy(p->lane_ev[l]);
+  }
+  if (p->fork_ev) cudaEventDestroy(p->fork_ev);
   delete p;
   return SDCT_OK;
 }
@@ -860,6 +873,61 @@ int sdct_exec(sdct_plan_t p, int kind, const void* d_in, void* d_out, void* d_ws
   if (!p || !d_in || !d_out) return fail(SDCT_ERR_ARG, "null argument to sdct_exec");
   if (d_in == d_out) return fail(SDCT_ERR_ARG, "sdct_exec is out of place: d_in == d_out");
   return dispatch(p, kind, -1, d_in, d_out, d_ws, static_cast<cudaStream_t>(stream), nullptr);
+}
+
+int sdct_exec_host_pipelined(sdct_plan_t p, const int* kinds, int nkinds, const void* h_in, int64_t in_stride,
+                             void* h_out, int64_t out_stride, int64_t count, void* stream) {
+  if (!p || !kinds || nkinds < 1 || !h_in || !h_out || count < 0 || in_stride < 0 || out_stride < 0)
+    return fail(SDCT_ERR_ARG, "bad argument to sdct_exec_host_pipelined");
+  for (int k = 0; k < nkinds; ++k)
+    if (!kind_ok(p, kinds[k])) return fail(SDCT_ERR_PLAN, "transform kind does not match the plan rank");
+  std::lock_guard<std::mutex> lock(p->mu);
+  DeviceGuard g(p->device);
+  const size_t bytes = static_cast<size_t>(p->batch) * p->item_bytes();
+  cudaError_t e;
+  constexpr int L = sdct_plan_s::kLanes;
+  if (!p->lane_st[0]) {
+    for (int l = 0; l < L; ++l) {
+      if ((e = cudaStreamCreateWithFlags(&p->lane_st[l], cudaStreamNonBlocking)) != cudaSuccess)
+        return cuda_fail(e, "creating pipeline stream");
+      if ((e = cudaEventCreateWithFlags(&p->lane_ev[l], cudaEventDisableTiming)) != cudaSuccess)
+        return cuda_fail(e, "creating pipeline event");
+      for (int b = 0; b < 3; ++b) {
+        const size_t sz = b < 2 ? bytes : p->ws_bytes;
+        if ((e = cudaMalloc(&p->lane_buf[l][b], sz)) != cudaSuccess) return cuda_fail(e, "allocating pipeline buffers");
+      }
+    }
+    if ((e = cudaEventCreateWithFlags(&p->fork_ev, cudaEventDisableTiming)) != cudaSuccess)
+      return cuda_fail(e, "creating pipeline event");
+  }
+  cudaStream_t caller = static_cast<cudaStream_t>(stream);
+  // fork: every lane starts after the work already queued on the caller's stream
+  if ((e = cudaEventRecord(p->fork_ev, caller)) != cudaSuccess) return cuda_fail(e, "recording fork event");
+  for (int l = 0; l < L; ++l)
+    if ((e = cudaStreamWaitEvent(p->lane_st[l], p->fork_ev, 0)) != cudaSuccess) return cuda_fail(e, "fork");
+  const unsigned char* hi = static_cast<const unsigned char*>(h_in);
+  unsigned char* ho = static_cast<unsigned char*>(h_out);
+  for (int64_t i = 0; i < count; ++i) {
+    const int l = static_cast<int>(i % L);
+    cudaStream_t st = p->lane_st[l];
+    void* a = p->lane_buf[l][0];
+    void* b = p->lane_buf[l][1];
+    if ((e = cudaMemcpyAsync(a, hi + i * in_stride, bytes, cudaMemcpyHostToDevice, st)) != cudaSuccess)
+      return cuda_fail(e, "copying input to device");
+    for (int k = 0; k < nkinds; ++k) {
+      const int rc = dispatch(p, kinds[k], -1, a, b, p->lane_buf[l][2], st, nullptr);
+      if (rc != SDCT_OK) return rc;
+      std::swap(a, b);
+    }
+    if ((e = cudaMemcpyAsync(ho + i * out_stride, a, bytes, cudaMemcpyDeviceToHost, st)) != cudaSuccess)
+      return cuda_fail(e, "copying output to host");
+  }
+  // join: the caller's stream continues once every lane has drained
+  for (int l = 0; l < L; ++l) {
+    if ((e = cudaEventRecord(p->lane_ev[l], p->lane_st[l])) != cudaSuccess) return cuda_fail(e, "join");
+    if ((e = cudaStreamWaitEvent(caller, p->lane_ev[l], 0)) != cudaSuccess) return cuda_fail(e, "join");
+  }
+  return SDCT_OK;
 }
 
 int sdct_exec_host(sdct_plan_t p, int kind, const void* h_in, void* h_out, void* stream) {

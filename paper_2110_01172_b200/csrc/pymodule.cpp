@@ -160,6 +160,16 @@ PYBIND11_MODULE(_sdct, m) {
            },
            py::arg("kind"), py::arg("stage"), py::arg("d_in"), py::arg("d_out"), py::arg("stream") = 0,
            py::arg("workspace") = 0)
+      .def("run_host_pipelined",
+           [](const sdct::DevicePlan& p, const std::vector<int>& kinds, std::uintptr_t h_in, std::int64_t in_stride,
+              std::uintptr_t h_out, std::int64_t out_stride, std::int64_t count, std::uintptr_t stream) {
+             py::gil_scoped_release nogil;
+             sdct::detail::check(sdct_exec_host_pipelined(
+                 p.handle(), kinds.data(), static_cast<int>(kinds.size()), reinterpret_cast<const void*>(h_in),
+                 in_stride, reinterpret_cast<void*>(h_out), out_stride, count, reinterpret_cast<void*>(stream)));
+           },
+           py::arg("kinds"), py::arg("h_in"), py::arg("in_stride"), py::arg("h_out"), py::arg("out_stride"),
+           py::arg("count"), py::arg("stream") = 0)
       .def("stage_count",
            [](const sdct::DevicePlan& p, int kind) {
              int n = 0;

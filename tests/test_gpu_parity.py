@@ -345,3 +345,22 @@ def test_torch_entry_points(cuda):
         assert y.dtype == dt and y.device == xt.device and y.shape == xt.shape
         for i in range(3):
             assert oracle.rel_l2(y[i].double().cpu().numpy(), oracle.port.dct_2d(x[i])) <= tol * 10
+
+
+def test_stream_host_pipeline_matches_device_path(cuda):
+    # sdct_exec_host_pipelined: items overlap across three lanes; every item
+    # must equal the one-shot device transform bit for bit
+    torch = _torch()
+    import paper_2110_01172_b200 as sd
+
+    for dtype in (torch.float64, torch.float32):
+        x = torch.tensor(rnd((7, 64, 128), 31), dtype=dtype).pin_memory()
+        out = sd.stream_host(["dct_2d", "idct_idxst_2d"], x)
+        for i in range(7):
+            want = sd.idct_idxst_2d(sd.dct_2d(x[i].cuda())).cpu()
+            assert torch.equal(out[i], want), (dtype, i)
+        # reused input / output buffers (stride 0)
+        one = sd.stream_host("dct_2d", x[:1], count=4)
+        assert one.shape[0] == 1 and torch.equal(one[0], sd.dct_2d(x[0].cuda()).cpu())
+    with pytest.raises(ValueError):
+        sd.stream_host(["dct_2d", "dct_3d"], x)

@@ -1,5 +1,5 @@
 mkdir -p gpurun_out
 timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -3
-for f in 0 1; do for m in 0 1; do SDCT_DEV_FLAGS=$f SDCT_ROW2_MODE=$m timeout 120 python tools/stage_time.py --dtype float64; done; done
-SDCT_ROW2_MODE=0 timeout 120 python tools/stage_time.py --dtype float32
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:"row2" -c 2 -o gpurun_out/row2_m0 python tools/prof_step.py --iters 1 > gpurun_out/ncu_full.log 2>&1; tail -1 gpurun_out/ncu_full.log
+timeout 400 python bench.py > gpurun_out/bench_c2.json 2> gpurun_out/bench_c2.err; tail -2 gpurun_out/bench_c2.err; cat gpurun_out/bench_c2.json
+for wl in c1 c3 c4 c5; do timeout 400 python bench.py --workload $wl --steps 50 > gpurun_out/bench_$wl.json 2> gpurun_out/bench_$wl.err; tail -2 gpurun_out/bench_$wl.err; cat gpurun_out/bench_$wl.json; done
+timeout 300 python bench.py --dtype float32 --no-cpu > gpurun_out/bench_c2_f32.json 2>&1; cat gpurun_out/bench_c2_f32.json
