@@ -1,5 +1,4 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -3
-timeout 400 python bench.py > gpurun_out/bench_c2.json 2> gpurun_out/bench_c2.err; tail -2 gpurun_out/bench_c2.err; cat gpurun_out/bench_c2.json
-for wl in c1 c3 c4 c5; do timeout 400 python bench.py --workload $wl --steps 50 > gpurun_out/bench_$wl.json 2> gpurun_out/bench_$wl.err; tail -2 gpurun_out/bench_$wl.err; cat gpurun_out/bench_$wl.json; done
-timeout 300 python bench.py --dtype float32 --no-cpu > gpurun_out/bench_c2_f32.json 2>&1; cat gpurun_out/bench_c2_f32.json
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file gpurun_out/launches_c2_f64.csv python bench.py --steps 4 --warmup 3 --no-cpu > /dev/null 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"col_kernel|row" -c 4 -o gpurun_out/full_c2_f64 python tools/prof_step.py --iters 1 > gpurun_out/ncu_full.log 2>&1; tail -1 gpurun_out/ncu_full.log
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"col_kernel|row" -c 4 -o gpurun_out/full_c2_f32 python tools/prof_step.py --iters 1 --dtype float32 > gpurun_out/ncu_full32.log 2>&1; tail -1 gpurun_out/ncu_full32.log

@@ -40,6 +40,7 @@ def main():
     ap.add_argument("--launches")
     ap.add_argument("--stage-map", default="")
     ap.add_argument("--title", default="")
+    ap.add_argument("--traffic-prefix", default="", help="key prefix in profiles/traffic.json, e.g. c2:float64:")
     a = ap.parse_args()
     ks = raw(a.report)
     smap = dict(kv.split("=", 1) for kv in a.stage_map.split(";") if kv)
@@ -59,9 +60,8 @@ def main():
                      f"{g('launch__registers_per_thread')} | {g('launch__block_size')} | {g('launch__grid_size')} | "
                      f"{float(g('launch__shared_mem_per_block_dynamic') or 0)/1024:.0f} | "
                      f"{g('sm__warps_active.avg.pct_of_peak_sustained_active')} | {g('l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum')} |")
-        for stage, pat in smap.items():
-            if pat in k["name"] and stage not in traffic:
-                traffic[stage] = rd + wr
+        if i < len(smap):  # stage-map entries name the captured launches in order
+            traffic[a.traffic_prefix + list(smap)[i]] = rd + wr
     if a.launches:
         lines += ["", "## launch list (gpu__time_duration.sum, cold-cache, serialised)", ""]
         rows = list(csv.reader(open(a.launches)))
