@@ -122,14 +122,18 @@ class ClockSampler:
 
 # ---------------------------------------------------------------------------
 # Workloads (BASELINE.json configs). mode "chain": kinds applied in sequence
-# to the step's input; "fan": each kind applied to the same input.
+# to the step's input; "fan": each kind applied to the same input; "force":
+# the spectral force-field step (dct_2d, weighting, both composites), whose
+# `kinds` list the transforms it is made of.
 WORKLOADS = {
     "c2": dict(dims=(4096, 4096), kinds=["dct_2d", "idct_2d"], mode="chain", dtype="float64", batch=1,
                desc="2D DCT-II -> IDCT round trip 4096x4096 {dt} per rank (BASELINE configs[1])"),
     "c1": dict(dims=(1024, 1024), kinds=["dct_2d"], mode="chain", dtype="float64", batch=1,
                desc="2D DCT-II 1024x1024 {dt} per rank (BASELINE configs[0])"),
-    "c3": dict(dims=(2048, 2048), kinds=["idct_idxst_2d", "idxst_idct_2d"], mode="fan", dtype="float64", batch=1,
-               desc="IDCT/IDXST + IDXST/IDCT composites 2048x2048 {dt} per rank (BASELINE configs[2])"),
+    "c3": dict(dims=(2048, 2048), kinds=["dct_2d", "idct_idxst_2d", "idxst_idct_2d"], mode="force",
+               dtype="float64", batch=1,
+               desc="DREAMPlace-style field step 2048x2048 {dt} per rank: dct_2d, weighting, IDCT/IDXST + "
+                    "IDXST/IDCT composites (BASELINE configs[2]; force_demo_fields)"),
     "c4": dict(dims=(256, 256, 256), kinds=["dct_3d"], mode="chain", dtype="float32", batch=1,
                desc="3D DCT-II 256^3 {dt} per rank (BASELINE configs[3])"),
     "c5": dict(dims=(2048, 2048), kinds=["dct_2d"], mode="chain", dtype="float32", batch=512, sharded=True,
@@ -171,12 +175,16 @@ def cpu_reference_rate(w, budget_s: float, max_steps: int | None = None):
     if oracle.ref_available():
         kind = "reference"
         fns = [lambda a, k=k: oracle.ref.run(k, a, threads=0) for k in kinds]  # noqa: E731
+        force = lambda a: oracle.ref.force_demo_fields(a, threads=0)  # noqa: E731
     else:
         kind = "port"
         fns = [getattr(oracle.port, k) for k in kinds]
+        force = oracle.port.force_demo_fields
 
     def unit():
-        if w["mode"] == "chain":
+        if w["mode"] == "force":
+            force(x)
+        elif w["mode"] == "chain":
             y = x
             for f in fns:
                 y = f(y)
@@ -195,7 +203,8 @@ def cpu_reference_rate(w, budget_s: float, max_steps: int | None = None):
         unit()
     dt = (time.perf_counter() - t0) / n
     bytes_unit = 2.0 * _numel(dims) * 8 * len(kinds)
-    what = " then ".join(kinds) if w["mode"] == "chain" else " + ".join(kinds)
+    what = ("force_demo_fields" if w["mode"] == "force" else
+            " then ".join(kinds) if w["mode"] == "chain" else " + ".join(kinds))
     sample = (f"{n} x ({what}) of one {'x'.join(map(str, dims))} fp64 image on the host, prebuilt plans, "
               f"threads=0 ({dt * 1e3:.1f} ms each)")
     if w.get("sharded"):
@@ -302,7 +311,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     job_bytes_step = world * bytes_step if not w.get("sharded") else 2.0 * numel * esz * w["batch"] * len(kinds)
 
     # rotation sets so that no step reads L2-resident inputs of the previous one
-    set_bytes = item_bytes * B * (2 if w["mode"] == "fan" else len(kinds) + 1)
+    set_bytes = item_bytes * B * (2 if w["mode"] == "fan" else 3 if w["mode"] == "force" else len(kinds) + 1)
     rot = 1 if set_bytes >= 2 * L2_BYTES else -(-2 * L2_BYTES // set_bytes) + 1
     g = torch.Generator(device="cpu").manual_seed(2 + rank)
     x_host = (torch.rand((B,) + dims, generator=g, dtype=torch.float64) * 2 - 1).to(dt) if B <= 4 else None
@@ -323,6 +332,9 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     def step(i):
         r = i % rot
         src = xs[r]
+        if w["mode"] == "force":
+            plan.force_fields(src.data_ptr(), outs[r][0].data_ptr(), outs[r][1].data_ptr(), s, ws.data_ptr())
+            return
         for j, k in enumerate(kinds):
             dst = outs[r][j]
             plan.run(k, src.data_ptr(), dst.data_ptr(), s, ws.data_ptr())
@@ -340,9 +352,13 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     if w["kinds"] == ["dct_2d", "idct_2d"]:
         scale = numel / 4.0
         parity["round_trip_rel_l2"] = float(((outs[0][1] / scale - xs[0]).norm() / xs[0].norm()).item())
-    elif rank == 0:
-        import numpy as np
+    elif rank == 0 and w["mode"] == "force":
+        import oracle
 
+        w1, w2 = oracle.port.force_demo_fields(xs[0][0].double().cpu().numpy())
+        parity["xi1_rel_l2_vs_oracle"] = float(oracle.rel_l2(outs[0][0][0].double().cpu().numpy(), w1))
+        parity["xi2_rel_l2_vs_oracle"] = float(oracle.rel_l2(outs[0][1][0].double().cpu().numpy(), w2))
+    elif rank == 0:
         import oracle
 
         for j, k in enumerate(w["kinds"]):
@@ -419,6 +435,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                 "all_kernels": [{k2: (round(v, 4) if isinstance(v, float) else v) for k2, v in k_.items()}
                                 for k_ in kernels],
                 "step_frac": round(value / world / peak, 4),
+                **({"note": "force step: the composite kernels are timed without the fused field weighting"}
+                   if w["mode"] == "force" else {}),
                 "step_frac_2pass_normalised": round(2 * value / world / peak, 4)}
 
     # ---- cuFFT on the same shape (library baseline, reported alongside) -----
@@ -454,18 +472,40 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     # caller's stream, which the pipeline forks from and joins back into.
     x_pin = xs[0][:1].cpu().pin_memory()
     out_pin = torch.empty_like(x_pin).pin_memory()
-    chains = [w["kinds"]] if w["mode"] == "chain" else [[k] for k in w["kinds"]]
-    for ch in chains:
-        sd.stream_host(ch, x_pin, out_pin, count=3, device=local_rank)  # warm-up (lane buffers)
-    torch.cuda.synchronize()
-    barrier()
+    chains = ([w["kinds"]] if w["mode"] == "chain" else [[k] for k in w["kinds"]] if w["mode"] == "fan" else [])
     e_steps = 1 if B > 16 else max(5, min(args.steps, 50))
     a = torch.cuda.Event(enable_timing=True)
     b = torch.cuda.Event(enable_timing=True)
-    a.record(stream)
-    for ch in chains:
-        sd.stream_host(ch, x_pin, out_pin, count=e_steps * B, device=local_rank, sync=False)
-    b.record(stream)
+    if w["mode"] == "force":
+        # sd.force_demo_fields on a device tensor, with the density copied in and
+        # both fields copied out every step (one stream, not pipelined)
+        xd = torch.empty_like(xs[0][:1])
+        o2 = torch.empty_like(out_pin).pin_memory()
+
+        def e2e_force():
+            xd.copy_(x_pin, non_blocking=True)
+            f1, f2 = sd.force_demo_fields(xd[0])
+            out_pin[0].copy_(f1, non_blocking=True)
+            o2[0].copy_(f2, non_blocking=True)
+
+        e2e_force()
+        torch.cuda.synchronize()
+        barrier()
+        a.record(stream)
+        for _ in range(e_steps):
+            e2e_force()
+        b.record(stream)
+        n_out = 2
+    else:
+        for ch in chains:
+            sd.stream_host(ch, x_pin, out_pin, count=3, device=local_rank)  # warm-up (lane buffers)
+        torch.cuda.synchronize()
+        barrier()
+        a.record(stream)
+        for ch in chains:
+            sd.stream_host(ch, x_pin, out_pin, count=e_steps * B, device=local_rank, sync=False)
+        b.record(stream)
+        n_out = len(chains)
     torch.cuda.synchronize()
     e_ms = a.elapsed_time(b)
     if world > 1:
@@ -502,11 +542,14 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                        "bytes_per_step_per_gpu": bytes_step},
             "roofline": roofline,
             "cpu_baseline": cpu,
-            "e2e": {"value": round(e2e_val, 3), "unit": UNIT, "h2d_bytes_per_step": item_bytes * B * len(chains),
-                    "d2h_bytes_per_step": item_bytes * B * len(chains), "steps": e_steps,
+            "e2e": {"value": round(e2e_val, 3), "unit": UNIT,
+                    "h2d_bytes_per_step": item_bytes * B * max(1, len(chains)),
+                    "d2h_bytes_per_step": item_bytes * B * n_out, "steps": e_steps,
                     "ms_per_step": round(e_ms / e_steps, 4),
-                    "path": f"pinned host -> paper_2110_01172_b200.stream_host({w['kinds']}) "
-                            "(sdct_exec_host_pipelined, 3 overlapped lanes) -> pinned host"},
+                    "path": ("pinned host -> paper_2110_01172_b200.force_demo_fields (torch CUDA) -> pinned host"
+                             if w["mode"] == "force" else
+                             f"pinned host -> paper_2110_01172_b200.stream_host({w['kinds']}) "
+                             "(sdct_exec_host_pipelined, 3 overlapped lanes) -> pinned host")},
             "gpu_launches": args.steps * sum(plan.stage_count(k) for k in kinds),
             "clocks": clk,
             "cufft": cufft,

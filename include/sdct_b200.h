@@ -112,6 +112,18 @@ int sdct_exec(sdct_plan_t plan, int kind, const void* d_in, void* d_out, void* d
  * RealTensor out, proj/include/sdct/tensor.hpp:34-78) calls. */
 int sdct_exec_host(sdct_plan_t plan, int kind, const void* h_in, void* h_out, void* stream);
 
+/* DREAMPlace-style spectral force fields — replaces sdct::force_demo_fields
+ * (proj/src/force.cpp:11-37, proj/include/sdct/force.hpp:23): a = dct_2d(density),
+ * a1 = a w1/(w1^2+w2^2), a2 = a w2/(w1^2+w2^2) (w_d = pi k_d / n_d, 0 at DC),
+ * xi1 = idct_idxst_2d(a1), xi2 = idxst_idct_2d(a2). Device buffers of one
+ * plan-sized batch; the weighting is fused into the inverse passes' loads (no
+ * a1/a2 arrays). d_workspace as for sdct_exec (NULL = the plan's own).
+ * Stream-ordered. */
+int sdct_force_fields(sdct_plan_t plan, const void* d_density, void* d_xi1, void* d_xi2, void* d_workspace,
+                      void* stream);
+/* Same on host memory (H2D, the fused device pipeline, D2H, synchronised). */
+int sdct_force_fields_host(sdct_plan_t plan, const void* h_density, void* h_xi1, void* h_xi2, void* stream);
+
 /* Host streaming: `count` independent items (each one plan-sized batch) go
  * host -> device -> kinds[0] -> ... -> kinds[nkinds-1] -> host. Item i's input
  * is at h_in + i*in_stride bytes and its result is written to

@@ -67,6 +67,7 @@ def _port_lib():
         for name in ("dct_direct_1d", "idct_direct_1d", "idxst_direct_1d"):
             getattr(lib, "sdct_oracle_" + name).argtypes = [P, S, P]
         lib.sdct_oracle_dct_direct_2d.argtypes = [P, S, S, P]
+        lib.sdct_oracle_force_fields_2d.argtypes = [P, S, S, P, P]
         _port = lib
     return _port
 
@@ -87,6 +88,10 @@ def _ref_lib():
             ctypes.c_uint, ctypes.c_int,
         ]
         lib.sdct_ref_run.restype = ctypes.c_int
+        lib.sdct_ref_force.argtypes = [ctypes.c_size_t, ctypes.c_size_t, ctypes.POINTER(ctypes.c_double),
+                                       ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double),
+                                       ctypes.c_uint, ctypes.c_int]
+        lib.sdct_ref_force.restype = ctypes.c_int
         lib.sdct_ref_last_error.restype = ctypes.c_char_p
         _ref = lib
     return _ref
@@ -137,6 +142,16 @@ class _Port:
     def idct_idxst_2d(self, x):
         return self._idct_family(x, 2)
 
+    def force_demo_fields(self, x):
+        """(xi1, xi2) of a rank-2 density (proj/src/force.cpp:11-37)."""
+        lib = _port_lib()
+        x = _as64(x)
+        if x.ndim != 2:
+            raise ValueError("force_demo_fields expects a rank-2 density grid")
+        xi1, xi2 = np.empty_like(x), np.empty_like(x)
+        lib.sdct_oracle_force_fields_2d(_dp(x), x.shape[0], x.shape[1], _dp(xi1), _dp(xi2))
+        return xi1, xi2
+
     def dct_3d(self, x):
         lib = _port_lib()
         return self._batched(
@@ -180,6 +195,18 @@ class _Ref:
             msg = lib.sdct_ref_last_error().decode()
             raise ValueError(msg) if rc == 1 else RuntimeError(msg)
         return out
+
+    def force_demo_fields(self, x, threads: int = 0, reps: int = 1):
+        lib = _ref_lib()
+        x = _as64(x)
+        if x.ndim != 2:
+            raise ValueError("force_demo_fields expects a rank-2 density grid")
+        xi1, xi2 = np.empty_like(x), np.empty_like(x)
+        rc = lib.sdct_ref_force(x.shape[0], x.shape[1], _dp(x), _dp(xi1), _dp(xi2), threads, reps)
+        if rc != 0:
+            msg = lib.sdct_ref_last_error().decode()
+            raise ValueError(msg) if rc == 1 else RuntimeError(msg)
+        return xi1, xi2
 
     def __getattr__(self, name):
         if name in KINDS:

@@ -17,6 +17,7 @@
 
 #include "sdct/dct2d.hpp"
 #include "sdct/errors.hpp"
+#include "sdct/force.hpp"
 #include "sdct/exec.hpp"
 #include "sdct/transforms_ext.hpp"
 
@@ -69,6 +70,31 @@ int sdct_ref_run(int kind, int rank, const std::size_t* dims, const double* in, 
       }
     }
     std::memcpy(out, y.data(), y.size() * sizeof(double));
+    return 0;
+  } catch (const sdct::ShapeError& e) {
+    g_err = e.what();
+    return 1;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 2;
+  }
+}
+
+}  // extern "C"
+
+extern "C" {
+
+// sdct::force_demo_fields (proj/src/force.cpp:11-37) on an n1 x n2 density.
+int sdct_ref_force(std::size_t n1, std::size_t n2, const double* in, double* xi1, double* xi2, unsigned threads,
+                   int reps) {
+  try {
+    sdct::ExecConfig cfg;
+    cfg.parallelism_degree = threads;
+    sdct::RealTensor x(sdct::Shape{n1, n2}, std::vector<double>(in, in + n1 * n2));
+    sdct::ForceFields f;
+    for (int r = 0; r < reps; ++r) f = sdct::force_demo_fields(x, cfg);
+    std::memcpy(xi1, f.xi1.data(), n1 * n2 * sizeof(double));
+    std::memcpy(xi2, f.xi2.data(), n1 * n2 * sizeof(double));
     return 0;
   } catch (const sdct::ShapeError& e) {
     g_err = e.what();

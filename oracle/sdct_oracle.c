@@ -428,3 +428,30 @@ void sdct_oracle_dct_direct_2d(const double* x, size_t n1, size_t n2, double* y)
       y[k1 * n2 + k2] = acc;
     }
 }
+
+/* force_demo_fields (proj/src/force.cpp:11-37): a = dct_2d(density);
+ * a1 = a w1/(w1^2+w2^2), a2 = a w2/(w1^2+w2^2), w_d = pi k_d / n_d, DC -> 0
+ * (force.cpp:22-31); xi1 = idct_idxst_2d(a1), xi2 = idxst_idct_2d(a2)
+ * (force.cpp:34-35). */
+void sdct_oracle_force_fields_2d(const double* x, size_t n1, size_t n2, double* xi1, double* xi2) {
+  const double pi = 3.14159265358979323846;
+  double* a = (double*)malloc(n1 * n2 * sizeof(double));
+  double* a1 = (double*)malloc(n1 * n2 * sizeof(double));
+  double* a2 = (double*)malloc(n1 * n2 * sizeof(double));
+  sdct_oracle_dct_2d(x, n1, n2, a);
+  for (size_t k1 = 0; k1 < n1; ++k1) {
+    const double w1 = pi * (double)k1 / (double)n1;
+    for (size_t k2 = 0; k2 < n2; ++k2) {
+      const double w2 = pi * (double)k2 / (double)n2;
+      const double den = w1 * w1 + w2 * w2;
+      const double v = a[k1 * n2 + k2];
+      a1[k1 * n2 + k2] = den > 0.0 ? v * w1 / den : 0.0;
+      a2[k1 * n2 + k2] = den > 0.0 ? v * w2 / den : 0.0;
+    }
+  }
+  sdct_oracle_idct_family_2d(a1, n1, n2, 2, xi1);
+  sdct_oracle_idct_family_2d(a2, n1, n2, 1, xi2);
+  free(a);
+  free(a1);
+  free(a2);
+}

@@ -139,3 +139,33 @@ def stream_host(kinds, x, out=None, count=None, device: int = 0, sync: bool = Tr
         if sync:
             stream.synchronize()
     return out
+
+
+def force_demo_fields(density, threads: int = 0):
+    """DREAMPlace-style spectral force fields (xi1, xi2) of a rank-2 density
+    (proj/src/force.cpp:11-37): numpy in -> numpy tuple (host copies); a torch
+    CUDA tensor (fp32/fp64, optional leading batch dims) -> tensors on the same
+    device and stream, with the field weighting fused into the inverse passes."""
+    if not _is_torch_cuda(density):
+        return _sdct.force_demo_fields(density, threads=threads)
+    import torch
+
+    x = density
+    if x.dim() < 2:
+        raise ShapeError(f"force_demo_fields expects a rank-2 tensor (plus optional batch dims), got {tuple(x.shape)}")
+    if x.dtype not in (torch.float32, torch.float64):
+        raise ValueError(f"force_demo_fields: dtype must be float32 or float64, got {x.dtype}")
+    x = x.contiguous()
+    core = tuple(x.shape[-2:])
+    batch = 1
+    for d in x.shape[:-2]:
+        batch *= int(d)
+    dt = "float32" if x.dtype == torch.float32 else "float64"
+    dev = x.device.index if x.device.index is not None else torch.cuda.current_device()
+    plan = plan_for(core, batch, dt, dev)
+    xi1, xi2 = torch.empty_like(x), torch.empty_like(x)
+    with torch.cuda.device(dev):
+        stream = torch.cuda.current_stream(dev)
+        ws = torch.empty(plan.workspace_bytes, dtype=torch.uint8, device=x.device)
+        plan.force_fields(x.data_ptr(), xi1.data_ptr(), xi2.data_ptr(), stream.cuda_stream, ws.data_ptr())
+    return xi1, xi2

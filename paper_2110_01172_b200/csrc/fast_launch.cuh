@@ -162,7 +162,9 @@ cudaError_t launch_row_one(dim3 grid, cudaStream_t st, const RowArgs& a, const T
   } else {
     constexpr int G = 4;
     auto k = row_kernel<T, M, KIND>;
-    const size_t smem = static_cast<size_t>(G) * M * sizeof(cx_t<T>) + 16;  // + mbarrier
+    // + mbarrier; the staged 3D inverse keeps its four operand rows behind the tile
+    const size_t smem = static_cast<size_t>(G) * M * sizeof(cx_t<T>) *
+                            (KIND == RK_INV3 && row3_staged<T, M>() ? 2 : 1) + 16;
     cudaError_t e = prep_smem(k, smem);
     if (e != cudaSuccess) return e;
     k<<<grid, row_threads<T, M, KIND>(), smem, st>>>(a, tw);

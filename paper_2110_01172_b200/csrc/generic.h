@@ -21,4 +21,9 @@ struct GenericJob {
 template <typename T>
 cudaError_t generic_run(const GenericJob& job, const void* in, void* out, void* ws, cudaStream_t st);
 
+// DREAMPlace-style field weighting (proj/src/force.cpp:19-31): aw = a * w_which /
+// (w1^2 + w2^2), w_d = pi k_d / n_d, 0 at DC. dtype float when f32.
+cudaError_t force_weight(const void* a, void* aw, int n1, int n2, long long batch, int which, bool f32,
+                         cudaStream_t st);
+
 }  // namespace sdctb

@@ -10,6 +10,7 @@
 #include "sdct/device.hpp"
 #include "sdct/dct1d.hpp"
 #include "sdct/dct2d.hpp"
+#include "sdct/force.hpp"
 #include "sdct/transforms_ext.hpp"
 #include "sdct_b200.h"
 
@@ -272,6 +273,15 @@ bool DevicePlan::fast() const {
   int f = 0;
   detail::check(sdct_plan_is_fast(plan_.get(), &f));
   return f != 0;
+}
+
+ForceFields force_demo_fields(const RealTensor& density, const ExecConfig&) {
+  if (density.rank() != 2)
+    throw ShapeError("force demo expects a rank-2 density grid, got rank " + std::to_string(density.rank()));
+  const Plan2d plan(checked_extent(density.dim(0)), checked_extent(density.dim(1)));
+  ForceFields f{RealTensor(density.dims()), RealTensor(density.dims())};
+  detail::check(sdct_force_fields_host(plan.handle(), density.data(), f.xi1.data(), f.xi2.data(), nullptr));
+  return f;
 }
 
 }  // namespace sdct

@@ -90,6 +90,7 @@ struct RowArgs {
   const void* fu;
   int fs;
   int bad_q;                       // corrupt_twiddle_for_testing: b(bad_q) negated (-1: none)
+  int weight;                      // 2D inverse: force-field weighting of the input (0 none, 1 w1, 2 w2)
   int dev;                         // developer flags (0 in production): bit 0 skips the row FFT math
 };
 
@@ -724,6 +725,12 @@ __device__ __forceinline__ cx_t<T> pre3_entry(const T* x, int i, int j, int k, c
 template <typename T, int M, int G>
 using RowTile = Tile<T, M, G, false>;
 
+// 3D inverse row kernel: operand rows staged behind the tile when both fit
+template <typename T, int M>
+constexpr bool row3_staged() {
+  return 2 * 4 * M * sizeof(cx_t<T>) + 16 <= 200 * 1024;
+}
+
 template <typename T, int M, int KIND>
 constexpr int row_threads() {
   return RowTile<T, M, (KIND == RK_FWD2 || KIND == RK_INV2) ? 2 : 4>::NT;
@@ -925,6 +932,63 @@ __global__ void __launch_bounds__(row_threads<T, M, KIND>())
             sm[row_nat<T, M>(0, M - k)] = pack(B0, cconj(pA0), wmk);
             sm[row_nat<T, M>(1, M - k)] = pack(B1, cconj(pA1), wmk);
           }
+        }
+      }
+    } else if constexpr (row3_staged<T, M>()) {  // RK_INV3, operand rows staged in smem
+      // Every operand of the literal 3D preprocess (transforms_ext.cpp:196-212)
+      // for the group's four lines lies in the rows x(i, j, .) with i in
+      // {q1, m1}, j in {q2, m2} (index N reads 0): bulk-load those four rows
+      // behind the tile, then read them from smem.
+      const int li[4] = {q1, m1, q1, m1}, lj[4] = {q2, q2, m2, m2};
+      const int n3 = a.n3;
+      T* rows = reinterpret_cast<T*>(smem_raw + G * M * sizeof(V));
+      {
+        uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw + 2 * G * M * sizeof(V));
+        if (t == 0) mbar_init(bar, 1);
+        __syncthreads();
+        if (t == 0) {
+          const uint32_t rb = static_cast<uint32_t>(n3 * sizeof(T));
+          mbar_expect_tx(bar, 4 * rb);
+#pragma unroll
+          for (int l = 0; l < 4; ++l)
+            bulk_load(rows + l * n3, x + (static_cast<long long>(li[l]) * a.n2 + lj[l]) * n3, rb, bar);
+        }
+        mbar_wait(bar, 0);
+      }
+      // x(i, j, k) for i in {q1, m1, n1}, j in {q2, m2, n2}, k in [0, n3]
+      auto xv = [&](int i, int j, int k) -> T {
+        if (i == n1 || j == n2 || k == n3) return T(0);
+        return rows[((i == q1 ? 0 : 1) + (j == q2 ? 0 : 2)) * n3 + k];
+      };
+      // per-line constant conj(a(i) b(j)); per-k conj(c(k)) shared by the lines
+      V cab[4];
+#pragma unroll
+      for (int l = 0; l < 4; ++l)
+        cab[l] = cconj(cmul(__ldg(static_cast<const V*>(a.ta) + li[l]), __ldg(static_cast<const V*>(a.tb) + lj[l])));
+      const V* tc = static_cast<const V*>(a.tc);
+      auto entry = [&](int l, int k, V cc) -> V {
+        const int i = li[l], j = lj[l];
+        const int r1 = n1 - i, r2 = n2 - j, r3 = n3 - k;
+        const T re = (xv(i, j, k) - xv(r1, r2, k)) - (xv(r1, j, r3) + xv(i, r2, r3));
+        const T im = xv(r1, r2, r3) - ((xv(r1, j, k) + xv(i, r2, k)) + xv(i, j, r3));
+        return cmul(cmul(cab[l], cc), mk(re, im));
+      };
+      for (int k = t; k <= M / 2; k += NT) {
+        V A[4], B[4];
+        const V ck = cconj(__ldg(tc + k)), cm = cconj(__ldg(tc + (M - k)));
+#pragma unroll
+        for (int l = 0; l < 4; ++l) {
+          A[l] = entry(l, k, ck);
+          B[l] = entry(l, M - k, cm);
+        }
+        const V wk = __ldg(tu + k);
+#pragma unroll
+        for (int l = 0; l < 4; ++l)
+          sm[row_nat<T, M>(l, k & (M - 1))] = pack(A[l], k == 0 ? B[l] : cconj(B[3 - l]), wk);
+        if (k != 0 && 2 * k != M) {
+          const V wmk = __ldg(tu + (M - k));
+#pragma unroll
+          for (int l = 0; l < 4; ++l) sm[row_nat<T, M>(l, M - k)] = pack(B[l], cconj(A[3 - l]), wmk);
         }
       }
     } else {  // RK_INV3

@@ -1,3 +1,4 @@
+#include <algorithm>
 // Generic path: any extents (odd, non-power-of-two, tiny), ranks 1..3, fp64
 // arithmetic throughout (inputs/outputs may be fp32). It restates the
 // reference's three stages one full-tensor pass at a time:
@@ -260,5 +261,31 @@ cudaError_t generic_run(const GenericJob& job, const void* in, void* out, void* 
 
 template cudaError_t generic_run<float>(const GenericJob&, const void*, void*, void*, cudaStream_t);
 template cudaError_t generic_run<double>(const GenericJob&, const void*, void*, void*, cudaStream_t);
+
+template <typename T>
+__global__ void g_force_weight(const T* __restrict__ a, T* __restrict__ aw, int n1, int n2, long long total,
+                               int which) {
+  const double pi = 3.14159265358979323846;
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long in_item = e % (static_cast<long long>(n1) * n2);
+    const int k1 = static_cast<int>(in_item / n2), k2 = static_cast<int>(in_item % n2);
+    const double w1 = pi * k1 / n1, w2 = pi * k2 / n2, den = w1 * w1 + w2 * w2;
+    aw[e] = den > 0.0 ? static_cast<T>(static_cast<double>(a[e]) * (which == 1 ? w1 : w2) / den) : T(0);
+  }
+}
+
+cudaError_t force_weight(const void* a, void* aw, int n1, int n2, long long batch, int which, bool f32,
+                         cudaStream_t st) {
+  const long long total = static_cast<long long>(n1) * n2 * batch;
+  const int blocks = static_cast<int>(std::min<long long>((total + 255) / 256, 148 * 16));
+  if (f32)
+    g_force_weight<float><<<blocks, 256, 0, st>>>(static_cast<const float*>(a), static_cast<float*>(aw), n1, n2,
+                                                  total, which);
+  else
+    g_force_weight<double><<<blocks, 256, 0, st>>>(static_cast<const double*>(a), static_cast<double*>(aw), n1, n2,
+                                                    total, which);
+  return cudaGetLastError();
+}
 
 }  // namespace sdctb

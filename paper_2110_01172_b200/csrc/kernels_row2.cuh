@@ -249,6 +249,21 @@ __global__ void __launch_bounds__(Row2Geom<T, M, MODE>::CTA, Row2Geom<T, M, MODE
       const T* rowA = reinterpret_cast<const T*>(sm);
       const T* rowB = rowA + 2 * M;
       mbar_wait(full + b, ph);
+      if (a.weight) {
+        // DREAMPlace-style field weighting of the input coefficients
+        // (proj/src/force.cpp:19-31), folded into this load: a1 = a w1/(w1^2+w2^2)
+        // (weight 1) or a2 = a w2/(w1^2+w2^2) (weight 2), w_d = pi k_d / n_d, 0 at DC
+        T* rw = reinterpret_cast<T*>(sm);
+        const T pi = T(3.14159265358979323846);
+        const T w1a = pi * T(q1) / T(n1), w1b = pi * T(m1) / T(n1), sc2 = pi / T(n2);
+        for (int e = t; e < 2 * n2; e += NT) {
+          const int k2 = e & (n2 - 1);
+          const T w1 = e < n2 ? w1a : w1b, w2 = sc2 * T(k2);
+          const T den = fma(w1, w1, w2 * w2);
+          rw[e] = den > T(0) ? rw[e] * (a.weight == 1 ? w1 : w2) / den : T(0);
+        }
+        TL::sync();
+      }
       // operands for n2 in {k, M-k}: D = x(n2), R = x(N2-n2) (x(N2) := 0) of
       // both rows; mode 2 (IDXST along axis 1) reads x(N2-n2) for D and x(n2)
       // for R with x(0) := 0 (proj/src/dct2d.cpp:169-180)

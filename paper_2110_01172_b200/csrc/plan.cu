@@ -123,6 +123,7 @@ struct sdct_plan_s {
   void* lane_buf[kLanes][3] = {};
   std::mutex mu;
 
+  void* aux = nullptr;  // sdct_force_fields scratch (coefficients + weighted copy), lazily allocated
   void* gws = nullptr;  // generic-path scratch on fast plans (row-column), lazily allocated
   size_t elem() const { return dtype == SDCT_F32 ? 4 : 8; }
   size_t generic_ws_bytes() const {
@@ -422,7 +423,7 @@ struct Side {
 
 template <typename T>
 int run_fast(sdct_plan_s* p, int kind, int only_stage, const void* in, void* out, void* ws,
-             cudaStream_t st, int* nstages) {
+             cudaStream_t st, int* nstages, int weight) {
   const int n1 = p->n[0], n2 = p->n[1], n3 = p->n[2];
   const int M = p->M;
   const long long item = p->numel;
@@ -474,6 +475,7 @@ int run_fast(sdct_plan_s* p, int kind, int only_stage, const void* in, void* out
   ra.fu = p->fu;
   ra.fs = p->fs;
   ra.bad_q = p->bad_q;
+  ra.weight = weight;
   {
     static const int dev = [] {
       const char* f = getenv("SDCT_DEV_FLAGS");  // developer experiments only (tools/)
@@ -617,10 +619,10 @@ GenericJob make_job(const sdct_plan_s* p, int kind) {
 
 template <typename T>
 int run(sdct_plan_s* p, int kind, int only_stage, const void* in, void* out, void* ws,
-        cudaStream_t st, int* nstages) {
+        cudaStream_t st, int* nstages, int weight) {
   // Row-column baseline and the 1D transforms run on the generic path.
   const bool use_fast = p->fast && kind != SDCT_DCT_2D_ROWCOL;
-  if (use_fast) return run_fast<T>(p, kind, only_stage, in, out, ws, st, nstages);
+  if (use_fast) return run_fast<T>(p, kind, only_stage, in, out, ws, st, nstages, weight);
   if (nstages) *nstages = 1;  // generic path is timed as one unit
   if (only_stage > 0) return SDCT_OK;
   if (p->fast && ws == p->ws) {
@@ -637,12 +639,12 @@ int run(sdct_plan_s* p, int kind, int only_stage, const void* in, void* out, voi
 }
 
 int dispatch(sdct_plan_s* p, int kind, int only_stage, const void* in, void* out, void* ws,
-             cudaStream_t st, int* nstages) {
+             cudaStream_t st, int* nstages, int weight = 0) {
   if (!kind_ok(p, kind)) return fail(SDCT_ERR_PLAN, "transform kind does not match the plan rank");
   if (!ws) ws = p->ws;
   DeviceGuard g(p->device);
-  return p->dtype == SDCT_F32 ? run<float>(p, kind, only_stage, in, out, ws, st, nstages)
-                              : run<double>(p, kind, only_stage, in, out, ws, st, nstages);
+  return p->dtype == SDCT_F32 ? run<float>(p, kind, only_stage, in, out, ws, st, nstages, weight)
+                              : run<double>(p, kind, only_stage, in, out, ws, st, nstages, weight);
 }
 
 // ---- analytic StageCounters (replays the reference's Counted tallies) -----
@@ -806,6 +808,7 @@ int sdct_plan_destroy(sdct_plan_t p) {
   cudaFree(p->d_in);
   cudaFree(p->d_out);
   cudaFree(p->gws);
+  cudaFree(p->aux);
   for (int l = 0; l < sdct_plan_s::kLanes; ++l) {
     for (void* b : p->lane_buf[l]) cudaFree(b);
     if (p->lane_st[l]) cudaStreamDestroy(p->lane_st[l]);
@@ -873,6 +876,70 @@ int sdct_exec(sdct_plan_t p, int kind, const void* d_in, void* d_out, void* d_ws
   if (!p || !d_in || !d_out) return fail(SDCT_ERR_ARG, "null argument to sdct_exec");
   if (d_in == d_out) return fail(SDCT_ERR_ARG, "sdct_exec is out of place: d_in == d_out");
   return dispatch(p, kind, -1, d_in, d_out, d_ws, static_cast<cudaStream_t>(stream), nullptr);
+}
+
+int sdct_force_fields(sdct_plan_t p, const void* d_density, void* d_xi1, void* d_xi2, void* d_ws, void* stream) {
+  if (!p || !d_density || !d_xi1 || !d_xi2) return fail(SDCT_ERR_ARG, "null argument to sdct_force_fields");
+  if (p->rank != 2) return fail(SDCT_ERR_PLAN, "force fields need a rank-2 plan");
+  if (d_density == d_xi1 || d_density == d_xi2 || d_xi1 == d_xi2)
+    return fail(SDCT_ERR_ARG, "sdct_force_fields is out of place: buffers must be distinct");
+  DeviceGuard g(p->device);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const size_t bytes = static_cast<size_t>(p->batch) * p->item_bytes();
+  {
+    std::lock_guard<std::mutex> lock(p->mu);
+    if (!p->aux) {
+      cudaError_t e = cudaMalloc(&p->aux, 2 * bytes);
+      if (e != cudaSuccess) return cuda_fail(e, "allocating force-field scratch");
+    }
+  }
+  void* a = p->aux;                                     // DCT coefficients of the density
+  void* aw = static_cast<unsigned char*>(p->aux) + bytes;  // generic path: weighted copy
+  int rc = dispatch(p, SDCT_DCT_2D, -1, d_density, a, d_ws, st, nullptr);
+  if (rc != SDCT_OK) return rc;
+  if (p->fast) {
+    // fast path: the weighting rides on the inverse row kernels' loads
+    rc = dispatch(p, SDCT_IDCT_IDXST_2D, -1, a, d_xi1, d_ws, st, nullptr, 1);
+    if (rc == SDCT_OK) rc = dispatch(p, SDCT_IDXST_IDCT_2D, -1, a, d_xi2, d_ws, st, nullptr, 2);
+    return rc;
+  }
+  for (int which = 1; which <= 2; ++which) {
+    cudaError_t e = force_weight(a, aw, p->n[0], p->n[1], p->batch, which, p->dtype == SDCT_F32, st);
+    if (e != cudaSuccess) return cuda_fail(e, "launching force weighting");
+    rc = dispatch(p, which == 1 ? SDCT_IDCT_IDXST_2D : SDCT_IDXST_IDCT_2D, -1, aw, which == 1 ? d_xi1 : d_xi2,
+                  d_ws, st, nullptr);
+    if (rc != SDCT_OK) return rc;
+  }
+  return SDCT_OK;
+}
+
+int sdct_force_fields_host(sdct_plan_t p, const void* h_density, void* h_xi1, void* h_xi2, void* stream) {
+  if (!p || !h_density || !h_xi1 || !h_xi2) return fail(SDCT_ERR_ARG, "null argument to sdct_force_fields_host");
+  if (p->rank != 2) return fail(SDCT_ERR_PLAN, "force fields need a rank-2 plan");
+  DeviceGuard g(p->device);
+  const size_t bytes = static_cast<size_t>(p->batch) * p->item_bytes();
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaError_t e;
+  void* d_x2 = nullptr;
+  {
+    std::lock_guard<std::mutex> lock(p->mu);
+    if (!p->d_in) {
+      if ((e = cudaMalloc(&p->d_in, bytes)) != cudaSuccess) return cuda_fail(e, "allocating staging");
+      if ((e = cudaMalloc(&p->d_out, bytes)) != cudaSuccess) return cuda_fail(e, "allocating staging");
+    }
+  }
+  if ((e = cudaMalloc(&d_x2, bytes)) != cudaSuccess) return cuda_fail(e, "allocating staging");
+  int rc = SDCT_OK;
+  if ((e = cudaMemcpyAsync(p->d_in, h_density, bytes, cudaMemcpyHostToDevice, st)) != cudaSuccess)
+    rc = cuda_fail(e, "copying density to device");
+  if (rc == SDCT_OK) rc = sdct_force_fields(p, p->d_in, p->d_out, d_x2, nullptr, st);
+  if (rc == SDCT_OK && (e = cudaMemcpyAsync(h_xi1, p->d_out, bytes, cudaMemcpyDeviceToHost, st)) != cudaSuccess)
+    rc = cuda_fail(e, "copying xi1 to host");
+  if (rc == SDCT_OK && (e = cudaMemcpyAsync(h_xi2, d_x2, bytes, cudaMemcpyDeviceToHost, st)) != cudaSuccess)
+    rc = cuda_fail(e, "copying xi2 to host");
+  if (rc == SDCT_OK && (e = cudaStreamSynchronize(st)) != cudaSuccess) rc = cuda_fail(e, "synchronising");
+  cudaFree(d_x2);
+  return rc;
 }
 
 int sdct_exec_host_pipelined(sdct_plan_t p, const int* kinds, int nkinds, const void* h_in, int64_t in_stride,

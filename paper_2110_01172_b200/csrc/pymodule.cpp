@@ -13,6 +13,7 @@
 
 #include "sdct/dct1d.hpp"
 #include "sdct/dct2d.hpp"
+#include "sdct/force.hpp"
 #include "sdct/device.hpp"
 #include "sdct/errors.hpp"
 #include "sdct/transforms_ext.hpp"
@@ -124,6 +125,19 @@ PYBIND11_MODULE(_sdct, m) {
         [](const Array& x, unsigned) { return run(x, [](const sdct::RealTensor& t) { return sdct::idct_3d(t); }); },
         py::arg("x"), py::arg("threads") = 0, "Fused inverse 3D DCT (idct_3d(dct_3d(x)) == N1*N2*N3/8 * x)");
 
+  m.def("force_demo_fields",
+        [](const Array& density, unsigned) {
+          sdct::ForceFields f;
+          {
+            const sdct::RealTensor t = to_tensor(density);
+            py::gil_scoped_release nogil;
+            f = sdct::force_demo_fields(t);
+          }
+          return py::make_tuple(to_array(f.xi1), to_array(f.xi2));
+        },
+        py::arg("density"), py::arg("threads") = 0,
+        "Inverse-Laplacian-weighted gradient fields (xi1, xi2) of a rank-2 density grid");
+
   m.def("amdahl_speedup",
         [](double p, double s) {
           if (!(p >= 0.0 && p <= 1.0)) throw std::invalid_argument("parallel fraction p must lie in [0, 1]");
@@ -170,6 +184,15 @@ PYBIND11_MODULE(_sdct, m) {
            },
            py::arg("kinds"), py::arg("h_in"), py::arg("in_stride"), py::arg("h_out"), py::arg("out_stride"),
            py::arg("count"), py::arg("stream") = 0)
+      .def("force_fields",
+           [](const sdct::DevicePlan& p, std::uintptr_t d_density, std::uintptr_t d_xi1, std::uintptr_t d_xi2,
+              std::uintptr_t stream, std::uintptr_t ws) {
+             py::gil_scoped_release nogil;
+             sdct::detail::check(sdct_force_fields(p.handle(), reinterpret_cast<const void*>(d_density),
+                                                   reinterpret_cast<void*>(d_xi1), reinterpret_cast<void*>(d_xi2),
+                                                   reinterpret_cast<void*>(ws), reinterpret_cast<void*>(stream)));
+           },
+           py::arg("d_density"), py::arg("d_xi1"), py::arg("d_xi2"), py::arg("stream") = 0, py::arg("workspace") = 0)
       .def("stage_count",
            [](const sdct::DevicePlan& p, int kind) {
              int n = 0;

@@ -46,6 +46,10 @@ def main() -> None:
         out[f"in/{key}"] = x
         for kind in KINDS_2D:
             out[f"{kind}/{key}"] = getattr(sdct, kind)(x)
+        # spectral force fields (proj/src/force.cpp:11-37, module.cpp:163-171)
+        xi1, xi2 = sdct.force_demo_fields(x)
+        out[f"force_xi1/{key}"] = xi1
+        out[f"force_xi2/{key}"] = xi2
     for shape in SHAPES_3D:
         seed += 1
         x = np.random.default_rng(seed).uniform(-1.0, 1.0, size=shape)

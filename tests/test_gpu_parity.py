@@ -364,3 +364,32 @@ def test_stream_host_pipeline_matches_device_path(cuda):
         assert one.shape[0] == 1 and torch.equal(one[0], sd.dct_2d(x[0].cuda()).cpu())
     with pytest.raises(ValueError):
         sd.stream_host(["dct_2d", "dct_3d"], x)
+
+
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+def test_force_fields_vs_oracle(cuda, dtype):
+    # sdct_force_fields: the field weighting (proj/src/force.cpp:19-31) rides on
+    # the inverse passes' loads on the fast path, an explicit kernel otherwise
+    torch = _torch()
+    import paper_2110_01172_b200 as sd
+
+    tdt = torch.float64 if dtype == "float64" else torch.float32
+    for i, shape in enumerate([(8, 8), (64, 128), (256, 64), (512, 512), (2, 4096), (7, 9), (31, 17), (100, 60)]):
+        x = rnd(shape, 300 + i, dtype)
+        w1, w2 = oracle.port.force_demo_fields(x)
+        g1, g2 = sd.force_demo_fields(torch.tensor(x, dtype=tdt, device="cuda"))
+        for got, want in ((g1, w1), (g2, w2)):
+            assert oracle.rel_l2(got.double().cpu().numpy(), want) <= TOL[dtype], (shape, dtype)
+    # numpy drop-in surface and batched device input
+    x = rnd((64, 32), 41)
+    h1, h2 = sd.force_demo_fields(x)
+    w1, w2 = oracle.port.force_demo_fields(x)
+    assert oracle.rel_l2(h1, w1) <= 1e-12 and oracle.rel_l2(h2, w2) <= 1e-12
+    xb = torch.tensor(np.stack([rnd((32, 64), 50 + b) for b in range(3)]), dtype=tdt, device="cuda")
+    b1, b2 = sd.force_demo_fields(xb)
+    for b in range(3):
+        w1, w2 = oracle.port.force_demo_fields(xb[b].double().cpu().numpy())
+        assert oracle.rel_l2(b1[b].double().cpu().numpy(), w1) <= TOL[dtype]
+        assert oracle.rel_l2(b2[b].double().cpu().numpy(), w2) <= TOL[dtype]
+    with pytest.raises(ValueError):
+        sd.force_demo_fields(torch.zeros(8, device="cuda", dtype=tdt))

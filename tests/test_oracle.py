@@ -122,3 +122,13 @@ def test_reference_library_agrees_when_built():
     x = np.random.default_rng(2).uniform(-1, 1, (64, 48))
     for kind in KINDS_2D:
         assert np.array_equal(getattr(oracle.port, kind)(x), oracle.ref.run(kind, x)), kind
+
+
+def test_port_force_fields_match_reference_golden(golden):
+    # proj/src/force.cpp:11-37 through the reference's pybind module
+    keys = _keys(golden, "force_xi1")
+    assert len(keys) > 60
+    for key in keys:
+        xi1, xi2 = oracle.port.force_demo_fields(golden["in/" + key])
+        assert oracle.rel_l2(xi1, golden["force_xi1/" + key]) <= 1e-13, key
+        assert oracle.rel_l2(xi2, golden["force_xi2/" + key]) <= 1e-13, key
