@@ -9,6 +9,7 @@
 
 #include "kernels_fast.cuh"
 #include "kernels_row2.cuh"
+#include "kernels_col2.cuh"
 
 namespace sdctb {
 
@@ -29,6 +30,12 @@ __host__ __device__ constexpr int nl_default(int esize, int L) {
              : (64 * 1024) / ((col_split(L) ? L / 2 : L) * 2 * esize);
 }
 
+// Cluster-split column pass (kernels_col2.cuh): 2D fp64 columns of 4096 rows
+// with 2-complex (32-B) bands run as two 64 KB halves per 2-CTA cluster.
+__host__ __device__ constexpr bool col2_used(int esize, int L, int planes, int nl) {
+  return esize == 8 && L == 4096 && planes == 1 && nl == 2;
+}
+
 // Opt each kernel instantiation in to > 48 KB dynamic shared memory (once).
 cudaError_t prep_smem_ptr(const void* kernel, size_t smem);
 template <typename K>
@@ -42,6 +49,8 @@ cudaError_t launch_col(int variant, int L, int nl, dim3 grid, cudaStream_t st, c
                        const CUtensorMap& omap, const ColArgs& a, const TwSet& tw);
 template <typename T>
 cudaError_t launch_row(int M, int kind, dim3 grid, cudaStream_t st, const RowArgs& a, const TwSet& tw);
+cudaError_t launch_col2(bool inv, int bands, int batch, cudaStream_t st, const CUtensorMap& map, const CUtensorMap& omap,
+                        const ColArgs& a, const TwSet& tw);
 
 // threads per CTA (host side, must match the kernels' compile-time geometry)
 inline int tile_threads(int L, int nl) {

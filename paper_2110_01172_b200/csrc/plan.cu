@@ -94,6 +94,8 @@ struct sdct_plan_s {
   int nl[2] = {2, 2};   // column-kernel band widths: pass over axis 0, pass over axis 1 (3D)
   TwSet tw_col[2] = {};  // per-stage twiddle tables: axis-0 / axis-1 column FFTs
   TwSet tw_row = {};     // row FFT (length M)
+  TwSet tw_col2 = {};    // cluster-split column pass: H-point stage tables (H = n1 / 2)
+  bool col2 = false;     // 2D column passes run cluster-split (col2_used)
   void* tw_comb[2] = {nullptr, nullptr};  // split column passes: W_L^k, k < L/2
   // device tables (one allocation)
   void* tables = nullptr;
@@ -221,7 +223,7 @@ int build_plan(sdct_plan_s* p) {
   std::vector<long double> re, im;
   size_t off_ta = 0, off_tb = 0, off_tc = 0, off_tu = 0;
   size_t off_gq[3] = {0, 0, 0}, off_gc[3] = {0, 0, 0};
-  size_t st_c0[4], st_c1[4], st_r[4];
+  size_t st_c0[4], st_c1[4], st_r[4], st_c2[4] = {SIZE_MAX, SIZE_MAX, SIZE_MAX, SIZE_MAX};
   size_t off_comb[2] = {SIZE_MAX, SIZE_MAX};
   size_t off_srow[2] = {SIZE_MAX, SIZE_MAX};
   size_t off_fb = 0, off_fu = 0;
@@ -241,6 +243,19 @@ int build_plan(sdct_plan_s* p) {
     stages(col_split(p->n[0]) ? p->n[0] / 2 : p->n[0], st_c0);
     if (r == 3) stages(col_split(p->n[1]) ? p->n[1] / 2 : p->n[1], st_c1);
     stages(p->M, st_r);
+    p->nl[0] = pick_nl(static_cast<int>(p->elem()), p->n[0], p->M, (r == 2 ? 1 : p->n[1]) * p->batch);
+    // measured slower than the single-CTA pass on B200 (108 vs 86 us at 4096^2,
+    // DESIGN.md §6): kept as an opt-in experiment (SDCT_COL2=1 at plan creation)
+    static const bool col2_opt = [] {
+      const char* f = getenv("SDCT_COL2");
+      return f && atoi(f) == 1;
+    }();
+    p->col2 = col2_opt && r == 2 && col2_used(static_cast<int>(p->elem()), p->n[0], 1, p->nl[0]);
+    if (p->col2) {
+      stages(p->n[0] / 2, st_c2);
+      circle(re, im, p->n[0] / 2, 1.0L, p->n[0]);  // W_L^k, k < L/2
+      put(off_comb[0]);
+    }
     for (int ax = 0; ax < (r == 3 ? 2 : 1); ++ax) {
       if (col_split(p->n[ax])) {
         circle(re, im, p->n[ax] / 2, 1.0L, p->n[ax]);
@@ -284,7 +299,9 @@ int build_plan(sdct_plan_s* p) {
       off_srow[ax] = (blob.size() + 255) & ~size_t(255);
       blob.resize(off_srow[ax] + p->n[ax] * sizeof(int));
       int* q = reinterpret_cast<int*>(blob.data() + off_srow[ax]);
-      for (int k = 0; k < p->n[ax]; ++k) q[k] = rt_srow(k, p->n[ax]);
+      const int L = p->n[ax], H = L / 2;
+      for (int k = 0; k < L; ++k)  // cluster-split passes: k = 2k' + c at row cH + sigma_H(k')
+        q[k] = (ax == 0 && p->col2) ? (k & 1) * H + rt_srow(k >> 1, H) : rt_srow(k, L);
     }
     const long long pb0 = (r == 2 ? 1 : p->n[1]) * p->batch;
     p->nl[0] = pick_nl(static_cast<int>(p->elem()), p->n[0], p->M, pb0);
@@ -312,6 +329,7 @@ int build_plan(sdct_plan_s* p) {
     tws(st_c0, p->tw_col[0]);
     if (r == 3) tws(st_c1, p->tw_col[1]);
     tws(st_r, p->tw_row);
+    if (p->col2) tws(st_c2, p->tw_col2);
     for (int ax = 0; ax < 2; ++ax) p->tw_comb[ax] = off_comb[ax] == SIZE_MAX ? nullptr : base + off_comb[ax];
     p->ta = base + off_ta;
     p->tb = base + off_tb;
@@ -457,6 +475,27 @@ int run_fast(sdct_plan_s* p, int kind, int only_stage, const void* in, void* out
     }
     ++stage;
   };
+  // cluster-split 2D column pass (kernels_col2.cuh): forward reads the source
+  // through the parity-class map, the inverse writes y through it
+  auto col2 = [&](bool inv, ColArgs a, const Side& in, const Side& o) {
+    a.twc = p->tw_comb[0];
+    if (want() && e == cudaSuccess && map_ok) {
+      CUtensorMap mi, mo;
+      if (!inv) {
+        map_ok = make_class_map(&mi, f32, a.src, in.inner, in.rows, in.row_stride * es, in.planes, in.plane_stride * es, B,
+                                in.batch_stride * es, p->nl[0]) &&
+                 make_col_map(&mo, f32, a.dst, o.inner, o.rows, o.row_stride * es, o.planes, o.plane_stride * es, B,
+                              o.batch_stride * es, p->nl[0], 256);
+      } else {
+        map_ok = make_col_map(&mi, f32, a.src, in.inner, in.rows, in.row_stride * es, in.planes, in.plane_stride * es, B,
+                              in.batch_stride * es, p->nl[0], 256) &&
+                 make_class_map(&mo, f32, a.dst, o.inner, o.rows, o.row_stride * es, o.planes, o.plane_stride * es, B,
+                                o.batch_stride * es, p->nl[0]);
+      }
+      if (map_ok) e = launch_col2(inv, M / p->nl[0], B, st, mi, mo, a, p->tw_col2);
+    }
+    ++stage;
+  };
   auto row = [&](int rk, int groups, const RowArgs& a) {
     if (want() && e == cudaSuccess) e = launch_row<T>(M, rk, dim3(groups, B), st, a, p->tw_row);
     ++stage;
@@ -493,8 +532,11 @@ int run_fast(sdct_plan_s* p, int kind, int only_stage, const void* in, void* out
       c.in_batch = item;
       c.out_row = M;
       c.out_batch = inter;
-      col(CV_FWD_SRC, n1, p->nl[0], 1, c, p->tw_col[0], Side{n2, n1, n2, 1, item, item},
-          Side{2LL * M, n1, 2LL * M, 1, 2 * inter, 2 * inter});
+      if (p->col2)
+        col2(false, c, Side{n2, n1, n2, 1, item, item}, Side{2LL * M, n1, 2LL * M, 1, 2 * inter, 2 * inter});
+      else
+        col(CV_FWD_SRC, n1, p->nl[0], 1, c, p->tw_col[0], Side{n2, n1, n2, 1, item, item},
+            Side{2LL * M, n1, 2LL * M, 1, 2 * inter, 2 * inter});
       ra.src = ws;
       ra.src_batch = inter;
       ra.dst = out;
@@ -518,8 +560,11 @@ int run_fast(sdct_plan_s* p, int kind, int only_stage, const void* in, void* out
       c.scale = 0.25;
       c.sign_row = mode == 1;
       c.sign_col = mode == 2;
-      col(CV_INV_DST, n1, p->nl[0], 1, c, p->tw_col[0], Side{2LL * M, n1, 2LL * M, 1, 2 * inter, 2 * inter},
-          Side{n2, n1, n2, 1, item, item});
+      if (p->col2)
+        col2(true, c, Side{2LL * M, n1, 2LL * M, 1, 2 * inter, 2 * inter}, Side{n2, n1, n2, 1, item, item});
+      else
+        col(CV_INV_DST, n1, p->nl[0], 1, c, p->tw_col[0], Side{2LL * M, n1, 2LL * M, 1, 2 * inter, 2 * inter},
+            Side{n2, n1, n2, 1, item, item});
     }
   } else {
     const long long inter = static_cast<long long>(n1) * n2 * M;
