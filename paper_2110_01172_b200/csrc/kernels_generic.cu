@@ -12,7 +12,8 @@
 //             as irfft_nd does, rfft.cpp:233-243) -> inverse DFT per axis ->
 //             real part, inverse parity gather, scale and sign (214-238).
 // It is the correctness path for shapes outside the power-of-two fast path;
-// cost is O(numel * sum(N_axis)).
+// cost is O(numel * sum(radices of N_axis)) with the shared-memory mixed-radix
+// line FFT (extents <= 4096), O(numel * N_axis) direct sums beyond.
 #include "generic.h"
 #include "sdct_common.cuh"
 
@@ -78,6 +79,129 @@ __global__ void g_dft_axis(const double2* __restrict__ in, double2* __restrict__
     }
     out[f] = make_double2(re, im);
   }
+}
+
+// ---- mixed-radix line FFT (Stockham autosort in shared memory) -------------
+// Replaces the O(n) direct sum per output with sum(radices) complex MACs per
+// element for composite n (any factorisation; a prime factor p costs p MACs,
+// so a prime extent degenerates to the direct sum, now from shared memory).
+// One CTA owns LPC lines of one axis: LPC consecutive i (inner > 1, each
+// step reads LPC contiguous elements) or LPC consecutive rows (inner == 1).
+// Pass t (radix R, Ns = product of the previous radices), for each output:
+//   y[(j / Ns) Ns R + j % Ns + k Ns] = sum_r x[j + r n/R] W_n^{r E},
+//   E = (j % Ns) n / (Ns R) + k n / R  (twiddle and radix-R DFT fused).
+struct Radices {
+  int count;
+  int r[24];
+};
+
+constexpr int kFftMaxN = 4096;  // two line buffers + table in shared memory
+
+__global__ void g_fft_axis_smem(const double2* __restrict__ in, double2* __restrict__ out, long long outer, int n,
+                                long long inner, const double2* __restrict__ tab, int inverse, Radices rad, int lpc) {
+  extern __shared__ __align__(16) double2 fsm[];
+  double2* tw = fsm;               // n
+  double2* b0 = fsm + n;           // lpc * n
+  double2* b1 = b0 + static_cast<long long>(lpc) * n;
+  const int t = threadIdx.x, nt = blockDim.x;
+  for (int e = t; e < n; e += nt) {
+    double2 w = tab[e];
+    if (inverse) w.y = -w.y;
+    tw[e] = w;
+  }
+  // tile of lines: (o, i0..i0+lpc) for inner > 1, rows o0..o0+lpc for inner == 1
+  const long long tiles_per_o = inner > 1 ? inner / lpc : 1;
+  const long long tile = blockIdx.x;
+  long long o, i0;
+  if (inner > 1) {
+    o = tile / tiles_per_o;
+    i0 = (tile % tiles_per_o) * lpc;
+  } else {
+    o = tile * lpc;
+    i0 = 0;
+  }
+  const long long lines = inner > 1 ? lpc : std::min<long long>(lpc, outer - o);
+  // load: element m of line l at b0[l * n + m]
+  for (long long e = t; e < lines * n; e += nt) {
+    long long l, m, src;
+    if (inner > 1) {
+      m = e / lpc;
+      l = e % lpc;
+      src = (o * n + m) * inner + i0 + l;
+    } else {
+      l = e / n;
+      m = e % n;
+      src = (o + l) * n + m;
+    }
+    b0[l * n + m] = in[src];
+  }
+  __syncthreads();
+  double2* x = b0;
+  double2* y = b1;
+  int ns = 1;
+  for (int s = 0; s < rad.count; ++s) {
+    const int R = rad.r[s];
+    const int nr = n / R;
+    for (long long e = t; e < lines * n; e += nt) {
+      const int l = static_cast<int>(e / n), q = static_cast<int>(e % n);
+      // output q = (j / ns) ns R + j % ns + k ns with j in [0, n/R), k in [0, R)
+      const int jr = q % ns, rest = q / ns;
+      const int k = rest % R, jq = rest / R;
+      const int j = jq * ns + jr;
+      const int E = (jr * (n / (ns * R)) + k * nr) % n;
+      const double2* xl = x + static_cast<long long>(l) * n + j;
+      double re = 0.0, im = 0.0;
+      int idx = 0;
+      for (int r = 0; r < R; ++r) {
+        const double2 v = xl[r * nr], w = tw[idx];
+        re += v.x * w.x - v.y * w.y;
+        im += v.x * w.y + v.y * w.x;
+        idx += E;
+        if (idx >= n) idx -= n;
+      }
+      y[static_cast<long long>(l) * n + q] = make_double2(re, im);
+    }
+    __syncthreads();
+    double2* tmp = x;
+    x = y;
+    y = tmp;
+    ns *= R;
+  }
+  for (long long e = t; e < lines * n; e += nt) {
+    long long l, m, dst;
+    if (inner > 1) {
+      m = e / lpc;
+      l = e % lpc;
+      dst = (o * n + m) * inner + i0 + l;
+    } else {
+      l = e / n;
+      m = e % n;
+      dst = (o + l) * n + m;
+    }
+    out[dst] = x[l * n + m];
+  }
+}
+
+Radices factorise(int n) {
+  Radices rad{};
+  // radix 8/4/2 first, then small odd primes, then whatever prime remains
+  for (int r : {8, 4, 2}) {
+    while (n % r == 0 && rad.count < 24) {
+      rad.r[rad.count++] = r;
+      n /= r;
+    }
+  }
+  for (int p = 3; n > 1 && rad.count < 24; p += 2) {
+    while (n % p == 0 && rad.count < 24) {
+      rad.r[rad.count++] = p;
+      n /= p;
+    }
+    if (p * p > n && n > 1) {
+      rad.r[rad.count++] = n;
+      n = 1;
+    }
+  }
+  return rad;
 }
 
 __device__ __forceinline__ double2 cm(double2 a, double2 b) {
@@ -234,7 +358,26 @@ cudaError_t generic_run(const GenericJob& job, const void* in, void* out, void* 
       long long inner = 1, outer = job.batch;
       for (int t = a + 1; t < job.rank; ++t) inner *= job.dims[t];
       for (int t = 0; t < a; ++t) outer *= job.dims[t];
-      if (job.dims[a] > 1) {
+      const int n = job.dims[a];
+      if (n > 1 && n <= kFftMaxN) {
+        // lines per CTA: contiguous tiles, two line buffers + table <= 192 KB
+        int lpc = 1;
+        while (lpc < 16 && static_cast<long long>(4 * lpc + 1) * n * 16 <= 192 * 1024 &&
+               (inner == 1 ? lpc * 2 <= outer : inner % (lpc * 2) == 0))
+          lpc *= 2;
+        const size_t smem = (static_cast<size_t>(2) * lpc * n + n) * sizeof(double2);
+        static bool attr_set = false;
+        if (!attr_set) {
+          cudaFuncSetAttribute(g_fft_axis_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+          attr_set = true;
+        }
+        const long long tiles = inner > 1 ? outer * (inner / lpc) : (outer + lpc - 1) / lpc;
+        g_fft_axis_smem<<<static_cast<unsigned>(tiles), kThreads, smem, st>>>(cur, nxt, outer, n, inner,
+                                                                            job.circle[a], inverse, factorise(n), lpc);
+        double2* t = cur;
+        cur = nxt;
+        nxt = t;
+      } else if (n > 1) {
         g_dft_axis<<<g, kThreads, 0, st>>>(cur, nxt, outer, job.dims[a], inner, job.circle[a], inverse);
         double2* t = cur;
         cur = nxt;

@@ -1,2 +1,3 @@
 mkdir -p gpurun_out
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:"col2" -c 2 -o gpurun_out/col2 python tools/prof_step.py --iters 1 > gpurun_out/ncu_full.log 2>&1; tail -1 gpurun_out/ncu_full.log
+timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -5
+for s in "1000 1000" "3000 2000" "1536 1536" "4099 256" "100 60 90"; do timeout 120 python tools/stage_time.py --dtype float64 --size $s --kinds dct_2d 2>&1 | tail -1; done
