@@ -13,7 +13,8 @@
 
 namespace sdctb {
 
-constexpr int kMaxFastLen = 4096;  // largest FFT length with a fast kernel
+constexpr int kMaxFastLen = 4096;  // largest FFT length with a fast (single-CTA) kernel
+constexpr int kMaxSplitLen = 8192; // 2D axis-0 length reachable through the cluster-split column pass
 
 // column-kernel variants
 enum ColVariant { CV_FWD_SRC = 0, CV_FWD_INTER = 1, CV_INV_INTER = 2, CV_INV_DST = 3 };
@@ -33,7 +34,7 @@ __host__ __device__ constexpr int nl_default(int esize, int L) {
 // Cluster-split column pass (kernels_col2.cuh): 2D fp64 columns of 4096 rows
 // with 2-complex (32-B) bands run as two 64 KB halves per 2-CTA cluster.
 __host__ __device__ constexpr bool col2_used(int esize, int L, int planes, int nl) {
-  return esize == 8 && L == 4096 && planes == 1 && nl == 2;
+  return planes == 1 && nl * esize == 16 && (L == 8192 || (esize == 8 && L == 4096));
 }
 
 // Opt each kernel instantiation in to > 48 KB dynamic shared memory (once).
@@ -49,8 +50,9 @@ cudaError_t launch_col(int variant, int L, int nl, dim3 grid, cudaStream_t st, c
                        const CUtensorMap& omap, const ColArgs& a, const TwSet& tw);
 template <typename T>
 cudaError_t launch_row(int M, int kind, dim3 grid, cudaStream_t st, const RowArgs& a, const TwSet& tw);
-cudaError_t launch_col2(bool inv, int bands, int batch, cudaStream_t st, const CUtensorMap& map, const CUtensorMap& omap,
-                        const ColArgs& a, const TwSet& tw);
+template <typename T>
+cudaError_t launch_col2(int L, bool inv, int bands, int batch, cudaStream_t st, const CUtensorMap& map,
+                        const CUtensorMap& omap, const ColArgs& a, const TwSet& tw);
 
 // threads per CTA (host side, must match the kernels' compile-time geometry)
 inline int tile_threads(int L, int nl) {

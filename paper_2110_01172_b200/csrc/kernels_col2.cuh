@@ -1,4 +1,6 @@
-// Cluster-split column kernels for long fp64 columns (L = 2H = 4096, 2D).
+// Cluster-split column kernels for long columns (L = 2H), 2D transforms: the
+// only fast column pass for L = 8192 (a whole band would not fit one SM's
+// shared memory), and an opt-in alternative for fp64 L = 4096.
 //
 // A whole 4096-row band of a 2D transform (4096 rows x 32 B = 128 KB) only
 // fits one CTA per SM, and then the band's load, math and stores serialise
@@ -35,10 +37,11 @@ struct Col2Geom {
   static constexpr int NT = TL::NT;
   static constexpr uint32_t TILE = static_cast<uint32_t>(H) * 2 * NL * sizeof(T);  // 64 KB for fp64 H=2048 NL=2
   static constexpr size_t SMEM = TILE + 64;                                      // + mbarrier
+  static constexpr int MINB = TILE <= 100u * 1024u ? 2 : 1;                      // CTAs per SM
 };
 
 template <typename T, int H, int NL, bool INV>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Col2Geom<T, H, NL>::NT, 2)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Col2Geom<T, H, NL>::NT, Col2Geom<T, H, NL>::MINB)
     col2_kernel(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUtensorMap tout, ColArgs a,
                 TwSet tw) {
   using G = Col2Geom<T, H, NL>;

@@ -162,6 +162,7 @@ void circle(std::vector<long double>& re, std::vector<long double>& im, long lon
 }
 
 int pick_nl(int esize, int L, int M, long long planes_batch) {
+  if (L > kMaxFastLen) return 16 / esize;  // cluster-split pass: 32-B band rows (kernels_col2.cuh)
   if (const char* f = getenv("SDCT_FORCE_NL")) {  // developer override (tools/)
     const int v = atoi(f);
     if (v >= 2 && v <= M) return v;
@@ -210,7 +211,7 @@ int build_plan(sdct_plan_s* p) {
   bool fast = false;
   if (r == 2) {
     const int n1 = p->n[0], n2 = p->n[1];
-    fast = is_pow2(n1) && is_pow2(n2) && n1 >= 2 && n2 >= 8 && n1 <= kMaxFastLen && n2 / 2 <= kMaxFastLen;
+    fast = is_pow2(n1) && is_pow2(n2) && n1 >= 2 && n2 >= 8 && n1 <= kMaxSplitLen && n2 / 2 <= kMaxFastLen;
   } else if (r == 3) {
     const int n1 = p->n[0], n2 = p->n[1], n3 = p->n[2];
     fast = is_pow2(n1) && is_pow2(n2) && is_pow2(n3) && n1 >= 2 && n2 >= 2 && n3 >= 8 &&
@@ -244,13 +245,15 @@ int build_plan(sdct_plan_s* p) {
     if (r == 3) stages(col_split(p->n[1]) ? p->n[1] / 2 : p->n[1], st_c1);
     stages(p->M, st_r);
     p->nl[0] = pick_nl(static_cast<int>(p->elem()), p->n[0], p->M, (r == 2 ? 1 : p->n[1]) * p->batch);
-    // measured slower than the single-CTA pass on B200 (108 vs 86 us at 4096^2,
-    // DESIGN.md §6): kept as an opt-in experiment (SDCT_COL2=1 at plan creation)
+    // L = 8192 columns only fit as cluster-split halves; for fp64 L = 4096 the
+    // split pass measured slower than the single-CTA pass on B200 (108 vs
+    // 86 us) and is an opt-in experiment (SDCT_COL2=1)
     static const bool col2_opt = [] {
       const char* f = getenv("SDCT_COL2");
       return f && atoi(f) == 1;
     }();
-    p->col2 = col2_opt && r == 2 && col2_used(static_cast<int>(p->elem()), p->n[0], 1, p->nl[0]);
+    p->col2 = r == 2 && col2_used(static_cast<int>(p->elem()), p->n[0], 1, p->nl[0]) &&
+              (p->n[0] > kMaxFastLen || col2_opt);
     if (p->col2) {
       stages(p->n[0] / 2, st_c2);
       circle(re, im, p->n[0] / 2, 1.0L, p->n[0]);  // W_L^k, k < L/2
@@ -492,7 +495,7 @@ int run_fast(sdct_plan_s* p, int kind, int only_stage, const void* in, void* out
                  make_class_map(&mo, f32, a.dst, o.inner, o.rows, o.row_stride * es, o.planes, o.plane_stride * es, B,
                                 o.batch_stride * es, p->nl[0]);
       }
-      if (map_ok) e = launch_col2(inv, M / p->nl[0], B, st, mi, mo, a, p->tw_col2);
+      if (map_ok) e = launch_col2<T>(n1, inv, M / p->nl[0], B, st, mi, mo, a, p->tw_col2);
     }
     ++stage;
   };

@@ -90,7 +90,8 @@ def test_known_answers(golden, cuda):
 
 # ------------------------------------------------------ oracle sweeps ------
 SHAPES_2D = [(2, 8), (4, 16), (8, 8), (16, 8), (8, 64), (64, 8), (128, 256), (256, 128), (512, 512),
-             (2, 4096), (4096, 8), (4096, 16), (4096, 64), (8, 8192), (5, 7), (31, 17), (16, 3), (3, 16), (100, 60), (1, 9), (9, 1)]
+             (2, 4096), (4096, 8), (4096, 16), (4096, 64), (8, 8192), (8192, 8), (8192, 64), (5, 7), (31, 17), (16, 3),
+             (3, 16), (100, 60), (1, 9), (9, 1), (1000, 24), (12, 1000), (4100, 6)]
 
 
 @pytest.mark.parametrize("dtype", ["float64", "float32"])
@@ -393,3 +394,21 @@ def test_force_fields_vs_oracle(cuda, dtype):
         assert oracle.rel_l2(b2[b].double().cpu().numpy(), w2) <= TOL[dtype]
     with pytest.raises(ValueError):
         sd.force_demo_fields(torch.zeros(8, device="cuda", dtype=tdt))
+
+
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+def test_cluster_split_8192_round_trip(cuda, dtype):
+    # n1 = 8192 columns run as cluster-split halves (kernels_col2.cuh): round
+    # trip at full size, plus an oracle spot check of one forward transform
+    torch = _torch()
+    import paper_2110_01172_b200 as sd
+
+    tdt = torch.float64 if dtype == "float64" else torch.float32
+    g = torch.Generator(device="cuda").manual_seed(7)
+    x = (torch.rand((8192, 1024), generator=g, device="cuda", dtype=torch.float64) * 2 - 1).to(tdt)
+    z = sd.idct_2d(sd.dct_2d(x))
+    err = float(((z.double() / (8192 * 1024 / 4) - x.double()).norm() / x.double().norm()).item())
+    assert err <= (1e-13 if dtype == "float64" else 1e-5), err
+    xs = x[:, :64].contiguous()
+    got = sd.dct_2d(xs).double().cpu().numpy()
+    assert oracle.rel_l2(got, oracle.port.dct_2d(xs.double().cpu().numpy())) <= TOL[dtype]
