@@ -97,15 +97,20 @@ struct Radices {
 
 constexpr int kFftMaxN = 4096;  // two line buffers + table in shared memory
 
-__global__ void g_fft_axis_smem(const double2* __restrict__ in, double2* __restrict__ out, long long outer, int n,
-                                long long inner, const double2* __restrict__ tab, int inverse, Radices rad, int lpc) {
+constexpr int kFftPerThread = 16;  // outputs a thread holds across one pass (lines * n <= 16 * 256)
+
+__global__ void __launch_bounds__(256) g_fft_axis_smem(const double2* __restrict__ in, double2* __restrict__ out,
+                                                       long long outer, int n, long long inner,
+                                                       const double2* __restrict__ tab, int tab_stride, int inverse,
+                                                       Radices rad, int lpc) {
+  // shared memory: twiddle table (n) + the lines (lpc * n); each pass computes
+  // its outputs into registers, synchronises, and writes them back in place
   extern __shared__ __align__(16) double2 fsm[];
-  double2* tw = fsm;               // n
-  double2* b0 = fsm + n;           // lpc * n
-  double2* b1 = b0 + static_cast<long long>(lpc) * n;
+  double2* tw = fsm;
+  double2* x = fsm + n;
   const int t = threadIdx.x, nt = blockDim.x;
   for (int e = t; e < n; e += nt) {
-    double2 w = tab[e];
+    double2 w = tab[static_cast<long long>(e) * tab_stride];  // e^{-2 pi i e / n} from a longer circle table
     if (inverse) w.y = -w.y;
     tw[e] = w;
   }
@@ -120,10 +125,11 @@ __global__ void g_fft_axis_smem(const double2* __restrict__ in, double2* __restr
     o = tile * lpc;
     i0 = 0;
   }
-  const long long lines = inner > 1 ? lpc : std::min<long long>(lpc, outer - o);
-  // load: element m of line l at b0[l * n + m]
-  for (long long e = t; e < lines * n; e += nt) {
-    long long l, m, src;
+  const int lines = static_cast<int>(inner > 1 ? lpc : std::min<long long>(lpc, outer - o));
+  const int total = lines * n;
+  for (int e = t; e < total; e += nt) {
+    long long src;
+    int l, m;
     if (inner > 1) {
       m = e / lpc;
       l = e % lpc;
@@ -133,42 +139,49 @@ __global__ void g_fft_axis_smem(const double2* __restrict__ in, double2* __restr
       m = e % n;
       src = (o + l) * n + m;
     }
-    b0[l * n + m] = in[src];
+    x[l * n + m] = in[src];
   }
   __syncthreads();
-  double2* x = b0;
-  double2* y = b1;
   int ns = 1;
   for (int s = 0; s < rad.count; ++s) {
     const int R = rad.r[s];
     const int nr = n / R;
-    for (long long e = t; e < lines * n; e += nt) {
-      const int l = static_cast<int>(e / n), q = static_cast<int>(e % n);
-      // output q = (j / ns) ns R + j % ns + k ns with j in [0, n/R), k in [0, R)
-      const int jr = q % ns, rest = q / ns;
-      const int k = rest % R, jq = rest / R;
-      const int j = jq * ns + jr;
-      const int E = (jr * (n / (ns * R)) + k * nr) % n;
-      const double2* xl = x + static_cast<long long>(l) * n + j;
-      double re = 0.0, im = 0.0;
-      int idx = 0;
-      for (int r = 0; r < R; ++r) {
-        const double2 v = xl[r * nr], w = tw[idx];
-        re += v.x * w.x - v.y * w.y;
-        im += v.x * w.y + v.y * w.x;
-        idx += E;
-        if (idx >= n) idx -= n;
+    double2 acc[kFftPerThread];
+#pragma unroll
+    for (int u = 0; u < kFftPerThread; ++u) {
+      const int e = t + u * nt;
+      if (e < total) {
+        const int l = e / n, q = e - l * n;
+        // output q = (j / ns) ns R + j % ns + k ns with j in [0, n/R), k in [0, R)
+        const int jr = q % ns, rest = q / ns;
+        const int k = rest % R, jq = rest / R;
+        const int j = jq * ns + jr;
+        const int E = (jr * (n / (ns * R)) + k * nr) % n;
+        const double2* xl = x + l * n + j;
+        double re = 0.0, im = 0.0;
+        int idx = 0;
+        for (int r = 0; r < R; ++r) {
+          const double2 v = xl[r * nr], w = tw[idx];
+          re = fma(v.x, w.x, fma(-v.y, w.y, re));
+          im = fma(v.x, w.y, fma(v.y, w.x, im));
+          idx += E;
+          if (idx >= n) idx -= n;
+        }
+        acc[u] = make_double2(re, im);
       }
-      y[static_cast<long long>(l) * n + q] = make_double2(re, im);
     }
     __syncthreads();
-    double2* tmp = x;
-    x = y;
-    y = tmp;
+#pragma unroll
+    for (int u = 0; u < kFftPerThread; ++u) {
+      const int e = t + u * nt;
+      if (e < total) x[e] = acc[u];
+    }
+    __syncthreads();
     ns *= R;
   }
-  for (long long e = t; e < lines * n; e += nt) {
-    long long l, m, dst;
+  for (int e = t; e < total; e += nt) {
+    long long dst;
+    int l, m;
     if (inner > 1) {
       m = e / lpc;
       l = e % lpc;
@@ -180,6 +193,76 @@ __global__ void g_fft_axis_smem(const double2* __restrict__ in, double2* __restr
     }
     out[dst] = x[l * n + m];
   }
+}
+
+// Split of a long axis n = a b (a, b <= kFftMaxN): the a-point FFTs over m1
+// (element b m1 + m2 -> slot b k1 + m2) run as line FFTs; this kernel then
+// finishes X(k) = sum_{m2 < b} Y(k1, m2) W_n^{m2 k}, k = k1 + a k2 (the
+// twiddle, the b-point DFT and the output permutation in one pass; b is the
+// small cofactor).
+__global__ void g_split_finish(const double2* __restrict__ y, double2* __restrict__ out, long long outer, int a, int b,
+                               long long inner, const double2* __restrict__ tab, int inverse) {
+  const long long n = static_cast<long long>(a) * b;
+  const long long total = outer * n * inner;
+  for (long long f = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; f < total;
+       f += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long i = f % inner, rest = f / inner;
+    const long long k = rest % n, o = rest / n;
+    const long long k1 = k % a;
+    const double2* src = y + (o * n + b * k1) * inner + i;
+    double re = 0.0, im = 0.0;
+    long long idx = 0;
+    for (int m2 = 0; m2 < b; ++m2) {
+      double2 w = tab[idx];
+      if (inverse) w.y = -w.y;
+      const double2 v = src[m2 * inner];
+      re = fma(v.x, w.x, fma(-v.y, w.y, re));
+      im = fma(v.x, w.y, fma(v.y, w.x, im));
+      idx += k;
+      if (idx >= n) idx -= n;
+    }
+    out[f] = make_double2(re, im);
+  }
+}
+
+// Batched transpose [o][r][c] -> [o][c][r] through 32 x 32 smem tiles.
+__global__ void g_transpose_k(const double2* __restrict__ in, double2* __restrict__ out, long long rows,
+                              long long cols) {
+  __shared__ double2 tile[32][33];
+  const long long o = blockIdx.z;
+  const long long r0 = static_cast<long long>(blockIdx.y) * 32, c0 = static_cast<long long>(blockIdx.x) * 32;
+  const double2* src = in + o * rows * cols;
+  double2* dst = out + o * rows * cols;
+  for (int dy = threadIdx.y; dy < 32; dy += blockDim.y) {
+    const long long r = r0 + dy, c = c0 + threadIdx.x;
+    if (r < rows && c < cols) tile[dy][threadIdx.x] = src[r * cols + c];
+  }
+  __syncthreads();
+  for (int dy = threadIdx.y; dy < 32; dy += blockDim.y) {
+    const long long c = c0 + dy, r = r0 + threadIdx.x;
+    if (r < rows && c < cols) dst[c * rows + r] = tile[threadIdx.x][dy];
+  }
+}
+
+void g_transpose(const double2* in, double2* out, long long outer, long long rows, long long cols, cudaStream_t st) {
+  // grid.z carries the outer index (chunked when it exceeds the 65535 limit)
+  for (long long o0 = 0; o0 < outer; o0 += 65535) {
+    const long long oc = std::min<long long>(65535, outer - o0);
+    dim3 grid(static_cast<unsigned>((cols + 31) / 32), static_cast<unsigned>((rows + 31) / 32),
+              static_cast<unsigned>(oc));
+    g_transpose_k<<<grid, dim3(32, 8), 0, st>>>(in + o0 * rows * cols, out + o0 * rows * cols, rows, cols);
+  }
+}
+
+// a * b = n with both factors <= kFftMaxN (a the larger), or {0, 0}
+void split_factors(int n, int& a, int& b) {
+  a = b = 0;
+  for (int d = kFftMaxN; d >= 2; --d)
+    if (n % d == 0 && n / d <= kFftMaxN) {
+      a = d;
+      b = n / d;
+      return;
+    }
 }
 
 Radices factorise(int n) {
@@ -359,24 +442,50 @@ cudaError_t generic_run(const GenericJob& job, const void* in, void* out, void* 
       for (int t = a + 1; t < job.rank; ++t) inner *= job.dims[t];
       for (int t = 0; t < a; ++t) outer *= job.dims[t];
       const int n = job.dims[a];
-      if (n > 1 && n <= kFftMaxN) {
-        // lines per CTA: contiguous tiles, two line buffers + table <= 192 KB
+      // shared-memory line FFT of length len over lines (outer', inner'), table stride ts
+      auto line_fft = [&](const double2* src, double2* dst, long long outer_, int len, long long inner_, int ts) {
         int lpc = 1;
-        while (lpc < 16 && static_cast<long long>(4 * lpc + 1) * n * 16 <= 192 * 1024 &&
-               (inner == 1 ? lpc * 2 <= outer : inner % (lpc * 2) == 0))
+        while (lpc < 16 && 2 * lpc * len <= kFftPerThread * kThreads &&
+               (inner_ == 1 ? lpc * 2 <= outer_ : inner_ % (lpc * 2) == 0))
           lpc *= 2;
-        const size_t smem = (static_cast<size_t>(2) * lpc * n + n) * sizeof(double2);
+        const size_t smem = (static_cast<size_t>(lpc) * len + len) * sizeof(double2);
         static bool attr_set = false;
         if (!attr_set) {
-          cudaFuncSetAttribute(g_fft_axis_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+          cudaFuncSetAttribute(g_fft_axis_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, 140 * 1024);
           attr_set = true;
         }
-        const long long tiles = inner > 1 ? outer * (inner / lpc) : (outer + lpc - 1) / lpc;
-        g_fft_axis_smem<<<static_cast<unsigned>(tiles), kThreads, smem, st>>>(cur, nxt, outer, n, inner,
-                                                                            job.circle[a], inverse, factorise(n), lpc);
-        double2* t = cur;
-        cur = nxt;
-        nxt = t;
+        const long long tiles = inner_ > 1 ? outer_ * (inner_ / lpc) : (outer_ + lpc - 1) / lpc;
+        g_fft_axis_smem<<<static_cast<unsigned>(tiles), kThreads, smem, st>>>(src, dst, outer_, len, inner_,
+                                                                            job.circle[a], ts, inverse,
+                                                                            factorise(len), lpc);
+      };
+      int fa = 0, fb = 0;
+      if (n > kFftMaxN) split_factors(n, fa, fb);
+      if ((n > 1 && n <= kFftMaxN) || fa > 0) {
+        // strided axes (inner > 1) whose lines would be read with little
+        // coalescing are transposed to rows first: [o][n][inner] -> [o][inner][n]
+        const bool tr = inner > 1 && (static_cast<long long>(16) * (fa > 0 ? fa : n) > kFftPerThread * kThreads ||
+                                      inner % 16 != 0);
+        long long o2 = outer, in2 = inner;
+        if (tr) {
+          g_transpose(cur, nxt, outer, n, inner, st);
+          std::swap(cur, nxt);
+          o2 = outer * inner;
+          in2 = 1;
+        }
+        if (fa == 0) {
+          line_fft(cur, nxt, o2, n, in2, 1);
+        } else {
+          // split: a-point line FFTs (stride b), then twiddle + b-point DFT + permutation
+          line_fft(cur, nxt, o2, fa, static_cast<long long>(fb) * in2, fb);
+          g_split_finish<<<g, kThreads, 0, st>>>(nxt, cur, o2, fa, fb, in2, job.circle[a], inverse);
+          std::swap(cur, nxt);
+        }
+        std::swap(cur, nxt);
+        if (tr) {
+          g_transpose(cur, nxt, outer, inner, n, st);  // back: [o][inner][n] -> [o][n][inner]
+          std::swap(cur, nxt);
+        }
       } else if (n > 1) {
         g_dft_axis<<<g, kThreads, 0, st>>>(cur, nxt, outer, job.dims[a], inner, job.circle[a], inverse);
         double2* t = cur;
