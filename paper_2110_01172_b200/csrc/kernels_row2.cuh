@@ -248,6 +248,7 @@ __global__ void __launch_bounds__(Row2Geom<T, M, MODE>::CTA, Row2Geom<T, M, MODE
       // buffer = rows q1 (A) and m1 (B) of x, 2M reals each
       const T* rowA = reinterpret_cast<const T*>(sm);
       const T* rowB = rowA + 2 * M;
+      // (the weighting below runs on the landed rows in their own order)
       mbar_wait(full + b, ph);
       if (a.weight) {
         // DREAMPlace-style field weighting of the input coefficients
@@ -267,6 +268,12 @@ __global__ void __launch_bounds__(Row2Geom<T, M, MODE>::CTA, Row2Geom<T, M, MODE
       // operands for n2 in {k, M-k}: D = x(n2), R = x(N2-n2) (x(N2) := 0) of
       // both rows; mode 2 (IDXST along axis 1) reads x(N2-n2) for D and x(n2)
       // for R with x(0) := 0 (proj/src/dct2d.cpp:169-180)
+      // IDXST along axis 0 (mode 1) swaps the two rows' roles for pairs
+      if (a.mode == 1 && P != 0) {
+        const T* tmp = rowA;
+        rowA = rowB;
+        rowB = tmp;
+      }
       T op[NI][8];
 #pragma unroll
       for (int i = 0; i < NI; ++i) {
@@ -302,13 +309,7 @@ __global__ void __launch_bounds__(Row2Geom<T, M, MODE>::CTA, Row2Geom<T, M, MODE
           x1 = cmul(c1, mk(o[2] - o[3], -(o[2] + o[3])));
           return;
         }
-        T p = o[0], sv = o[1], r = o[2], q = o[3];
-        if (a.mode == 1) {  // IDXST along axis 0 swaps the row roles
-          p = o[2];
-          sv = o[3];
-          r = o[0];
-          q = o[1];
-        }
+        const T p = o[0], sv = o[1], r = o[2], q = o[3];
         x0 = cmul(c0, mk(p - q, -(r + sv)));
         x1 = cmul(c1, mk(r - sv, -(p + q)));
       };
@@ -351,14 +352,22 @@ __global__ void __launch_bounds__(Row2Geom<T, M, MODE>::CTA, Row2Geom<T, M, MODE
       constexpr int CPV = 16 / sizeof(V);
       constexpr int VPR = M / CPV;
       const int irow[2] = {__ldg(a.s0 + q1), __ldg(a.s0 + m1)};
-#pragma unroll 4
-      for (int w = t; w < 2 * VPR; w += NT) {
-        const int line = w / VPR, ci = w - line * VPR;
+      // column s of the pair-interleaved row holds z(m), m = (s >> 1) ^ ((s & 1) (M - 1));
+      // m is GF(2)-linear in s, so with the linear swizzle each element's slot is
+      // one per-thread swizzle XOR a compile-time offset
+      const int swt = CPV == 1 ? TL::swz((t >> 1) ^ ((t & 1) ? M - 1 : 0)) : TL::swz(t);
+#pragma unroll
+      for (int it = 0; it < 2 * VPR / NT; ++it) {
+        const int line = (it * NT) / VPR, off = (it * NT) % VPR;
         V4 o;
         V* e = reinterpret_cast<V*>(&o);
+        if constexpr (CPV == 1) {
+          e[0] = sm[swt ^ TL::swzc(line * M + off / 2)];
+        } else {
 #pragma unroll
-        for (int c = 0; c < CPV; ++c) e[c] = sm[row_nat<T, M>(line, s_to_m(ci * CPV + c, M))];
-        *reinterpret_cast<V4*>(dst + static_cast<long long>(irow[line]) * M + ci * CPV) = o;
+          for (int c = 0; c < CPV; ++c) e[c] = sm[swt ^ TL::swzc(line * M + off) ^ (c ? TL::swzc(M - 1) : 0)];
+        }
+        *reinterpret_cast<V4*>(dst + static_cast<long long>(irow[line]) * M + (t + off) * CPV) = o;
       }
     }
     TL::sync();  // every read of buffer b by this group is done
