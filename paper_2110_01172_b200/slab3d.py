@@ -1,0 +1,79 @@
+"""Slab-decomposed 3D DCT-II / IDCT over several GPUs.
+
+One large 3D transform whose input is split along axis 0 across the ranks of a
+process group (one process per GPU): rank r holds planes
+[r*n1/G, (r+1)*n1/G) of x (n1, n2 divisible by G). The transform is separable
+with the reference's unnormalised conventions (dct_3d = dctn/8,
+proj/tests/python/test_smoke.py:46-50; dct_2d = dctn/4; dct_1d = dct/2), so
+
+    dct_3d(x)  = dct_1d along axis 0  o  dct_2d over axes (1, 2)
+    idct_3d(x) = idct_1d along axis 0 o  idct_2d over axes (1, 2)
+
+and the slab pipeline is:
+
+  1. local : batched 2D transform of this rank's planes (the fused fast path);
+  2. all-to-all #1 (NCCL over NVLink): every rank sends rank t the columns
+     j in t's axis-1 slab, receives all n1 planes of its own axis-1 slab,
+     laid out [j][k][i] so axis 0 is contiguous;
+  3. local : batched 1D transform along that contiguous axis;
+  4. all-to-all #2: back to axis-0 slabs.
+
+The exchanges are the only collectives (the transposes are the "standard
+communication operations" PAPER.md:649-660 mentions). The local transforms are
+injectable so the exchange logic runs under gloo on CPU in tests/.
+"""
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+
+def _all_to_all(send: torch.Tensor, group) -> torch.Tensor:
+    """Equal-split all-to-all of a contiguous [G, ...] tensor (block t goes to rank t)."""
+    recv = torch.empty_like(send)
+    if dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_to_all_single(recv, send, group=group)
+    else:
+        recv.copy_(send)
+    return recv
+
+
+def _slab_pipeline(x_local: torch.Tensor, n1: int, two_d, one_d, group) -> torch.Tensor:
+    G = dist.get_world_size(group) if dist.is_initialized() else 1
+    s1, n2, n3 = x_local.shape
+    if s1 * G != n1 or n2 % G:
+        raise ValueError(f"slab decomposition needs n1 = {s1}*{G} planes and n2 % {G} == 0")
+    s2 = n2 // G
+    # 1. 2D transform of every local plane (axes 1, 2)
+    a = two_d(x_local.contiguous())                                   # [s1][n2][n3]
+    # 2. block t = columns j of rank t's axis-1 slab: [G][s1][s2][n3]
+    send = a.reshape(s1, G, s2, n3).permute(1, 0, 2, 3).contiguous()
+    recv = _all_to_all(send, group)                                   # [G src][s1][s2][n3]: i = src*s1 + i_loc
+    b = recv.permute(2, 3, 0, 1).reshape(s2, n3, n1).contiguous()    # [j][k][i], axis 0 contiguous
+    # 3. 1D transform along axis 0 for every (j, k) of this slab
+    c = one_d(b)                                                      # [s2][n3][n1]
+    # 4. back to axis-0 slabs: block t = planes i of rank t: [G][s2][n3][s1]
+    send2 = c.reshape(s2, n3, G, s1).permute(2, 0, 1, 3).contiguous()
+    recv2 = _all_to_all(send2, group)                                 # [G src][s2][n3][s1]: j = src*s2 + j_loc
+    return recv2.permute(3, 0, 1, 2).reshape(s1, n2, n3).contiguous()
+
+
+def dct_3d_slab(x_local: torch.Tensor, n1: int, group=None, two_d=None, one_d=None) -> torch.Tensor:
+    """This rank's axis-0 slab of dct_3d(x), given its slab of x (CUDA tensor,
+    fp32/fp64). n1 is the global axis-0 extent."""
+    if two_d is None or one_d is None:
+        import paper_2110_01172_b200 as sd
+
+        two_d = two_d or sd.dct_2d
+        one_d = one_d or sd.dct_1d
+    return _slab_pipeline(x_local, n1, two_d, one_d, group)
+
+
+def idct_3d_slab(x_local: torch.Tensor, n1: int, group=None, two_d=None, one_d=None) -> torch.Tensor:
+    """This rank's axis-0 slab of idct_3d(x) (idct_3d(dct_3d(x)) = n1 n2 n3 / 8 x)."""
+    if two_d is None or one_d is None:
+        import paper_2110_01172_b200 as sd
+
+        two_d = two_d or sd.idct_2d
+        one_d = one_d or sd.idct_1d
+    return _slab_pipeline(x_local, n1, two_d, one_d, group)
