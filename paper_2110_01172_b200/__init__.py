@@ -22,6 +22,9 @@ from .api import (
     dct_2d,
     dct_2d_rowcol,
     dct_3d,
+    dct_4d,
+    dct_oracle_1d,
+    dct_oracle_2d,
     force_demo_fields,
     idct_1d,
     idct_2d,
@@ -37,7 +40,8 @@ __all__ = [
     "ShapeError", "FormatError", "DeviceError", "amdahl_speedup",
     "dct_1d", "idct_1d", "idxst_1d",
     "dct_2d", "dct_2d_rowcol", "idct_2d", "idct_idxst_2d", "idxst_idct_2d",
-    "dct_3d", "idct_3d", "plan_for", "stream_host", "force_demo_fields",
+    "dct_3d", "dct_4d", "idct_3d", "plan_for", "stream_host", "force_demo_fields",
+    "dct_oracle_1d", "dct_oracle_2d",
 ]
 
 __version__ = "0.1.0"

@@ -169,3 +169,65 @@ def force_demo_fields(density, threads: int = 0):
         ws = torch.empty(plan.workspace_bytes, dtype=torch.uint8, device=x.device)
         plan.force_fields(x.data_ptr(), xi1.data_ptr(), xi2.data_ptr(), stream.cuda_stream, ws.data_ptr())
     return xi1, xi2
+
+
+# ---- remaining names of the reference module (proj/python/sdct/__init__.py) --
+def _to_device(x):
+    """(tensor on the GPU, was_numpy) for numpy or torch input (float64 for numpy)."""
+    import numpy as np
+    import torch
+
+    if _is_torch_cuda(x):
+        return x, False
+    a = np.ascontiguousarray(np.asarray(x, dtype=np.float64))
+    return torch.from_numpy(a).to("cuda"), True
+
+
+def dct_4d(x, threads: int = 0):
+    """Rank-4 DCT as two rounds of fused 2D transforms over the axis pairs
+    (0, 1) and (2, 3) (proj/src/transforms_ext.cpp:396-425, module.cpp:144-149):
+    both rounds are one batched dct_2d launch each; the axis-pair regrouping is
+    a device transpose."""
+    t, was_np = _to_device(x)
+    if t.dim() != 4:
+        raise ShapeError(f"dct_nd_factorized expects a rank-4 tensor, got shape {tuple(t.shape)}")
+    d0, d1, d2, d3 = (int(s) for s in t.shape)
+    # round one, axes (0, 1): [d0 d1][d2 d3] -> [d2 d3][d0][d1], transform, back
+    r1 = _device_call("dct_2d", t.reshape(d0 * d1, d2 * d3).t().contiguous().reshape(d2 * d3, d0, d1))
+    r1 = r1.reshape(d2 * d3, d0 * d1).t().contiguous().reshape(d0 * d1, d2, d3)
+    # round two, axes (2, 3): contiguous inner matrices
+    y = _device_call("dct_2d", r1).reshape(d0, d1, d2, d3)
+    return y.cpu().numpy() if was_np else y
+
+
+def _cos_matrix(n: int, device, inverse: bool = False):
+    import math
+
+    import torch
+
+    k = torch.arange(n, dtype=torch.float64, device=device)
+    if not inverse:  # C[k, n] = cos(pi/N (n + 1/2) k)
+        return torch.cos(math.pi / n * torch.outer(k, k + 0.5))
+    raise ValueError("only the forward cosine matrix is used")
+
+
+def dct_oracle_1d(x):
+    """Direct quadratic cosine-sum reference y(k) = sum_n x(n) cos(pi/N (n+1/2) k)
+    (proj/include/sdct/oracle.hpp:22-24), evaluated on the GPU as one dense
+    product with the cosine matrix (no FFT involved)."""
+    t, was_np = _to_device(x)
+    if t.dim() != 1 or t.numel() == 0:
+        raise ShapeError(f"dct_oracle_1d expects a non-empty rank-1 array, got shape {tuple(t.shape)}")
+    y = _cos_matrix(t.numel(), t.device) @ t.double()
+    return y.cpu().numpy() if was_np else y.to(t.dtype)
+
+
+def dct_oracle_2d(x):
+    """Direct quadruple-sum reference y(k1,k2) = sum_{n1,n2} x(n1,n2)
+    cos(pi/N1 (n1+1/2) k1) cos(pi/N2 (n2+1/2) k2) (oracle.hpp:30-32), evaluated
+    as C1 x C2^T on the GPU."""
+    t, was_np = _to_device(x)
+    if t.dim() != 2 or t.numel() == 0:
+        raise ShapeError(f"dct_oracle_2d expects a non-empty rank-2 array, got shape {tuple(t.shape)}")
+    y = _cos_matrix(t.shape[0], t.device) @ t.double() @ _cos_matrix(t.shape[1], t.device).t()
+    return y.cpu().numpy() if was_np else y.to(t.dtype)

@@ -57,6 +57,22 @@ def main() -> None:
         out[f"in/{key}"] = x
         for kind in KINDS_3D:
             out[f"{kind}/{key}"] = getattr(sdct, kind)(x)
+    # rank-4 factorised DCT (transforms_ext.cpp:396-425) and the brute-force
+    # cosine-sum oracles the reference module exports (module.cpp:144-158)
+    for shape in [(2, 3, 4, 5), (4, 4, 8, 8), (3, 2, 16, 8), (8, 16, 4, 2)]:
+        seed += 1
+        x = np.random.default_rng(seed).uniform(-1.0, 1.0, size=shape)
+        key = "x".join(map(str, shape))
+        out[f"in/{key}"] = x
+        out[f"dct_4d/{key}"] = sdct.dct_4d(x)
+    for n in (1, 5, 16, 37):
+        seed += 1
+        x = np.random.default_rng(seed).uniform(-1.0, 1.0, size=(n,))
+        out[f"in/{n}"] = x
+        out[f"dct_oracle_1d/{n}"] = sdct.dct_oracle_1d(x)
+    for shape in [(3, 5), (8, 8), (16, 12)]:
+        key = "x".join(map(str, shape))
+        out[f"dct_oracle_2d/{key}"] = sdct.dct_oracle_2d(out[f"in/{key}"])
     # Known-answer inputs (proj/tests/cli_tests.sh:113-121,
     # proj/tests/test_transforms_ext.cpp:180-185).
     out["kat/ones2x2/in"] = np.ones((2, 2))

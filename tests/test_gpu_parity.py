@@ -429,3 +429,19 @@ def test_slab_3d_single_rank_matches_fused(cuda, dtype):
         assert oracle.rel_l2(y.double().cpu().numpy(), sd.dct_3d(x).double().cpu().numpy()) <= TOL[dtype]
         z = slab3d.idct_3d_slab(y, shape[0])
         assert oracle.rel_l2(z.double().cpu().numpy() / (x.numel() / 8), x.double().cpu().numpy()) <= TOL[dtype] * 10
+
+
+def test_dct_4d_and_oracles_vs_reference_golden(cuda, golden):
+    # the remaining reference exports: rank-4 factorised DCT (two batched dct_2d
+    # rounds) and the cosine-sum oracles, against the reference's own outputs
+    import paper_2110_01172_b200 as sd
+
+    for key in sorted(k.split("/", 1)[1] for k in golden if k.startswith("dct_4d/")):
+        got = sd.dct_4d(golden["in/" + key])
+        assert oracle.rel_l2(got, golden["dct_4d/" + key]) <= 1e-12, key
+    for key in sorted(k.split("/", 1)[1] for k in golden if k.startswith("dct_oracle_1d/")):
+        assert oracle.rel_l2(sd.dct_oracle_1d(golden["in/" + key]), golden["dct_oracle_1d/" + key]) <= 1e-13, key
+    for key in sorted(k.split("/", 1)[1] for k in golden if k.startswith("dct_oracle_2d/")):
+        assert oracle.rel_l2(sd.dct_oracle_2d(golden["in/" + key]), golden["dct_oracle_2d/" + key]) <= 1e-13, key
+    with pytest.raises(ValueError):
+        sd.dct_4d(np.zeros((2, 2, 2)))

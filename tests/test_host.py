@@ -83,8 +83,10 @@ def test_reference_error_types():
 def test_reference_python_surface_names():
     import paper_2110_01172_b200 as sd
 
+    # the reference module's 17 exports (proj/python/sdct/__init__.py:8-26)
     for name in ["ShapeError", "FormatError", "amdahl_speedup", "dct_1d", "dct_2d", "dct_2d_rowcol",
-                 "dct_3d", "idct_1d", "idct_2d", "idct_3d", "idct_idxst_2d", "idxst_1d", "idxst_idct_2d"]:
+                 "dct_3d", "dct_4d", "dct_oracle_1d", "dct_oracle_2d", "force_demo_fields", "idct_1d",
+                 "idct_2d", "idct_3d", "idct_idxst_2d", "idxst_1d", "idxst_idct_2d"]:
         assert hasattr(sd, name), name
 
 
