@@ -457,6 +457,19 @@ def run_ours(args, rank: int, world: int, local_rank: int):
             ours[kn] = a.elapsed_time(b) / reps
         cufft = {"api": "libcufft cufftPlanMany + cufftExec{D2Z,Z2D|R2C,C2R}, plan built outside timing",
                  "r2c_ms": round(r2c, 4), "c2r_ms": round(c2r, 4)}
+        if len(dims) == 2 and "dct_2d" in w["kinds"]:
+            # row-column DCT on the same shape (north_star: "reported alongside"):
+            # dct_2d_rowcol runs one pass per axis (gather, FFT along each axis,
+            # postprocess) on the generic GPU path
+            k_rc = _sdct.DCT_2D_ROWCOL
+            plan.run(k_rc, xs[0].data_ptr(), outs[0][0].data_ptr(), s, 0)
+            torch.cuda.synchronize()
+            a.record(stream)
+            for _ in range(3):
+                plan.run(k_rc, xs[0].data_ptr(), outs[0][0].data_ptr(), s, 0)
+            b.record(stream)
+            torch.cuda.synchronize()
+            cufft["rowcol_dct_2d_ms"] = round(a.elapsed_time(b) / 3, 4)
         for kn, v in ours.items():
             cufft[f"{kn}_ms"] = round(v, 4)
             base = r2c if kn.startswith("dct") else c2r

@@ -126,6 +126,7 @@ struct sdct_plan_s {
   std::mutex mu;
 
   void* aux = nullptr;  // sdct_force_fields scratch (coefficients + weighted copy), lazily allocated
+  std::mutex gws_mu;    // guards the lazy gws allocation
   void* gws = nullptr;  // generic-path scratch on fast plans (row-column), lazily allocated
   size_t elem() const { return dtype == SDCT_F32 ? 4 : 8; }
   size_t generic_ws_bytes() const {
@@ -673,11 +674,16 @@ int run(sdct_plan_s* p, int kind, int only_stage, const void* in, void* out, voi
   if (use_fast) return run_fast<T>(p, kind, only_stage, in, out, ws, st, nstages, weight);
   if (nstages) *nstages = 1;  // generic path is timed as one unit
   if (only_stage > 0) return SDCT_OK;
-  if (p->fast && ws == p->ws) {
-    // fast plan running a generic-path transform: needs the larger scratch
-    if (!p->gws) {
-      cudaError_t ea = cudaMalloc(&p->gws, p->generic_ws_bytes());
-      if (ea != cudaSuccess) return cuda_fail(ea, "allocating generic scratch");
+  if (p->fast) {
+    // fast plan running a generic-path transform (row-column, 1D): needs the
+    // larger generic scratch, which the plan owns (a caller's workspace is
+    // sized for the fast path by sdct_plan_workspace_size)
+    {
+      std::lock_guard<std::mutex> lock(p->gws_mu);  // not p->mu: host entry points hold it across dispatch
+      if (!p->gws) {
+        cudaError_t ea = cudaMalloc(&p->gws, p->generic_ws_bytes());
+        if (ea != cudaSuccess) return cuda_fail(ea, "allocating generic scratch");
+      }
     }
     ws = p->gws;
   }

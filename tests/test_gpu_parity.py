@@ -445,3 +445,21 @@ def test_dct_4d_and_oracles_vs_reference_golden(cuda, golden):
         assert oracle.rel_l2(sd.dct_oracle_2d(golden["in/" + key]), golden["dct_oracle_2d/" + key]) <= 1e-13, key
     with pytest.raises(ValueError):
         sd.dct_4d(np.zeros((2, 2, 2)))
+
+
+def test_generic_kind_on_fast_plan_ignores_small_caller_workspace(cuda):
+    # a caller workspace is sized for the fast path (sdct_plan_workspace_size);
+    # generic-path kinds (row-column) must use the plan's own larger scratch
+    torch = _torch()
+    import paper_2110_01172_b200 as sd
+    from paper_2110_01172_b200 import _sdct
+
+    x = torch.tensor(rnd((64, 64), 91), device="cuda")
+    plan = sd.plan_for((64, 64), 1, "float64", 0)
+    buf = torch.full((plan.workspace_bytes + (1 << 20),), 0x5A, dtype=torch.uint8, device="cuda")
+    out = torch.empty_like(x)
+    plan.run(_sdct.DCT_2D_ROWCOL, x.data_ptr(), out.data_ptr(), torch.cuda.current_stream().cuda_stream,
+             buf.data_ptr())
+    torch.cuda.synchronize()
+    assert bool((buf[plan.workspace_bytes:] == 0x5A).all()), "generic path wrote past the caller workspace"
+    assert oracle.rel_l2(out.cpu().numpy(), oracle.port.dct_2d(x.cpu().numpy())) <= 1e-12
