@@ -20,15 +20,13 @@ constexpr int kMaxSplitLen = 8192; // 2D axis-0 length reachable through the clu
 enum ColVariant { CV_FWD_SRC = 0, CV_FWD_INTER = 1, CV_INV_INTER = 2, CV_INV_DST = 3 };
 
 // Column tiles target 64 KB (two CTAs per SM) with rows of >= 32 B
-// (NL >= 16 / esize). L = 4096 cannot fit 32-B rows in 64 KB, so it runs the
-// cluster-split kernel: two CTAs per band, L/2 rows each.
-__host__ __device__ constexpr bool col_split(int L) { return false; }
+// (NL >= 16 / esize); long columns (4096 rows of 32 B = 128 KB) take one CTA
+// per SM.
 __host__ __device__ constexpr int nl_default(int esize, int L) {
-  // complex element = 2*esize bytes; tile (L or L/2) * NL * 2*esize <= 64 KB
-  return (64 * 1024) / ((col_split(L) ? L / 2 : L) * 2 * esize) >= 32 ? 32
-         : (64 * 1024) / ((col_split(L) ? L / 2 : L) * 2 * esize) <= 16 / esize
-             ? 16 / esize
-             : (64 * 1024) / ((col_split(L) ? L / 2 : L) * 2 * esize);
+  // complex element = 2*esize bytes; tile L * NL * 2*esize <= 64 KB
+  return (64 * 1024) / (L * 2 * esize) >= 32   ? 32
+         : (64 * 1024) / (L * 2 * esize) <= 16 / esize ? 16 / esize
+                                                       : (64 * 1024) / (L * 2 * esize);
 }
 
 // Cluster-split column pass (kernels_col2.cuh): 2D fp64 columns of 4096 rows

@@ -1,20 +1,16 @@
-// In-CTA power-of-two FFT engine.
-//
-// A CTA holds `nlines` independent lines of length L (complex, float2/double2)
-// in shared memory and transforms all of them in place with decimation-in-
-// frequency radix-R stages (R <= 16). Each thread loads R elements of one
-// butterfly into registers, runs a fully unrolled radix-R DFT, applies the
-// stage twiddles W_span^{j k}, and writes the R results back to the same slots.
-// After the last stage X(k) sits at slot digit_pos<L>(k) (mixed-radix digit
-// reversal); callers absorb that permutation into their store index math, so
-// no separate reorder pass exists.
+// Building blocks of the in-CTA power-of-two FFT engine (kernels_fast.cuh):
+// the radix plan (ceil(log2 L / 4) stages of radix <= 16), mixed-radix digit
+// reversal (after the DIF stages X(k) sits at slot digit_pos<L>(k); callers
+// absorb that permutation into their store index math, so no reorder pass
+// exists), the GF(2)-linear shared-memory swizzles, and the fully unrolled
+// in-register radix-R DFTs.
 //
 // This replaces the reference's scalar radix-2 FftWorkspace::pow2_fft
 // (proj/src/rfft.cpp:65-89) for the power-of-two extents of the hot path.
 //
 // Shared-memory layouts are XOR-swizzled so that every stage's access pattern
-// is bank-conflict free (checked by tests/test_swizzle.py, which replays the
-// exact index math below).
+// is bank-conflict free (tests/test_host.py replays the exact index math below
+// through tests/swizzle_model.py).
 #pragma once
 
 #include "sdct_common.cuh"
@@ -80,20 +76,6 @@ __host__ __device__ inline int rt_digit_pos(int k, int L) {
   }
   return pos;
 }
-__host__ __device__ inline int rt_digit_rev(int n, int L) {
-  int lg = 0;
-  while ((1 << lg) < L) ++lg;
-  if (lg == 0) return 0;
-  const int S = (lg + 3) / 4;
-  int span = L, k = 0, shift = 0;
-  for (int s = 0; s < S; ++s) {
-    const int b = lg / S + (s < lg % S ? 1 : 0);
-    span >>= b;
-    k |= ((n / span) & ((1 << b) - 1)) << shift;
-    shift += b;
-  }
-  return k;
-}
 
 // ---- bank-conflict-free swizzles (index in complex elements) ---------------
 // GF(2)-linear maps a -> a ^ g(a >> SH), g(h) = XOR of C[d % 4] over the set
@@ -101,7 +83,7 @@ __host__ __device__ inline int rt_digit_rev(int n, int L) {
 // elements (SH = 4) 16 lanes. Column tiles use constants that make every
 // aligned dyadic window injective; row tiles use constants found by
 // exhaustive search over the row kernel's stage patterns. tests/swizzle_model.py
-// replays this math and tests/test_swizzle.py asserts conflict degree 1.
+// replays this math and tests/test_host.py asserts conflict degree 1.
 // Linearity lets a butterfly swizzle its base once and XOR per-element offsets.
 template <int C0, int C1, int C2, int C3, int SH>
 struct LinSwz {
@@ -146,25 +128,6 @@ template <> struct SwzCol<float> : LinSwz<8, 12, 10, 15, 4> {};
 template <typename T> struct SwzRow;
 template <> struct SwzRow<double> : LinSwz<1, 2, 4, 1, 3> {};
 template <> struct SwzRow<float> : LinSwz<1, 6, 10, 8, 4> {};
-
-// Column tile: element (line c, n) at n*W + c (lines interleaved), W = 1 << lgw.
-template <typename T>
-struct ColLayout {
-  int lgw;
-  __device__ __forceinline__ int raw(int line, int n) const { return (n << lgw) + line; }
-  __device__ __forceinline__ int at(int line, int n) const { return SwzCol<T>::f(raw(line, n)); }
-  __device__ __forceinline__ static int swz(int a) { return SwzCol<T>::f(a); }
-  // swizzled offset of element stride q (used as XOR offsets inside a butterfly)
-  __device__ __forceinline__ int off(int q) const { return SwzCol<T>::f(q << lgw); }
-};
-// Row tile: element (line, n) at line*L + n (lines contiguous).
-template <typename T, int L>
-struct RowLayout {
-  __device__ __forceinline__ int raw(int line, int n) const { return line * L + n; }
-  __device__ __forceinline__ int at(int line, int n) const { return SwzRow<T>::f(raw(line, n)); }
-  __device__ __forceinline__ static int swz(int a) { return SwzRow<T>::f(a); }
-  __device__ __forceinline__ int off(int q) const { return SwzRow<T>::f(q); }
-};
 
 // ---- in-register radix-R DFT, natural order in and out ---------------------
 template <typename T> struct K16;
@@ -226,78 +189,6 @@ __device__ __forceinline__ void dft_reg(cx_t<T>* v) {
       v[k + R / 2] = csub(e[k], t);
     }
   }
-}
-
-// ---- one DIF stage over all lines -------------------------------------------
-// tw: circle table C[m] = exp(-2 pi i m / CL); W_L^1 = C[tw_step].
-// LINE_FAST: butterfly index decodes line first (column tiles) or j first.
-template <typename T, int L, int S_IDX, bool INV, bool LINE_FAST, class Lay>
-__device__ __forceinline__ void dif_stage(cx_t<T>* buf, const Lay& lay, int lg_lines, int tid,
-                                          int nthreads, const cx_t<T>* __restrict__ tw,
-                                          int tw_step) {
-  using P = RadixPlan<L>;
-  constexpr int R = P::R(S_IDX);
-  constexpr int SPAN = P::span(S_IDX);
-  constexpr int Q = SPAN / R;  // butterflies per block
-  constexpr int LG_Q = ilog2c(Q);
-  constexpr int LG_BLK = ilog2c(L / SPAN);
-  const int total = (L / R) << lg_lines;
-  // The element offsets r*Q occupy bits disjoint from base = b*SPAN + j (and
-  // from the line bits), so by linearity swz(base + r*Q) = swz(base) ^ swz(r*Q).
-  int xo[R];
-#pragma unroll
-  for (int r = 0; r < R; ++r) xo[r] = lay.off(r * Q);
-  for (int bf = tid; bf < total; bf += nthreads) {
-    int line, j, b;
-    if (LINE_FAST) {
-      line = bf & ((1 << lg_lines) - 1);
-      const int rest = bf >> lg_lines;
-      j = rest & (Q - 1);
-      b = rest >> LG_Q;
-    } else {
-      j = bf & (Q - 1);
-      const int rest = bf >> LG_Q;
-      b = rest & ((1 << LG_BLK) - 1);
-      line = rest >> LG_BLK;
-    }
-    const int base = b * SPAN + j;
-    const int sb = lay.at(line, base);
-    cx_t<T> v[R];
-#pragma unroll
-    for (int r = 0; r < R; ++r) v[r] = buf[sb ^ xo[r]];
-    dft_reg<T, R, INV>(v);
-    if (SPAN > R && j != 0) {
-      // W_SPAN^j = W_L^{j L/SPAN}
-      cx_t<T> w1 = __ldg(&tw[(j * (L / SPAN)) * tw_step]);
-      if (INV) w1 = cconj(w1);
-      cx_t<T> w = w1;
-#pragma unroll
-      for (int k = 1; k < R; ++k) {
-        v[k] = cmul(v[k], w);
-        if (k + 1 < R) w = cmul(w, w1);
-      }
-    }
-#pragma unroll
-    for (int r = 0; r < R; ++r) buf[sb ^ xo[r]] = v[r];
-  }
-}
-
-template <typename T, int L, int S_IDX, bool INV, bool LINE_FAST, class Lay>
-__device__ __forceinline__ void dif_stages(cx_t<T>* buf, const Lay& lay, int lg_lines, int tid,
-                                           int nthreads, const cx_t<T>* __restrict__ tw,
-                                           int tw_step) {
-  if constexpr (S_IDX < RadixPlan<L>::S) {
-    dif_stage<T, L, S_IDX, INV, LINE_FAST>(buf, lay, lg_lines, tid, nthreads, tw, tw_step);
-    __syncthreads();
-    dif_stages<T, L, S_IDX + 1, INV, LINE_FAST>(buf, lay, lg_lines, tid, nthreads, tw, tw_step);
-  }
-}
-
-// Full transform of every line; ends with a __syncthreads().
-template <typename T, int L, bool INV, bool LINE_FAST, class Lay>
-__device__ __forceinline__ void block_fft(cx_t<T>* buf, const Lay& lay, int lg_lines,
-                                          const cx_t<T>* __restrict__ tw, int tw_step) {
-  dif_stages<T, L, 0, INV, LINE_FAST>(buf, lay, lg_lines, threadIdx.x, blockDim.x, tw, tw_step);
 }
 
 }  // namespace sdctb

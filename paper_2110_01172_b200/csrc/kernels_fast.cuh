@@ -63,7 +63,7 @@ struct ColArgs {
   int sign_row, sign_col;                   // final gather: negate odd k along axis
   double scale;                             // final gather scale
   int tma_plane_par;                        // TMA plane coordinate = parity_embed(plane, n) when > 0
-  const void* twc;                          // split kernels: combine twiddles W_L^k, k < L/2
+  const void* twc;                          // cluster-split pass: W_L^k, k < L/2
   int nbands, nplanes, ntiles;              // persistent column kernels: tile = band + nbands*(plane + nplanes*batch)
   unsigned long long* trace;                // debug: per-tile phase timestamps (nullptr in production)
 };

@@ -96,7 +96,7 @@ struct sdct_plan_s {
   TwSet tw_row = {};     // row FFT (length M)
   TwSet tw_col2 = {};    // cluster-split column pass: H-point stage tables (H = n1 / 2)
   bool col2 = false;     // 2D column passes run cluster-split (col2_used)
-  void* tw_comb[2] = {nullptr, nullptr};  // split column passes: W_L^k, k < L/2
+  void* tw_comb = nullptr;  // cluster-split column pass: W_L^k, k < L/2
   // device tables (one allocation)
   void* tables = nullptr;
   void* ta = nullptr;    // dtype quarter-wave tables
@@ -170,11 +170,10 @@ int pick_nl(int esize, int L, int M, long long planes_batch) {
   }
   // nl_default: 64 KB tiles with >= 32-B rows (cluster-split for L = 4096).
   // Narrower bands when the problem is too narrow or offers < 2 CTAs per SM.
-  const int per_band = col_split(L) ? 2 : 1;
   const int nld = nl_default(esize, L);
-  if (nld <= M && (M / nld) * planes_batch * per_band >= 2 * 148) return nld;
+  if (nld <= M && (M / nld) * planes_batch >= 2 * 148) return nld;
   const int nmin = 16 / esize;  // 32-B rows
-  if (nmin < nld && nmin <= M && (M / nmin) * planes_batch * per_band >= 148) return nmin;
+  if (nmin < nld && nmin <= M && (M / nmin) * planes_batch >= 148) return nmin;
   return 2;
 }
 
@@ -226,7 +225,7 @@ int build_plan(sdct_plan_s* p) {
   size_t off_ta = 0, off_tb = 0, off_tc = 0, off_tu = 0;
   size_t off_gq[3] = {0, 0, 0}, off_gc[3] = {0, 0, 0};
   size_t st_c0[4], st_c1[4], st_r[4], st_c2[4] = {SIZE_MAX, SIZE_MAX, SIZE_MAX, SIZE_MAX};
-  size_t off_comb[2] = {SIZE_MAX, SIZE_MAX};
+  size_t off_comb = SIZE_MAX;
   size_t off_srow[2] = {SIZE_MAX, SIZE_MAX};
   size_t off_fb = 0, off_fu = 0;
   if (fast) {
@@ -242,8 +241,8 @@ int build_plan(sdct_plan_s* p) {
       else stage_tables<double>(blob, L, o);
     };
     // column FFTs of length L >= 4096 run cluster-split: local tables for L/2
-    stages(col_split(p->n[0]) ? p->n[0] / 2 : p->n[0], st_c0);
-    if (r == 3) stages(col_split(p->n[1]) ? p->n[1] / 2 : p->n[1], st_c1);
+    stages(p->n[0], st_c0);
+    if (r == 3) stages(p->n[1], st_c1);
     stages(p->M, st_r);
     p->nl[0] = pick_nl(static_cast<int>(p->elem()), p->n[0], p->M, (r == 2 ? 1 : p->n[1]) * p->batch);
     // L = 8192 columns only fit as cluster-split halves; for fp64 L = 4096 the
@@ -258,13 +257,7 @@ int build_plan(sdct_plan_s* p) {
     if (p->col2) {
       stages(p->n[0] / 2, st_c2);
       circle(re, im, p->n[0] / 2, 1.0L, p->n[0]);  // W_L^k, k < L/2
-      put(off_comb[0]);
-    }
-    for (int ax = 0; ax < (r == 3 ? 2 : 1); ++ax) {
-      if (col_split(p->n[ax])) {
-        circle(re, im, p->n[ax] / 2, 1.0L, p->n[ax]);
-        put(off_comb[ax]);
-      }
+      put(off_comb);
     }
     circle(re, im, p->n[0], 1.0L, 4.0L * p->n[0]);
     put(off_ta);
@@ -334,7 +327,7 @@ int build_plan(sdct_plan_s* p) {
     if (r == 3) tws(st_c1, p->tw_col[1]);
     tws(st_r, p->tw_row);
     if (p->col2) tws(st_c2, p->tw_col2);
-    for (int ax = 0; ax < 2; ++ax) p->tw_comb[ax] = off_comb[ax] == SIZE_MAX ? nullptr : base + off_comb[ax];
+    p->tw_comb = off_comb == SIZE_MAX ? nullptr : base + off_comb;
     p->ta = base + off_ta;
     p->tb = base + off_tb;
     p->tc = r == 3 ? base + off_tc : nullptr;
@@ -482,7 +475,7 @@ int run_fast(sdct_plan_s* p, int kind, int only_stage, const void* in, void* out
   // cluster-split 2D column pass (kernels_col2.cuh): forward reads the source
   // through the parity-class map, the inverse writes y through it
   auto col2 = [&](bool inv, ColArgs a, const Side& in, const Side& o) {
-    a.twc = p->tw_comb[0];
+    a.twc = p->tw_comb;
     if (want() && e == cudaSuccess && map_ok) {
       CUtensorMap mi, mo;
       if (!inv) {

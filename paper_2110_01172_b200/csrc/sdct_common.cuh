@@ -27,15 +27,11 @@ template <typename V> __device__ __forceinline__ V cmul(V a, V b) {
 template <typename V> __device__ __forceinline__ V cmulc(V a, V b) {
   return mk(a.x * b.x + a.y * b.y, a.y * b.x - a.x * b.y);
 }
-template <typename V, typename S> __device__ __forceinline__ V cscale(V a, S s) {
-  return mk(a.x * s, a.y * s);
-}
 // multiply by -i (forward) or +i (inverse)
 template <bool INV, typename V> __device__ __forceinline__ V mul_mi(V a) {
   return INV ? mk(-a.y, a.x) : mk(a.y, -a.x);
 }
 
-template <typename T> __device__ __forceinline__ cx_t<T> ldg_cx(const cx_t<T>* p) { return __ldg(p); }
 
 // Reference parity maps (proj/include/sdct/dct1d.hpp:70-79). The forward
 // reorder puts x(2m) in slot m for m <= (n-1)/2 and x(2n-2m-1) otherwise;
