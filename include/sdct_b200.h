@@ -124,6 +124,16 @@ int sdct_force_fields(sdct_plan_t plan, const void* d_density, void* d_xi1, void
 /* Same on host memory (H2D, the fused device pipeline, D2H, synchronised). */
 int sdct_force_fields_host(sdct_plan_t plan, const void* h_density, void* h_xi1, void* h_xi2, void* stream);
 
+/* Whole-image frequency-domain compression — the numeric core of
+ * sdct::compress_image (proj/src/compress.cpp:24-54): b = dct_2d(image); every
+ * coefficient with |b| < epsilon (raw, unnormalised magnitudes) is zeroed and
+ * counted into *d_zeroed (a device counter the caller zeroes; may be NULL);
+ * d_out = idct_2d(b) * 4/(N1 N2). The threshold and the normalisation ride on
+ * the inverse row kernels' loads. Rounding to 8-bit samples and PSNR are the
+ * image app's (out of scope). epsilon may be +inf; < 0 or NaN -> SDCT_ERR_ARG. */
+int sdct_compress(sdct_plan_t plan, const void* d_in, void* d_out, double epsilon, unsigned long long* d_zeroed,
+                  void* d_workspace, void* stream);
+
 /* Host streaming: `count` independent items (each one plan-sized batch) go
  * host -> device -> kinds[0] -> ... -> kinds[nkinds-1] -> host. Item i's input
  * is at h_in + i*in_stride bytes and its result is written to

@@ -152,6 +152,15 @@ class _Port:
         lib.sdct_oracle_force_fields_2d(_dp(x), x.shape[0], x.shape[1], _dp(xi1), _dp(xi2))
         return xi1, xi2
 
+    def compress(self, x, epsilon: float):
+        """Numeric core of compress_image (proj/src/compress.cpp:33-46): zero
+        |b| < epsilon of b = dct_2d(x), reconstruct idct_2d(b) * 4/(N1 N2).
+        Returns (reconstruction, zeroed count)."""
+        b = self.dct_2d(x)
+        drop = np.abs(b) < epsilon
+        b = np.where(drop, 0.0, b)
+        return self.idct_2d(b) * (4.0 / b.size), int(drop.sum())
+
     def dct_3d(self, x):
         lib = _port_lib()
         return self._batched(

@@ -18,6 +18,7 @@ from __future__ import annotations
 from . import _sdct  # noqa: F401  (raises ImportError when not built)
 from ._sdct import DeviceError, FormatError, ShapeError, amdahl_speedup
 from .api import (
+    compress,
     dct_1d,
     dct_2d,
     dct_2d_rowcol,
@@ -41,7 +42,7 @@ __all__ = [
     "dct_1d", "idct_1d", "idxst_1d",
     "dct_2d", "dct_2d_rowcol", "idct_2d", "idct_idxst_2d", "idxst_idct_2d",
     "dct_3d", "dct_4d", "idct_3d", "plan_for", "stream_host", "force_demo_fields",
-    "dct_oracle_1d", "dct_oracle_2d",
+    "dct_oracle_1d", "dct_oracle_2d", "compress",
 ]
 
 __version__ = "0.1.0"

@@ -231,3 +231,39 @@ def dct_oracle_2d(x):
         raise ShapeError(f"dct_oracle_2d expects a non-empty rank-2 array, got shape {tuple(t.shape)}")
     y = _cos_matrix(t.shape[0], t.device) @ t.double() @ _cos_matrix(t.shape[1], t.device).t()
     return y.cpu().numpy() if was_np else y.to(t.dtype)
+
+
+def compress(x, epsilon: float):
+    """Frequency-domain compression of a rank-2 array (the numeric core of
+    proj/src/compress.cpp:24-54): zero every 2D DCT coefficient with
+    |b| < epsilon, reconstruct with idct_2d * 4/(N1 N2). Returns
+    (reconstruction, stats) with stats = {total_coefficients,
+    zeroed_coefficients, zeroed_fraction}. The threshold and normalisation are
+    fused into the inverse row kernels (sdct_compress); 8-bit rounding, PSNR
+    and the PGM I/O of the reference's image app are not part of this path."""
+    import math
+
+    import torch
+
+    t, was_np = _to_device(x)
+    if t.dim() != 2:
+        raise ShapeError(f"compress expects a rank-2 array, got shape {tuple(t.shape)}")
+    if math.isnan(epsilon) or epsilon < 0:
+        raise ValueError("compress: epsilon must be >= 0")
+    if t.dtype not in (torch.float32, torch.float64):
+        raise ValueError(f"compress: dtype must be float32 or float64, got {t.dtype}")
+    t = t.contiguous()
+    dt = "float32" if t.dtype == torch.float32 else "float64"
+    dev = t.device.index if t.device.index is not None else torch.cuda.current_device()
+    plan = plan_for(tuple(t.shape), 1, dt, dev)
+    out = torch.empty_like(t)
+    zeroed = torch.zeros(1, dtype=torch.int64, device=t.device)
+    with torch.cuda.device(dev):
+        stream = torch.cuda.current_stream(dev)
+        ws = torch.empty(plan.workspace_bytes, dtype=torch.uint8, device=t.device)
+        plan.compress(t.data_ptr(), out.data_ptr(), float(epsilon), zeroed.data_ptr(), stream.cuda_stream,
+                      ws.data_ptr())
+    total = t.numel()
+    nz = int(zeroed.item())
+    stats = {"total_coefficients": total, "zeroed_coefficients": nz, "zeroed_fraction": nz / total}
+    return (out.cpu().numpy() if was_np else out), stats

@@ -35,6 +35,7 @@ SIGNATURES = [
     ("sdct_exec_host", ctypes.c_int, [_VP, ctypes.c_int, _VP, _VP, _VP]),
     ("sdct_force_fields", ctypes.c_int, [_VP, _VP, _VP, _VP, _VP, _VP]),
     ("sdct_force_fields_host", ctypes.c_int, [_VP, _VP, _VP, _VP, _VP]),
+    ("sdct_compress", ctypes.c_int, [_VP, _VP, _VP, ctypes.c_double, _VP, _VP, _VP]),
     ("sdct_exec_host_pipelined", ctypes.c_int, [_VP, ctypes.POINTER(ctypes.c_int), ctypes.c_int, _VP, ctypes.c_int64,
                                                 _VP, ctypes.c_int64, ctypes.c_int64, _VP]),
     ("sdct_stage_count", ctypes.c_int, [_VP, ctypes.c_int, ctypes.POINTER(ctypes.c_int)]),

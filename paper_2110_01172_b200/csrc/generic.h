@@ -26,4 +26,9 @@ cudaError_t generic_run(const GenericJob& job, const void* in, void* out, void* 
 cudaError_t force_weight(const void* a, void* aw, int n1, int n2, long long batch, int which, bool f32,
                          cudaStream_t st);
 
+// Compression threshold (proj/src/compress.cpp:37-45): out = |b| < eps ? 0 : b * scale,
+// zeroed coefficients added to *count (device counter, may be null).
+cudaError_t compress_threshold(const void* b, void* out, long long n, double eps, double scale,
+                               unsigned long long* count, bool f32, cudaStream_t st);
+
 }  // namespace sdctb

@@ -540,4 +540,32 @@ cudaError_t force_weight(const void* a, void* aw, int n1, int n2, long long batc
   return cudaGetLastError();
 }
 
+template <typename T>
+__global__ void g_compress_threshold(const T* __restrict__ b, T* __restrict__ out, long long n, double eps,
+                                     double scale, unsigned long long* count) {
+  unsigned cnt = 0;
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < n;
+       e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const double v = static_cast<double>(b[e]);
+    const bool drop = fabs(v) < eps;
+    cnt += drop ? 1u : 0u;
+    out[e] = drop ? T(0) : static_cast<T>(v * scale);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+  if ((threadIdx.x & 31) == 0 && cnt && count) atomicAdd(count, static_cast<unsigned long long>(cnt));
+}
+
+cudaError_t compress_threshold(const void* b, void* out, long long n, double eps, double scale,
+                               unsigned long long* count, bool f32, cudaStream_t st) {
+  const int blocks = static_cast<int>(std::min<long long>((n + 255) / 256, 148 * 16));
+  if (f32)
+    g_compress_threshold<float><<<blocks, 256, 0, st>>>(static_cast<const float*>(b), static_cast<float*>(out), n,
+                                                         eps, scale, count);
+  else
+    g_compress_threshold<double><<<blocks, 256, 0, st>>>(static_cast<const double*>(b), static_cast<double*>(out), n,
+                                                          eps, scale, count);
+  return cudaGetLastError();
+}
+
 }  // namespace sdctb

@@ -250,7 +250,26 @@ __global__ void __launch_bounds__(Row2Geom<T, M, MODE>::CTA, Row2Geom<T, M, MODE
       const T* rowB = rowA + 2 * M;
       // (the weighting below runs on the landed rows in their own order)
       mbar_wait(full + b, ph);
-      if (a.weight) {
+      if (a.weight == 3) {
+        // compression (proj/src/compress.cpp:33-45) folded into this load:
+        // zero every coefficient with |b| < eps (counted), scale the rest by
+        // the 4/(N1 N2) reconstruction normalisation (linear, so it commutes
+        // with the inverse transform)
+        T* rw = reinterpret_cast<T*>(sm);
+        const T eps = static_cast<T>(a.thr_eps), sc = static_cast<T>(a.thr_scale);
+        unsigned cnt = 0;
+        for (int e = t; e < 2 * n2; e += NT) {
+          const T v = rw[e];
+          const bool drop = fabs(v) < eps;
+          cnt += drop ? 1u : 0u;
+          rw[e] = drop ? T(0) : v * sc;
+        }
+        constexpr int W = NT < 32 ? NT : 32;  // lanes per warp in use
+#pragma unroll
+        for (int o = W / 2; o > 0; o >>= 1) cnt += __shfl_xor_sync(TL::MASK, cnt, o);
+        if ((threadIdx.x & 31) == 0 && cnt && a.thr_count) atomicAdd(a.thr_count, static_cast<unsigned long long>(cnt));
+        TL::sync();
+      } else if (a.weight) {
         // DREAMPlace-style field weighting of the input coefficients
         // (proj/src/force.cpp:19-31), folded into this load: a1 = a w1/(w1^2+w2^2)
         // (weight 1) or a2 = a w2/(w1^2+w2^2) (weight 2), w_d = pi k_d / n_d, 0 at DC

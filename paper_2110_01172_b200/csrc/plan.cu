@@ -431,6 +431,12 @@ bool make_class_map(CUtensorMap* map, bool f32, const void* base, long long inne
   return r == CUDA_SUCCESS;
 }
 
+// Compression threshold carried by the 2D inverse row kernels (weight 3).
+struct Threshold {
+  double eps = 0.0, scale = 1.0;
+  unsigned long long* count = nullptr;
+};
+
 // Geometry of one side (input or output) of a column pass, in reals.
 struct Side {
   long long inner, rows, row_stride, planes, plane_stride, batch_stride;
@@ -438,7 +444,7 @@ struct Side {
 
 template <typename T>
 int run_fast(sdct_plan_s* p, int kind, int only_stage, const void* in, void* out, void* ws,
-             cudaStream_t st, int* nstages, int weight) {
+             cudaStream_t st, int* nstages, int weight, const Threshold* thr) {
   const int n1 = p->n[0], n2 = p->n[1], n3 = p->n[2];
   const int M = p->M;
   const long long item = p->numel;
@@ -512,6 +518,11 @@ int run_fast(sdct_plan_s* p, int kind, int only_stage, const void* in, void* out
   ra.fs = p->fs;
   ra.bad_q = p->bad_q;
   ra.weight = weight;
+  if (thr) {
+    ra.thr_eps = thr->eps;
+    ra.thr_scale = thr->scale;
+    ra.thr_count = thr->count;
+  }
   {
     static const int dev = [] {
       const char* f = getenv("SDCT_DEV_FLAGS");  // developer experiments only (tools/)
@@ -661,10 +672,10 @@ GenericJob make_job(const sdct_plan_s* p, int kind) {
 
 template <typename T>
 int run(sdct_plan_s* p, int kind, int only_stage, const void* in, void* out, void* ws,
-        cudaStream_t st, int* nstages, int weight) {
+        cudaStream_t st, int* nstages, int weight, const Threshold* thr) {
   // Row-column baseline and the 1D transforms run on the generic path.
   const bool use_fast = p->fast && kind != SDCT_DCT_2D_ROWCOL;
-  if (use_fast) return run_fast<T>(p, kind, only_stage, in, out, ws, st, nstages, weight);
+  if (use_fast) return run_fast<T>(p, kind, only_stage, in, out, ws, st, nstages, weight, thr);
   if (nstages) *nstages = 1;  // generic path is timed as one unit
   if (only_stage > 0) return SDCT_OK;
   if (p->fast) {
@@ -686,12 +697,12 @@ int run(sdct_plan_s* p, int kind, int only_stage, const void* in, void* out, voi
 }
 
 int dispatch(sdct_plan_s* p, int kind, int only_stage, const void* in, void* out, void* ws,
-             cudaStream_t st, int* nstages, int weight = 0) {
+             cudaStream_t st, int* nstages, int weight = 0, const Threshold* thr = nullptr) {
   if (!kind_ok(p, kind)) return fail(SDCT_ERR_PLAN, "transform kind does not match the plan rank");
   if (!ws) ws = p->ws;
   DeviceGuard g(p->device);
-  return p->dtype == SDCT_F32 ? run<float>(p, kind, only_stage, in, out, ws, st, nstages, weight)
-                              : run<double>(p, kind, only_stage, in, out, ws, st, nstages, weight);
+  return p->dtype == SDCT_F32 ? run<float>(p, kind, only_stage, in, out, ws, st, nstages, weight, thr)
+                              : run<double>(p, kind, only_stage, in, out, ws, st, nstages, weight, thr);
 }
 
 // ---- analytic StageCounters (replays the reference's Counted tallies) -----
@@ -958,6 +969,37 @@ int sdct_force_fields(sdct_plan_t p, const void* d_density, void* d_xi1, void* d
     if (rc != SDCT_OK) return rc;
   }
   return SDCT_OK;
+}
+
+int sdct_compress(sdct_plan_t p, const void* d_in, void* d_out, double epsilon, unsigned long long* d_zeroed,
+                  void* d_ws, void* stream) {
+  if (!p || !d_in || !d_out) return fail(SDCT_ERR_ARG, "null argument to sdct_compress");
+  if (p->rank != 2) return fail(SDCT_ERR_PLAN, "compression needs a rank-2 plan");
+  if (std::isnan(epsilon) || epsilon < 0.0) return fail(SDCT_ERR_ARG, "compress: epsilon must be >= 0");
+  if (d_in == d_out) return fail(SDCT_ERR_ARG, "sdct_compress is out of place: d_in == d_out");
+  DeviceGuard g(p->device);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const size_t bytes = static_cast<size_t>(p->batch) * p->item_bytes();
+  {
+    std::lock_guard<std::mutex> lock(p->mu);
+    if (!p->aux) {
+      cudaError_t e = cudaMalloc(&p->aux, 2 * bytes);
+      if (e != cudaSuccess) return cuda_fail(e, "allocating coefficient scratch");
+    }
+  }
+  void* b = p->aux;
+  int rc = dispatch(p, SDCT_DCT_2D, -1, d_in, b, d_ws, st, nullptr);
+  if (rc != SDCT_OK) return rc;
+  Threshold thr;
+  thr.eps = epsilon;
+  thr.scale = 4.0 / (static_cast<double>(p->n[0]) * static_cast<double>(p->n[1]));
+  thr.count = d_zeroed;
+  if (p->fast) return dispatch(p, SDCT_IDCT_2D, -1, b, d_out, d_ws, st, nullptr, 3, &thr);
+  void* bw = static_cast<unsigned char*>(p->aux) + bytes;
+  cudaError_t e = compress_threshold(b, bw, static_cast<long long>(p->batch) * p->numel, thr.eps, thr.scale, d_zeroed,
+                                     p->dtype == SDCT_F32, st);
+  if (e != cudaSuccess) return cuda_fail(e, "launching compression threshold");
+  return dispatch(p, SDCT_IDCT_2D, -1, bw, d_out, d_ws, st, nullptr);
 }
 
 int sdct_force_fields_host(sdct_plan_t p, const void* h_density, void* h_xi1, void* h_xi2, void* stream) {

@@ -193,6 +193,17 @@ PYBIND11_MODULE(_sdct, m) {
                                                    reinterpret_cast<void*>(ws), reinterpret_cast<void*>(stream)));
            },
            py::arg("d_density"), py::arg("d_xi1"), py::arg("d_xi2"), py::arg("stream") = 0, py::arg("workspace") = 0)
+      .def("compress",
+           [](const sdct::DevicePlan& p, std::uintptr_t d_in, std::uintptr_t d_out, double eps, std::uintptr_t d_zeroed,
+              std::uintptr_t stream, std::uintptr_t ws) {
+             py::gil_scoped_release nogil;
+             sdct::detail::check(sdct_compress(p.handle(), reinterpret_cast<const void*>(d_in),
+                                               reinterpret_cast<void*>(d_out), eps,
+                                               reinterpret_cast<unsigned long long*>(d_zeroed),
+                                               reinterpret_cast<void*>(ws), reinterpret_cast<void*>(stream)));
+           },
+           py::arg("d_in"), py::arg("d_out"), py::arg("epsilon"), py::arg("d_zeroed") = 0, py::arg("stream") = 0,
+           py::arg("workspace") = 0)
       .def("stage_count",
            [](const sdct::DevicePlan& p, int kind) {
              int n = 0;

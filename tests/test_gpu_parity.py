@@ -463,3 +463,40 @@ def test_generic_kind_on_fast_plan_ignores_small_caller_workspace(cuda):
     torch.cuda.synchronize()
     assert bool((buf[plan.workspace_bytes:] == 0x5A).all()), "generic path wrote past the caller workspace"
     assert oracle.rel_l2(out.cpu().numpy(), oracle.port.dct_2d(x.cpu().numpy())) <= 1e-12
+
+
+def _gap_threshold(b, q=0.5, rel=1e-4):
+    # an epsilon strictly inside a gap of the sorted |b| near quantile q, so
+    # the GPU's and the oracle's coefficients fall on the same side of it
+    m = np.sort(np.abs(b).ravel())
+    i0 = int(q * (m.size - 1))
+    scale = max(float(m[-1]), 1e-300)
+    for d in range(m.size):
+        for i in (i0 + d, i0 - d):
+            if 0 <= i < m.size - 1 and m[i + 1] - m[i] > rel * scale:
+                return 0.5 * (m[i] + m[i + 1])
+    return float(m[-1]) * 2
+
+
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+def test_compress_vs_oracle(cuda, dtype):
+    # sdct_compress: threshold + 4/(N1 N2) fused into the inverse row kernels
+    # (fast shapes) or one threshold kernel (generic shapes)
+    torch = _torch()
+    import paper_2110_01172_b200 as sd
+
+    tdt = torch.float64 if dtype == "float64" else torch.float32
+    for i, shape in enumerate([(64, 128), (512, 256), (4096, 64), (31, 17), (100, 60)]):
+        x = rnd(shape, 400 + i, dtype)
+        b = oracle.port.dct_2d(x)
+        for eps in (0.0, _gap_threshold(b, 0.5), _gap_threshold(b, 0.95), float("inf")):
+            want, zeroed = oracle.port.compress(x, eps)
+            got, stats = sd.compress(torch.tensor(x, dtype=tdt, device="cuda"), eps)
+            assert stats["zeroed_coefficients"] == zeroed, (shape, eps)
+            assert stats["total_coefficients"] == x.size
+            if zeroed == x.size:
+                assert float(got.abs().max()) == 0.0
+            else:
+                assert oracle.rel_l2(got.double().cpu().numpy(), want) <= TOL[dtype], (shape, eps)
+    with pytest.raises(ValueError):
+        sd.compress(np.zeros((8, 8)), -1.0)

@@ -132,3 +132,19 @@ def test_port_force_fields_match_reference_golden(golden):
         xi1, xi2 = oracle.port.force_demo_fields(golden["in/" + key])
         assert oracle.rel_l2(xi1, golden["force_xi1/" + key]) <= 1e-13, key
         assert oracle.rel_l2(xi2, golden["force_xi2/" + key]) <= 1e-13, key
+
+
+def test_port_compress_matches_reference_composition():
+    # compress.cpp:33-46 restated: reference dct_2d, threshold, reference
+    # idct_2d, 4/(N1 N2) — against the port's own composition
+    if not oracle.ref_available():
+        pytest.skip("reference library not built")
+    x = np.random.default_rng(5).uniform(-1, 1, (24, 17))
+    b = oracle.ref.run("dct_2d", x)
+    eps = float(np.median(np.abs(b)))
+    want = oracle.ref.run("idct_2d", np.where(np.abs(b) < eps, 0.0, b)) * (4.0 / x.size)
+    got, zeroed = oracle.port.compress(x, eps)
+    assert oracle.rel_l2(got, want) <= 1e-13
+    assert zeroed == int((np.abs(b) < eps).sum())
+    r0, z0 = oracle.port.compress(x, 0.0)
+    assert z0 == 0 and oracle.rel_l2(r0, x) <= 1e-13
