@@ -34,6 +34,7 @@ cudaError_t launch_col2<double>(int L, bool inv, int bands, int batch, cudaStrea
 template <>
 cudaError_t launch_col2<float>(int L, bool inv, int bands, int batch, cudaStream_t st, const CUtensorMap& map,
                                const CUtensorMap& omap, const ColArgs& a, const TwSet& tw) {
+  if (L == 4096) return launch_col2_h<float, 2048>(inv, bands, batch, st, map, omap, a, tw);
   if (L == 8192) return launch_col2_h<float, 4096>(inv, bands, batch, st, map, omap, a, tw);
   return cudaErrorInvalidValue;
 }

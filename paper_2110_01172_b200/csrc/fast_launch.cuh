@@ -32,7 +32,7 @@ __host__ __device__ constexpr int nl_default(int esize, int L) {
 // Cluster-split column pass (kernels_col2.cuh): 2D fp64 columns of 4096 rows
 // with 2-complex (32-B) bands run as two 64 KB halves per 2-CTA cluster.
 __host__ __device__ constexpr bool col2_used(int esize, int L, int planes, int nl) {
-  return planes == 1 && nl * esize == 16 && (L == 8192 || (esize == 8 && L == 4096));
+  return planes == 1 && nl * esize == 16 && (L == 8192 || L == 4096);
 }
 
 // Opt each kernel instantiation in to > 48 KB dynamic shared memory (once).
