@@ -444,11 +444,11 @@ struct Side {
 
 template <typename T>
 int run_fast(sdct_plan_s* p, int kind, int only_stage, const void* in, void* out, void* ws,
-             cudaStream_t st, int* nstages, int weight, const Threshold* thr) {
+             cudaStream_t st, int* nstages, int weight, const Threshold* thr, int bcount) {
   const int n1 = p->n[0], n2 = p->n[1], n3 = p->n[2];
   const int M = p->M;
   const long long item = p->numel;
-  const int B = static_cast<int>(p->batch);
+  const int B = bcount;  // items of this launch set (<= 65535, see run())
   int stage = 0;
   cudaError_t e = cudaSuccess;
   auto want = [&](void) { return only_stage < 0 || only_stage == stage; };
@@ -675,7 +675,19 @@ int run(sdct_plan_s* p, int kind, int only_stage, const void* in, void* out, voi
         cudaStream_t st, int* nstages, int weight, const Threshold* thr) {
   // Row-column baseline and the 1D transforms run on the generic path.
   const bool use_fast = p->fast && kind != SDCT_DCT_2D_ROWCOL;
-  if (use_fast) return run_fast<T>(p, kind, only_stage, in, out, ws, st, nstages, weight, thr);
+  if (use_fast) {
+    // batch items ride on grid.y / grid.z (<= 65535): larger batches run as
+    // consecutive launch sets over contiguous chunks (same workspace layout)
+    const long long chunk = 65535;
+    const size_t ib = p->item_bytes();
+    int rc = SDCT_OK;
+    for (long long b0 = 0; b0 < p->batch && rc == SDCT_OK; b0 += chunk) {
+      const int bc = static_cast<int>(std::min<long long>(chunk, p->batch - b0));
+      rc = run_fast<T>(p, kind, only_stage, static_cast<const unsigned char*>(in) + b0 * ib,
+                       static_cast<unsigned char*>(out) + b0 * ib, ws, st, nstages, weight, thr, bc);
+    }
+    return rc;
+  }
   if (nstages) *nstages = 1;  // generic path is timed as one unit
   if (only_stage > 0) return SDCT_OK;
   if (p->fast) {

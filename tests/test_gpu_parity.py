@@ -500,3 +500,17 @@ def test_compress_vs_oracle(cuda, dtype):
                 assert oracle.rel_l2(got.double().cpu().numpy(), want) <= TOL[dtype], (shape, eps)
     with pytest.raises(ValueError):
         sd.compress(np.zeros((8, 8)), -1.0)
+
+
+def test_batch_beyond_grid_limit(cuda):
+    # batches above 65535 items run as consecutive launch sets
+    torch = _torch()
+    import paper_2110_01172_b200 as sd
+
+    g = torch.Generator(device="cuda").manual_seed(3)
+    x = torch.rand((70001, 8, 16), generator=g, device="cuda", dtype=torch.float64) * 2 - 1
+    y = sd.dct_2d(x)
+    z = sd.idct_2d(y)
+    assert float(((z / 32.0 - x).norm() / x.norm()).item()) <= 1e-13
+    for b in (0, 65534, 65535, 70000):
+        assert oracle.rel_l2(y[b].cpu().numpy(), oracle.port.dct_2d(x[b].cpu().numpy())) <= 1e-12, b
