@@ -78,7 +78,8 @@ struct Row2Geom {
   static constexpr int NT = TL::NT;  // threads per group
   static constexpr int CTA = NT * GROUPS;
   static constexpr int MINB = MODE == 1 ? 2 : 1;
-  static constexpr size_t SMEM = static_cast<size_t>(NBUF) * BUF + 16 * NBUF + 16;  // + full/empty mbarriers
+  static constexpr size_t STASH = static_cast<size_t>(NBUF) * BUF + 16 * NBUF + 16;  // after the mbarriers
+  static constexpr size_t SMEM = STASH + 64 * GROUPS;  // + per-group stash of 8 operands
 };
 
 template <typename T, int M, bool INV, int MODE>
@@ -293,24 +294,33 @@ __global__ void __launch_bounds__(Row2Geom<T, M, MODE>::CTA, Row2Geom<T, M, MODE
         rowA = rowB;
         rowB = tmp;
       }
-      T op[NI][8];
+      // operands of item kk (n2 in {kk, M-kk}): {DA, RA, DB, RB} per n2
+      auto load_ops = [&](int kk, T* o) {
 #pragma unroll
-      for (int i = 0; i < NI; ++i) {
-        const int kk = t + i * NT;
-        if (kk <= M / 2) {
-#pragma unroll
-          for (int u = 0; u < 2; ++u) {
-            const int nn = u ? M - kk : kk;
-            const bool z = nn == 0;
-            const int pd = a.mode == 2 ? n2 - nn : nn;
-            const int pr = a.mode == 2 ? nn : n2 - nn;
-            const bool zd = a.mode == 2 && z;
-            op[i][4 * u + 0] = zd ? T(0) : rowA[pd & (n2 - 1)];
-            op[i][4 * u + 1] = z ? T(0) : rowA[pr & (n2 - 1)];
-            op[i][4 * u + 2] = zd ? T(0) : rowB[pd & (n2 - 1)];
-            op[i][4 * u + 3] = z ? T(0) : rowB[pr & (n2 - 1)];
-          }
+        for (int u = 0; u < 2; ++u) {
+          const int nn = u ? M - kk : kk;
+          const bool z = nn == 0;
+          const int pd = a.mode == 2 ? n2 - nn : nn;
+          const int pr = a.mode == 2 ? nn : n2 - nn;
+          const bool zd = a.mode == 2 && z;
+          o[4 * u + 0] = zd ? T(0) : rowA[pd & (n2 - 1)];
+          o[4 * u + 1] = z ? T(0) : rowA[pr & (n2 - 1)];
+          o[4 * u + 2] = zd ? T(0) : rowB[pd & (n2 - 1)];
+          o[4 * u + 3] = z ? T(0) : rowB[pr & (n2 - 1)];
         }
+      };
+      // items kk = t + i NT < M/2 in registers; the one left, kk = M/2 (its
+      // own mirror), goes through a per-group stash so it costs no registers
+      constexpr int NIM = (M / 2) / NT;
+      T op[NIM][8];
+#pragma unroll
+      for (int i = 0; i < NIM; ++i) load_ops(t + i * NT, op[i]);
+      T* stash = reinterpret_cast<T*>(smem_raw + G::STASH) + grp * 8;
+      if (t == 0) {
+        T ox[8];
+        load_ops(M / 2, ox);
+#pragma unroll
+        for (int c = 0; c < 8; ++c) stash[c] = ox[c];
       }
       const V* ta = static_cast<const V*>(a.ta);
       const V* fb = static_cast<const V*>(a.fb);
@@ -332,31 +342,36 @@ __global__ void __launch_bounds__(Row2Geom<T, M, MODE>::CTA, Row2Geom<T, M, MODE
         x0 = cmul(c0, mk(p - q, -(r + sv)));
         x1 = cmul(c1, mk(r - sv, -(p + q)));
       };
-      const int sw0 = sw_t;
-#pragma unroll
-      for (int i = 0; i < NI; ++i) {
-        const int kk = t + i * NT;
-        if (kk <= M / 2) {
-          V A0, A1, B0, B1;  // X'(line, k), X'(line, M-k)
-          V bk = fac_lookup(fb, kk, a.fs), bm = mirror_b(bk);
-          if (kk == a.bad_q) bk = mk(-bk.x, -bk.y);
-          if (M - kk == a.bad_q) bm = mk(-bm.x, -bm.y);
-          xp(&op[i][0], cconj(bk), A0, A1);
-          xp(&op[i][4], cconj(bm), B0, B1);
-          // partner line of each row (-k1): swap for pairs, self for P == 0
-          const V pA0 = P != 0 ? A1 : A0, pA1 = P != 0 ? A0 : A1;
-          const V pB0 = P != 0 ? B1 : B0, pB1 = P != 0 ? B0 : B1;
-          const V wk = fac_lookup(fu, kk, a.fs), wmk = mk(-wk.x, wk.y);  // W_N2^k, W_N2^{M-k}
-          const int sa = sw0 ^ TL::swzc(i * NT);  // natural slot of k (mod M) in line 0
-          const int sa_ = kk == 0 ? 0 : sa;        // k == 0 -> slot 0 (kk = 0 only at t = 0, i = 0)
-          sm[sa_] = pack(A0, kk == 0 ? B0 : cconj(pB0), wk);
-          sm[sa_ ^ TL::swzc(M)] = pack(A1, kk == 0 ? B1 : cconj(pB1), wk);
-          if (kk != 0 && 2 * kk != M) {
-            const int sb = t ? (sw_nt ^ TL::swzc(M - (i + 1) * NT)) : TL::swzc((M - i * NT) & (M - 1));  // slot of M - k
-            sm[sb] = pack(B0, cconj(pA0), wmk);
-            sm[sb ^ TL::swzc(M)] = pack(B1, cconj(pA1), wmk);
-          }
+      // packed spectrum of item kk at natural slots sa (k) and sb (M - k) of line 0
+      auto pack_item = [&](int kk, const T* o, int sa, int sb) {
+        V A0, A1, B0, B1;  // X'(line, k), X'(line, M-k)
+        V bk = fac_lookup(fb, kk, a.fs), bm = mirror_b(bk);
+        if (kk == a.bad_q) bk = mk(-bk.x, -bk.y);
+        if (M - kk == a.bad_q) bm = mk(-bm.x, -bm.y);
+        xp(o, cconj(bk), A0, A1);
+        xp(o + 4, cconj(bm), B0, B1);
+        // partner line of each row (-k1): swap for pairs, self for P == 0
+        const V pA0 = P != 0 ? A1 : A0, pA1 = P != 0 ? A0 : A1;
+        const V pB0 = P != 0 ? B1 : B0, pB1 = P != 0 ? B0 : B1;
+        const V wk = fac_lookup(fu, kk, a.fs), wmk = mk(-wk.x, wk.y);  // W_N2^k, W_N2^{M-k}
+        sm[sa] = pack(A0, kk == 0 ? B0 : cconj(pB0), wk);
+        sm[sa ^ TL::swzc(M)] = pack(A1, kk == 0 ? B1 : cconj(pB1), wk);
+        if (kk != 0 && 2 * kk != M) {
+          sm[sb] = pack(B0, cconj(pA0), wmk);
+          sm[sb ^ TL::swzc(M)] = pack(B1, cconj(pA1), wmk);
         }
+      };
+#pragma unroll
+      for (int i = 0; i < NIM; ++i) {
+        const int sa = sw_t ^ TL::swzc(i * NT);  // natural slot of k = t + i NT in line 0
+        const int sb = t ? (sw_nt ^ TL::swzc(M - (i + 1) * NT)) : TL::swzc((M - i * NT) & (M - 1));  // slot of M - k
+        pack_item(t + i * NT, op[i], sa, sb);
+      }
+      if (t == 0) {
+        T ox[8];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) ox[c] = stash[c];
+        pack_item(M / 2, ox, TL::swzc(M / 2), 0);
       }
       StageTw<TL, 0> w0;
       w0.load(tw.st[0], t);
