@@ -99,6 +99,102 @@ constexpr int kFftMaxN = 4096;  // two line buffers + table in shared memory
 
 constexpr int kFftPerThread = 16;  // outputs a thread holds across one pass (lines * n <= 16 * 256)
 
+// One Stockham pass of radix R (compile time) over lines of length n in
+// shared memory, in place: each thread takes whole butterflies j (inputs
+// x[j + r n/R], r < R), applies the twiddles W_{ns R}^{(j % ns) r} and the
+// radix-R DFT, keeps the R outputs in registers across the barrier and writes
+// them to y[(j / ns) ns R + j % ns + k ns].
+template <int R>
+__device__ __forceinline__ void stockham_pass(double2* x, const double2* tw, int n, int ns, int total, int t,
+                                              int nt) {
+  constexpr int BMAX = (kFftPerThread + R - 1) / R;  // butterflies per thread (lines * n <= 16 * 256)
+  const int nr = n / R;
+  const int nb = total / R;  // butterflies over all lines of the tile
+  const int tstep = n / (ns * R);
+  double2 out[BMAX][R];
+#pragma unroll
+  for (int u = 0; u < BMAX; ++u) {
+    const int bq = t + u * nt;
+    if (bq < nb) {
+      const int l = bq / nr, j = bq - l * nr;
+      const int jr = j % ns;
+      const double2* xl = x + l * n + j;
+      double2 v[R];
+      v[0] = xl[0];
+      const int e1 = jr * tstep;  // W_n^{e1 r} = W_{ns R}^{(j % ns) r}
+      int e = e1;
+#pragma unroll
+      for (int r = 1; r < R; ++r) {
+        const double2 a = xl[r * nr], w = tw[e];
+        v[r] = make_double2(fma(a.x, w.x, -a.y * w.y), fma(a.x, w.y, a.y * w.x));
+        e += e1;
+        if (e >= n) e -= n;
+      }
+      // radix-R DFT: out[k] = sum_r v[r] W_R^{r k}, W_R^m = tw[m n / R]
+#pragma unroll
+      for (int k = 0; k < R; ++k) {
+        double re = v[0].x, im = v[0].y;
+#pragma unroll
+        for (int r = 1; r < R; ++r) {
+          const double2 w = tw[((r * k) % R) * nr];
+          re = fma(v[r].x, w.x, fma(-v[r].y, w.y, re));
+          im = fma(v[r].x, w.y, fma(v[r].y, w.x, im));
+        }
+        out[u][k] = make_double2(re, im);
+      }
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < BMAX; ++u) {
+    const int bq = t + u * nt;
+    if (bq < nb) {
+      const int l = bq / nr, j = bq - l * nr;
+      const int base = l * n + (j / ns) * ns * R + j % ns;
+#pragma unroll
+      for (int k = 0; k < R; ++k) x[base + k * ns] = out[u][k];
+    }
+  }
+  __syncthreads();
+}
+
+// Radix-R pass for other (prime) R: one thread per output, R MACs each.
+__device__ __forceinline__ void generic_pass(double2* x, const double2* tw, int n, int ns, int R, int total, int t,
+                                             int nt) {
+  const int nr = n / R;
+  double2 acc[kFftPerThread];
+#pragma unroll
+  for (int u = 0; u < kFftPerThread; ++u) {
+    const int e = t + u * nt;
+    if (e < total) {
+      const int l = e / n, q = e - l * n;
+      // output q = (j / ns) ns R + j % ns + k ns with j in [0, n/R), k in [0, R)
+      const int jr = q % ns, rest = q / ns;
+      const int k = rest % R, jq = rest / R;
+      const int j = jq * ns + jr;
+      const int E = (jr * (n / (ns * R)) + k * nr) % n;
+      const double2* xl = x + l * n + j;
+      double re = 0.0, im = 0.0;
+      int idx = 0;
+      for (int r = 0; r < R; ++r) {
+        const double2 v = xl[r * nr], w = tw[idx];
+        re = fma(v.x, w.x, fma(-v.y, w.y, re));
+        im = fma(v.x, w.y, fma(v.y, w.x, im));
+        idx += E;
+        if (idx >= n) idx -= n;
+      }
+      acc[u] = make_double2(re, im);
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < kFftPerThread; ++u) {
+    const int e = t + u * nt;
+    if (e < total) x[e] = acc[u];
+  }
+  __syncthreads();
+}
+
 __global__ void __launch_bounds__(256) g_fft_axis_smem(const double2* __restrict__ in, double2* __restrict__ out,
                                                        long long outer, int n, long long inner,
                                                        const double2* __restrict__ tab, int tab_stride, int inverse,
@@ -145,38 +241,15 @@ __global__ void __launch_bounds__(256) g_fft_axis_smem(const double2* __restrict
   int ns = 1;
   for (int s = 0; s < rad.count; ++s) {
     const int R = rad.r[s];
-    const int nr = n / R;
-    double2 acc[kFftPerThread];
-#pragma unroll
-    for (int u = 0; u < kFftPerThread; ++u) {
-      const int e = t + u * nt;
-      if (e < total) {
-        const int l = e / n, q = e - l * n;
-        // output q = (j / ns) ns R + j % ns + k ns with j in [0, n/R), k in [0, R)
-        const int jr = q % ns, rest = q / ns;
-        const int k = rest % R, jq = rest / R;
-        const int j = jq * ns + jr;
-        const int E = (jr * (n / (ns * R)) + k * nr) % n;
-        const double2* xl = x + l * n + j;
-        double re = 0.0, im = 0.0;
-        int idx = 0;
-        for (int r = 0; r < R; ++r) {
-          const double2 v = xl[r * nr], w = tw[idx];
-          re = fma(v.x, w.x, fma(-v.y, w.y, re));
-          im = fma(v.x, w.y, fma(v.y, w.x, im));
-          idx += E;
-          if (idx >= n) idx -= n;
-        }
-        acc[u] = make_double2(re, im);
-      }
+    switch (R) {  // butterfly-per-thread passes for the common radices
+      case 2: stockham_pass<2>(x, tw, n, ns, total, t, nt); break;
+      case 3: stockham_pass<3>(x, tw, n, ns, total, t, nt); break;
+      case 4: stockham_pass<4>(x, tw, n, ns, total, t, nt); break;
+      case 5: stockham_pass<5>(x, tw, n, ns, total, t, nt); break;
+      case 7: stockham_pass<7>(x, tw, n, ns, total, t, nt); break;
+      case 8: stockham_pass<8>(x, tw, n, ns, total, t, nt); break;
+      default: generic_pass(x, tw, n, ns, R, total, t, nt); break;
     }
-    __syncthreads();
-#pragma unroll
-    for (int u = 0; u < kFftPerThread; ++u) {
-      const int e = t + u * nt;
-      if (e < total) x[e] = acc[u];
-    }
-    __syncthreads();
     ns *= R;
   }
   for (int e = t; e < total; e += nt) {
