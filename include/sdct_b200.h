@@ -118,7 +118,8 @@ int sdct_exec_host(sdct_plan_t plan, int kind, const void* h_in, void* h_out, vo
  * xi1 = idct_idxst_2d(a1), xi2 = idxst_idct_2d(a2). Device buffers of one
  * plan-sized batch; the weighting is fused into the inverse passes' loads (no
  * a1/a2 arrays). d_workspace as for sdct_exec (NULL = the plan's own).
- * Stream-ordered. */
+ * Stream-ordered; the coefficients live in a plan-owned scratch buffer, so
+ * concurrent calls on one plan must be ordered by the caller (one stream). */
 int sdct_force_fields(sdct_plan_t plan, const void* d_density, void* d_xi1, void* d_xi2, void* d_workspace,
                       void* stream);
 /* Same on host memory (H2D, the fused device pipeline, D2H, synchronised). */
@@ -130,7 +131,9 @@ int sdct_force_fields_host(sdct_plan_t plan, const void* h_density, void* h_xi1,
  * counted into *d_zeroed (a device counter the caller zeroes; may be NULL);
  * d_out = idct_2d(b) * 4/(N1 N2). The threshold and the normalisation ride on
  * the inverse row kernels' loads. Rounding to 8-bit samples and PSNR are the
- * image app's (out of scope). epsilon may be +inf; < 0 or NaN -> SDCT_ERR_ARG. */
+ * image app's (out of scope). epsilon may be +inf; < 0 or NaN -> SDCT_ERR_ARG.
+ * Shares the plan-owned coefficient scratch with sdct_force_fields (order
+ * concurrent calls on one plan). */
 int sdct_compress(sdct_plan_t plan, const void* d_in, void* d_out, double epsilon, unsigned long long* d_zeroed,
                   void* d_workspace, void* stream);
 
