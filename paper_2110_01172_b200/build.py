@@ -90,6 +90,12 @@ def build(verbose: bool = False, jobs: int | None = None) -> str:
         _run(["g++"] + CXXFLAGS + ["-shared", "-I", pybind11.get_include(),
                                    "-I", sysconfig.get_paths()["include"], pysrc, "-o", PYMOD,
                                    "-L", LIB, "-lsdct_b200", "-Wl,-rpath,$ORIGIN/lib"])
+    # C++ drop-in check program (tests/cpp/api_smoke.cpp) against the C++ API
+    src = os.path.join(ROOT, "tests", "cpp", "api_smoke.cpp")
+    exe = os.path.join(LIB, "api_smoke")
+    if os.path.exists(src) and (not os.path.exists(exe) or os.path.getmtime(exe) < max(
+            os.path.getmtime(src), os.path.getmtime(LIBSO), hdr_time)):
+        _run(["g++"] + CXXFLAGS + [src, "-o", exe, "-L", LIB, "-lsdct_b200", "-Wl,-rpath,$ORIGIN"])
     return LIBSO
 
 

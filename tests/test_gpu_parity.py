@@ -514,3 +514,17 @@ def test_batch_beyond_grid_limit(cuda):
     assert float(((z / 32.0 - x).norm() / x.norm()).item()) <= 1e-13
     for b in (0, 65534, 65535, 70000):
         assert oracle.rel_l2(y[b].cpu().numpy(), oracle.port.dct_2d(x[b].cpu().numpy())) <= 1e-12, b
+
+
+def test_cpp_api_program(cuda):
+    # a program written against the reference's C++ operator API, compiled
+    # against include/sdct and linked with libsdct_b200.so (build.py)
+    import os
+    import subprocess
+
+    exe = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                       "paper_2110_01172_b200", "lib", "api_smoke")
+    assert os.path.exists(exe), "tests/cpp/api_smoke.cpp not built (run __graft_entry__.build())"
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert r.stdout.count("PASS") == 7, r.stdout

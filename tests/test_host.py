@@ -112,3 +112,12 @@ def test_swizzle_is_a_bijection():
 def test_digit_reversal_is_a_permutation():
     for L in (2, 8, 32, 512, 2048, 4096):
         assert sorted(sm.digit_pos(L, k) for k in range(L)) == list(range(L))
+
+
+def test_cpp_api_program_is_built():
+    # the C++ drop-in check links against the library without a GPU present
+    import os
+
+    exe = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                       "paper_2110_01172_b200", "lib", "api_smoke")
+    assert os.path.exists(exe)
