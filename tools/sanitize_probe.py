@@ -1,0 +1,21 @@
+"""Small transforms of every kernel family for compute-sanitizer runs (developer tool)."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+import paper_2110_01172_b200 as sd
+
+torch.manual_seed(0)
+for dt in (torch.float64, torch.float32):
+    for shape in [(64, 128), (2048, 2048), (16, 4096)]:
+        x = torch.rand(shape, dtype=dt, device="cuda")
+        for f in (sd.dct_2d, sd.idct_2d, sd.idct_idxst_2d, sd.idxst_idct_2d):
+            f(x)
+        sd.force_demo_fields(x)
+        sd.compress(x, 0.5)
+    x3 = torch.rand((16, 8, 32), dtype=dt, device="cuda")
+    sd.dct_3d(x3)
+    sd.idct_3d(x3)
+    sd.dct_2d(torch.rand((7, 9), dtype=dt, device="cuda"))
+    sd.dct_2d(torch.rand((8192, 16), dtype=dt, device="cuda"))
+torch.cuda.synchronize()
+print("probe done")
