@@ -97,7 +97,7 @@ struct Radices {
 
 constexpr int kFftMaxN = 4096;  // two line buffers + table in shared memory
 
-constexpr int kFftPerThread = 16;  // outputs a thread holds across one pass (lines * n <= 16 * 256)
+constexpr int kFftPerThread = 8;  // outputs a thread holds across one pass (lines * n <= 8 * threads)
 
 // One Stockham pass of radix R (compile time) over lines of length n in
 // shared memory, in place: each thread takes whole butterflies j (inputs
@@ -195,7 +195,7 @@ __device__ __forceinline__ void generic_pass(double2* x, const double2* tw, int 
   __syncthreads();
 }
 
-__global__ void __launch_bounds__(256) g_fft_axis_smem(const double2* __restrict__ in, double2* __restrict__ out,
+__global__ void __launch_bounds__(512) g_fft_axis_smem(const double2* __restrict__ in, double2* __restrict__ out,
                                                        long long outer, int n, long long inner,
                                                        const double2* __restrict__ tab, int tab_stride, int inverse,
                                                        Radices rad, int lpc) {
@@ -517,8 +517,11 @@ cudaError_t generic_run(const GenericJob& job, const void* in, void* out, void* 
       const int n = job.dims[a];
       // shared-memory line FFT of length len over lines (outer', inner'), table stride ts
       auto line_fft = [&](const double2* src, double2* dst, long long outer_, int len, long long inner_, int ts) {
+        // threads per CTA: the fewest (>= 128) that hold a whole line at
+        // kFftPerThread outputs each (small CTAs: the passes are latency bound)
+        const int nt = len <= 1024 ? 128 : len <= 2048 ? 256 : 512;
         int lpc = 1;
-        while (lpc < 16 && 2 * lpc * len <= kFftPerThread * kThreads &&
+        while (lpc < 16 && 2 * lpc * len <= kFftPerThread * nt &&
                (inner_ == 1 ? lpc * 2 <= outer_ : inner_ % (lpc * 2) == 0))
           lpc *= 2;
         const size_t smem = (static_cast<size_t>(lpc) * len + len) * sizeof(double2);
@@ -528,7 +531,7 @@ cudaError_t generic_run(const GenericJob& job, const void* in, void* out, void* 
           attr_set = true;
         }
         const long long tiles = inner_ > 1 ? outer_ * (inner_ / lpc) : (outer_ + lpc - 1) / lpc;
-        g_fft_axis_smem<<<static_cast<unsigned>(tiles), kThreads, smem, st>>>(src, dst, outer_, len, inner_,
+        g_fft_axis_smem<<<static_cast<unsigned>(tiles), nt, smem, st>>>(src, dst, outer_, len, inner_,
                                                                             job.circle[a], ts, inverse,
                                                                             factorise(len), lpc);
       };
