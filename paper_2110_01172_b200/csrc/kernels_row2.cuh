@@ -77,7 +77,7 @@ struct Row2Geom {
   using TL = Row2Tile<T, M, false, GROUPS>;
   static constexpr int NT = TL::NT;  // threads per group
   static constexpr int CTA = NT * GROUPS;
-  static constexpr int MINB = MODE == 1 ? 2 : 1;
+  static constexpr int MINB = MODE == 1 ? (sizeof(T) == 4 ? 3 : 2) : 1;  // fp32: 3 CTAs/SM (inverse row 56 -> 52 us at 4096^2); fp64 spills at 3
   static constexpr size_t STASH = static_cast<size_t>(NBUF) * BUF + 16 * NBUF + 16;  // after the mbarriers
   static constexpr size_t SMEM = STASH + 64 * GROUPS;  // + per-group stash of 8 operands
 };
