@@ -157,14 +157,16 @@ cudaError_t launch_row2(dim3 grid, cudaStream_t st, const RowArgs& a, const TwSe
 template <typename T, int M, int KIND>
 cudaError_t launch_row_one(dim3 grid, cudaStream_t st, const RowArgs& a, const TwSet& tw) {
   if constexpr (KIND == RK_FWD2 || KIND == RK_INV2) {
-    // measured on B200 at 4096^2 (tools/stage_time.py): the forward kernel
-    // gains from the persistent grouped ring, the inverse (heavier register
-    // use in its preprocess) runs best as one item per CTA
+    // measured on B200 (tools/stage_time.py): the forward kernel gains from
+    // the persistent grouped ring; the inverse (heavier register use in its
+    // preprocess) runs best as one item per CTA for long rows (M = 2048:
+    // 92 vs 96 us fp64 at 4096^2) and in the ring for shorter ones (M = 1024:
+    // 32.8 vs 34.8 us fp64 at 2048^2)
     static const int forced = [] {
       const char* f = getenv("SDCT_ROW2_MODE");  // developer override: 0 / 1
       return f ? atoi(f) : -1;
     }();
-    const bool one = forced >= 0 ? forced == 1 : KIND == RK_INV2;
+    const bool one = forced >= 0 ? forced == 1 : (KIND == RK_INV2 && M > 1024);
     if (one || row2_mode<T, M>() == 1) return launch_row2<T, M, KIND == RK_INV2, 1>(grid, st, a, tw);
     if constexpr (row2_mode<T, M>() == 0) return launch_row2<T, M, KIND == RK_INV2, 0>(grid, st, a, tw);
     return cudaErrorInvalidValue;
