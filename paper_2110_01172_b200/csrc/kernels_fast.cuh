@@ -93,7 +93,6 @@ struct RowArgs {
   int weight;                      // 2D inverse input: 0 none, 1/2 force-field weight w1/w2, 3 compression threshold
   double thr_eps, thr_scale;       // weight 3: zero |b| < thr_eps, scale the rest
   unsigned long long* thr_count;   // weight 3: zeroed coefficients (device counter, may be null)
-  int dev;                         // developer flags (0 in production): bit 0 skips the row FFT math
 };
 
 // ---- small helpers ----------------------------------------------------------

@@ -18,7 +18,8 @@
 // (16 warps), and no grid-wide phase alignment of load/compute/store forms.
 // A consumer waits `empty` (release of item k-NBUF) before `full`, which
 // keeps every mbarrier waiter at most one phase behind (parity-safe).
-// MODE 1 (small rows): one item per CTA, many CTAs per SM.
+// MODE 1 (small rows, and the inverse for M > 1024 where it measures
+// faster): one item per CTA, several CTAs per SM.
 //
 //   forward (RK_FWD2): rows srow(k1), srow(N1-k1) of the column pass's
 //     intermediate Z (pair-interleaved complex) -> row FFT -> Hermitian
@@ -173,7 +174,7 @@ __global__ void __launch_bounds__(Row2Geom<T, M, MODE>::CTA, Row2Geom<T, M, MODE
         }
       }
       TL::sync();  // landing rows consumed: the buffer becomes the exchange buffer
-      if (!(a.dev & 1)) fft_regs<TL, false>(v, sm, tw, w0, t);
+      fft_regs<TL, false>(v, sm, tw, w0, t);
       TL::sync();
       last_to_natural<TL>(v, sm, t);
       TL::sync();
@@ -377,7 +378,7 @@ __global__ void __launch_bounds__(Row2Geom<T, M, MODE>::CTA, Row2Geom<T, M, MODE
       w0.load(tw.st[0], t);
       TL::sync();
       from_smem<TL, 0>(v, sm, t);
-      if (!(a.dev & 1)) fft_regs<TL, true>(v, sm, tw, w0, t);
+      fft_regs<TL, true>(v, sm, tw, w0, t);
       TL::sync();
       last_to_natural<TL>(v, sm, t);
       TL::sync();

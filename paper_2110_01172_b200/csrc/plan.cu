@@ -523,13 +523,6 @@ int run_fast(sdct_plan_s* p, int kind, int only_stage, const void* in, void* out
     ra.thr_scale = thr->scale;
     ra.thr_count = thr->count;
   }
-  {
-    static const int dev = [] {
-      const char* f = getenv("SDCT_DEV_FLAGS");  // developer experiments only (tools/)
-      return f ? atoi(f) : 0;
-    }();
-    ra.dev = dev;
-  }
   if (p->rank == 2) {
     const long long inter = static_cast<long long>(n1) * M;
     if (kind == SDCT_DCT_2D) {
