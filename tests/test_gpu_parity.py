@@ -528,3 +528,33 @@ def test_cpp_api_program(cuda):
     r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0, r.stdout + r.stderr
     assert r.stdout.count("PASS") == 7, r.stdout
+
+
+def test_orientation_and_threads_do_not_change_results(cuda):
+    # Plan2d's forced orientation (dct2d.hpp:43-46, test_dct2d.cpp:144-158) and
+    # the threads= knob (module.cpp:72-149) select the reference's CPU
+    # strategy; on the GPU both are bookkeeping and the results are identical
+    torch = _torch()
+    import paper_2110_01172_b200 as sd
+    from paper_2110_01172_b200 import capi
+
+    for shape in [(64, 16), (256, 32), (8, 8), (33, 7)]:
+        x = torch.tensor(rnd(shape, 61), device="cuda")
+        outs = []
+        for orient in (capi.ORIENT_DIRECT, capi.ORIENT_TRANSPOSED):
+            plan = capi.Plan(shape, orientation=orient)
+            assert plan.orientation == orient
+            for kind in ("dct_2d", "idct_2d", "idct_idxst_2d"):
+                y = torch.empty_like(x)
+                plan.exec(kind, x.data_ptr(), y.data_ptr())
+                outs.append((orient, kind, y))
+        torch.cuda.synchronize()
+        by_kind = {}
+        for orient, kind, y in outs:
+            by_kind.setdefault(kind, []).append(y)
+        for kind, ys in by_kind.items():
+            assert torch.equal(ys[0], ys[1]), (shape, kind)
+        xh = x.cpu().numpy()
+        assert np.array_equal(sd.dct_2d(xh, threads=1), sd.dct_2d(xh, threads=8))
+        # counters follow the oriented extents like the reference (dct2d.cpp:371-374)
+        assert capi.Plan(shape, orientation=capi.ORIENT_TRANSPOSED).counters("dct_2d")[0] == 3
