@@ -138,6 +138,10 @@ WORKLOADS = {
                desc="3D DCT-II 256^3 {dt} per rank (BASELINE configs[3])"),
     "c5": dict(dims=(2048, 2048), kinds=["dct_2d"], mode="chain", dtype="float32", batch=512, sharded=True,
                desc="batched DCT-II 512 x 2048x2048 {dt}, batch sharded over ranks (BASELINE configs[4])"),
+    # SURVEY §8f next rows, measured like the configs
+    "cz": dict(dims=(4096, 4096), kinds=["dct_2d", "idct_2d"], mode="compress", dtype="float64", batch=1,
+               desc="compression round trip 4096x4096 {dt} per rank: dct_2d, |b| < median zeroed, "
+                    "idct_2d * 4/(N1 N2) (compress.cpp:24-54 numeric core)"),
 }
 L2_BYTES = 126 * 1024 * 1024
 
@@ -182,7 +186,12 @@ def cpu_reference_rate(w, budget_s: float, max_steps: int | None = None):
         force = oracle.port.force_demo_fields
 
     def unit():
-        if w["mode"] == "force":
+        if w["mode"] == "compress":
+            import numpy as np_
+
+            b = fns[0](x)
+            fns[1](np_.where(np_.abs(b) < np_.median(np_.abs(b)), 0.0, b)) * (4.0 / b.size)
+        elif w["mode"] == "force":
             force(x)
         elif w["mode"] == "chain":
             y = x
@@ -204,6 +213,7 @@ def cpu_reference_rate(w, budget_s: float, max_steps: int | None = None):
     dt = (time.perf_counter() - t0) / n
     bytes_unit = 2.0 * _numel(dims) * 8 * len(kinds)
     what = ("force_demo_fields" if w["mode"] == "force" else
+            "dct_2d, threshold at the median |b|, idct_2d, 4/(N1 N2)" if w["mode"] == "compress" else
             " then ".join(kinds) if w["mode"] == "chain" else " + ".join(kinds))
     sample = (f"{n} x ({what}) of one {'x'.join(map(str, dims))} fp64 image on the host, prebuilt plans, "
               f"threads=0 ({dt * 1e3:.1f} ms each)")
@@ -329,11 +339,23 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     plan = sd.plan_for(dims, B, dtype, local_rank)
     ws = torch.empty(plan.workspace_bytes, dtype=torch.uint8, device=dev)
 
+    eps_c = 0.0
+    zeroed = torch.zeros(1, dtype=torch.int64, device=dev)
+    if w["mode"] == "compress":
+        # threshold = the median coefficient magnitude of the (first) input
+        b0 = torch.empty_like(xs[0])
+        plan.run(_sdct.DCT_2D, xs[0].data_ptr(), b0.data_ptr(), s, ws.data_ptr())
+        eps_c = float(b0.abs().median().item())
+        del b0
+
     def step(i):
         r = i % rot
         src = xs[r]
         if w["mode"] == "force":
             plan.force_fields(src.data_ptr(), outs[r][0].data_ptr(), outs[r][1].data_ptr(), s, ws.data_ptr())
+            return
+        if w["mode"] == "compress":
+            plan.compress(src.data_ptr(), outs[r][0].data_ptr(), eps_c, zeroed.data_ptr(), s, ws.data_ptr())
             return
         for j, k in enumerate(kinds):
             dst = outs[r][j]
@@ -349,9 +371,14 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     step(0)
     torch.cuda.synchronize()
     parity = {}
-    if w["kinds"] == ["dct_2d", "idct_2d"]:
+    if w["mode"] == "chain" and w["kinds"] == ["dct_2d", "idct_2d"]:
         scale = numel / 4.0
         parity["round_trip_rel_l2"] = float(((outs[0][1] / scale - xs[0]).norm() / xs[0].norm()).item())
+    elif w["mode"] == "compress":
+        zeroed.zero_()
+        step(0)
+        torch.cuda.synchronize()
+        parity["zeroed_fraction"] = float(zeroed.item()) / (B * numel)
     elif rank == 0 and w["mode"] == "force":
         import oracle
 
@@ -516,10 +543,29 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     x_pin = xs[0][:1].cpu().pin_memory()
     out_pin = torch.empty_like(x_pin).pin_memory()
     chains = ([w["kinds"]] if w["mode"] == "chain" else [[k] for k in w["kinds"]] if w["mode"] == "fan" else [])
+    if w["mode"] == "compress":
+        chains = []
     e_steps = 1 if B > 16 else max(5, min(args.steps, 50))
     a = torch.cuda.Event(enable_timing=True)
     b = torch.cuda.Event(enable_timing=True)
-    if w["mode"] == "force":
+    if w["mode"] == "compress":
+        # sd.compress on a device tensor: image in, reconstruction out every step
+        xd = torch.empty_like(xs[0][:1])
+
+        def e2e_compress():
+            xd.copy_(x_pin, non_blocking=True)
+            rec, _ = sd.compress(xd[0], eps_c)
+            out_pin[0].copy_(rec, non_blocking=True)
+
+        e2e_compress()
+        torch.cuda.synchronize()
+        barrier()
+        a.record(stream)
+        for _ in range(e_steps):
+            e2e_compress()
+        b.record(stream)
+        n_out = 1
+    elif w["mode"] == "force":
         # sd.force_demo_fields on a device tensor, with the density copied in and
         # both fields copied out every step (one stream, not pipelined)
         xd = torch.empty_like(xs[0][:1])
@@ -556,7 +602,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e_ms = float(t.item())
     e2e_val = job_bytes_step * e_steps / (e_ms / 1e3) / 1e9
-    if w["kinds"] == ["dct_2d", "idct_2d"]:
+    if w["mode"] == "chain" and w["kinds"] == ["dct_2d", "idct_2d"]:
         x0 = x_pin[0].to(torch.float64)
         parity["e2e_round_trip_rel_l2"] = float(((out_pin[0].to(torch.float64) / (numel / 4.0) - x0).norm()
                                                  / x0.norm()).item())
@@ -591,6 +637,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                     "ms_per_step": round(e_ms / e_steps, 4),
                     "path": ("pinned host -> paper_2110_01172_b200.force_demo_fields (torch CUDA) -> pinned host"
                              if w["mode"] == "force" else
+                             "pinned host -> paper_2110_01172_b200.compress (torch CUDA) -> pinned host"
+                             if w["mode"] == "compress" else
                              f"pinned host -> paper_2110_01172_b200.stream_host({w['kinds']}) "
                              "(sdct_exec_host_pipelined, 3 overlapped lanes) -> pinned host")},
             "gpu_launches": args.steps * sum(plan.stage_count(k) for k in kinds),
