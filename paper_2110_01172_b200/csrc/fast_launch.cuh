@@ -147,8 +147,9 @@ cudaError_t launch_row2(dim3 grid, cudaStream_t st, const RowArgs& a, const TwSe
     resident = sms * (per > 0 ? per : 1);
   }
   const int nitems = static_cast<int>(grid.x * grid.y);
-  // MODE 0: persistent, at most one CTA per two items so both groups work
-  const int want = MODE == 1 ? nitems : (nitems + 1) / 2;
+  // MODE 0: persistent, at most one CTA per two items so both groups work;
+  // MODE 2: persistent, one item at a time per CTA; MODE 1: one CTA per item
+  const int want = MODE == 0 ? (nitems + 1) / 2 : nitems;
   const int ctas = want < resident || MODE == 1 ? want : resident;
   k<<<ctas, Geo::CTA, Geo::SMEM, st>>>(a, tw, nitems);
   return cudaGetLastError();
@@ -166,6 +167,10 @@ cudaError_t launch_row_one(dim3 grid, cudaStream_t st, const RowArgs& a, const T
       const char* f = getenv("SDCT_ROW2_MODE");  // developer override: 0 / 1
       return f ? atoi(f) : -1;
     }();
+    // fp32 forward rows up to M = 1024: the split-prefetch CTA pair per SM
+    // measured best (2048^2: 20.5 vs 22.5 us)
+    const bool split = forced >= 0 ? forced == 2 : (KIND == RK_FWD2 && sizeof(T) == 4 && M <= 1024 && M >= 256);
+    if (split) return launch_row2<T, M, KIND == RK_INV2, 2>(grid, st, a, tw);
     const bool one = forced >= 0 ? forced == 1 : (KIND == RK_INV2 && M > 1024);
     if (one || row2_mode<T, M>() == 1) return launch_row2<T, M, KIND == RK_INV2, 1>(grid, st, a, tw);
     if constexpr (row2_mode<T, M>() == 0) return launch_row2<T, M, KIND == RK_INV2, 0>(grid, st, a, tw);

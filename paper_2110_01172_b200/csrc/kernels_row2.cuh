@@ -68,18 +68,27 @@ constexpr int row2_mode() {
   return Tile<T, M, 2, false>::NT >= 128 && 2u * (2u * M * sizeof(cx_t<T>)) <= 200u * 1024u ? 0 : 1;
 }
 
+// MODE 0: persistent, two consumer groups, ring of NBUF full buffers.
+// MODE 1: one item per CTA.
+// MODE 2: persistent, one group, two CTAs per SM; a full buffer holds row B
+//         and serves as the exchange buffer, a half buffer prefetches the
+//         next item's row A while the current item computes (row B of the
+//         next item loads once the exchange buffer is free).
 template <typename T, int M, int MODE>
 struct Row2Geom {
   static constexpr unsigned BUF = 2u * M * sizeof(cx_t<T>);  // one pair: 2 complex rows == 2 real rows of 2M
   static constexpr int GROUPS = MODE == 0 ? 2 : 1;
-  static constexpr int NBUF = MODE == 1 ? 1
+  static constexpr int NBUF = MODE != 0 ? 1
                               : (200u * 1024u) / BUF >= 4 ? 4
                               : ((200u * 1024u) / BUF < 2 ? 2 : static_cast<int>((200u * 1024u) / BUF));
   using TL = Row2Tile<T, M, false, GROUPS>;
   static constexpr int NT = TL::NT;  // threads per group
   static constexpr int CTA = NT * GROUPS;
-  static constexpr int MINB = MODE == 1 ? (sizeof(T) == 4 ? 3 : 2) : 1;  // fp32: 3 CTAs/SM (inverse row 56 -> 52 us at 4096^2); fp64 spills at 3
-  static constexpr size_t STASH = static_cast<size_t>(NBUF) * BUF + 16 * NBUF + 16;  // after the mbarriers
+  // fp32: 3 CTAs/SM (inverse row 56 -> 52 us at 4096^2); fp64 spills at 3
+  static constexpr int MINB = MODE == 0 ? 1 : (sizeof(T) == 4 ? 3 : 2);
+  static constexpr size_t PREF = MODE == 2 ? BUF / 2 : 0;                               // row-A prefetch region
+  static constexpr size_t BARS = static_cast<size_t>(NBUF) * BUF + PREF;                // mbarriers
+  static constexpr size_t STASH = BARS + 16 * NBUF + 16;                                // after the mbarriers
   static constexpr size_t SMEM = STASH + 64 * GROUPS;  // + per-group stash of 8 operands
 };
 
@@ -94,8 +103,9 @@ __global__ void __launch_bounds__(Row2Geom<T, M, MODE>::CTA, Row2Geom<T, M, MODE
   constexpr int R0 = TL::R0, Q0 = M / R0, NBF0 = TL::E / R0;
   constexpr int NI = (M / 2) / NT + 1;  // postprocess / preprocess items k in [0, M/2] per thread
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + NBUF * G::BUF);
-  uint64_t* empty = full + NBUF;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + G::BARS);
+  uint64_t* empty = full + NBUF;  // MODE 2: empty[0] is the row-A (prefetch region) barrier
+  unsigned char* pref = smem_raw + NBUF * G::BUF;  // MODE 2 row-A region
   const int grp = GROUPS == 1 ? 0 : static_cast<int>(threadIdx.x) / NT;
   const int t = static_cast<int>(threadIdx.x) - grp * NT;  // thread index within the group
   const int n1 = a.n1, n2 = a.n2, half = n1 / 2;
@@ -104,23 +114,37 @@ __global__ void __launch_bounds__(Row2Geom<T, M, MODE>::CTA, Row2Geom<T, M, MODE
     q1 = P;
     m1 = P == 0 ? half : n1 - P;
   };
-  // thread 0: land item `it` in buffer b
-  auto issue = [&](int it, int b) {
+  // thread 0: land row A (which = 0) or row B (which = 1) of item `it` at dst,
+  // completing on bar
+  auto issue_row = [&](int it, int which, unsigned char* dst, uint64_t* bar) {
     const int P = it % half, batch = it / half;
     int q1, m1;
     rows_of(P, q1, m1);
+    const int row = which ? m1 : q1;
+    if constexpr (!INV) {
+      const V* src = static_cast<const V*>(a.src) + batch * a.src_batch;
+      bulk_load(dst, src + static_cast<long long>(__ldg(a.s0 + row)) * M, G::BUF / 2, bar);
+    } else {
+      const T* src = static_cast<const T*>(a.src) + batch * a.src_batch;
+      bulk_load(dst, src + static_cast<long long>(row) * n2, G::BUF / 2, bar);
+    }
+  };
+  // thread 0: land item `it` in buffer b (MODE 0 / 1)
+  auto issue = [&](int it, int b) {
     unsigned char* dst = smem_raw + b * G::BUF;
     uint64_t* bar = full + b;
     mbar_expect_tx(bar, G::BUF);
-    if constexpr (!INV) {
-      const V* src = static_cast<const V*>(a.src) + batch * a.src_batch;
-      bulk_load(dst, src + static_cast<long long>(__ldg(a.s0 + q1)) * M, G::BUF / 2, bar);
-      bulk_load(dst + G::BUF / 2, src + static_cast<long long>(__ldg(a.s0 + m1)) * M, G::BUF / 2, bar);
-    } else {
-      const T* src = static_cast<const T*>(a.src) + batch * a.src_batch;
-      bulk_load(dst, src + static_cast<long long>(q1) * n2, G::BUF / 2, bar);
-      bulk_load(dst + G::BUF / 2, src + static_cast<long long>(m1) * n2, G::BUF / 2, bar);
-    }
+    issue_row(it, 0, dst, bar);
+    issue_row(it, 1, dst + G::BUF / 2, bar);
+  };
+  // MODE 2: row A into the prefetch region, row B into the second half of the buffer
+  auto issue_a = [&](int it) {
+    mbar_expect_tx(empty, G::BUF / 2);
+    issue_row(it, 0, pref, empty);
+  };
+  auto issue_b = [&](int it) {
+    mbar_expect_tx(full, G::BUF / 2);
+    issue_row(it, 1, smem_raw + G::BUF / 2, full);
   };
 
   if (threadIdx.x == 0) {
@@ -132,10 +156,17 @@ __global__ void __launch_bounds__(Row2Geom<T, M, MODE>::CTA, Row2Geom<T, M, MODE
   }
   __syncthreads();
   if (threadIdx.x == 0) {
+    if constexpr (MODE == 2) {
+      if (static_cast<int>(blockIdx.x) < nitems) {
+        issue_a(blockIdx.x);
+        issue_b(blockIdx.x);
+      }
+    } else {
 #pragma unroll 1
-    for (int b = 0; b < NBUF; ++b) {
-      const int it = blockIdx.x + b * gridDim.x;
-      if (it < nitems) issue(it, b);
+      for (int b = 0; b < NBUF; ++b) {
+        const int it = blockIdx.x + b * gridDim.x;
+        if (it < nitems) issue(it, b);
+      }
     }
   }
 
@@ -150,7 +181,8 @@ __global__ void __launch_bounds__(Row2Geom<T, M, MODE>::CTA, Row2Geom<T, M, MODE
     if (it >= nitems) break;
     const int b = k % NBUF;
     const uint32_t ph = static_cast<uint32_t>(k / NBUF) & 1u;
-    if (k >= NBUF) mbar_wait(empty + b, ph ^ 1u);  // item k-NBUF released the buffer
+    if (MODE == 0 && k >= NBUF) mbar_wait(empty + b, ph ^ 1u);  // item k-NBUF released the buffer
+    const int nxt = it + static_cast<int>(gridDim.x);          // MODE 2: the CTA's next item
     V* sm = reinterpret_cast<V*>(smem_raw + b * G::BUF);
     const int P = it % half, batch = it / half;
     int q1, m1;
@@ -162,6 +194,8 @@ __global__ void __launch_bounds__(Row2Geom<T, M, MODE>::CTA, Row2Geom<T, M, MODE
       StageTw<TL, 0> w0;
       w0.load(tw.st[0], t);
       mbar_wait(full + b, ph);
+      if constexpr (MODE == 2) mbar_wait(empty, ph);
+      const V* line0 = MODE == 2 ? reinterpret_cast<const V*>(pref) : sm;
 #pragma unroll
       for (int i = 0; i < NBF0; ++i) {
         int line, j, bb;
@@ -170,10 +204,16 @@ __global__ void __launch_bounds__(Row2Geom<T, M, MODE>::CTA, Row2Geom<T, M, MODE
         for (int r = 0; r < R0; ++r) {
           const int n = j + r * Q0;
           const int s = (r < R0 / 2) ? 2 * n : 2 * M - 1 - 2 * n;  // pair-interleaved column of z(n)
-          v[i * R0 + r] = sm[line * M + s];
+          v[i * R0 + r] = line ? sm[M + s] : line0[s];
         }
       }
       TL::sync();  // landing rows consumed: the buffer becomes the exchange buffer
+      if constexpr (MODE == 2) {
+        if (t == 0 && nxt < nitems) {
+          fence_async_smem();
+          issue_a(nxt);  // the next item's row A streams in under this item's math
+        }
+      }
       fft_regs<TL, false>(v, sm, tw, w0, t);
       TL::sync();
       last_to_natural<TL>(v, sm, t);
@@ -248,23 +288,25 @@ __global__ void __launch_bounds__(Row2Geom<T, M, MODE>::CTA, Row2Geom<T, M, MODE
     } else {
       // ============ inverse: merged preprocess + packing + inverse FFT =======
       // buffer = rows q1 (A) and m1 (B) of x, 2M reals each
-      const T* rowA = reinterpret_cast<const T*>(sm);
-      const T* rowB = rowA + 2 * M;
+      const T* rowA = MODE == 2 ? reinterpret_cast<const T*>(pref) : reinterpret_cast<const T*>(sm);
+      const T* rowB = reinterpret_cast<const T*>(sm) + 2 * M;
       // (the weighting below runs on the landed rows in their own order)
       mbar_wait(full + b, ph);
+      if constexpr (MODE == 2) mbar_wait(empty, ph);
       if (a.weight == 3) {
         // compression (proj/src/compress.cpp:33-45) folded into this load:
         // zero every coefficient with |b| < eps (counted), scale the rest by
         // the 4/(N1 N2) reconstruction normalisation (linear, so it commutes
         // with the inverse transform)
-        T* rw = reinterpret_cast<T*>(sm);
+        T* const rws[2] = {const_cast<T*>(rowA), const_cast<T*>(rowB)};
         const T eps = static_cast<T>(a.thr_eps), sc = static_cast<T>(a.thr_scale);
         unsigned cnt = 0;
         for (int e = t; e < 2 * n2; e += NT) {
-          const T v = rw[e];
+          T* rw = rws[e >= n2] + (e & (n2 - 1));
+          const T v = *rw;
           const bool drop = fabs(v) < eps;
           cnt += drop ? 1u : 0u;
-          rw[e] = drop ? T(0) : v * sc;
+          *rw = drop ? T(0) : v * sc;
         }
         constexpr int W = NT < 32 ? NT : 32;  // lanes per warp in use
 #pragma unroll
@@ -275,14 +317,15 @@ __global__ void __launch_bounds__(Row2Geom<T, M, MODE>::CTA, Row2Geom<T, M, MODE
         // DREAMPlace-style field weighting of the input coefficients
         // (proj/src/force.cpp:19-31), folded into this load: a1 = a w1/(w1^2+w2^2)
         // (weight 1) or a2 = a w2/(w1^2+w2^2) (weight 2), w_d = pi k_d / n_d, 0 at DC
-        T* rw = reinterpret_cast<T*>(sm);
+        T* const rws[2] = {const_cast<T*>(rowA), const_cast<T*>(rowB)};
         const T pi = T(3.14159265358979323846);
         const T w1a = pi * T(q1) / T(n1), w1b = pi * T(m1) / T(n1), sc2 = pi / T(n2);
         for (int e = t; e < 2 * n2; e += NT) {
           const int k2 = e & (n2 - 1);
+          T* rw = rws[e >= n2] + k2;
           const T w1 = e < n2 ? w1a : w1b, w2 = sc2 * T(k2);
           const T den = fma(w1, w1, w2 * w2);
-          rw[e] = den > T(0) ? rw[e] * (a.weight == 1 ? w1 : w2) / den : T(0);
+          *rw = den > T(0) ? *rw * (a.weight == 1 ? w1 : w2) / den : T(0);
         }
         TL::sync();
       }
@@ -328,6 +371,12 @@ __global__ void __launch_bounds__(Row2Geom<T, M, MODE>::CTA, Row2Geom<T, M, MODE
       const V* fu = static_cast<const V*>(a.fu);
       const V ca0 = cconj(__ldg(ta + q1)), ca1 = cconj(__ldg(ta + m1));
       TL::sync();  // operands read: the buffer becomes the packed spectrum
+      if constexpr (MODE == 2) {
+        if (t == 0 && nxt < nitems) {
+          fence_async_smem();
+          issue_a(nxt);  // the next item's row A streams in under this item's math
+        }
+      }
       // X'(line, n2) from o = {DA, RA, DB, RB} (proj/src/dct2d.cpp:182-195)
       auto xp = [&](const T* o, V cb, V& x0, V& x1) {
         const V c0 = cmul(ca0, cb), c1 = cmul(ca1, cb);
@@ -407,11 +456,18 @@ __global__ void __launch_bounds__(Row2Geom<T, M, MODE>::CTA, Row2Geom<T, M, MODE
     }
     TL::sync();  // every read of buffer b by this group is done
     if (t == 0) {
-      mbar_arrive(empty + b);
-      const int nxt = it + NBUF * static_cast<int>(gridDim.x);
-      if (nxt < nitems) {
-        fence_async_smem();  // generic-proxy smem accesses before the async refill
-        issue(nxt, b);
+      if constexpr (MODE == 2) {
+        if (nxt < nitems) {
+          fence_async_smem();
+          issue_b(nxt);
+        }
+      } else {
+        mbar_arrive(empty + b);
+        const int nxt0 = it + NBUF * static_cast<int>(gridDim.x);
+        if (nxt0 < nitems) {
+          fence_async_smem();  // generic-proxy smem accesses before the async refill
+          issue(nxt0, b);
+        }
       }
     }
   }
