@@ -44,6 +44,14 @@
 namespace sdctb {
 
 enum ColLoad { LD_SRC = 0, LD_INTER = 1 };
+
+// The forward source pass lands its rows by parity class (even rows, then odd
+// rows) when the odd-class half starts 128-B aligned in shared memory (TMA
+// destination alignment); otherwise in natural row order. Host and kernel
+// pick the tensor map / index math from this one predicate.
+__host__ __device__ constexpr bool col_class_load(int esize, int L, int nl) {
+  return L >= 2 && ((L / 2) * 2 * nl * esize) % 128 == 0;
+}
 enum ColStore { ST_INTER = 0, ST_DST = 1 };
 enum RowKind { RK_FWD2 = 0, RK_INV2 = 1, RK_FWD3 = 2, RK_INV3 = 3 };
 
@@ -457,10 +465,23 @@ __global__ void __launch_bounds__(Tile<T, L, NL, true>::NT)
     coords(tile, band, plane, batch);
     const int pc = a.tma_plane_par ? parity_embed(plane, a.tma_plane_par) : plane;
     mbar_expect_tx(bar, TILE_BYTES);
+    if constexpr (LOAD == LD_SRC && col_class_load(sizeof(T), L, NL)) {
+      // source rows by parity class through the {reals, class, pair, plane,
+      // batch} map: even rows 2p land at smem row p, odd rows 2p+1 at L/2 + p,
+      // so the parity gather below reads consecutive rows (conflict-free)
+      constexpr int HALFR = L / 2, BOXP = HALFR < 256 ? HALFR : 256;
 #pragma unroll 1
-    for (int r0 = 0; r0 < L; r0 += BOXR)
-      tma_load_4d(reinterpret_cast<T*>(smem_raw) + static_cast<size_t>(r0) * 2 * NL, &tin, band * 2 * NL, r0, pc,
-                  batch, bar);
+      for (int cls = 0; cls < 2; ++cls)
+#pragma unroll 1
+        for (int p0 = 0; p0 < HALFR; p0 += BOXP)
+          tma_load_5d(reinterpret_cast<T*>(smem_raw) + static_cast<size_t>(cls * HALFR + p0) * 2 * NL, &tin,
+                      band * 2 * NL, cls, p0, pc, batch, bar);
+    } else {
+#pragma unroll 1
+      for (int r0 = 0; r0 < L; r0 += BOXR)
+        tma_load_4d(reinterpret_cast<T*>(smem_raw) + static_cast<size_t>(r0) * 2 * NL, &tin, band * 2 * NL, r0, pc,
+                    batch, bar);
+    }
   };
   if (t == 0) {
     prefetch_tmap(&tin);
@@ -486,7 +507,7 @@ __global__ void __launch_bounds__(Tile<T, L, NL, true>::NT)
       phase ^= 1;
       if (a.trace && t == 0) tr1 = gtimer();
       if constexpr (LOAD == LD_SRC) {
-        // slot n reads source row pe(n); line 2g+h is z(u) (h=0) or z(M-1-u)
+        // slot n reads source row pe(n) (landed by parity class); line 2g+h is z(u) (h=0) or z(M-1-u)
         // (h=1) of source quad g: lanes h=0/1 read the halves, swap one real
         const V2* raw = reinterpret_cast<const V2*>(smem_raw);
 #pragma unroll
@@ -497,7 +518,9 @@ __global__ void __launch_bounds__(Tile<T, L, NL, true>::NT)
 #pragma unroll
           for (int r = 0; r < R0; ++r) {
             const int n = j + r * Q0;
-            const int row = (r < R0 / 2) ? 2 * n : 2 * L - 1 - 2 * n;
+            // source row pe(n) = 2n or 2(L-1-n)+1; landed by class: smem row n / L/2 + L-1-n
+            const int row = col_class_load(sizeof(T), L, NL) ? ((r < R0 / 2) ? n : L / 2 + (L - 1 - n))
+                                                             : ((r < R0 / 2) ? 2 * n : 2 * L - 1 - 2 * n);
             const V2 x = raw[row * NL + line];
             const T send = h ? x.x : x.y;
             const T recv = __shfl_xor_sync(TL::MASK, send, 1);

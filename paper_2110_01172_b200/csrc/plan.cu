@@ -464,8 +464,12 @@ int run_fast(sdct_plan_s* p, int kind, int only_stage, const void* in, void* out
     a.trace = g_trace;
     if (want() && e == cudaSuccess && map_ok) {
       CUtensorMap mi, mo;
-      map_ok = make_col_map(&mi, f32, a.src, in.inner, in.rows, in.row_stride * es, in.planes,
-                            in.plane_stride * es, B, in.batch_stride * es, nl, L);
+      // the forward source pass loads rows by parity class (5D class map)
+      map_ok = variant == CV_FWD_SRC && col_class_load(static_cast<int>(es), L, nl)
+                   ? make_class_map(&mi, f32, a.src, in.inner, in.rows, in.row_stride * es, in.planes,
+                                    in.plane_stride * es, B, in.batch_stride * es, nl)
+                   : make_col_map(&mi, f32, a.src, in.inner, in.rows, in.row_stride * es, in.planes,
+                                  in.plane_stride * es, B, in.batch_stride * es, nl, L);
       if (map_ok) {
         if (variant == CV_INV_DST)
           map_ok = make_class_map(&mo, f32, a.dst, o.inner, o.rows, o.row_stride * es, o.planes, o.plane_stride * es,
