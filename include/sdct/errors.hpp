@@ -25,8 +25,7 @@ struct PlanError : ShapeError {
   explicit PlanError(const std::string& m) : ShapeError(m) {}
 };
 
-/// Malformed file contents. Kept for API compatibility; the DCTB/PGM file
-/// formats are outside this library's hot path.
+/// Malformed file contents (DCTB containers, sdct/io.hpp).
 struct FormatError : std::runtime_error {
   explicit FormatError(const std::string& m) : std::runtime_error(m) {}
 };

@@ -92,6 +92,13 @@ def _ref_lib():
                                        ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double),
                                        ctypes.c_uint, ctypes.c_int]
         lib.sdct_ref_force.restype = ctypes.c_int
+        lib.sdct_ref_write_dctb.argtypes = [ctypes.c_char_p, ctypes.c_int, ctypes.POINTER(ctypes.c_size_t),
+                                            ctypes.POINTER(ctypes.c_double)]
+        lib.sdct_ref_write_dctb.restype = ctypes.c_int
+        lib.sdct_ref_read_dctb.argtypes = [ctypes.c_char_p, ctypes.POINTER(ctypes.c_int),
+                                           ctypes.POINTER(ctypes.c_size_t), ctypes.POINTER(ctypes.c_double),
+                                           ctypes.c_size_t]
+        lib.sdct_ref_read_dctb.restype = ctypes.c_int
         lib.sdct_ref_last_error.restype = ctypes.c_char_p
         _ref = lib
     return _ref
@@ -216,6 +223,27 @@ class _Ref:
             msg = lib.sdct_ref_last_error().decode()
             raise ValueError(msg) if rc == 1 else RuntimeError(msg)
         return xi1, xi2
+
+    def write_dctb(self, path: str, x) -> int:
+        """sdct::write_dctb (proj/src/io.cpp:96-107); returns the shim status
+        (0 ok, 1 ShapeError, 3 FormatError)."""
+        lib = _ref_lib()
+        x = np.ascontiguousarray(np.asarray(x, dtype=np.float64))
+        dims = (ctypes.c_size_t * max(x.ndim, 1))(*x.shape)
+        return lib.sdct_ref_write_dctb(os.fsencode(path), x.ndim, dims, _dp(x))
+
+    def read_dctb(self, path: str):
+        """sdct::read_dctb (proj/src/io.cpp:60-94): (status, array or None);
+        status 0 ok, 3 FormatError."""
+        lib = _ref_lib()
+        rank = ctypes.c_int(0)
+        dims = (ctypes.c_size_t * 4)()
+        rc = lib.sdct_ref_read_dctb(os.fsencode(path), ctypes.byref(rank), dims, None, 0)
+        if rc != 0:
+            return rc, None
+        out = np.empty(tuple(dims[: rank.value]), dtype=np.float64)
+        rc = lib.sdct_ref_read_dctb(os.fsencode(path), ctypes.byref(rank), dims, _dp(out), out.size)
+        return rc, out
 
     def __getattr__(self, name):
         if name in KINDS:

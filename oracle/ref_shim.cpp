@@ -18,6 +18,7 @@
 #include "sdct/dct2d.hpp"
 #include "sdct/errors.hpp"
 #include "sdct/force.hpp"
+#include "sdct/io.hpp"
 #include "sdct/exec.hpp"
 #include "sdct/transforms_ext.hpp"
 
@@ -96,6 +97,50 @@ int sdct_ref_force(std::size_t n1, std::size_t n2, const double* in, double* xi1
     std::memcpy(xi1, f.xi1.data(), n1 * n2 * sizeof(double));
     std::memcpy(xi2, f.xi2.data(), n1 * n2 * sizeof(double));
     return 0;
+  } catch (const sdct::ShapeError& e) {
+    g_err = e.what();
+    return 1;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 2;
+  }
+}
+
+}  // extern "C"
+
+extern "C" {
+
+// sdct::write_dctb (proj/src/io.cpp:96-107) of a rank-`rank` tensor.
+int sdct_ref_write_dctb(const char* path, int rank, const std::size_t* dims, const double* data) {
+  try {
+    sdct::Shape shape(dims, dims + rank);
+    sdct::RealTensor x(shape, std::vector<double>(data, data + (rank ? sdct::numel(shape) : 0)));
+    sdct::write_dctb(path, x);
+    return 0;
+  } catch (const sdct::ShapeError& e) {
+    g_err = e.what();
+    return 1;
+  } catch (const sdct::FormatError& e) {
+    g_err = e.what();
+    return 3;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 2;
+  }
+}
+
+// sdct::read_dctb (proj/src/io.cpp:60-94): 0 and rank/dims (+ payload when
+// cap >= numel) on success, 3 on FormatError.
+int sdct_ref_read_dctb(const char* path, int* rank, std::size_t* dims, double* out, std::size_t cap) {
+  try {
+    const sdct::RealTensor x = sdct::read_dctb(path);
+    *rank = static_cast<int>(x.rank());
+    for (std::size_t d = 0; d < x.rank(); ++d) dims[d] = x.dim(d);
+    if (out && cap >= x.size()) std::memcpy(out, x.data(), x.size() * sizeof(double));
+    return 0;
+  } catch (const sdct::FormatError& e) {
+    g_err = e.what();
+    return 3;
   } catch (const sdct::ShapeError& e) {
     g_err = e.what();
     return 1;

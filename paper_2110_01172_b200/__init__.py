@@ -36,6 +36,7 @@ from .api import (
     plan_for,
     stream_host,
 )
+from .dctb import read_dctb, transform_file, write_dctb
 
 __all__ = [
     "ShapeError", "FormatError", "DeviceError", "amdahl_speedup",
@@ -43,6 +44,7 @@ __all__ = [
     "dct_2d", "dct_2d_rowcol", "idct_2d", "idct_idxst_2d", "idxst_idct_2d",
     "dct_3d", "dct_4d", "idct_3d", "plan_for", "stream_host", "force_demo_fields",
     "dct_oracle_1d", "dct_oracle_2d", "compress",
+    "read_dctb", "write_dctb", "transform_file",
 ]
 
 __version__ = "0.1.0"
