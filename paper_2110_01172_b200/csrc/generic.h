@@ -13,6 +13,7 @@ struct GenericJob {
   int mode = 0;          // inverse composite embedding: 0 none, 1 axis 0, 2 axis 1 (rank 1: 2 = idxst)
   int sign_axis = -1;    // inverse: negate odd k along this axis
   double scale = 1.0;    // inverse gather scale (1/4 in 2D, 1/8 in 3D, 1/2 in 1D)
+  bool legacy = false;   // 2D: one full-tensor pass per stage (the row-column comparator)
   const double2* quarter[3] = {nullptr, nullptr, nullptr};  // e^{-i pi k/(2 N_a)}
   const double2* circle[3] = {nullptr, nullptr, nullptr};   // e^{-2 pi i t / N_a}
 };

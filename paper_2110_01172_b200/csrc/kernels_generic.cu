@@ -14,6 +14,7 @@
 // It is the correctness path for shapes outside the power-of-two fast path;
 // cost is O(numel * sum(radices of N_axis)) with the shared-memory mixed-radix
 // line FFT (extents <= 4096), O(numel * N_axis) direct sums beyond.
+#include "fft_block.cuh"
 #include "generic.h"
 #include "sdct_common.cuh"
 
@@ -90,36 +91,114 @@ __global__ void g_dft_axis(const double2* __restrict__ in, double2* __restrict__
 // Pass t (radix R, Ns = product of the previous radices), for each output:
 //   y[(j / Ns) Ns R + j % Ns + k Ns] = sum_r x[j + r n/R] W_n^{r E},
 //   E = (j % Ns) n / (Ns R) + k n / R  (twiddle and radix-R DFT fused).
+// Division by a run-time constant d >= 1 for 0 <= x < 2^31 as one multiply-
+// high, an add and a shift (m = floor(2^32 (2^s - d) / d) + 1, s = ceil(log2 d));
+// the line FFTs' index math divides by line lengths and pass strides
+// everywhere, and the generic integer division sequence dominated their
+// instruction count. tests/test_host.py checks the formula.
+struct FastDiv {
+  unsigned d = 1, m = 1, s = 0;
+  __host__ __device__ FastDiv() {}
+  __host__ __device__ explicit FastDiv(unsigned dd) : d(dd) {
+    while ((1u << s) < d) ++s;
+    m = static_cast<unsigned>(((1ull << 32) * ((1ull << s) - d)) / d + 1);
+  }
+  __device__ __forceinline__ int div(int x) const {
+    return static_cast<int>((__umulhi(static_cast<unsigned>(x), m) + static_cast<unsigned>(x)) >> s);
+  }
+  __device__ __forceinline__ int mod(int x, int q) const { return x - q * static_cast<int>(d); }
+};
+
 struct Radices {
   int count;
   int r[24];
+  FastDiv nr[24];  // n / r[s]
+  FastDiv ns[24];  // product of r[0..s)
+  FastDiv n;       // line length
 };
 
 constexpr int kFftMaxN = 4096;  // two line buffers + table in shared memory
 
 constexpr int kFftPerThread = 8;  // outputs a thread holds across one pass (lines * n <= 8 * threads)
 
+// Radix-R DFT constants W_R^m = e^{-+2 pi i m / R} for the odd radices
+// (compile time; the powers of two use the in-register dft_reg of fft_block.cuh)
+template <int R> struct OddRoots;
+template <> struct OddRoots<3> {
+  __device__ __forceinline__ static constexpr double c(int m) { return m == 0 ? 1.0 : -0.5; }
+  __device__ __forceinline__ static constexpr double s(int m) {
+    return m == 0 ? 0.0 : m == 1 ? 0.86602540378443864676 : -0.86602540378443864676;
+  }
+};
+template <> struct OddRoots<5> {
+  __device__ __forceinline__ static constexpr double c(int m) {
+    return m == 0 ? 1.0 : (m == 1 || m == 4) ? 0.30901699437494742410 : -0.80901699437494742410;
+  }
+  __device__ __forceinline__ static constexpr double s(int m) {
+    return m == 0 ? 0.0 : m == 1 ? 0.95105651629515357212 : m == 2 ? 0.58778525229247312917
+         : m == 3 ? -0.58778525229247312917 : -0.95105651629515357212;
+  }
+};
+template <> struct OddRoots<7> {
+  __device__ __forceinline__ static constexpr double c(int m) {
+    return m == 0 ? 1.0 : (m == 1 || m == 6) ? 0.62348980185873353053
+         : (m == 2 || m == 5) ? -0.22252093395631440429 : -0.90096886790241912624;
+  }
+  __device__ __forceinline__ static constexpr double s(int m) {
+    return m == 0 ? 0.0 : m == 1 ? 0.78183148246802980871 : m == 2 ? 0.97492791218182360702
+         : m == 3 ? 0.43388373911755812048 : m == 4 ? -0.43388373911755812048
+         : m == 5 ? -0.97492791218182360702 : -0.78183148246802980871;
+  }
+};
+
+// in-register radix-R DFT, natural order: v[k] <- sum_r v[r] W_R^{r k}
+template <int R, bool INV>
+__device__ __forceinline__ void radix_dft(double2* v) {
+  if constexpr ((R & (R - 1)) == 0) {
+    dft_reg<double, R, INV>(v);
+  } else {
+    double2 o[R];
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      double re = v[0].x, im = v[0].y;
+#pragma unroll
+      for (int r = 1; r < R; ++r) {
+        const int m = (r * k) % R;
+        const double c = OddRoots<R>::c(m), sn = INV ? OddRoots<R>::s(m) : -OddRoots<R>::s(m);
+        re = fma(v[r].x, c, fma(-v[r].y, sn, re));
+        im = fma(v[r].x, sn, fma(v[r].y, c, im));
+      }
+      o[k] = make_double2(re, im);
+    }
+#pragma unroll
+    for (int k = 0; k < R; ++k) v[k] = o[k];
+  }
+}
+
 // One Stockham pass of radix R (compile time) over lines of length n in
-// shared memory, in place: each thread takes whole butterflies j (inputs
-// x[j + r n/R], r < R), applies the twiddles W_{ns R}^{(j % ns) r} and the
-// radix-R DFT, keeps the R outputs in registers across the barrier and writes
-// them to y[(j / ns) ns R + j % ns + k ns].
-template <int R>
+// shared memory (line stride ld), in place: each thread takes whole
+// butterflies j (inputs x[j + r n/R], r < R), applies the twiddles
+// W_{ns R}^{(j % ns) r} from the table (already conjugated for the inverse)
+// and the radix-R DFT with compile-time constants, keeps the R outputs in
+// registers across the barrier and writes them to y[(j / ns) ns R + j % ns + k ns].
+template <int R, int FPT, bool INV>
 __device__ __forceinline__ void stockham_pass(double2* x, const double2* tw, int n, int ns, int total, int t,
-                                              int nt) {
-  constexpr int BMAX = (kFftPerThread + R - 1) / R;  // butterflies per thread (lines * n <= 16 * 256)
+                                              int nt, int ld, const FastDiv& fnr, const FastDiv& fns) {
+  constexpr int BMAX = (FPT + R - 1) / R;  // butterflies per thread (lines * n <= FPT * nt)
   const int nr = n / R;
   const int nb = total / R;  // butterflies over all lines of the tile
   const int tstep = n / (ns * R);
   double2 out[BMAX][R];
+  int jq[BMAX];  // j / ns, reused by the write-back
 #pragma unroll
   for (int u = 0; u < BMAX; ++u) {
     const int bq = t + u * nt;
     if (bq < nb) {
-      const int l = bq / nr, j = bq - l * nr;
-      const int jr = j % ns;
-      const double2* xl = x + l * n + j;
-      double2 v[R];
+      const int l = fnr.div(bq), j = bq - l * nr;
+      jq[u] = fns.div(j);
+      const int jr = j - jq[u] * ns;
+      const double2* xl = x + l * ld + j;
+      double2* v = out[u];
       v[0] = xl[0];
       const int e1 = jr * tstep;  // W_n^{e1 r} = W_{ns R}^{(j % ns) r}
       int e = e1;
@@ -130,18 +209,7 @@ __device__ __forceinline__ void stockham_pass(double2* x, const double2* tw, int
         e += e1;
         if (e >= n) e -= n;
       }
-      // radix-R DFT: out[k] = sum_r v[r] W_R^{r k}, W_R^m = tw[m n / R]
-#pragma unroll
-      for (int k = 0; k < R; ++k) {
-        double re = v[0].x, im = v[0].y;
-#pragma unroll
-        for (int r = 1; r < R; ++r) {
-          const double2 w = tw[((r * k) % R) * nr];
-          re = fma(v[r].x, w.x, fma(-v[r].y, w.y, re));
-          im = fma(v[r].x, w.y, fma(v[r].y, w.x, im));
-        }
-        out[u][k] = make_double2(re, im);
-      }
+      radix_dft<R, INV>(v);
     }
   }
   __syncthreads();
@@ -149,8 +217,8 @@ __device__ __forceinline__ void stockham_pass(double2* x, const double2* tw, int
   for (int u = 0; u < BMAX; ++u) {
     const int bq = t + u * nt;
     if (bq < nb) {
-      const int l = bq / nr, j = bq - l * nr;
-      const int base = l * n + (j / ns) * ns * R + j % ns;
+      const int l = fnr.div(bq), j = bq - l * nr;
+      const int base = l * ld + jq[u] * ns * (R - 1) + j;  // (j / ns) ns R + j % ns
 #pragma unroll
       for (int k = 0; k < R; ++k) x[base + k * ns] = out[u][k];
     }
@@ -159,21 +227,22 @@ __device__ __forceinline__ void stockham_pass(double2* x, const double2* tw, int
 }
 
 // Radix-R pass for other (prime) R: one thread per output, R MACs each.
+template <int FPT = kFftPerThread>
 __device__ __forceinline__ void generic_pass(double2* x, const double2* tw, int n, int ns, int R, int total, int t,
-                                             int nt) {
+                                             int nt, int ld, const FastDiv& fn, const FastDiv& fns) {
   const int nr = n / R;
-  double2 acc[kFftPerThread];
+  double2 acc[FPT];
 #pragma unroll
-  for (int u = 0; u < kFftPerThread; ++u) {
+  for (int u = 0; u < FPT; ++u) {
     const int e = t + u * nt;
     if (e < total) {
-      const int l = e / n, q = e - l * n;
+      const int l = fn.div(e), q = e - l * n;
       // output q = (j / ns) ns R + j % ns + k ns with j in [0, n/R), k in [0, R)
-      const int jr = q % ns, rest = q / ns;
-      const int k = rest % R, jq = rest / R;
+      const int rest = fns.div(q), jr = q - rest * ns;
+      const int jq = rest / R, k = rest - jq * R;
       const int j = jq * ns + jr;
       const int E = (jr * (n / (ns * R)) + k * nr) % n;
-      const double2* xl = x + l * n + j;
+      const double2* xl = x + l * ld + j;
       double re = 0.0, im = 0.0;
       int idx = 0;
       for (int r = 0; r < R; ++r) {
@@ -188,11 +257,35 @@ __device__ __forceinline__ void generic_pass(double2* x, const double2* tw, int 
   }
   __syncthreads();
 #pragma unroll
-  for (int u = 0; u < kFftPerThread; ++u) {
+  for (int u = 0; u < FPT; ++u) {
     const int e = t + u * nt;
-    if (e < total) x[e] = acc[u];
+    if (e < total) {
+      const int l = fn.div(e);
+      x[l * ld + (e - l * n)] = acc[u];
+    }
   }
   __syncthreads();
+}
+
+// All passes of one line FFT over `total` = lines * n elements in smem
+// (line stride ld); tw holds e^{-+2 pi i e / n}.
+template <int FPT, bool INV>
+__device__ __forceinline__ void line_passes(double2* x, const double2* tw, int n, const Radices& rad, int total, int t,
+                                            int nt, int ld) {
+  // factorise() emits 8s, 4s, 2s, then odd primes in ascending order: one
+  // loop per radix (a single switch over all radices inside one loop makes
+  // ptxas keep the pass outputs in local memory)
+  int ns = 1, s = 0;
+  while (s < rad.count && rad.r[s] == 8) { stockham_pass<8, FPT, INV>(x, tw, n, ns, total, t, nt, ld, rad.nr[s], rad.ns[s]); ns *= 8; ++s; }
+  while (s < rad.count && rad.r[s] == 4) { stockham_pass<4, FPT, INV>(x, tw, n, ns, total, t, nt, ld, rad.nr[s], rad.ns[s]); ns *= 4; ++s; }
+  while (s < rad.count && rad.r[s] == 2) { stockham_pass<2, FPT, INV>(x, tw, n, ns, total, t, nt, ld, rad.nr[s], rad.ns[s]); ns *= 2; ++s; }
+  while (s < rad.count && rad.r[s] == 3) { stockham_pass<3, FPT, INV>(x, tw, n, ns, total, t, nt, ld, rad.nr[s], rad.ns[s]); ns *= 3; ++s; }
+  while (s < rad.count && rad.r[s] == 5) { stockham_pass<5, FPT, INV>(x, tw, n, ns, total, t, nt, ld, rad.nr[s], rad.ns[s]); ns *= 5; ++s; }
+  while (s < rad.count && rad.r[s] == 7) { stockham_pass<7, FPT, INV>(x, tw, n, ns, total, t, nt, ld, rad.nr[s], rad.ns[s]); ns *= 7; ++s; }
+  for (; s < rad.count; ++s) {
+    generic_pass<FPT>(x, tw, n, ns, rad.r[s], total, t, nt, ld, rad.n, rad.ns[s]);
+    ns *= rad.r[s];
+  }
 }
 
 __global__ void __launch_bounds__(512) g_fft_axis_smem(const double2* __restrict__ in, double2* __restrict__ out,
@@ -238,20 +331,10 @@ __global__ void __launch_bounds__(512) g_fft_axis_smem(const double2* __restrict
     x[l * n + m] = in[src];
   }
   __syncthreads();
-  int ns = 1;
-  for (int s = 0; s < rad.count; ++s) {
-    const int R = rad.r[s];
-    switch (R) {  // butterfly-per-thread passes for the common radices
-      case 2: stockham_pass<2>(x, tw, n, ns, total, t, nt); break;
-      case 3: stockham_pass<3>(x, tw, n, ns, total, t, nt); break;
-      case 4: stockham_pass<4>(x, tw, n, ns, total, t, nt); break;
-      case 5: stockham_pass<5>(x, tw, n, ns, total, t, nt); break;
-      case 7: stockham_pass<7>(x, tw, n, ns, total, t, nt); break;
-      case 8: stockham_pass<8>(x, tw, n, ns, total, t, nt); break;
-      default: generic_pass(x, tw, n, ns, R, total, t, nt); break;
-    }
-    ns *= R;
-  }
+  if (inverse)
+    line_passes<kFftPerThread, true>(x, tw, n, rad, total, t, nt, n);
+  else
+    line_passes<kFftPerThread, false>(x, tw, n, rad, total, t, nt, n);
   for (int e = t; e < total; e += nt) {
     long long dst;
     int l, m;
@@ -339,6 +422,7 @@ void split_factors(int n, int& a, int& b) {
 }
 
 Radices factorise(int n) {
+  const int n0 = n;
   Radices rad{};
   // radix 8/4/2 first, then small odd primes, then whatever prime remains
   for (int r : {8, 4, 2}) {
@@ -357,6 +441,13 @@ Radices factorise(int n) {
       n = 1;
     }
   }
+  int ns = 1;
+  for (int q = 0; q < rad.count; ++q) {
+    rad.nr[q] = FastDiv(static_cast<unsigned>(n0 / rad.r[q]));
+    rad.ns[q] = FastDiv(static_cast<unsigned>(ns));
+    ns *= rad.r[q];
+  }
+  rad.n = FastDiv(static_cast<unsigned>(n0));
   return rad;
 }
 
@@ -495,6 +586,186 @@ __global__ void g_gather_inv(const double2* __restrict__ z, T* __restrict__ y, D
   }
 }
 
+// ---- two-pass 2D pipeline for extents <= kFftMaxN -------------------------
+// The same three stages with the gathers, the postprocess and the merged
+// preprocess fused into the line FFTs' loads and stores, so a 2D transform is
+// two passes over HBM (one per axis) instead of gather + transpose + FFT +
+// transpose + FFT + post:
+//   forward : G2_FWD_ROWS  x row pe(i), columns scattered by ps (= pe^-1)
+//                          -> FFT along axis 1 -> W row i
+//             G2_FWD_COLS  W columns c0.. -> FFT along axis 0 -> the
+//                          postprocess of dct2d.hpp:6 (column-local) -> y
+//   inverse : G2_INV_COLS  merged preprocess (dct2d.cpp:161-198, Hermitian
+//                          fill) for columns c0.. -> inverse FFT along axis 0
+//                          -> W columns
+//             G2_INV_ROWS  W row ps(k1) -> inverse FFT along axis 1 -> the
+//                          inverse gather (dct2d.cpp:214-238, row-local) -> y
+// Column tiles hold `lines` consecutive columns with an odd line stride in
+// shared memory (conflict-free strided loads); row tiles hold `lines` rows.
+enum { G2_FWD_ROWS = 0, G2_FWD_COLS = 1, G2_INV_COLS = 2, G2_INV_ROWS = 3 };
+constexpr int kG2Fpt = 16;      // elements per thread across one pass
+constexpr int kG2Threads = 512;
+constexpr int kG2Cap = kG2Fpt * kG2Threads;  // elements per tile
+
+struct G2Args {
+  const void* src;
+  void* dst;
+  int n1, n2;
+  long long batch;
+  int lines;         // lines per tile
+  int mode, sign_axis;
+  double scale;
+  const double2* circle;  // circle table of the FFT axis
+  const double2* ta;      // quarter-wave tables of axes 0 and 1
+  const double2* tb;
+  Radices rad;
+  FastDiv fn1, fn2;
+};
+
+template <typename T, int KIND>
+__global__ void __launch_bounds__(kG2Threads) g2_kernel(G2Args a) {
+  constexpr bool ROWS = KIND == G2_FWD_ROWS || KIND == G2_INV_ROWS;
+  constexpr bool INV = KIND == G2_INV_COLS || KIND == G2_INV_ROWS;
+  extern __shared__ __align__(16) double2 g2sm[];
+  const int n1 = a.n1, n2 = a.n2;
+  const int n = ROWS ? n2 : n1;               // FFT length
+  const int ld = ROWS ? n : (n | 1);          // line stride in smem
+  double2* tw = g2sm;
+  double2* x = g2sm + n;
+  const int t = threadIdx.x, nt = blockDim.x;
+  for (int e = t; e < n; e += nt) {
+    double2 w = a.circle[e];
+    if (INV) w.y = -w.y;
+    tw[e] = w;
+  }
+  const long long plane = static_cast<long long>(n1) * n2;
+  long long r0 = 0, b = 0;
+  int c0 = 0, lines;
+  if constexpr (ROWS) {
+    r0 = static_cast<long long>(blockIdx.x) * a.lines;  // flattened (batch, row)
+    lines = static_cast<int>(min(static_cast<long long>(a.lines), a.batch * n1 - r0));
+  } else {
+    const int tpb = (n2 + a.lines - 1) / a.lines;
+    b = blockIdx.x / tpb;
+    c0 = static_cast<int>(blockIdx.x % tpb) * a.lines;
+    lines = min(a.lines, n2 - c0);
+  }
+  const int total = lines * n;
+  const FastDiv fl(static_cast<unsigned>(lines));  // column tiles: element -> (row, line)
+
+  // ---- load ----
+  if constexpr (KIND == G2_FWD_ROWS) {
+    const T* xs = static_cast<const T*>(a.src);
+    for (int e = t; e < total; e += nt) {
+      const int l = a.fn2.div(e), c = e - l * n2;
+      const int R = static_cast<int>(r0) + l, bb = a.fn1.div(R);
+      const int i = R - bb * n1;
+      const T v = xs[static_cast<long long>(bb) * plane + static_cast<long long>(parity_embed(i, n1)) * n2 + c];
+      x[l * ld + parity_source(c, n2)] = make_double2(static_cast<double>(v), 0.0);
+    }
+  } else if constexpr (KIND == G2_FWD_COLS) {
+    const double2* W = static_cast<const double2*>(a.src) + b * plane;
+    for (int e = t; e < total; e += nt) {
+      const int m = fl.div(e), l = e - m * lines;
+      x[l * ld + m] = W[static_cast<long long>(m) * n2 + c0 + l];
+    }
+  } else if constexpr (KIND == G2_INV_COLS) {
+    // full Hermitian spectrum of the merged preprocess, column m2 = c0 + l
+    const T* xb = static_cast<const T*>(a.src) + b * plane;
+    for (int e = t; e < total; e += nt) {
+      const int k1 = fl.div(e), l = e - k1 * lines;
+      const int m2c = c0 + l;
+      const bool flip = m2c > n2 / 2;  // upper half of the last axis: conj of the mirrored entry
+      const int e1 = flip && k1 ? n1 - k1 : k1;
+      const int m2 = flip ? n2 - m2c : m2c;  // m2c > n2 / 2 >= 0: never wraps
+      const bool direct = e1 <= n1 / 2;
+      const int q1 = direct ? e1 : n1 - e1;
+      const double p = fetch2g(xb, q1, m2, n1, n2, a.mode);
+      const double q = fetch2g(xb, n1 - q1, n2 - m2, n1, n2, a.mode);
+      const double r = fetch2g(xb, n1 - q1, m2, n1, n2, a.mode);
+      const double sv = fetch2g(xb, q1, n2 - m2, n1, n2, a.mode);
+      const double2 w = cj(cm(a.ta[e1], a.tb[m2]));
+      const double2 val = direct ? cm(w, make_double2(p - q, -(r + sv))) : cm(w, make_double2(r - sv, -(p + q)));
+      x[l * ld + k1] = flip ? cj(val) : val;
+    }
+  } else {  // G2_INV_ROWS: y row k1 comes from z row ps(k1)
+    const double2* W = static_cast<const double2*>(a.src);
+    for (int e = t; e < total; e += nt) {
+      const int l = a.fn2.div(e), c = e - l * n2;
+      const int R = static_cast<int>(r0) + l, bb = a.fn1.div(R);
+      const int k1 = R - bb * n1;
+      x[l * ld + c] = W[static_cast<long long>(bb) * plane + static_cast<long long>(parity_source(k1, n1)) * n2 + c];
+    }
+  }
+  __syncthreads();
+  line_passes<kG2Fpt, INV>(x, tw, n, a.rad, total, t, nt, ld);
+
+  // ---- store ----
+  if constexpr (KIND == G2_FWD_ROWS) {
+    double2* W = static_cast<double2*>(a.dst);
+    for (int e = t; e < total; e += nt) {
+      const int l = a.fn2.div(e), c = e - l * n2;
+      W[(r0 + l) * n2 + c] = x[l * ld + c];
+    }
+  } else if constexpr (KIND == G2_FWD_COLS) {
+    // y = 1/2 Re(b(k2) (a(k1) X(k1, k2) + conj(a(k1)) X(-k1, k2)))   (dct2d.hpp:6)
+    T* y = static_cast<T*>(a.dst) + b * plane;
+    for (int e = t; e < total; e += nt) {
+      const int k1 = fl.div(e), l = e - k1 * lines;
+      const int k2 = c0 + l;
+      const double2 aa = a.ta[k1];
+      const double2 x1 = x[l * ld + k1], x2 = x[l * ld + (k1 ? n1 - k1 : 0)];
+      const double v = 0.5 * cm(a.tb[k2], ca(cm(aa, x1), cm(cj(aa), x2))).x;
+      y[static_cast<long long>(k1) * n2 + k2] = static_cast<T>(v);
+    }
+  } else if constexpr (KIND == G2_INV_COLS) {
+    double2* W = static_cast<double2*>(a.dst) + b * plane;
+    for (int e = t; e < total; e += nt) {
+      const int m = fl.div(e), l = e - m * lines;
+      W[static_cast<long long>(m) * n2 + c0 + l] = x[l * ld + m];
+    }
+  } else {
+    T* y = static_cast<T*>(a.dst);
+    for (int e = t; e < total; e += nt) {
+      const int l = a.fn2.div(e), k2 = e - l * n2;
+      const int R = static_cast<int>(r0) + l, bb = a.fn1.div(R);
+      const int k1 = R - bb * n1;
+      double v = a.scale * x[l * ld + parity_source(k2, n2)].x;
+      if ((a.sign_axis == 0 && (k1 & 1)) || (a.sign_axis == 1 && (k2 & 1))) v = -v;
+      y[static_cast<long long>(R) * n2 + k2] = static_cast<T>(v);
+    }
+  }
+}
+
+template <typename T, int KIND>
+cudaError_t g2_launch(G2Args a, cudaStream_t st) {
+  const bool rows = KIND == G2_FWD_ROWS || KIND == G2_INV_ROWS;
+  const int n = rows ? a.n2 : a.n1;
+  const int ld = rows ? n : (n | 1);
+  // lines per tile: as many as the tile capacity allows (columns: at most 32,
+  // rows: at most 64), fewer threads for small tiles
+  int lines = kG2Cap / n;
+  lines = std::max(1, std::min(lines, rows ? 64 : 32));
+  if (!rows) lines = std::min(lines, a.n2);
+  a.lines = lines;
+  a.rad = factorise(n);
+  a.fn1 = FastDiv(static_cast<unsigned>(a.n1));
+  a.fn2 = FastDiv(static_cast<unsigned>(a.n2));
+  const int total = lines * n;
+  int nt = (total + kG2Fpt - 1) / kG2Fpt;
+  nt = std::min(kG2Threads, std::max(64, (nt + 31) / 32 * 32));
+  const size_t smem = (static_cast<size_t>(lines) * ld + n) * sizeof(double2);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(g2_kernel<T, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  const long long tiles = rows ? (a.batch * a.n1 + lines - 1) / lines : a.batch * ((a.n2 + lines - 1) / lines);
+  // grid.x limit 2^31-1: batches beyond it are not reachable at these extents
+  g2_kernel<T, KIND><<<static_cast<unsigned>(tiles), nt, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -572,6 +843,33 @@ cudaError_t generic_run(const GenericJob& job, const void* in, void* out, void* 
   };
   double2* cur = A;
   double2* nxt = B;
+  if (job.rank == 2 && !job.legacy && job.dims[0] <= kFftMaxN && job.dims[1] <= kFftMaxN) {
+    // two-pass pipeline (gathers / pre / post fused into the line FFTs)
+    G2Args a{};
+    a.n1 = job.dims[0];
+    a.n2 = job.dims[1];
+    a.batch = job.batch;
+    a.mode = job.mode;
+    a.sign_axis = job.sign_axis;
+    a.scale = job.scale;
+    a.ta = job.quarter[0];
+    a.tb = job.quarter[1];
+    cudaError_t e;
+    if (!job.inverse) {
+      a.src = in, a.dst = A, a.circle = job.circle[1];
+      e = g2_launch<T, G2_FWD_ROWS>(a, st);
+      if (e != cudaSuccess) return e;
+      a.src = A, a.dst = out, a.circle = job.circle[0];
+      e = g2_launch<T, G2_FWD_COLS>(a, st);
+    } else {
+      a.src = in, a.dst = A, a.circle = job.circle[0];
+      e = g2_launch<T, G2_INV_COLS>(a, st);
+      if (e != cudaSuccess) return e;
+      a.src = A, a.dst = out, a.circle = job.circle[1];
+      e = g2_launch<T, G2_INV_ROWS>(a, st);
+    }
+    return e;
+  }
   if (!job.inverse) {
     g_gather_fwd<T><<<g, kThreads, 0, st>>>(static_cast<const T*>(in), A, d, job.batch);
     dft_all(cur, nxt, 0);

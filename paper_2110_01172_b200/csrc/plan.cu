@@ -654,6 +654,7 @@ GenericJob make_job(const sdct_plan_s* p, int kind) {
     j.circle[a] = p->gc[a];
   }
   j.batch = p->batch;
+  j.legacy = kind == SDCT_DCT_2D_ROWCOL;
   switch (kind) {
     case SDCT_IDCT_2D: j.inverse = true; j.scale = 0.25; break;
     case SDCT_IDXST_IDCT_2D: j.inverse = true; j.scale = 0.25; j.mode = 1; j.sign_axis = 0; break;

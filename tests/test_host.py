@@ -121,3 +121,24 @@ def test_cpp_api_program_is_built():
     exe = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
                        "paper_2110_01172_b200", "lib", "api_smoke")
     assert os.path.exists(exe)
+
+
+def test_fastdiv_formula():
+    # kernels_generic.cu FastDiv: q = (umulhi(x, m) + x) >> s with
+    # s = ceil(log2 d), m = floor(2^32 (2^s - d) / d) + 1, for 0 <= x < 2^31
+    rng = np.random.default_rng(5)
+    ds = list(range(1, 70)) + [125, 250, 1000, 2000, 2047, 2049, 4093, 4095, 4096, 4097, 65535, 1 << 20,
+                                (1 << 31) - 1] + rng.integers(1, 1 << 31, 200).tolist()
+    for d in ds:
+        s = 0
+        while (1 << s) < d:
+            s += 1
+        m = ((1 << 32) * ((1 << s) - d)) // d + 1
+        assert m < (1 << 32)
+        ks = np.unique(np.concatenate([np.arange(0, 4), rng.integers(0, ((1 << 31) - 2) // d + 1, 40)]))
+        edges = np.concatenate([ks * d - 1, ks * d, ks * d + 1])  # around multiples of d
+        edges = edges[(edges >= 0) & (edges < (1 << 31))]
+        xs = np.concatenate([rng.integers(0, 1 << 31, 300), edges, np.array([(1 << 31) - 1, (1 << 31) - 2])])
+        for x in xs.tolist():
+            q = ((((x * m) >> 32) + x) & 0xFFFFFFFF) >> s
+            assert q == x // d, (d, x)
