@@ -157,18 +157,41 @@ __device__ __forceinline__ void radix_dft(double2* v) {
   if constexpr ((R & (R - 1)) == 0) {
     dft_reg<double, R, INV>(v);
   } else {
+    // symmetric form: with s_r = v[r] + v[R-r], d_r = v[r] - v[R-r]
+    // (r = 1..H), out[k] = A_k -+ i B_k and out[R-k] = A_k +- i B_k, where
+    // A_k = v0 + sum_r cos(2 pi r k / R) s_r, B_k = sum_r sin(2 pi r k / R) d_r
+    constexpr int H = (R - 1) / 2;
+    double2 sr[H], dr[H];
+    double2 o0 = v[0];
+#pragma unroll
+    for (int r = 1; r <= H; ++r) {
+      sr[r - 1] = make_double2(v[r].x + v[R - r].x, v[r].y + v[R - r].y);
+      dr[r - 1] = make_double2(v[r].x - v[R - r].x, v[r].y - v[R - r].y);
+      o0.x += sr[r - 1].x;
+      o0.y += sr[r - 1].y;
+    }
     double2 o[R];
+    o[0] = o0;
 #pragma unroll
-    for (int k = 0; k < R; ++k) {
-      double re = v[0].x, im = v[0].y;
+    for (int k = 1; k <= H; ++k) {
+      double ax = v[0].x, ay = v[0].y, bx = 0.0, by = 0.0;
 #pragma unroll
-      for (int r = 1; r < R; ++r) {
+      for (int r = 1; r <= H; ++r) {
         const int m = (r * k) % R;
-        const double c = OddRoots<R>::c(m), sn = INV ? OddRoots<R>::s(m) : -OddRoots<R>::s(m);
-        re = fma(v[r].x, c, fma(-v[r].y, sn, re));
-        im = fma(v[r].x, sn, fma(v[r].y, c, im));
+        const double c = OddRoots<R>::c(m), sn = OddRoots<R>::s(m);
+        ax = fma(c, sr[r - 1].x, ax);
+        ay = fma(c, sr[r - 1].y, ay);
+        bx = fma(sn, dr[r - 1].x, bx);
+        by = fma(sn, dr[r - 1].y, by);
       }
-      o[k] = make_double2(re, im);
+      // forward W = e^{-i theta}: out[k] = A - i B = (ax + by, ay - bx)
+      if (!INV) {
+        o[k] = make_double2(ax + by, ay - bx);
+        o[R - k] = make_double2(ax - by, ay + bx);
+      } else {
+        o[k] = make_double2(ax - by, ay + bx);
+        o[R - k] = make_double2(ax + by, ay - bx);
+      }
     }
 #pragma unroll
     for (int k = 0; k < R; ++k) v[k] = o[k];
@@ -181,7 +204,7 @@ __device__ __forceinline__ void radix_dft(double2* v) {
 // W_{ns R}^{(j % ns) r} from the table (already conjugated for the inverse)
 // and the radix-R DFT with compile-time constants, keeps the R outputs in
 // registers across the barrier and writes them to y[(j / ns) ns R + j % ns + k ns].
-template <int R, int FPT, bool INV>
+template <int R, int FPT, bool INV, bool CJ>
 __device__ __forceinline__ void stockham_pass(double2* x, const double2* tw, int n, int ns, int total, int t,
                                               int nt, int ld, const FastDiv& fnr, const FastDiv& fns) {
   constexpr int BMAX = (FPT + R - 1) / R;  // butterflies per thread (lines * n <= FPT * nt)
@@ -204,7 +227,9 @@ __device__ __forceinline__ void stockham_pass(double2* x, const double2* tw, int
       int e = e1;
 #pragma unroll
       for (int r = 1; r < R; ++r) {
-        const double2 a = xl[r * nr], w = tw[e];
+        const double2 a = xl[r * nr];
+        double2 w = tw[e];
+        if (CJ && INV) w.y = -w.y;
         v[r] = make_double2(fma(a.x, w.x, -a.y * w.y), fma(a.x, w.y, a.y * w.x));
         e += e1;
         if (e >= n) e -= n;
@@ -227,7 +252,7 @@ __device__ __forceinline__ void stockham_pass(double2* x, const double2* tw, int
 }
 
 // Radix-R pass for other (prime) R: one thread per output, R MACs each.
-template <int FPT = kFftPerThread>
+template <int FPT, bool CJ>
 __device__ __forceinline__ void generic_pass(double2* x, const double2* tw, int n, int ns, int R, int total, int t,
                                              int nt, int ld, const FastDiv& fn, const FastDiv& fns) {
   const int nr = n / R;
@@ -246,7 +271,9 @@ __device__ __forceinline__ void generic_pass(double2* x, const double2* tw, int 
       double re = 0.0, im = 0.0;
       int idx = 0;
       for (int r = 0; r < R; ++r) {
-        const double2 v = xl[r * nr], w = tw[idx];
+        const double2 v = xl[r * nr];
+        double2 w = tw[idx];
+        if (CJ) w.y = -w.y;
         re = fma(v.x, w.x, fma(-v.y, w.y, re));
         im = fma(v.x, w.y, fma(v.y, w.x, im));
         idx += E;
@@ -269,21 +296,23 @@ __device__ __forceinline__ void generic_pass(double2* x, const double2* tw, int 
 
 // All passes of one line FFT over `total` = lines * n elements in smem
 // (line stride ld); tw holds e^{-+2 pi i e / n}.
-template <int FPT, bool INV>
+// CJ: tw is the forward table and the inverse conjugates at use (tables read
+// from global memory through L1); otherwise tw is already conjugated for INV.
+template <int FPT, bool INV, bool CJ = false>
 __device__ __forceinline__ void line_passes(double2* x, const double2* tw, int n, const Radices& rad, int total, int t,
                                             int nt, int ld) {
   // factorise() emits 8s, 4s, 2s, then odd primes in ascending order: one
   // loop per radix (a single switch over all radices inside one loop makes
   // ptxas keep the pass outputs in local memory)
   int ns = 1, s = 0;
-  while (s < rad.count && rad.r[s] == 8) { stockham_pass<8, FPT, INV>(x, tw, n, ns, total, t, nt, ld, rad.nr[s], rad.ns[s]); ns *= 8; ++s; }
-  while (s < rad.count && rad.r[s] == 4) { stockham_pass<4, FPT, INV>(x, tw, n, ns, total, t, nt, ld, rad.nr[s], rad.ns[s]); ns *= 4; ++s; }
-  while (s < rad.count && rad.r[s] == 2) { stockham_pass<2, FPT, INV>(x, tw, n, ns, total, t, nt, ld, rad.nr[s], rad.ns[s]); ns *= 2; ++s; }
-  while (s < rad.count && rad.r[s] == 3) { stockham_pass<3, FPT, INV>(x, tw, n, ns, total, t, nt, ld, rad.nr[s], rad.ns[s]); ns *= 3; ++s; }
-  while (s < rad.count && rad.r[s] == 5) { stockham_pass<5, FPT, INV>(x, tw, n, ns, total, t, nt, ld, rad.nr[s], rad.ns[s]); ns *= 5; ++s; }
-  while (s < rad.count && rad.r[s] == 7) { stockham_pass<7, FPT, INV>(x, tw, n, ns, total, t, nt, ld, rad.nr[s], rad.ns[s]); ns *= 7; ++s; }
+  while (s < rad.count && rad.r[s] == 8) { stockham_pass<8, FPT, INV, CJ>(x, tw, n, ns, total, t, nt, ld, rad.nr[s], rad.ns[s]); ns *= 8; ++s; }
+  while (s < rad.count && rad.r[s] == 4) { stockham_pass<4, FPT, INV, CJ>(x, tw, n, ns, total, t, nt, ld, rad.nr[s], rad.ns[s]); ns *= 4; ++s; }
+  while (s < rad.count && rad.r[s] == 2) { stockham_pass<2, FPT, INV, CJ>(x, tw, n, ns, total, t, nt, ld, rad.nr[s], rad.ns[s]); ns *= 2; ++s; }
+  while (s < rad.count && rad.r[s] == 3) { stockham_pass<3, FPT, INV, CJ>(x, tw, n, ns, total, t, nt, ld, rad.nr[s], rad.ns[s]); ns *= 3; ++s; }
+  while (s < rad.count && rad.r[s] == 5) { stockham_pass<5, FPT, INV, CJ>(x, tw, n, ns, total, t, nt, ld, rad.nr[s], rad.ns[s]); ns *= 5; ++s; }
+  while (s < rad.count && rad.r[s] == 7) { stockham_pass<7, FPT, INV, CJ>(x, tw, n, ns, total, t, nt, ld, rad.nr[s], rad.ns[s]); ns *= 7; ++s; }
   for (; s < rad.count; ++s) {
-    generic_pass<FPT>(x, tw, n, ns, rad.r[s], total, t, nt, ld, rad.n, rad.ns[s]);
+    generic_pass<FPT, CJ && INV>(x, tw, n, ns, rad.r[s], total, t, nt, ld, rad.n, rad.ns[s]);
     ns *= rad.r[s];
   }
 }
@@ -603,9 +632,12 @@ __global__ void g_gather_inv(const double2* __restrict__ z, T* __restrict__ y, D
 // Column tiles hold `lines` consecutive columns with an odd line stride in
 // shared memory (conflict-free strided loads); row tiles hold `lines` rows.
 enum { G2_FWD_ROWS = 0, G2_FWD_COLS = 1, G2_INV_COLS = 2, G2_INV_ROWS = 3 };
-constexpr int kG2Fpt = 16;      // elements per thread across one pass
-constexpr int kG2Threads = 512;
-constexpr int kG2Cap = kG2Fpt * kG2Threads;  // elements per tile
+// Two tile shapes: lines up to 2048 run 256-thread CTAs at 8 elements per
+// thread (three CTAs per SM: one CTA's global loads overlap another's passes),
+// longer lines 512-thread CTAs at 16 per thread.
+template <int FPT> struct G2Cfg;
+template <> struct G2Cfg<8> { static constexpr int NT = 256, MINB = 3, CAP = 8 * 256; };
+template <> struct G2Cfg<16> { static constexpr int NT = 512, MINB = 1, CAP = 16 * 512; };
 
 struct G2Args {
   const void* src;
@@ -622,22 +654,17 @@ struct G2Args {
   FastDiv fn1, fn2;
 };
 
-template <typename T, int KIND>
-__global__ void __launch_bounds__(kG2Threads) g2_kernel(G2Args a) {
+template <typename T, int KIND, int FPT>
+__global__ void __launch_bounds__(G2Cfg<FPT>::NT, G2Cfg<FPT>::MINB) g2_kernel(G2Args a) {
   constexpr bool ROWS = KIND == G2_FWD_ROWS || KIND == G2_INV_ROWS;
   constexpr bool INV = KIND == G2_INV_COLS || KIND == G2_INV_ROWS;
   extern __shared__ __align__(16) double2 g2sm[];
   const int n1 = a.n1, n2 = a.n2;
   const int n = ROWS ? n2 : n1;               // FFT length
   const int ld = ROWS ? n : (n | 1);          // line stride in smem
-  double2* tw = g2sm;
-  double2* x = g2sm + n;
+  const double2* tw = a.circle;               // forward circle table, L1-resident
+  double2* x = g2sm;
   const int t = threadIdx.x, nt = blockDim.x;
-  for (int e = t; e < n; e += nt) {
-    double2 w = a.circle[e];
-    if (INV) w.y = -w.y;
-    tw[e] = w;
-  }
   const long long plane = static_cast<long long>(n1) * n2;
   long long r0 = 0, b = 0;
   int c0 = 0, lines;
@@ -653,52 +680,95 @@ __global__ void __launch_bounds__(kG2Threads) g2_kernel(G2Args a) {
   const int total = lines * n;
   const FastDiv fl(static_cast<unsigned>(lines));  // column tiles: element -> (row, line)
 
-  // ---- load ----
+  // ---- load ---- (total <= FPT * nt: each thread issues all its global
+  // loads before the first shared-memory store, so their latencies overlap)
   if constexpr (KIND == G2_FWD_ROWS) {
     const T* xs = static_cast<const T*>(a.src);
-    for (int e = t; e < total; e += nt) {
-      const int l = a.fn2.div(e), c = e - l * n2;
-      const int R = static_cast<int>(r0) + l, bb = a.fn1.div(R);
-      const int i = R - bb * n1;
-      const T v = xs[static_cast<long long>(bb) * plane + static_cast<long long>(parity_embed(i, n1)) * n2 + c];
-      x[l * ld + parity_source(c, n2)] = make_double2(static_cast<double>(v), 0.0);
+    T v[FPT];
+    int slot[FPT];
+#pragma unroll
+    for (int u = 0; u < FPT; ++u) {
+      const int e = t + u * nt;
+      if (e < total) {
+        const int l = a.fn2.div(e), c = e - l * n2;
+        const int R = static_cast<int>(r0) + l, bb = a.fn1.div(R);
+        const int i = R - bb * n1;
+        v[u] = xs[static_cast<long long>(bb) * plane + static_cast<long long>(parity_embed(i, n1)) * n2 + c];
+        slot[u] = l * ld + parity_source(c, n2);
+      }
     }
-  } else if constexpr (KIND == G2_FWD_COLS) {
-    const double2* W = static_cast<const double2*>(a.src) + b * plane;
-    for (int e = t; e < total; e += nt) {
-      const int m = fl.div(e), l = e - m * lines;
-      x[l * ld + m] = W[static_cast<long long>(m) * n2 + c0 + l];
+#pragma unroll
+    for (int u = 0; u < FPT; ++u)
+      if (t + u * nt < total) x[slot[u]] = make_double2(static_cast<double>(v[u]), 0.0);
+  } else if constexpr (KIND == G2_FWD_COLS || KIND == G2_INV_ROWS) {
+    const double2* W = static_cast<const double2*>(a.src);
+    double2 v[FPT];
+    int slot[FPT];
+#pragma unroll
+    for (int u = 0; u < FPT; ++u) {
+      const int e = t + u * nt;
+      if (e < total) {
+        if constexpr (KIND == G2_FWD_COLS) {
+          const int m = fl.div(e), l = e - m * lines;
+          v[u] = W[b * plane + static_cast<long long>(m) * n2 + c0 + l];
+          slot[u] = l * ld + m;
+        } else {  // y row k1 comes from z row ps(k1)
+          const int l = a.fn2.div(e), c = e - l * n2;
+          const int R = static_cast<int>(r0) + l, bb = a.fn1.div(R);
+          const int k1 = R - bb * n1;
+          v[u] = W[static_cast<long long>(bb) * plane + static_cast<long long>(parity_source(k1, n1)) * n2 + c];
+          slot[u] = l * ld + c;
+        }
+      }
     }
-  } else if constexpr (KIND == G2_INV_COLS) {
+#pragma unroll
+    for (int u = 0; u < FPT; ++u)
+      if (t + u * nt < total) x[slot[u]] = v[u];
+  } else {  // G2_INV_COLS
     // full Hermitian spectrum of the merged preprocess, column m2 = c0 + l
     const T* xb = static_cast<const T*>(a.src) + b * plane;
-    for (int e = t; e < total; e += nt) {
-      const int k1 = fl.div(e), l = e - k1 * lines;
-      const int m2c = c0 + l;
-      const bool flip = m2c > n2 / 2;  // upper half of the last axis: conj of the mirrored entry
-      const int e1 = flip && k1 ? n1 - k1 : k1;
-      const int m2 = flip ? n2 - m2c : m2c;  // m2c > n2 / 2 >= 0: never wraps
-      const bool direct = e1 <= n1 / 2;
-      const int q1 = direct ? e1 : n1 - e1;
-      const double p = fetch2g(xb, q1, m2, n1, n2, a.mode);
-      const double q = fetch2g(xb, n1 - q1, n2 - m2, n1, n2, a.mode);
-      const double r = fetch2g(xb, n1 - q1, m2, n1, n2, a.mode);
-      const double sv = fetch2g(xb, q1, n2 - m2, n1, n2, a.mode);
-      const double2 w = cj(cm(a.ta[e1], a.tb[m2]));
-      const double2 val = direct ? cm(w, make_double2(p - q, -(r + sv))) : cm(w, make_double2(r - sv, -(p + q)));
-      x[l * ld + k1] = flip ? cj(val) : val;
-    }
-  } else {  // G2_INV_ROWS: y row k1 comes from z row ps(k1)
-    const double2* W = static_cast<const double2*>(a.src);
-    for (int e = t; e < total; e += nt) {
-      const int l = a.fn2.div(e), c = e - l * n2;
-      const int R = static_cast<int>(r0) + l, bb = a.fn1.div(R);
-      const int k1 = R - bb * n1;
-      x[l * ld + c] = W[static_cast<long long>(bb) * plane + static_cast<long long>(parity_source(k1, n1)) * n2 + c];
+    constexpr int UB = 4;  // elements per load batch (4 operands each)
+#pragma unroll
+    for (int u0 = 0; u0 < FPT; u0 += UB) {
+      double op[UB][4];
+      int e1s[UB], m2s[UB], slot[UB];
+      bool fl_[UB], dir[UB];
+#pragma unroll
+      for (int u = u0; u < u0 + UB; ++u) {
+        const int e = t + u * nt;
+        if (e < total) {
+          const int k1 = fl.div(e), l = e - k1 * lines;
+          const int m2c = c0 + l;
+          const bool flip = m2c > n2 / 2;  // upper half of the last axis: conj of the mirrored entry
+          const int e1 = flip && k1 ? n1 - k1 : k1;
+          const int m2 = flip ? n2 - m2c : m2c;  // m2c > n2 / 2 >= 0: never wraps
+          const bool direct = e1 <= n1 / 2;
+          const int q1 = direct ? e1 : n1 - e1;
+          op[u - u0][0] = fetch2g(xb, q1, m2, n1, n2, a.mode);
+          op[u - u0][1] = fetch2g(xb, n1 - q1, n2 - m2, n1, n2, a.mode);
+          op[u - u0][2] = fetch2g(xb, n1 - q1, m2, n1, n2, a.mode);
+          op[u - u0][3] = fetch2g(xb, q1, n2 - m2, n1, n2, a.mode);
+          e1s[u - u0] = e1;
+          m2s[u - u0] = m2;
+          fl_[u - u0] = flip;
+          dir[u - u0] = direct;
+          slot[u - u0] = l * ld + k1;
+        }
+      }
+#pragma unroll
+      for (int u = u0; u < u0 + UB; ++u) {
+        if (t + u * nt < total) {
+          const double* o = op[u - u0];
+          const double2 w = cj(cm(a.ta[e1s[u - u0]], a.tb[m2s[u - u0]]));
+          const double2 val = dir[u - u0] ? cm(w, make_double2(o[0] - o[1], -(o[2] + o[3])))
+                                          : cm(w, make_double2(o[2] - o[3], -(o[0] + o[1])));
+          x[slot[u - u0]] = fl_[u - u0] ? cj(val) : val;
+        }
+      }
     }
   }
   __syncthreads();
-  line_passes<kG2Fpt, INV>(x, tw, n, a.rad, total, t, nt, ld);
+  line_passes<FPT, INV, true>(x, tw, n, a.rad, total, t, nt, ld);
 
   // ---- store ----
   if constexpr (KIND == G2_FWD_ROWS) {
@@ -737,14 +807,15 @@ __global__ void __launch_bounds__(kG2Threads) g2_kernel(G2Args a) {
   }
 }
 
-template <typename T, int KIND>
-cudaError_t g2_launch(G2Args a, cudaStream_t st) {
+template <typename T, int KIND, int FPT>
+cudaError_t g2_launch_cfg(G2Args a, cudaStream_t st) {
+  using C = G2Cfg<FPT>;
   const bool rows = KIND == G2_FWD_ROWS || KIND == G2_INV_ROWS;
   const int n = rows ? a.n2 : a.n1;
   const int ld = rows ? n : (n | 1);
   // lines per tile: as many as the tile capacity allows (columns: at most 32,
   // rows: at most 64), fewer threads for small tiles
-  int lines = kG2Cap / n;
+  int lines = C::CAP / n;
   lines = std::max(1, std::min(lines, rows ? 64 : 32));
   if (!rows) lines = std::min(lines, a.n2);
   a.lines = lines;
@@ -752,18 +823,24 @@ cudaError_t g2_launch(G2Args a, cudaStream_t st) {
   a.fn1 = FastDiv(static_cast<unsigned>(a.n1));
   a.fn2 = FastDiv(static_cast<unsigned>(a.n2));
   const int total = lines * n;
-  int nt = (total + kG2Fpt - 1) / kG2Fpt;
-  nt = std::min(kG2Threads, std::max(64, (nt + 31) / 32 * 32));
-  const size_t smem = (static_cast<size_t>(lines) * ld + n) * sizeof(double2);
+  int nt = (total + FPT - 1) / FPT;
+  nt = std::min(C::NT, std::max(64, (nt + 31) / 32 * 32));
+  const size_t smem = static_cast<size_t>(lines) * ld * sizeof(double2);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(g2_kernel<T, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(g2_kernel<T, KIND, FPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr = true;
   }
   const long long tiles = rows ? (a.batch * a.n1 + lines - 1) / lines : a.batch * ((a.n2 + lines - 1) / lines);
   // grid.x limit 2^31-1: batches beyond it are not reachable at these extents
-  g2_kernel<T, KIND><<<static_cast<unsigned>(tiles), nt, smem, st>>>(a);
+  g2_kernel<T, KIND, FPT><<<static_cast<unsigned>(tiles), nt, smem, st>>>(a);
   return cudaGetLastError();
+}
+
+template <typename T, int KIND>
+cudaError_t g2_launch(G2Args a, cudaStream_t st) {
+  const int n = (KIND == G2_FWD_ROWS || KIND == G2_INV_ROWS) ? a.n2 : a.n1;
+  return n <= G2Cfg<8>::CAP ? g2_launch_cfg<T, KIND, 8>(a, st) : g2_launch_cfg<T, KIND, 16>(a, st);
 }
 
 }  // namespace
