@@ -105,6 +105,40 @@ def test_2d_vs_oracle(cuda, dtype, kind):
         assert err <= TOL[dtype], (kind, shape, dtype, err)
 
 
+# generic two-pass 2D pipeline (kernels_generic.cu g2_kernel): short / long
+# lines, both tile configurations (lines <= 2048 and > 2048), odd and prime
+# extents (direct-sum passes), several lines per tile
+SHAPES_G2 = [(2000, 3), (3, 2000), (300, 500), (999, 1001), (2500, 40), (40, 3000), (97, 2047), (4095, 6)]
+
+
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+@pytest.mark.parametrize("kind", KINDS_2D)
+def test_generic_2d_pipeline_vs_oracle(cuda, dtype, kind):
+    for i, shape in enumerate(SHAPES_G2):
+        x = rnd(shape, 300 + i, dtype)
+        err = oracle.rel_l2(run_capi(kind, x, dtype), getattr(oracle.port, kind)(x))
+        assert err <= TOL[dtype], (kind, shape, dtype, err)
+    # batched items through the same tiles
+    x = rnd((3, 70, 45), 399, dtype)
+    got = run_capi(kind, x, dtype, batch_shape=(3,))
+    want = np.stack([getattr(oracle.port, kind)(x[b]) for b in range(3)])
+    assert oracle.rel_l2(got, want) <= TOL[dtype]
+
+
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+def test_generic_2d_round_trip_large(cuda, dtype):
+    # size-independent property at a large non-power-of-two shape:
+    # idct_2d(dct_2d(x)) = N1 N2 / 4 x (proj/tests/test_dct2d.cpp:160-172)
+    torch = _torch()
+    import paper_2110_01172_b200 as sd
+
+    tdt = torch.float64 if dtype == "float64" else torch.float32
+    x = torch.rand((3000, 2000), dtype=tdt, device="cuda", generator=torch.Generator("cuda").manual_seed(9)) * 2 - 1
+    y = sd.idct_2d(sd.dct_2d(x)) * (4.0 / (3000 * 2000))
+    err = (torch.linalg.norm((y - x).double()) / torch.linalg.norm(x.double())).item()
+    assert err <= (1e-13 if dtype == "float64" else 1e-5), err
+
+
 SHAPES_3D = [(2, 2, 8), (4, 8, 16), (16, 4, 8), (8, 8, 64), (32, 32, 32), (3, 4, 5), (2, 6, 9), (64, 16, 16),
              (4096, 2, 8), (2, 4096, 8), (4, 4, 8192)]
 
