@@ -620,14 +620,17 @@ __global__ void g_gather_inv(const double2* __restrict__ z, T* __restrict__ y, D
 // preprocess fused into the line FFTs' loads and stores, so a 2D transform is
 // two passes over HBM (one per axis) instead of gather + transpose + FFT +
 // transpose + FFT + post:
+// W holds the one-sided spectrum, columns k2 < h = n2/2 + 1 (the layout of
+// the reference's rfft_nd / irfft_nd, rfft.cpp:182-245):
 //   forward : G2_FWD_ROWS  x row pe(i), columns scattered by ps (= pe^-1)
-//                          -> FFT along axis 1 -> W row i
+//                          -> FFT along axis 1 -> W row i (k2 < h)
 //             G2_FWD_COLS  W columns c0.. -> FFT along axis 0 -> the
-//                          postprocess of dct2d.hpp:6 (column-local) -> y
-//   inverse : G2_INV_COLS  merged preprocess (dct2d.cpp:161-198, Hermitian
-//                          fill) for columns c0.. -> inverse FFT along axis 0
-//                          -> W columns
-//             G2_INV_ROWS  W row ps(k1) -> inverse FFT along axis 1 -> the
+//                          postprocess of dct2d.hpp:6 for y columns c and
+//                          n2 - c (X(k1, n2 - c) = conj X(-k1, c)) -> y
+//   inverse : G2_INV_COLS  merged preprocess (dct2d.cpp:161-198) for columns
+//                          c0.. < h -> inverse FFT along axis 0 -> W columns
+//             G2_INV_ROWS  W row ps(k1), Hermitian fill of k2 >= h as
+//                          irfft_nd does -> inverse FFT along axis 1 -> the
 //                          inverse gather (dct2d.cpp:214-238, row-local) -> y
 // Column tiles hold `lines` consecutive columns with an odd line stride in
 // shared memory (conflict-free strided loads); row tiles hold `lines` rows.
@@ -651,7 +654,8 @@ struct G2Args {
   const double2* ta;      // quarter-wave tables of axes 0 and 1
   const double2* tb;
   Radices rad;
-  FastDiv fn1, fn2;
+  FastDiv fn1, fn2, fh;
+  int h;             // stored spectrum columns, n2 / 2 + 1
 };
 
 template <typename T, int KIND, int FPT>
@@ -666,16 +670,18 @@ __global__ void __launch_bounds__(G2Cfg<FPT>::NT, G2Cfg<FPT>::MINB) g2_kernel(G2
   double2* x = g2sm;
   const int t = threadIdx.x, nt = blockDim.x;
   const long long plane = static_cast<long long>(n1) * n2;
+  const int h = a.h;
+  const long long wplane = static_cast<long long>(n1) * h;  // one-sided spectrum per item
   long long r0 = 0, b = 0;
   int c0 = 0, lines;
   if constexpr (ROWS) {
     r0 = static_cast<long long>(blockIdx.x) * a.lines;  // flattened (batch, row)
     lines = static_cast<int>(min(static_cast<long long>(a.lines), a.batch * n1 - r0));
   } else {
-    const int tpb = (n2 + a.lines - 1) / a.lines;
+    const int tpb = (a.h + a.lines - 1) / a.lines;
     b = blockIdx.x / tpb;
     c0 = static_cast<int>(blockIdx.x % tpb) * a.lines;
-    lines = min(a.lines, n2 - c0);
+    lines = min(a.lines, a.h - c0);
   }
   const int total = lines * n;
   const FastDiv fl(static_cast<unsigned>(lines));  // column tiles: element -> (row, line)
@@ -710,13 +716,16 @@ __global__ void __launch_bounds__(G2Cfg<FPT>::NT, G2Cfg<FPT>::MINB) g2_kernel(G2
       if (e < total) {
         if constexpr (KIND == G2_FWD_COLS) {
           const int m = fl.div(e), l = e - m * lines;
-          v[u] = W[b * plane + static_cast<long long>(m) * n2 + c0 + l];
+          v[u] = W[b * wplane + static_cast<long long>(m) * h + c0 + l];
           slot[u] = l * ld + m;
-        } else {  // y row k1 comes from z row ps(k1)
+        } else {  // y row k1 comes from z row ps(k1); k2 >= h is the conjugate mirror
           const int l = a.fn2.div(e), c = e - l * n2;
           const int R = static_cast<int>(r0) + l, bb = a.fn1.div(R);
           const int k1 = R - bb * n1;
-          v[u] = W[static_cast<long long>(bb) * plane + static_cast<long long>(parity_source(k1, n1)) * n2 + c];
+          const bool mir = c >= h;
+          const double2 w = W[static_cast<long long>(bb) * wplane + static_cast<long long>(parity_source(k1, n1)) * h +
+                              (mir ? n2 - c : c)];
+          v[u] = mir ? cj(w) : w;
           slot[u] = l * ld + c;
         }
       }
@@ -732,16 +741,14 @@ __global__ void __launch_bounds__(G2Cfg<FPT>::NT, G2Cfg<FPT>::MINB) g2_kernel(G2
     for (int u0 = 0; u0 < FPT; u0 += UB) {
       double op[UB][4];
       int e1s[UB], m2s[UB], slot[UB];
-      bool fl_[UB], dir[UB];
+      bool dir[UB];
 #pragma unroll
       for (int u = u0; u < u0 + UB; ++u) {
         const int e = t + u * nt;
         if (e < total) {
           const int k1 = fl.div(e), l = e - k1 * lines;
-          const int m2c = c0 + l;
-          const bool flip = m2c > n2 / 2;  // upper half of the last axis: conj of the mirrored entry
-          const int e1 = flip && k1 ? n1 - k1 : k1;
-          const int m2 = flip ? n2 - m2c : m2c;  // m2c > n2 / 2 >= 0: never wraps
+          const int m2 = c0 + l;  // < h: the one-sided half, no Hermitian fill here
+          const int e1 = k1;
           const bool direct = e1 <= n1 / 2;
           const int q1 = direct ? e1 : n1 - e1;
           op[u - u0][0] = fetch2g(xb, q1, m2, n1, n2, a.mode);
@@ -750,7 +757,6 @@ __global__ void __launch_bounds__(G2Cfg<FPT>::NT, G2Cfg<FPT>::MINB) g2_kernel(G2
           op[u - u0][3] = fetch2g(xb, q1, n2 - m2, n1, n2, a.mode);
           e1s[u - u0] = e1;
           m2s[u - u0] = m2;
-          fl_[u - u0] = flip;
           dir[u - u0] = direct;
           slot[u - u0] = l * ld + k1;
         }
@@ -762,7 +768,7 @@ __global__ void __launch_bounds__(G2Cfg<FPT>::NT, G2Cfg<FPT>::MINB) g2_kernel(G2
           const double2 w = cj(cm(a.ta[e1s[u - u0]], a.tb[m2s[u - u0]]));
           const double2 val = dir[u - u0] ? cm(w, make_double2(o[0] - o[1], -(o[2] + o[3])))
                                           : cm(w, make_double2(o[2] - o[3], -(o[0] + o[1])));
-          x[slot[u - u0]] = fl_[u - u0] ? cj(val) : val;
+          x[slot[u - u0]] = val;
         }
       }
     }
@@ -773,9 +779,9 @@ __global__ void __launch_bounds__(G2Cfg<FPT>::NT, G2Cfg<FPT>::MINB) g2_kernel(G2
   // ---- store ----
   if constexpr (KIND == G2_FWD_ROWS) {
     double2* W = static_cast<double2*>(a.dst);
-    for (int e = t; e < total; e += nt) {
-      const int l = a.fn2.div(e), c = e - l * n2;
-      W[(r0 + l) * n2 + c] = x[l * ld + c];
+    for (int e = t; e < lines * h; e += nt) {
+      const int l = a.fh.div(e), c = e - l * h;
+      W[(r0 + l) * h + c] = x[l * ld + c];
     }
   } else if constexpr (KIND == G2_FWD_COLS) {
     // y = 1/2 Re(b(k2) (a(k1) X(k1, k2) + conj(a(k1)) X(-k1, k2)))   (dct2d.hpp:6)
@@ -787,12 +793,18 @@ __global__ void __launch_bounds__(G2Cfg<FPT>::NT, G2Cfg<FPT>::MINB) g2_kernel(G2
       const double2 x1 = x[l * ld + k1], x2 = x[l * ld + (k1 ? n1 - k1 : 0)];
       const double v = 0.5 * cm(a.tb[k2], ca(cm(aa, x1), cm(cj(aa), x2))).x;
       y[static_cast<long long>(k1) * n2 + k2] = static_cast<T>(v);
+      // mirrored column n2 - k2: X(k1, n2 - k2) = conj X(-k1, k2), X(-k1, n2 - k2) = conj X(k1, k2)
+      const int km = n2 - k2;
+      if (k2 > 0 && km != k2) {
+        const double vm = 0.5 * cm(a.tb[km], ca(cm(aa, cj(x2)), cm(cj(aa), cj(x1)))).x;
+        y[static_cast<long long>(k1) * n2 + km] = static_cast<T>(vm);
+      }
     }
   } else if constexpr (KIND == G2_INV_COLS) {
-    double2* W = static_cast<double2*>(a.dst) + b * plane;
+    double2* W = static_cast<double2*>(a.dst) + b * wplane;
     for (int e = t; e < total; e += nt) {
       const int m = fl.div(e), l = e - m * lines;
-      W[static_cast<long long>(m) * n2 + c0 + l] = x[l * ld + m];
+      W[static_cast<long long>(m) * h + c0 + l] = x[l * ld + m];
     }
   } else {
     T* y = static_cast<T*>(a.dst);
@@ -817,8 +829,10 @@ cudaError_t g2_launch_cfg(G2Args a, cudaStream_t st) {
   // rows: at most 64), fewer threads for small tiles
   int lines = C::CAP / n;
   lines = std::max(1, std::min(lines, rows ? 64 : 32));
-  if (!rows) lines = std::min(lines, a.n2);
+  a.h = a.n2 / 2 + 1;
+  if (!rows) lines = std::min(lines, a.h);
   a.lines = lines;
+  a.fh = FastDiv(static_cast<unsigned>(a.h));
   a.rad = factorise(n);
   a.fn1 = FastDiv(static_cast<unsigned>(a.n1));
   a.fn2 = FastDiv(static_cast<unsigned>(a.n2));
@@ -831,7 +845,7 @@ cudaError_t g2_launch_cfg(G2Args a, cudaStream_t st) {
     cudaFuncSetAttribute(g2_kernel<T, KIND, FPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr = true;
   }
-  const long long tiles = rows ? (a.batch * a.n1 + lines - 1) / lines : a.batch * ((a.n2 + lines - 1) / lines);
+  const long long tiles = rows ? (a.batch * a.n1 + lines - 1) / lines : a.batch * ((a.h + lines - 1) / lines);
   // grid.x limit 2^31-1: batches beyond it are not reachable at these extents
   g2_kernel<T, KIND, FPT><<<static_cast<unsigned>(tiles), nt, smem, st>>>(a);
   return cudaGetLastError();
