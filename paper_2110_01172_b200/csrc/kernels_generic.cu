@@ -674,9 +674,11 @@ __global__ void __launch_bounds__(G2Cfg<FPT>::NT, G2Cfg<FPT>::MINB) g2_kernel(G2
   const long long wplane = static_cast<long long>(n1) * h;  // one-sided spectrum per item
   long long r0 = 0, b = 0;
   int c0 = 0, lines;
+  int rows = 0;  // row tiles: rows of y / x in this tile; two rows share one complex line
   if constexpr (ROWS) {
-    r0 = static_cast<long long>(blockIdx.x) * a.lines;  // flattened (batch, row)
-    lines = static_cast<int>(min(static_cast<long long>(a.lines), a.batch * n1 - r0));
+    r0 = static_cast<long long>(blockIdx.x) * a.lines;  // flattened (batch, row); a.lines = rows per tile
+    rows = static_cast<int>(min(static_cast<long long>(a.lines), a.batch * n1 - r0));
+    lines = (rows + 1) / 2;
   } else {
     const int tpb = (a.h + a.lines - 1) / a.lines;
     b = blockIdx.x / tpb;
@@ -689,23 +691,30 @@ __global__ void __launch_bounds__(G2Cfg<FPT>::NT, G2Cfg<FPT>::MINB) g2_kernel(G2
   // ---- load ---- (total <= FPT * nt: each thread issues all its global
   // loads before the first shared-memory store, so their latencies overlap)
   if constexpr (KIND == G2_FWD_ROWS) {
+    // rows 2l and 2l+1 of the tile as the real and imaginary parts of line l
     const T* xs = static_cast<const T*>(a.src);
-    T v[FPT];
+    T va[FPT], vb[FPT];
     int slot[FPT];
 #pragma unroll
     for (int u = 0; u < FPT; ++u) {
       const int e = t + u * nt;
       if (e < total) {
         const int l = a.fn2.div(e), c = e - l * n2;
-        const int R = static_cast<int>(r0) + l, bb = a.fn1.div(R);
+        const int R = static_cast<int>(r0) + 2 * l, bb = a.fn1.div(R);
         const int i = R - bb * n1;
-        v[u] = xs[static_cast<long long>(bb) * plane + static_cast<long long>(parity_embed(i, n1)) * n2 + c];
+        va[u] = xs[static_cast<long long>(bb) * plane + static_cast<long long>(parity_embed(i, n1)) * n2 + c];
+        vb[u] = T(0);
+        if (2 * l + 1 < rows) {
+          const int R2 = R + 1, bb2 = a.fn1.div(R2);
+          const int i2 = R2 - bb2 * n1;
+          vb[u] = xs[static_cast<long long>(bb2) * plane + static_cast<long long>(parity_embed(i2, n1)) * n2 + c];
+        }
         slot[u] = l * ld + parity_source(c, n2);
       }
     }
 #pragma unroll
     for (int u = 0; u < FPT; ++u)
-      if (t + u * nt < total) x[slot[u]] = make_double2(static_cast<double>(v[u]), 0.0);
+      if (t + u * nt < total) x[slot[u]] = make_double2(static_cast<double>(va[u]), static_cast<double>(vb[u]));
   } else if constexpr (KIND == G2_FWD_COLS || KIND == G2_INV_ROWS) {
     const double2* W = static_cast<const double2*>(a.src);
     double2 v[FPT];
@@ -718,14 +727,27 @@ __global__ void __launch_bounds__(G2Cfg<FPT>::NT, G2Cfg<FPT>::MINB) g2_kernel(G2
           const int m = fl.div(e), l = e - m * lines;
           v[u] = W[b * wplane + static_cast<long long>(m) * h + c0 + l];
           slot[u] = l * ld + m;
-        } else {  // y row k1 comes from z row ps(k1); k2 >= h is the conjugate mirror
+        } else {
+          // y row k1 comes from z row ps(k1); k2 >= h is the conjugate mirror
+          // (irfft_nd's Hermitian fill). Line l carries rows 2l (real part of
+          // the result) and 2l+1 (imaginary part): Z = Wa + i Wb.
           const int l = a.fn2.div(e), c = e - l * n2;
-          const int R = static_cast<int>(r0) + l, bb = a.fn1.div(R);
-          const int k1 = R - bb * n1;
           const bool mir = c >= h;
-          const double2 w = W[static_cast<long long>(bb) * wplane + static_cast<long long>(parity_source(k1, n1)) * h +
-                              (mir ? n2 - c : c)];
-          v[u] = mir ? cj(w) : w;
+          const int cc = mir ? n2 - c : c;
+          const int R = static_cast<int>(r0) + 2 * l, bb = a.fn1.div(R);
+          const int k1 = R - bb * n1;
+          double2 wa = W[static_cast<long long>(bb) * wplane + static_cast<long long>(parity_source(k1, n1)) * h + cc];
+          double2 wb = make_double2(0.0, 0.0);
+          if (2 * l + 1 < rows) {
+            const int R2 = R + 1, bb2 = a.fn1.div(R2);
+            const int k1b = R2 - bb2 * n1;
+            wb = W[static_cast<long long>(bb2) * wplane + static_cast<long long>(parity_source(k1b, n1)) * h + cc];
+          }
+          if (mir) {
+            wa = cj(wa);
+            wb = cj(wb);
+          }
+          v[u] = make_double2(wa.x - wb.y, wa.y + wb.x);
           slot[u] = l * ld + c;
         }
       }
@@ -778,10 +800,13 @@ __global__ void __launch_bounds__(G2Cfg<FPT>::NT, G2Cfg<FPT>::MINB) g2_kernel(G2
 
   // ---- store ----
   if constexpr (KIND == G2_FWD_ROWS) {
+    // Z = FFT(xa + i xb): Xa(k) = (Z(k) + conj Z(-k)) / 2, Xb(k) = (Z(k) - conj Z(-k)) / 2i
     double2* W = static_cast<double2*>(a.dst);
     for (int e = t; e < lines * h; e += nt) {
       const int l = a.fh.div(e), c = e - l * h;
-      W[(r0 + l) * h + c] = x[l * ld + c];
+      const double2 z = x[l * ld + c], zm = x[l * ld + (c ? n2 - c : 0)];
+      W[(r0 + 2 * l) * h + c] = make_double2(0.5 * (z.x + zm.x), 0.5 * (z.y - zm.y));
+      if (2 * l + 1 < rows) W[(r0 + 2 * l + 1) * h + c] = make_double2(0.5 * (z.y + zm.y), 0.5 * (zm.x - z.x));
     }
   } else if constexpr (KIND == G2_FWD_COLS) {
     // y = 1/2 Re(b(k2) (a(k1) X(k1, k2) + conj(a(k1)) X(-k1, k2)))   (dct2d.hpp:6)
@@ -808,11 +833,12 @@ __global__ void __launch_bounds__(G2Cfg<FPT>::NT, G2Cfg<FPT>::MINB) g2_kernel(G2
     }
   } else {
     T* y = static_cast<T*>(a.dst);
-    for (int e = t; e < total; e += nt) {
-      const int l = a.fn2.div(e), k2 = e - l * n2;
-      const int R = static_cast<int>(r0) + l, bb = a.fn1.div(R);
+    for (int e = t; e < rows * n2; e += nt) {
+      const int r = a.fn2.div(e), k2 = e - r * n2;  // tile row r = line r / 2, part r & 1
+      const int R = static_cast<int>(r0) + r, bb = a.fn1.div(R);
       const int k1 = R - bb * n1;
-      double v = a.scale * x[l * ld + parity_source(k2, n2)].x;
+      const double2 z = x[(r >> 1) * ld + parity_source(k2, n2)];
+      double v = a.scale * ((r & 1) ? z.y : z.x);
       if ((a.sign_axis == 0 && (k1 & 1)) || (a.sign_axis == 1 && (k2 & 1))) v = -v;
       y[static_cast<long long>(R) * n2 + k2] = static_cast<T>(v);
     }
@@ -827,11 +853,11 @@ cudaError_t g2_launch_cfg(G2Args a, cudaStream_t st) {
   const int ld = rows ? n : (n | 1);
   // lines per tile: as many as the tile capacity allows (columns: at most 32,
   // rows: at most 64), fewer threads for small tiles
-  int lines = C::CAP / n;
-  lines = std::max(1, std::min(lines, rows ? 64 : 32));
+  int lines = C::CAP / n;  // complex lines per tile (row tiles: two rows per line)
+  lines = std::max(1, std::min(lines, 32));
   a.h = a.n2 / 2 + 1;
   if (!rows) lines = std::min(lines, a.h);
-  a.lines = lines;
+  a.lines = rows ? 2 * lines : lines;
   a.fh = FastDiv(static_cast<unsigned>(a.h));
   a.rad = factorise(n);
   a.fn1 = FastDiv(static_cast<unsigned>(a.n1));
@@ -845,7 +871,7 @@ cudaError_t g2_launch_cfg(G2Args a, cudaStream_t st) {
     cudaFuncSetAttribute(g2_kernel<T, KIND, FPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr = true;
   }
-  const long long tiles = rows ? (a.batch * a.n1 + lines - 1) / lines : a.batch * ((a.h + lines - 1) / lines);
+  const long long tiles = rows ? (a.batch * a.n1 + a.lines - 1) / a.lines : a.batch * ((a.h + lines - 1) / lines);
   // grid.x limit 2^31-1: batches beyond it are not reachable at these extents
   g2_kernel<T, KIND, FPT><<<static_cast<unsigned>(tiles), nt, smem, st>>>(a);
   return cudaGetLastError();
