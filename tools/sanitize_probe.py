@@ -16,6 +16,11 @@ for dt in (torch.float64, torch.float32):
     sd.dct_3d(x3)
     sd.idct_3d(x3)
     sd.dct_2d(torch.rand((7, 9), dtype=dt, device="cuda"))
+    # generic two-pass 2D pipeline: both tile configurations, odd / prime extents, batch
+    for shape in [(100, 60), (33, 17), (3, 2500), (2500, 3), (97, 101), (2, 50, 30)]:
+        xg = torch.rand(shape, dtype=dt, device="cuda")
+        for f in (sd.dct_2d, sd.idct_2d, sd.idct_idxst_2d, sd.idxst_idct_2d):
+            f(xg)
     sd.dct_2d(torch.rand((8192, 16), dtype=dt, device="cuda"))
 torch.cuda.synchronize()
 print("probe done")
