@@ -443,14 +443,12 @@ __global__ void __launch_bounds__(Tile<T, L, NL, true>::NT)
   constexpr int R0 = TL::R0, Q0 = L / R0, NBF0 = TL::E / R0;
   constexpr int RL = P::R(SL), NBFL = TL::E / RL;
   constexpr int BOXR = L < 256 ? L : 256;
-  constexpr int HALF = L / 2;
-  constexpr int BOXH = HALF < 256 ? HALF : 256;
   constexpr uint32_t TILE_BYTES = static_cast<uint32_t>(L) * 2 * NL * sizeof(T);
   constexpr uint32_t STG_OFF = (TILE_BYTES + 127u) & ~127u;                      // TMA needs 128-B aligned smem
   constexpr uint32_t BAR_OFF = (STG_OFF + TILE_BYTES / 2 + 127u) & ~127u;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   V* sm = reinterpret_cast<V*>(smem_raw);
-  T* stg = reinterpret_cast<T*>(smem_raw + STG_OFF);  // half-tile staging [HALF][2*NL]
+  T* stg = reinterpret_cast<T*>(smem_raw + STG_OFF);  // half-tile staging [L/2][2*NL]
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw + BAR_OFF);
   const int t = threadIdx.x;
 
@@ -555,25 +553,33 @@ __global__ void __launch_bounds__(Tile<T, L, NL, true>::NT)
       }
       stage_compute<TL, SL, false>(v, wl);
       // ---- store: slot n = b*RL + r -> row sigma(n) = b + (L/RL)*r ----
+      // PL parts of L/PL rows; with four parts the staging holds two
+      // quarter buffers, so writing part q overlaps the TMA read of part q-1
+      // (L >= 1024 only: the output maps' box is min(L/2, 256) rows)
+      constexpr int PL = (RL >= 4 && L >= 1024) ? 4 : 2, NSB = PL == 4 ? 2 : 1, PSL = L / PL, BOXQ = PSL < 256 ? PSL : 256;
 #pragma unroll
-      for (int half = 0; half < 2; ++half) {
-        if (t == 0) bulk_wait_read();  // staging free again
+      for (int q = 0; q < PL; ++q) {
+        if (t == 0) {
+          if constexpr (NSB == 2) bulk_wait_read_1();  // this buffer's previous part read
+          else bulk_wait_read();
+        }
         __syncthreads();
-        V* sv = reinterpret_cast<V*>(stg);
+        T* sb = stg + static_cast<size_t>(q % NSB) * PSL * 2 * NL;
+        V* sv = reinterpret_cast<V*>(sb);
 #pragma unroll
         for (int i = 0; i < NBFL; ++i) {
           int line, b;
           last_decode<TL>(t + i * NT, line, b);
 #pragma unroll
-          for (int r = half * (RL / 2); r < (half + 1) * (RL / 2); ++r)
-            sv[(b + (L / RL) * (r - half * (RL / 2))) * NL + line] = v[i * RL + r];
+          for (int r = q * (RL / PL); r < (q + 1) * (RL / PL); ++r)
+            sv[(b + (L / RL) * (r - q * (RL / PL))) * NL + line] = v[i * RL + r];
         }
         fence_async_smem();
         __syncthreads();
         if (t == 0) {
 #pragma unroll 1
-          for (int r0 = 0; r0 < HALF; r0 += BOXH)
-            tma_store_4d(&tout, band * 2 * NL, half * HALF + r0, plane, batch, stg + static_cast<size_t>(r0) * 2 * NL);
+          for (int r0 = 0; r0 < PSL; r0 += BOXQ)
+            tma_store_4d(&tout, band * 2 * NL, q * PSL + r0, plane, batch, sb + static_cast<size_t>(r0) * 2 * NL);
           bulk_commit();
         }
       }
@@ -608,27 +614,32 @@ __global__ void __launch_bounds__(Tile<T, L, NL, true>::NT)
         issue(tile + gridDim.x);
       }
       // outputs: stage-0 butterfly (line, j) holds natural index ii = j + r*Q0
+      // PI parts of L/PI rows (two quarter buffers when PI == 4, see the forward)
+      constexpr int PI = (R0 >= 4 && L >= 1024) ? 4 : 2, NSB = PI == 4 ? 2 : 1, PSI = L / PI, BOXQ = PSI < 256 ? PSI : 256;
       if constexpr (STORE == ST_INTER) {
 #pragma unroll
-        for (int half = 0; half < 2; ++half) {
-          if (t == 0) bulk_wait_read();
+        for (int q = 0; q < PI; ++q) {
+          if (t == 0) {
+            if constexpr (NSB == 2) bulk_wait_read_1();
+            else bulk_wait_read();
+          }
           __syncthreads();
-          V* sv = reinterpret_cast<V*>(stg);
+          T* sb = stg + static_cast<size_t>(q % NSB) * PSI * 2 * NL;
+          V* sv = reinterpret_cast<V*>(sb);
 #pragma unroll
           for (int i = 0; i < NBF0; ++i) {
             const int bf = t + i * NT;
             const int line = bf & (NL - 1), j = bf >> TL::LGNL;
 #pragma unroll
-            for (int r = half * (R0 / 2); r < (half + 1) * (R0 / 2); ++r)
-              sv[(j + (r - half * (R0 / 2)) * Q0) * NL + line] = v[i * R0 + r];
+            for (int r = q * (R0 / PI); r < (q + 1) * (R0 / PI); ++r)
+              sv[(j + (r - q * (R0 / PI)) * Q0) * NL + line] = v[i * R0 + r];
           }
           fence_async_smem();
           __syncthreads();
           if (t == 0) {
 #pragma unroll 1
-            for (int r0 = 0; r0 < HALF; r0 += BOXH)
-              tma_store_4d(&tout, band * 2 * NL, half * HALF + r0, plane, batch,
-                           stg + static_cast<size_t>(r0) * 2 * NL);
+            for (int r0 = 0; r0 < PSI; r0 += BOXQ)
+              tma_store_4d(&tout, band * 2 * NL, q * PSI + r0, plane, batch, sb + static_cast<size_t>(r0) * 2 * NL);
             bulk_commit();
           }
         }
@@ -639,21 +650,29 @@ __global__ void __launch_bounds__(Tile<T, L, NL, true>::NT)
         const T sc = static_cast<T>(a.scale);
         int pl = plane;
         if (a.out_plane_map == 1) pl = parity_embed(plane, a.out_plane_n);
+        // part q holds ii in [q L/PI, (q+1) L/PI): class q / (PI/2) (even rows
+        // 2ii, then odd rows 2L-1-2ii), row pairs from pbase
 #pragma unroll
-        for (int half = 0; half < 2; ++half) {
-          if (t == 0) bulk_wait_read();
+        for (int q = 0; q < PI; ++q) {
+          const int half = q / (PI / 2);
+          const int pbase = half == 0 ? q * PSI : L - (q + 1) * PSI;  // first row pair of the part
+          if (t == 0) {
+            if constexpr (NSB == 2) bulk_wait_read_1();
+            else bulk_wait_read();
+          }
           __syncthreads();
-          V2* sv = reinterpret_cast<V2*>(stg);
+          T* sb = stg + static_cast<size_t>(q % NSB) * PSI * 2 * NL;
+          V2* sv = reinterpret_cast<V2*>(sb);
 #pragma unroll
           for (int i = 0; i < NBF0; ++i) {
             const int bf = t + i * NT;
             const int line = bf & (NL - 1), j = bf >> TL::LGNL;
             const int h = line & 1;
 #pragma unroll
-            for (int r = half * (R0 / 2); r < (half + 1) * (R0 / 2); ++r) {
+            for (int r = q * (R0 / PI); r < (q + 1) * (R0 / PI); ++r) {
               const int ii = j + r * Q0;
               const int k1 = half == 0 ? 2 * ii : 2 * L - 1 - 2 * ii;  // pe(ii)
-              const int srow = half == 0 ? ii : L - 1 - ii;             // pair index
+              const int srow = (half == 0 ? ii : L - 1 - ii) - pbase;   // pair index within the part
               const V z = v[i * R0 + r];
               const T recv = __shfl_xor_sync(TL::MASK, z.y, 1);
               const T s0 = (a.sign_row && (k1 & 1)) ? -sc : sc;
@@ -666,8 +685,8 @@ __global__ void __launch_bounds__(Tile<T, L, NL, true>::NT)
           __syncthreads();
           if (t == 0) {
 #pragma unroll 1
-            for (int r0 = 0; r0 < HALF; r0 += BOXH)
-              tma_store_5d(&tout, band * 2 * NL, half, r0, pl, batch, stg + static_cast<size_t>(r0) * 2 * NL);
+            for (int r0 = 0; r0 < PSI; r0 += BOXQ)
+              tma_store_5d(&tout, band * 2 * NL, half, pbase + r0, pl, batch, sb + static_cast<size_t>(r0) * 2 * NL);
             bulk_commit();
           }
         }
