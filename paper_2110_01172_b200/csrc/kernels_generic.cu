@@ -615,7 +615,7 @@ __global__ void g_gather_inv(const double2* __restrict__ z, T* __restrict__ y, D
   }
 }
 
-// ---- two-pass 2D pipeline for extents <= kFftMaxN -------------------------
+// ---- two-pass 2D pipeline for extents <= 8192 (one line per tile at most) ----
 // The same three stages with the gathers, the postprocess and the merged
 // preprocess fused into the line FFTs' loads and stores, so a 2D transform is
 // two passes over HBM (one per axis) instead of gather + transpose + FFT +
@@ -960,7 +960,7 @@ cudaError_t generic_run(const GenericJob& job, const void* in, void* out, void* 
   };
   double2* cur = A;
   double2* nxt = B;
-  if (job.rank == 2 && !job.legacy && job.dims[0] <= kFftMaxN && job.dims[1] <= kFftMaxN) {
+  if (job.rank == 2 && !job.legacy && job.dims[0] <= G2Cfg<16>::CAP && job.dims[1] <= G2Cfg<16>::CAP) {
     // two-pass pipeline (gathers / pre / post fused into the line FFTs)
     G2Args a{};
     a.n1 = job.dims[0];
