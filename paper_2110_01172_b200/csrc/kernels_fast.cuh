@@ -555,8 +555,8 @@ __global__ void __launch_bounds__(Tile<T, L, NL, true>::NT)
       // ---- store: slot n = b*RL + r -> row sigma(n) = b + (L/RL)*r ----
       // PL parts of L/PL rows; with four parts the staging holds two
       // quarter buffers, so writing part q overlaps the TMA read of part q-1
-      // (L >= 1024 only: the output maps' box is min(L/2, 256) rows)
-      constexpr int PL = (RL >= 4 && L >= 1024) ? 4 : 2, NSB = PL == 4 ? 2 : 1, PSL = L / PL, BOXQ = PSL < 256 ? PSL : 256;
+      // (L >= 4096 only: measured neutral-to-worse on smaller tiles)
+      constexpr int PL = (RL >= 4 && L >= 4096) ? 4 : 2, NSB = PL == 4 ? 2 : 1, PSL = L / PL, BOXQ = PSL < 256 ? PSL : 256;
 #pragma unroll
       for (int q = 0; q < PL; ++q) {
         if (t == 0) {
@@ -615,7 +615,7 @@ __global__ void __launch_bounds__(Tile<T, L, NL, true>::NT)
       }
       // outputs: stage-0 butterfly (line, j) holds natural index ii = j + r*Q0
       // PI parts of L/PI rows (two quarter buffers when PI == 4, see the forward)
-      constexpr int PI = (R0 >= 4 && L >= 1024) ? 4 : 2, NSB = PI == 4 ? 2 : 1, PSI = L / PI, BOXQ = PSI < 256 ? PSI : 256;
+      constexpr int PI = (R0 >= 4 && L >= 4096) ? 4 : 2, NSB = PI == 4 ? 2 : 1, PSI = L / PI, BOXQ = PSI < 256 ? PSI : 256;
       if constexpr (STORE == ST_INTER) {
 #pragma unroll
         for (int q = 0; q < PI; ++q) {
