@@ -16,7 +16,18 @@ struct GenericJob {
   bool legacy = false;   // 2D: one full-tensor pass per stage (the row-column comparator)
   const double2* quarter[3] = {nullptr, nullptr, nullptr};  // e^{-i pi k/(2 N_a)}
   const double2* circle[3] = {nullptr, nullptr, nullptr};   // e^{-2 pi i t / N_a}
+  // Bluestein tables of axes whose largest prime factor is large (2D
+  // pipeline): chirp c_j = e^{-i pi j^2 / N} (j < N), bhat = FFT_M of the
+  // conjugate chirp wrapped to length M (pow2 >= 2N-1), circle of length M
+  int blue_m[3] = {0, 0, 0};
+  const double2* blue_chirp[3] = {nullptr, nullptr, nullptr};
+  const double2* blue_hat[3] = {nullptr, nullptr, nullptr};
+  const double2* blue_circle[3] = {nullptr, nullptr, nullptr};
 };
+
+// Bluestein length for an axis of extent n (0 = mixed radix is used): the
+// pow2 M >= 2n - 1 when n's largest prime factor exceeds 64 and M <= 8192.
+int bluestein_len(int n);
 
 // Workspace: 2 * numel * batch * sizeof(double2) bytes.
 template <typename T>

@@ -656,6 +656,13 @@ struct G2Args {
   Radices rad;
   FastDiv fn1, fn2, fh;
   int h;             // stored spectrum columns, n2 / 2 + 1
+  // Bluestein on the FFT axis (bm = pow2 convolution length, 0 = mixed radix):
+  // x_m c_m -> FFT_M -> * bhat -> inverse FFT_M -> c_k / M (conjugated chirp
+  // and kernel for the inverse transform); rad then describes M
+  int bm;
+  const double2* bchirp;
+  const double2* bhat;
+  const double2* bcircle;
 };
 
 template <typename T, int KIND, int FPT>
@@ -665,9 +672,24 @@ __global__ void __launch_bounds__(G2Cfg<FPT>::NT, G2Cfg<FPT>::MINB) g2_kernel(G2
   extern __shared__ __align__(16) double2 g2sm[];
   const int n1 = a.n1, n2 = a.n2;
   const int n = ROWS ? n2 : n1;               // FFT length
-  const int ld = ROWS ? n : (n | 1);          // line stride in smem
+  const int nb = a.bm ? a.bm : n;             // line length in smem (Bluestein: M)
+  const int ld = ROWS ? nb : (nb | 1);        // line stride in smem
   const double2* tw = a.circle;               // forward circle table, L1-resident
   double2* x = g2sm;
+  // Bluestein pre/post chirp multiplies ride on the loads and stores
+  const bool blue = a.bm != 0;
+  auto chirp = [&](int m) {
+    const double2 c = a.bchirp[m];
+    return INV ? cj(c) : c;
+  };
+  auto put = [&](int slot, double2 v) { x[slot] = blue ? cm(v, chirp(slot % ld)) : v; };
+  const double inv_m = blue ? 1.0 / a.bm : 1.0;
+  auto get = [&](int l, int k) {
+    const double2 v = x[l * ld + k];
+    if (!blue) return v;
+    const double2 w = cm(v, chirp(k));
+    return make_double2(w.x * inv_m, w.y * inv_m);
+  };
   const int t = threadIdx.x, nt = blockDim.x;
   const long long plane = static_cast<long long>(n1) * n2;
   const int h = a.h;
@@ -714,7 +736,8 @@ __global__ void __launch_bounds__(G2Cfg<FPT>::NT, G2Cfg<FPT>::MINB) g2_kernel(G2
     }
 #pragma unroll
     for (int u = 0; u < FPT; ++u)
-      if (t + u * nt < total) x[slot[u]] = make_double2(static_cast<double>(va[u]), static_cast<double>(vb[u]));
+      if (t + u * nt < total)
+        put(slot[u], make_double2(static_cast<double>(va[u]), static_cast<double>(vb[u])));
   } else if constexpr (KIND == G2_FWD_COLS || KIND == G2_INV_ROWS) {
     const double2* W = static_cast<const double2*>(a.src);
     double2 v[FPT];
@@ -754,7 +777,7 @@ __global__ void __launch_bounds__(G2Cfg<FPT>::NT, G2Cfg<FPT>::MINB) g2_kernel(G2
     }
 #pragma unroll
     for (int u = 0; u < FPT; ++u)
-      if (t + u * nt < total) x[slot[u]] = v[u];
+      if (t + u * nt < total) put(slot[u], v[u]);
   } else {  // G2_INV_COLS
     // full Hermitian spectrum of the merged preprocess, column m2 = c0 + l
     const T* xb = static_cast<const T*>(a.src) + b * plane;
@@ -790,13 +813,32 @@ __global__ void __launch_bounds__(G2Cfg<FPT>::NT, G2Cfg<FPT>::MINB) g2_kernel(G2
           const double2 w = cj(cm(a.ta[e1s[u - u0]], a.tb[m2s[u - u0]]));
           const double2 val = dir[u - u0] ? cm(w, make_double2(o[0] - o[1], -(o[2] + o[3])))
                                           : cm(w, make_double2(o[2] - o[3], -(o[0] + o[1])));
-          x[slot[u - u0]] = val;
+          put(slot[u - u0], val);
         }
       }
     }
   }
+  if (blue) {  // zero padding of each line to the convolution length
+    const int pad = nb - n;
+    for (int e = t; e < lines * pad; e += nt) {
+      const int l = e / pad;
+      x[l * ld + n + (e - l * pad)] = make_double2(0.0, 0.0);
+    }
+  }
   __syncthreads();
-  line_passes<FPT, INV, true>(x, tw, n, a.rad, total, t, nt, ld);
+  if (!blue) {
+    line_passes<FPT, INV, true>(x, tw, n, a.rad, total, t, nt, ld);
+  } else {
+    const int totalm = lines * nb;
+    line_passes<FPT, false, true>(x, a.bcircle, nb, a.rad, totalm, t, nt, ld);
+    for (int e = t; e < totalm; e += nt) {
+      const int l = a.rad.n.div(e), k = e - l * nb;
+      const double2 hk = a.bhat[k];
+      x[l * ld + k] = cm(x[l * ld + k], INV ? cj(hk) : hk);
+    }
+    __syncthreads();
+    line_passes<FPT, true, true>(x, a.bcircle, nb, a.rad, totalm, t, nt, ld);
+  }
 
   // ---- store ----
   if constexpr (KIND == G2_FWD_ROWS) {
@@ -804,7 +846,7 @@ __global__ void __launch_bounds__(G2Cfg<FPT>::NT, G2Cfg<FPT>::MINB) g2_kernel(G2
     double2* W = static_cast<double2*>(a.dst);
     for (int e = t; e < lines * h; e += nt) {
       const int l = a.fh.div(e), c = e - l * h;
-      const double2 z = x[l * ld + c], zm = x[l * ld + (c ? n2 - c : 0)];
+      const double2 z = get(l, c), zm = get(l, c ? n2 - c : 0);
       W[(r0 + 2 * l) * h + c] = make_double2(0.5 * (z.x + zm.x), 0.5 * (z.y - zm.y));
       if (2 * l + 1 < rows) W[(r0 + 2 * l + 1) * h + c] = make_double2(0.5 * (z.y + zm.y), 0.5 * (zm.x - z.x));
     }
@@ -815,7 +857,7 @@ __global__ void __launch_bounds__(G2Cfg<FPT>::NT, G2Cfg<FPT>::MINB) g2_kernel(G2
       const int k1 = fl.div(e), l = e - k1 * lines;
       const int k2 = c0 + l;
       const double2 aa = a.ta[k1];
-      const double2 x1 = x[l * ld + k1], x2 = x[l * ld + (k1 ? n1 - k1 : 0)];
+      const double2 x1 = get(l, k1), x2 = get(l, k1 ? n1 - k1 : 0);
       const double v = 0.5 * cm(a.tb[k2], ca(cm(aa, x1), cm(cj(aa), x2))).x;
       y[static_cast<long long>(k1) * n2 + k2] = static_cast<T>(v);
       // mirrored column n2 - k2: X(k1, n2 - k2) = conj X(-k1, k2), X(-k1, n2 - k2) = conj X(k1, k2)
@@ -829,7 +871,7 @@ __global__ void __launch_bounds__(G2Cfg<FPT>::NT, G2Cfg<FPT>::MINB) g2_kernel(G2
     double2* W = static_cast<double2*>(a.dst) + b * wplane;
     for (int e = t; e < total; e += nt) {
       const int m = fl.div(e), l = e - m * lines;
-      W[static_cast<long long>(m) * h + c0 + l] = x[l * ld + m];
+      W[static_cast<long long>(m) * h + c0 + l] = get(l, m);
     }
   } else {
     T* y = static_cast<T*>(a.dst);
@@ -837,7 +879,7 @@ __global__ void __launch_bounds__(G2Cfg<FPT>::NT, G2Cfg<FPT>::MINB) g2_kernel(G2
       const int r = a.fn2.div(e), k2 = e - r * n2;  // tile row r = line r / 2, part r & 1
       const int R = static_cast<int>(r0) + r, bb = a.fn1.div(R);
       const int k1 = R - bb * n1;
-      const double2 z = x[(r >> 1) * ld + parity_source(k2, n2)];
+      const double2 z = get(r >> 1, parity_source(k2, n2));
       double v = a.scale * ((r & 1) ? z.y : z.x);
       if ((a.sign_axis == 0 && (k1 & 1)) || (a.sign_axis == 1 && (k2 & 1))) v = -v;
       y[static_cast<long long>(R) * n2 + k2] = static_cast<T>(v);
@@ -849,7 +891,7 @@ template <typename T, int KIND, int FPT>
 cudaError_t g2_launch_cfg(G2Args a, cudaStream_t st) {
   using C = G2Cfg<FPT>;
   const bool rows = KIND == G2_FWD_ROWS || KIND == G2_INV_ROWS;
-  const int n = rows ? a.n2 : a.n1;
+  const int n = a.bm ? a.bm : (rows ? a.n2 : a.n1);  // line length in smem
   const int ld = rows ? n : (n | 1);
   // lines per tile: as many as the tile capacity allows (columns: at most 32,
   // rows: at most 64), fewer threads for small tiles
@@ -879,11 +921,25 @@ cudaError_t g2_launch_cfg(G2Args a, cudaStream_t st) {
 
 template <typename T, int KIND>
 cudaError_t g2_launch(G2Args a, cudaStream_t st) {
-  const int n = (KIND == G2_FWD_ROWS || KIND == G2_INV_ROWS) ? a.n2 : a.n1;
+  const int n = a.bm ? a.bm : (KIND == G2_FWD_ROWS || KIND == G2_INV_ROWS) ? a.n2 : a.n1;
   return n <= G2Cfg<8>::CAP ? g2_launch_cfg<T, KIND, 8>(a, st) : g2_launch_cfg<T, KIND, 16>(a, st);
 }
 
 }  // namespace
+
+int bluestein_len(int n) {
+  int m = n, p = 1;
+  for (int d = 2; d * d <= m; ++d)
+    while (m % d == 0) {
+      p = std::max(p, d);
+      m /= d;
+    }
+  if (m > 1) p = std::max(p, m);
+  if (p <= 64) return 0;
+  int M = 1;
+  while (M < 2 * n - 1) M <<= 1;
+  return M <= 8192 ? M : 0;
+}
 
 // ---------------------------------------------------------------------------
 template <typename T>
@@ -972,17 +1028,28 @@ cudaError_t generic_run(const GenericJob& job, const void* in, void* out, void* 
     a.ta = job.quarter[0];
     a.tb = job.quarter[1];
     cudaError_t e;
+    auto axis = [&](int ax) {  // FFT-axis tables (mixed radix or Bluestein)
+      a.circle = job.circle[ax];
+      a.bm = job.blue_m[ax];
+      a.bchirp = job.blue_chirp[ax];
+      a.bhat = job.blue_hat[ax];
+      a.bcircle = job.blue_circle[ax];
+    };
     if (!job.inverse) {
-      a.src = in, a.dst = A, a.circle = job.circle[1];
+      a.src = in, a.dst = A;
+      axis(1);
       e = g2_launch<T, G2_FWD_ROWS>(a, st);
       if (e != cudaSuccess) return e;
-      a.src = A, a.dst = out, a.circle = job.circle[0];
+      a.src = A, a.dst = out;
+      axis(0);
       e = g2_launch<T, G2_FWD_COLS>(a, st);
     } else {
-      a.src = in, a.dst = A, a.circle = job.circle[0];
+      a.src = in, a.dst = A;
+      axis(0);
       e = g2_launch<T, G2_INV_COLS>(a, st);
       if (e != cudaSuccess) return e;
-      a.src = A, a.dst = out, a.circle = job.circle[1];
+      a.src = A, a.dst = out;
+      axis(1);
       e = g2_launch<T, G2_INV_ROWS>(a, st);
     }
     return e;

@@ -110,6 +110,10 @@ struct sdct_plan_s {
   int bad_q = -1;        // corrupt_twiddle_for_testing index (row kernels), -1 = none  // intermediate storage row of frequency k: axis 0, axis 1 (3D)
   double2* gq[3] = {nullptr, nullptr, nullptr};  // generic fp64 quarter-wave tables
   double2* gc[3] = {nullptr, nullptr, nullptr};  // generic fp64 circle tables
+  int bm[3] = {0, 0, 0};                          // Bluestein length per axis (0 = none)
+  double2* bchirp[3] = {nullptr, nullptr, nullptr};
+  double2* bhat[3] = {nullptr, nullptr, nullptr};
+  double2* bcircle[3] = {nullptr, nullptr, nullptr};
   size_t b_offset_fast = 0, b_offset_gen = 0;    // element offsets of table b (corrupt hook)
   // workspace + host staging
   void* ws = nullptr;
@@ -159,6 +163,36 @@ void circle(std::vector<long double>& re, std::vector<long double>& im, long lon
     const long double ph = -2.0L * pi * num * static_cast<long double>(k) / den;
     re[k] = cosl(ph);
     im[k] = sinl(ph);
+  }
+}
+
+// In-place iterative radix-2 DFT (sign -1) of a power-of-two length, long
+// double: the Bluestein kernel spectrum is computed once per plan on the host.
+void host_fft_pow2(std::vector<long double>& re, std::vector<long double>& im) {
+  const size_t n = re.size();
+  for (size_t i = 1, j = 0; i < n; ++i) {
+    size_t bit = n >> 1;
+    for (; j & bit; bit >>= 1) j ^= bit;
+    j ^= bit;
+    if (i < j) {
+      std::swap(re[i], re[j]);
+      std::swap(im[i], im[j]);
+    }
+  }
+  const long double pi = 3.141592653589793238462643383279502884L;
+  for (size_t len = 2; len <= n; len <<= 1) {
+    for (size_t k = 0; k < len / 2; ++k) {
+      const long double ang = -2.0L * pi * static_cast<long double>(k) / static_cast<long double>(len);
+      const long double wr = cosl(ang), wi = sinl(ang);
+      for (size_t i = 0; i < n; i += len) {
+        const size_t a = i + k, b = a + len / 2;
+        const long double xr = re[b] * wr - im[b] * wi, xi = re[b] * wi + im[b] * wr;
+        re[b] = re[a] - xr;
+        im[b] = im[a] - xi;
+        re[a] += xr;
+        im[a] += xi;
+      }
+    }
   }
 }
 
@@ -308,11 +342,36 @@ int build_plan(sdct_plan_s* p) {
     p->ws_bytes = p->generic_ws_bytes();
   }
   // generic-path tables are always present (odd shapes, row-column, 1D)
+  size_t off_bc[3] = {0, 0, 0}, off_bh[3] = {0, 0, 0}, off_bm[3] = {0, 0, 0};
   for (int a = 0; a < r; ++a) {
     circle(re, im, p->n[a], 1.0L, 4.0L * p->n[a]);
     fill_table<double>(blob, off_gq[a], re, im);
     circle(re, im, p->n[a], 1.0L, p->n[a]);
     fill_table<double>(blob, off_gc[a], re, im);
+    // Bluestein (2D generic pipeline, axes with a large prime factor)
+    p->bm[a] = (!fast && r == 2) ? bluestein_len(p->n[a]) : 0;
+    if (p->bm[a]) {
+      const int n = p->n[a], M = p->bm[a];
+      const long double pi = 3.141592653589793238462643383279502884L;
+      std::vector<long double> cr(n), ci(n), hr(M, 0.0L), hi(M, 0.0L);
+      for (int j = 0; j < n; ++j) {
+        const long long jj = (static_cast<long long>(j) * j) % (2LL * n);  // j^2 mod 2n keeps the phase exact
+        const long double ph = -pi * static_cast<long double>(jj) / n;
+        cr[j] = cosl(ph);
+        ci[j] = sinl(ph);
+        hr[j] = cr[j];  // b_j = conj(c_j), wrapped: b_{M-j} = b_j
+        hi[j] = -ci[j];
+        if (j) {
+          hr[M - j] = cr[j];
+          hi[M - j] = -ci[j];
+        }
+      }
+      host_fft_pow2(hr, hi);
+      fill_table<double>(blob, off_bc[a], cr, ci);
+      fill_table<double>(blob, off_bh[a], hr, hi);
+      circle(re, im, M, 1.0L, M);
+      fill_table<double>(blob, off_bm[a], re, im);
+    }
   }
   cudaError_t e = cudaMalloc(&p->tables, blob.size());
   if (e != cudaSuccess) return cuda_fail(e, "allocating plan tables");
@@ -341,6 +400,11 @@ int build_plan(sdct_plan_s* p) {
   for (int a = 0; a < r; ++a) {
     p->gq[a] = reinterpret_cast<double2*>(base + off_gq[a]);
     p->gc[a] = reinterpret_cast<double2*>(base + off_gc[a]);
+    if (p->bm[a]) {
+      p->bchirp[a] = reinterpret_cast<double2*>(base + off_bc[a]);
+      p->bhat[a] = reinterpret_cast<double2*>(base + off_bh[a]);
+      p->bcircle[a] = reinterpret_cast<double2*>(base + off_bm[a]);
+    }
   }
   p->b_offset_gen = r >= 2 ? off_gq[1] : off_gq[0];
   e = cudaMalloc(&p->ws, p->ws_bytes);
@@ -652,6 +716,10 @@ GenericJob make_job(const sdct_plan_s* p, int kind) {
     j.dims[a] = p->n[a];
     j.quarter[a] = p->gq[a];
     j.circle[a] = p->gc[a];
+    j.blue_m[a] = p->bm[a];
+    j.blue_chirp[a] = p->bchirp[a];
+    j.blue_hat[a] = p->bhat[a];
+    j.blue_circle[a] = p->bcircle[a];
   }
   j.batch = p->batch;
   j.legacy = kind == SDCT_DCT_2D_ROWCOL;

@@ -109,7 +109,9 @@ def test_2d_vs_oracle(cuda, dtype, kind):
 # lines, both tile configurations (lines <= 2048 and > 2048), odd and prime
 # extents (direct-sum passes), several lines per tile
 SHAPES_G2 = [(2000, 3), (3, 2000), (300, 500), (999, 1001), (2500, 40), (40, 3000), (97, 2047), (4095, 6),
-             (6000, 5), (7, 8000), (8190, 3)]
+             (6000, 5), (7, 8000), (8190, 3),
+             # Bluestein axes (largest prime factor > 64): columns, rows, both
+             (4093, 3), (3, 4093), (1021, 127), (130, 2039)]
 
 
 @pytest.mark.parametrize("dtype", ["float64", "float32"])
