@@ -622,18 +622,22 @@ __global__ void g_gather_inv(const double2* __restrict__ z, T* __restrict__ y, D
 // transpose + FFT + post:
 // W holds the one-sided spectrum, columns k2 < h = n2/2 + 1 (the layout of
 // the reference's rfft_nd / irfft_nd, rfft.cpp:182-245):
-//   forward : G2_FWD_ROWS  x row pe(i), columns scattered by ps (= pe^-1)
-//                          -> FFT along axis 1 -> W row i (k2 < h)
+//   forward : G2_FWD_ROWS  x rows pe(i), pe(i+1) as the real / imaginary
+//                          parts of one line, columns scattered by ps (= pe^-1)
+//                          -> FFT along axis 1 -> the two spectra separated by
+//                          Hermitian symmetry -> W rows i, i+1 (k2 < h)
 //             G2_FWD_COLS  W columns c0.. -> FFT along axis 0 -> the
 //                          postprocess of dct2d.hpp:6 for y columns c and
 //                          n2 - c (X(k1, n2 - c) = conj X(-k1, c)) -> y
 //   inverse : G2_INV_COLS  merged preprocess (dct2d.cpp:161-198) for columns
 //                          c0.. < h -> inverse FFT along axis 0 -> W columns
-//             G2_INV_ROWS  W row ps(k1), Hermitian fill of k2 >= h as
-//                          irfft_nd does -> inverse FFT along axis 1 -> the
-//                          inverse gather (dct2d.cpp:214-238, row-local) -> y
+//             G2_INV_ROWS  W rows ps(k1) + i ps(k1+1), Hermitian fill of
+//                          k2 >= h as irfft_nd does -> inverse FFT along axis 1
+//                          -> real / imaginary parts through the inverse gather
+//                          (dct2d.cpp:214-238, row-local) -> y rows k1, k1+1
 // Column tiles hold `lines` consecutive columns with an odd line stride in
-// shared memory (conflict-free strided loads); row tiles hold `lines` rows.
+// shared memory (conflict-free strided loads); row tiles hold `lines` rows
+// (two per complex line).
 enum { G2_FWD_ROWS = 0, G2_FWD_COLS = 1, G2_INV_COLS = 2, G2_INV_ROWS = 3 };
 // Two tile shapes: lines up to 2048 run 256-thread CTAs at 8 elements per
 // thread (three CTAs per SM: one CTA's global loads overlap another's passes),
@@ -647,7 +651,7 @@ struct G2Args {
   void* dst;
   int n1, n2;
   long long batch;
-  int lines;         // lines per tile
+  int lines;         // columns per column tile / rows per row tile
   int mode, sign_axis;
   double scale;
   const double2* circle;  // circle table of the FFT axis
