@@ -6,6 +6,7 @@
 #pragma once
 
 #include <cstdlib>
+#include <utility>
 
 #include "kernels_fast.cuh"
 #include "kernels_row2.cuh"
@@ -33,6 +34,34 @@ __host__ __device__ constexpr int nl_default(int esize, int L) {
 // with 2-complex (32-B) bands run as two 64 KB halves per 2-CTA cluster.
 __host__ __device__ constexpr bool col2_used(int esize, int L, int planes, int nl) {
   return planes == 1 && nl * esize == 16 && (L == 8192 || L == 4096);
+}
+
+// Launch with programmatic stream serialization: the kernel may start while
+// the previous kernel of the stream drains (both kernels call pdl_trigger /
+// pdl_wait, tma.cuh), hiding launch latency and prologue at pass boundaries.
+// SDCT_NO_PDL=1 falls back to plain launches (A/B and debugging).
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args&&... args) {
+  static const bool off = [] {
+    const char* f = getenv("SDCT_NO_PDL");
+    return f && atoi(f) == 1;
+  }();
+  if (off) {
+    k<<<grid, block, smem, st>>>(std::forward<Args>(args)...);
+    return cudaGetLastError();
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
 }
 
 // Opt each kernel instantiation in to > 48 KB dynamic shared memory (once).
@@ -90,8 +119,7 @@ cudaError_t launch_col_one(dim3 grid, cudaStream_t st, const CUtensorMap& map, c
   b.nplanes = static_cast<int>(grid.y);
   b.ntiles = static_cast<int>(grid.x * grid.y * grid.z);
   const int ctas = b.ntiles < resident ? b.ntiles : resident;
-  k<<<ctas, NT, smem, st>>>(map, omap, b, tw);
-  return cudaGetLastError();
+  return launch_pdl(k, dim3(ctas), dim3(NT), smem, st, map, omap, b, tw);
 }
 
 template <typename T, int L, int VAR>
@@ -151,8 +179,7 @@ cudaError_t launch_row2(dim3 grid, cudaStream_t st, const RowArgs& a, const TwSe
   // MODE 2: persistent, one item at a time per CTA; MODE 1: one CTA per item
   const int want = MODE == 0 ? (nitems + 1) / 2 : nitems;
   const int ctas = want < resident || MODE == 1 ? want : resident;
-  k<<<ctas, Geo::CTA, Geo::SMEM, st>>>(a, tw, nitems);
-  return cudaGetLastError();
+  return launch_pdl(k, dim3(ctas), dim3(Geo::CTA), Geo::SMEM, st, a, tw, nitems);
 }
 
 template <typename T, int M, int KIND>
@@ -183,8 +210,7 @@ cudaError_t launch_row_one(dim3 grid, cudaStream_t st, const RowArgs& a, const T
                             (KIND == RK_INV3 && row3_staged<T, M>() ? 2 : 1) + 16;
     cudaError_t e = prep_smem(k, smem);
     if (e != cudaSuccess) return e;
-    k<<<grid, row_threads<T, M, KIND>(), smem, st>>>(a, tw);
-    return cudaGetLastError();
+    return launch_pdl(k, grid, dim3(row_threads<T, M, KIND>()), smem, st, a, tw);
   }
 }
 

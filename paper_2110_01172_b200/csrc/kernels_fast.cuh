@@ -487,6 +487,8 @@ __global__ void __launch_bounds__(Tile<T, L, NL, true>::NT)
     mbar_init(bar, 1);
   }
   __syncthreads();
+  pdl_trigger();
+  pdl_wait();  // the previous kernel's output is complete before the first load
   if (t == 0 && static_cast<int>(blockIdx.x) < a.ntiles) issue(blockIdx.x);
 
   uint32_t phase = 0;
@@ -817,6 +819,8 @@ __global__ void __launch_bounds__(row_threads<T, M, KIND>())
   const int t = threadIdx.x;
   const int P = blockIdx.x, batch = blockIdx.y;
   const int n1 = a.n1, n2 = a.n2;
+  pdl_trigger();
+  pdl_wait();  // the previous kernel's output is complete before any buffer access
 
   // frequency rows of this group, their storage rows in the intermediate
   // (srow = sigma(digit_pos), the column FFTs' order), and degeneracy

@@ -680,6 +680,8 @@ __global__ void __launch_bounds__(G2Cfg<FPT>::NT, G2Cfg<FPT>::MINB) g2_kernel(G2
   const int ld = ROWS ? nb : (nb | 1);        // line stride in smem
   const double2* tw = a.circle;               // forward circle table, L1-resident
   double2* x = g2sm;
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // previous kernel complete (PDL launch)
   // Bluestein pre/post chirp multiplies ride on the loads and stores
   const bool blue = a.bm != 0;
   auto chirp = [&](int m) {
@@ -919,8 +921,18 @@ cudaError_t g2_launch_cfg(G2Args a, cudaStream_t st) {
   }
   const long long tiles = rows ? (a.batch * a.n1 + a.lines - 1) / a.lines : a.batch * ((a.h + lines - 1) / lines);
   // grid.x limit 2^31-1: batches beyond it are not reachable at these extents
-  g2_kernel<T, KIND, FPT><<<static_cast<unsigned>(tiles), nt, smem, st>>>(a);
-  return cudaGetLastError();
+  // programmatic dependent launch: the second pass's CTAs start as the first drains
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(tiles));
+  cfg.blockDim = dim3(nt);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute lattr[1];
+  lattr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  lattr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = lattr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, g2_kernel<T, KIND, FPT>, a);
 }
 
 template <typename T, int KIND>

@@ -155,6 +155,8 @@ __global__ void __launch_bounds__(Row2Geom<T, M, MODE>::CTA, Row2Geom<T, M, MODE
     }
   }
   __syncthreads();
+  pdl_trigger();
+  pdl_wait();  // the previous kernel's output is complete before the first load
   if (threadIdx.x == 0) {
     if constexpr (MODE == 2) {
       if (static_cast<int>(blockIdx.x) < nitems) {
