@@ -334,6 +334,38 @@ def test_non_default_stream(cuda):
     assert oracle.rel_l2(out.cpu().numpy(), oracle.port.dct_2d(x.cpu().numpy())) <= 1e-12
 
 
+@pytest.mark.parametrize("shape", [(1024, 1024), (300, 500)])
+def test_cuda_graph_capture_and_replay(cuda, shape):
+    # the launches (programmatic-dependent-launch attribute included) can be
+    # captured into a CUDA graph and replayed: fast path and generic path
+    torch = _torch()
+    from paper_2110_01172_b200 import capi
+
+    x = torch.tensor(rnd(shape, 16), device="cuda")
+    plan = capi.Plan(shape)
+    ws = torch.empty(max(plan.workspace_bytes, 1), dtype=torch.uint8, device="cuda")
+    y = torch.empty_like(x)
+    z = torch.empty_like(x)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):  # warm-up outside capture (lazy per-kernel setup)
+        plan.exec("dct_2d", x.data_ptr(), y.data_ptr(), ws.data_ptr(), s.cuda_stream)
+        plan.exec("idct_2d", y.data_ptr(), z.data_ptr(), ws.data_ptr(), s.cuda_stream)
+    s.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        plan.exec("dct_2d", x.data_ptr(), y.data_ptr(), ws.data_ptr(), s.cuda_stream)
+        plan.exec("idct_2d", y.data_ptr(), z.data_ptr(), ws.data_ptr(), s.cuda_stream)
+    y.zero_()
+    z.zero_()
+    x.copy_(torch.tensor(rnd(shape, 17), device="cuda"))
+    g.replay()
+    torch.cuda.synchronize()
+    xn = x.cpu().numpy()
+    assert oracle.rel_l2(y.cpu().numpy(), oracle.port.dct_2d(xn)) <= 1e-12
+    assert oracle.rel_l2(z.cpu().numpy() * 4.0 / (shape[0] * shape[1]), xn) <= 1e-12
+
+
 # --------------------------------------- reference python surface (ported) --
 def test_reference_smoke_surface(cuda):
     """proj/tests/python/test_smoke.py, against this package's numpy surface."""
