@@ -106,14 +106,13 @@ cudaError_t launch_col_one(dim3 grid, cudaStream_t st, const CUtensorMap& map, c
   const size_t smem = ((((tile + 127) & ~size_t(127)) + tile / 2 + 127) & ~size_t(127)) + 16;
   cudaError_t e = prep_smem(k, smem);
   if (e != cudaSuccess) return e;
-  static int resident = 0;
-  if (!resident) {
+  static const int resident = [&] {  // thread-safe one-time query (same on every B200)
     int dev = 0, sms = 0, per = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, NT, smem);
-    resident = sms * (per > 0 ? per : 1);
-  }
+    return sms * (per > 0 ? per : 1);
+  }();
   ColArgs b = a;
   b.nbands = static_cast<int>(grid.x);
   b.nplanes = static_cast<int>(grid.y);
@@ -166,14 +165,13 @@ cudaError_t launch_row2(dim3 grid, cudaStream_t st, const RowArgs& a, const TwSe
   using Geo = Row2Geom<T, M, MODE>;
   cudaError_t e = prep_smem(k, Geo::SMEM);
   if (e != cudaSuccess) return e;
-  static int resident = 0;
-  if (!resident) {
+  static const int resident = [&] {  // thread-safe one-time query (same on every B200)
     int dev = 0, sms = 0, per = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, Geo::CTA, Geo::SMEM);
-    resident = sms * (per > 0 ? per : 1);
-  }
+    return sms * (per > 0 ? per : 1);
+  }();
   const int nitems = static_cast<int>(grid.x * grid.y);
   // MODE 0: persistent, at most one CTA per two items so both groups work;
   // MODE 2: persistent, one item at a time per CTA; MODE 1: one CTA per item

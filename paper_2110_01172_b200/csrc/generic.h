@@ -29,6 +29,10 @@ struct GenericJob {
 // pow2 M >= 2n - 1 when n's largest prime factor exceeds 64 and M <= 8192.
 int bluestein_len(int n);
 
+// Opt a kernel in to `smem` bytes of dynamic shared memory on the current
+// device (cached per device and kernel; plan.cu).
+cudaError_t prep_smem_ptr(const void* kernel, size_t smem);
+
 // Workspace: 2 * numel * batch * sizeof(double2) bytes.
 template <typename T>
 cudaError_t generic_run(const GenericJob& job, const void* in, void* out, void* ws, cudaStream_t st);

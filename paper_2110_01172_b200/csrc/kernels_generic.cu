@@ -914,10 +914,9 @@ cudaError_t g2_launch_cfg(G2Args a, cudaStream_t st) {
   int nt = (total + FPT - 1) / FPT;
   nt = std::min(C::NT, std::max(64, (nt + 31) / 32 * 32));
   const size_t smem = static_cast<size_t>(lines) * ld * sizeof(double2);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(g2_kernel<T, KIND, FPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = true;
+  if (smem > 48 * 1024) {
+    const cudaError_t pe = prep_smem_ptr(reinterpret_cast<const void*>(g2_kernel<T, KIND, FPT>), 200 * 1024);
+    if (pe != cudaSuccess) return pe;
   }
   const long long tiles = rows ? (a.batch * a.n1 + a.lines - 1) / a.lines : a.batch * ((a.h + lines - 1) / lines);
   // grid.x limit 2^31-1: batches beyond it are not reachable at these extents
@@ -985,11 +984,7 @@ cudaError_t generic_run(const GenericJob& job, const void* in, void* out, void* 
                (inner_ == 1 ? lpc * 2 <= outer_ : inner_ % (lpc * 2) == 0))
           lpc *= 2;
         const size_t smem = (static_cast<size_t>(lpc) * len + len) * sizeof(double2);
-        static bool attr_set = false;
-        if (!attr_set) {
-          cudaFuncSetAttribute(g_fft_axis_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, 140 * 1024);
-          attr_set = true;
-        }
+        if (smem > 48 * 1024) prep_smem_ptr(reinterpret_cast<const void*>(g_fft_axis_smem), 140 * 1024);
         const long long tiles = inner_ > 1 ? outer_ * (inner_ / lpc) : (outer_ + lpc - 1) / lpc;
         g_fft_axis_smem<<<static_cast<unsigned>(tiles), nt, smem, st>>>(src, dst, outer_, len, inner_,
                                                                             job.circle[a], ts, inverse,

@@ -68,15 +68,19 @@ class DeviceGuard {
 
 }  // namespace
 
+// The attribute is per device: cache grants by (device, kernel).
 cudaError_t sdctb::prep_smem_ptr(const void* kernel, size_t smem) {
   static std::mutex mu;
-  static std::unordered_map<const void*, size_t> granted;
+  static std::unordered_map<const void*, size_t> granted[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
   std::lock_guard<std::mutex> lock(mu);
-  auto it = granted.find(kernel);
-  if (it != granted.end() && it->second >= smem) return cudaSuccess;
+  auto& g = granted[dev & 63];
+  auto it = g.find(kernel);
+  if (it != g.end() && it->second >= smem) return cudaSuccess;
   cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
-  if (e == cudaSuccess) granted[kernel] = smem;
+  if (e == cudaSuccess) g[kernel] = smem;
   return e;
 }
 
