@@ -95,7 +95,7 @@ def build(verbose: bool = False, jobs: int | None = None) -> str:
     exe = os.path.join(LIB, "api_smoke")
     if os.path.exists(src) and (not os.path.exists(exe) or os.path.getmtime(exe) < max(
             os.path.getmtime(src), os.path.getmtime(LIBSO), hdr_time)):
-        _run(["g++"] + CXXFLAGS + [src, "-o", exe, "-L", LIB, "-lsdct_b200", "-Wl,-rpath,$ORIGIN"])
+        _run(["g++"] + CXXFLAGS + [src, "-o", exe, "-L", LIB, "-lsdct_b200", "-pthread", "-Wl,-rpath,$ORIGIN"])
     return LIBSO
 
 

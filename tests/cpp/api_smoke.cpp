@@ -3,9 +3,12 @@
 // force_demo_fields, StageCounters, the exception types) compiled against
 // include/sdct and linked with libsdct_b200.so instead of sdct_core.
 // Prints one line per check; exit code 0 when every check passes.
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <random>
+#include <thread>
+#include <vector>
 
 #include "sdct/dct2d.hpp"
 #include "sdct/errors.hpp"
@@ -84,6 +87,33 @@ int main() {
     double fm = 0.0;
     for (std::size_t i = 0; i < f.xi1.size(); ++i) fm = std::fmax(fm, std::fabs(f.xi1[i]) + std::fabs(f.xi2[i]));
     check(fm < 1e-9, "force fields of a constant density", fm);
+
+    // concurrent host calls (the reference's calls are reentrant):
+    // four threads sharing one plan and four with their own plans, fast and
+    // generic shapes, agree bit for bit with serial results
+    {
+      const sdct::RealTensor xa = random_tensor(sdct::Shape{512, 256}, 21);
+      const sdct::RealTensor xb = random_tensor(sdct::Shape{300, 200}, 22);
+      const sdct::Plan2d shared(512, 256);
+      const sdct::RealTensor ya = sdct::dct_2d(xa, shared);
+      const sdct::RealTensor yb = sdct::idct_2d(xb, sdct::Plan2d(300, 200));
+      std::atomic<int> bad{0};
+      std::vector<std::thread> ts;
+      for (int i = 0; i < 8; ++i)
+        ts.emplace_back([&, i] {
+          for (int r = 0; r < 5; ++r) {
+            if (i < 4) {
+              const sdct::RealTensor o = sdct::dct_2d(xa, shared);
+              if (o.storage() != ya.storage()) ++bad;
+            } else {
+              const sdct::RealTensor o = sdct::idct_2d(xb, sdct::Plan2d(300, 200));
+              if (o.storage() != yb.storage()) ++bad;
+            }
+          }
+        });
+      for (auto& th : ts) th.join();
+      check(bad.load() == 0, "8 threads x 5 calls (shared + private plans) match serial", bad.load());
+    }
 
     // errors keep the reference's types (proj/include/sdct/errors.hpp:11-33)
     bool threw = false;
