@@ -129,6 +129,28 @@ def test_generic_2d_pipeline_vs_oracle(cuda, dtype, kind):
 
 
 @pytest.mark.parametrize("dtype", ["float64", "float32"])
+def test_random_shapes_sweep(cuda, dtype):
+    # seeded sweep over random extents 1..300 (powers of two, odd, prime,
+    # degenerate 1/2) and every 2D kind, plus a random batch: fast and generic
+    # paths against the oracle
+    rng = np.random.default_rng(2024)
+    for i in range(24):
+        n1, n2 = (int(v) for v in rng.integers(1, 301, 2))
+        if i % 6 == 0:
+            n1 = 1 << int(rng.integers(1, 9))
+        if i % 8 == 1:
+            n2 = int(rng.choice([1, 2, 127, 251, 256]))
+        x = rnd((n1, n2), 500 + i, dtype)
+        for kind in KINDS_2D:
+            err = oracle.rel_l2(run_capi(kind, x, dtype), getattr(oracle.port, kind)(x))
+            assert err <= TOL[dtype], (kind, (n1, n2), dtype, err)
+    x = rnd((5, 37, 64), 599, dtype)
+    got = run_capi("dct_2d", x, dtype, batch_shape=(5,))
+    want = np.stack([oracle.port.dct_2d(x[b]) for b in range(5)])
+    assert oracle.rel_l2(got, want) <= TOL[dtype]
+
+
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
 def test_generic_2d_round_trip_large(cuda, dtype):
     # size-independent property at a large non-power-of-two shape:
     # idct_2d(dct_2d(x)) = N1 N2 / 4 x (proj/tests/test_dct2d.cpp:160-172)
