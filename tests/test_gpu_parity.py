@@ -618,7 +618,8 @@ def test_cpp_api_program(cuda):
     assert os.path.exists(exe), "tests/cpp/api_smoke.cpp not built (run __graft_entry__.build())"
     r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0, r.stdout + r.stderr
-    assert r.stdout.count("PASS") == 7, r.stdout
+    # one line per check of tests/cpp/api_smoke.cpp (incl. the 8-thread reentrancy check)
+    assert "FAIL" not in r.stdout and r.stdout.count("PASS") == 8, r.stdout
 
 
 def test_orientation_and_threads_do_not_change_results(cuda):
