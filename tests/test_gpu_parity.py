@@ -22,8 +22,11 @@ def _torch():
     return torch
 
 
-def run_capi(kind, x, dtype="float64", batch_shape=()):
-    """Run one transform through the C ABI on device memory; returns float64 numpy."""
+def run_capi(kind, x, dtype="float64", batch_shape=(), poison=False):
+    """Run one transform through the C ABI on device memory; returns float64 numpy.
+    poison=True pre-fills the output with NaN and the workspace with 0xFF bytes
+    (a NaN pattern at both widths), so an element the kernels never write, or a
+    workspace slot read before it is written, shows up as a non-finite result."""
     torch = _torch()
     from paper_2110_01172_b200 import capi
 
@@ -33,8 +36,10 @@ def run_capi(kind, x, dtype="float64", batch_shape=()):
     core = xt.shape[xt.dim() - rank:]
     batch = int(np.prod(xt.shape[: xt.dim() - rank])) if xt.dim() > rank else 1
     plan = capi.Plan(core, batch=batch, dtype=capi.F64 if dtype == "float64" else capi.F32)
-    out = torch.empty_like(xt)
+    out = torch.full_like(xt, float("nan")) if poison else torch.empty_like(xt)
     ws = torch.empty(max(plan.workspace_bytes, 1), dtype=torch.uint8, device="cuda")
+    if poison:
+        ws.fill_(0xFF)
     plan.exec(kind, xt.data_ptr(), out.data_ptr(), ws.data_ptr(), torch.cuda.current_stream().cuda_stream)
     torch.cuda.synchronize()
     plan.close()
@@ -162,6 +167,27 @@ def test_generic_2d_round_trip_large(cuda, dtype):
     y = sd.idct_2d(sd.dct_2d(x)) * (4.0 / (3000 * 2000))
     err = (torch.linalg.norm((y - x).double()) / torch.linalg.norm(x.double())).item()
     assert err <= (1e-13 if dtype == "float64" else 1e-5), err
+
+
+# every output element written, no workspace read before it is written: the
+# column passes store through TMA (cp.async.bulk.tensor global<-shared), which
+# compute-sanitizer's initcheck cannot see, so coverage is proven by poisoning
+SHAPES_POISON = [(1, 1), (2, 8), (64, 128), (256, 256), (1024, 64), (8192, 4), (30, 45), (97, 2047), (1021, 127),
+                 (4, 8, 16), (32, 32, 32), (3, 4, 5), (4, 4, 8192)]
+
+
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+def test_outputs_fully_written_poisoned_buffers(cuda, dtype):
+    for i, shape in enumerate(SHAPES_POISON):
+        kinds = KINDS_2D if len(shape) == 2 else ["dct_3d", "idct_3d"]
+        for kind in kinds:
+            for batch in (1, 3):
+                x = rnd((batch,) + shape if batch > 1 else shape, 700 + i, dtype)
+                got = run_capi(kind, x, dtype, batch_shape=(batch,) if batch > 1 else (), poison=True)
+                assert np.isfinite(got).all(), (kind, shape, batch, dtype)
+                xs = x if batch > 1 else x[None]
+                want = np.stack([getattr(oracle.port, kind)(xs[b]) for b in range(batch)]).reshape(got.shape)
+                assert oracle.rel_l2(got, want) <= TOL[dtype], (kind, shape, batch, dtype)
 
 
 SHAPES_3D = [(2, 2, 8), (4, 8, 16), (16, 4, 8), (8, 8, 64), (32, 32, 32), (3, 4, 5), (2, 6, 9), (64, 16, 16),
