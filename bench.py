@@ -207,15 +207,29 @@ def cpu_reference_rate(w, budget_s: float, max_steps: int | None = None):
     n = max(1, int(budget_s / max(t_u, 1e-3)))
     if max_steps is not None:
         n = min(n, max_steps)
-    t0 = time.perf_counter()
-    for _ in range(n):
-        unit()
-    dt = (time.perf_counter() - t0) / n
+    if kind == "reference" and w["mode"] in ("chain", "fan", "force"):
+        # plans and input tensors built once outside the clock; only the
+        # transform calls are timed (inside the reference library)
+        if w["mode"] == "force":
+            _, dt = oracle.ref.force_timed(x, threads=0, reps=n)
+        else:
+            dt, y = 0.0, x
+            for k in kinds:
+                out, s = oracle.ref.run_timed(k, y if w["mode"] == "chain" else x, threads=0, reps=n)
+                dt += s
+                y = out
+        timing = "prebuilt plans, transform calls timed inside the library"
+    else:
+        t0 = time.perf_counter()
+        for _ in range(n):
+            unit()
+        dt = (time.perf_counter() - t0) / n
+        timing = "whole calls timed (plan built per call)" if kind == "reference" else "C restatement, 1 thread"
     bytes_unit = 2.0 * _numel(dims) * 8 * len(kinds)
     what = ("force_demo_fields" if w["mode"] == "force" else
             "dct_2d, threshold at the median |b|, idct_2d, 4/(N1 N2)" if w["mode"] == "compress" else
             " then ".join(kinds) if w["mode"] == "chain" else " + ".join(kinds))
-    sample = (f"{n} x ({what}) of one {'x'.join(map(str, dims))} fp64 image on the host, prebuilt plans, "
+    sample = (f"{n} x ({what}) of one {'x'.join(map(str, dims))} fp64 image on the host, {timing}, "
               f"threads=0 ({dt * 1e3:.1f} ms each)")
     if w.get("sharded"):
         sample += f"; the {w['batch']}-image batch is {w['batch']} such units (rate is per byte, batch-independent)"
@@ -275,6 +289,15 @@ def cufft_times(x, dims, batch, stream, reps):
 
 
 # ---------------------------------------------------------------------------
+def job_config(args, w, world: int) -> dict:
+    """The workload description both arms print (identical dicts)."""
+    dtype = args.dtype or w["dtype"]
+    return {"workload": w["desc"].format(dt=dtype), "name": args.workload,
+            "global_batch": w["batch"] if w.get("sharded") else world * w["batch"],
+            "parallelism": (f"batch sharded x{world} (contiguous shards, no collective)" if w.get("sharded")
+                            else f"replicas x{world} (independent images, no collective)")}
+
+
 def run_reference(args, rank: int, world: int):
     if rank != 0:
         return
@@ -284,11 +307,12 @@ def run_reference(args, rank: int, world: int):
     cores, quota = _cores()
     line = {
         "impl": "reference", "metric": METRIC, "value": round(rate, 4), "unit": UNIT,
-        "n_gpus": args.gpus, "steps": steps, "warmup": 1, "ms_per_step": round(dt * 1e3, 3),
+        "n_gpus": world, "steps": steps, "warmup": args.requested_warmup, "ms_per_step": round(dt * 1e3, 3),
         "higher_is_better": True, "scaling": "strong" if w.get("sharded") else "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic uniform(-1,1)",
-        "config": {"workload": w["desc"].format(dt="fp64 (reference is fp64-only)"),
-                   "requested_steps": args.steps, "requested_warmup": args.warmup},
+        "config": job_config(args, w, world),
+        "measurement": {"requested_steps": args.steps, "requested_warmup": args.requested_warmup,
+                        "note": "reference is fp64-only; CPU arm runs on rank 0 (host cores), one warm-up unit"},
         "cpu_baseline": {"value": round(rate, 4), "unit": UNIT, "cores": cores, "kind": kind,
                          "cgroup_cpu_quota": quota, "sample": sample},
         "e2e": {"value": round(rate, 4), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -297,7 +321,7 @@ def run_reference(args, rank: int, world: int):
 
 
 # ---------------------------------------------------------------------------
-def run_ours(args, rank: int, world: int, local_rank: int):
+def run_ours(args, rank: int, world: int, local_rank: int, backend: str | None = None):
     import torch
     import torch.distributed as dist
 
@@ -367,6 +391,13 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         if world > 1:
             dist.barrier()
 
+    def max_over_ranks(v: float) -> float:
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev if backend == "nccl" else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
     # parity spot check of this rank's own data
     step(0)
     torch.cuda.synchronize()
@@ -385,6 +416,19 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         w1, w2 = oracle.port.force_demo_fields(xs[0][0].double().cpu().numpy())
         parity["xi1_rel_l2_vs_oracle"] = float(oracle.rel_l2(outs[0][0][0].double().cpu().numpy(), w1))
         parity["xi2_rel_l2_vs_oracle"] = float(oracle.rel_l2(outs[0][1][0].double().cpu().numpy(), w2))
+    elif w.get("sharded"):
+        # every rank checks the first and last image of its own shard against
+        # the C oracle (the shard-boundary images of BASELINE.md §4); the line
+        # reports the worst over ranks
+        import oracle
+
+        errs = []
+        for bi in sorted({0, B - 1}):
+            x0 = xs[0][bi].double().cpu().numpy()
+            errs.append(oracle.rel_l2(outs[0][0][bi].double().cpu().numpy(), oracle.port.dct_2d(x0)))
+        parity["shard_images_checked"] = [lo, lo + B - 1]
+        parity["dct_2d_rel_l2_vs_oracle_max_over_ranks"] = max_over_ranks(max(errs))
+        parity["images_checked_total"] = len({0, B - 1}) * world
     elif rank == 0:
         import oracle
 
@@ -418,10 +462,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     barrier()
     ms = e0.elapsed_time(e1)
     clk = clocks.stop()
-    if world > 1:
-        t = torch.tensor([ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = max_over_ranks(ms)
     ms_per_step = ms / args.steps
     value = job_bytes_step * args.steps / (ms / 1e3) / 1e9
 
@@ -487,7 +528,9 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     roofline = {"bound": "hbm", "achieved": round(dom["gbs"], 2), "peak": peak, "unit": "GB/s",
                 "frac": round(dom["gbs"] / peak, 4), "traffic": traffic, "kernel": dom["kernel"],
                 "peak_kind": peak_kind, "per_launch_bytes": bytes_transform,
-                "timing": f"live: {n_inst} steps of the timed loop with an event between kernels",
+                "timing": (f"live: {n_inst} steps of the timed loop with an event between kernels (the events "
+                           "stop programmatic dependent launch from overlapping kernel tails, so the per-kernel "
+                           "times sum to more than ms_per_step)"),
                 "all_kernels": [{k2: (round(v, 4) if isinstance(v, float) else v) for k2, v in k_.items()}
                                 for k_ in kernels],
                 "cold_l2_flushed": cold,
@@ -596,11 +639,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         b.record(stream)
         n_out = len(chains)
     torch.cuda.synchronize()
-    e_ms = a.elapsed_time(b)
-    if world > 1:
-        t = torch.tensor([e_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e_ms = float(t.item())
+    e_ms = max_over_ranks(a.elapsed_time(b))
     e2e_val = job_bytes_step * e_steps / (e_ms / 1e3) / 1e9
     if w["mode"] == "chain" and w["kinds"] == ["dct_2d", "idct_2d"]:
         x0 = x_pin[0].to(torch.float64)
@@ -612,23 +651,23 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     if rank == 0 and world == 1 and not args.no_cpu:
         rate, dtr, n_units, kind, sample = cpu_reference_rate(w, budget_s=args.cpu_budget)
         cores, quota = _cores()
-        cpu = {"value": round(rate, 4), "unit": UNIT, "cores": cores, "kind": kind, "cgroup_cpu_quota": quota,
-               "sample": sample}
+        cpu = {"value": round(rate, 4), "unit": UNIT, "cores": cores if kind == "reference" else 1, "kind": kind,
+               "cgroup_cpu_quota": quota, "sample": sample}
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world,
-            "steps": args.steps, "warmup": warm_done, "ms_per_step": round(ms_per_step, 5),
+            "steps": args.steps, "warmup": args.requested_warmup, "ms_per_step": round(ms_per_step, 5),
             "higher_is_better": True, "scaling": "strong" if w.get("sharded") else "weak", "vs_baseline": None,
             "dtype": "f64" if dt == torch.float64 else "f32",
             "data": "synthetic uniform(-1,1), device-resident",
-            "config": {"workload": w["desc"].format(dt=dtype), "name": args.workload,
-                       "global_batch": w["batch"] if w.get("sharded") else world * B,
-                       "parallelism": (f"batch sharded x{world} (contiguous shards, no collective)" if w.get("sharded")
-                                       else f"replicas x{world} (independent images, no collective)"),
-                       "l2": ("working set per step > 2x the 126 MB L2 (no flush needed)" if rot == 1 else
-                              f"inputs/outputs rotate over {rot} sets ({rot * set_bytes / 2**20:.0f} MB > 2x L2)"),
-                       "bytes_per_step_per_gpu": bytes_step},
+            "config": job_config(args, w, world),
+            "measurement": {"l2": ("working set per step > 2x the 126 MB L2 (no flush needed)" if rot == 1 else
+                                   f"inputs/outputs rotate over {rot} sets ({rot * set_bytes / 2**20:.0f} MB > 2x L2)"),
+                            "bytes_per_step_per_gpu": bytes_step, "warmup_steps_run": warm_done,
+                            "warmup_rule": f">= {args.warmup} untimed steps and >= 1 s of soak before timing",
+                            "ranks": world, "control_plane": backend or "none (1 rank)",
+                            "devices": torch.cuda.device_count()},
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": {"value": round(e2e_val, 3), "unit": UNIT,
@@ -649,6 +688,57 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         print(json.dumps(line), flush=True)
 
 
+def _free_port() -> int:
+    import socket
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def spawn_ranks(n: int) -> int:
+    """`python bench.py --gpus N` without torchrun: re-launch this script as N
+    ranks (one process per GPU, the torchrun environment contract) on
+    127.0.0.1 and wait for all of them. Rank 0 prints the JSON line."""
+    port = _free_port()
+    procs = []
+    for r in range(n):
+        env = dict(os.environ, RANK=str(r), LOCAL_RANK=str(r), WORLD_SIZE=str(n), LOCAL_WORLD_SIZE=str(n),
+                   MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        procs.append(subprocess.Popen([sys.executable, os.path.abspath(__file__)] + sys.argv[1:], env=env))
+    rc = 0
+    for p in procs:
+        rc = max(rc, p.wait())
+    return rc
+
+
+def dry_orchestration(args, rank: int, world: int):
+    """The multi-rank control plane of run_ours without the GPU work: gloo
+    process group, this rank's shard, barrier, max-over-ranks of a per-rank
+    'time', rank 0 prints one JSON line (tests/test_dist.py)."""
+    import torch
+    import torch.distributed as dist
+
+    w = WORKLOADS[args.workload]
+    if world > 1:
+        dist.init_process_group("gloo")
+    lo, b = _shard(w, world, rank)
+    t = torch.tensor([10.0 + rank, float(lo), float(lo + b)], dtype=torch.float64)
+    if world > 1:
+        dist.barrier()
+        got = [torch.zeros(3, dtype=torch.float64) for _ in range(world)]
+        dist.all_gather(got, t)
+        dist.destroy_process_group()
+    else:
+        got = [t]
+    if rank == 0:
+        print(json.dumps({"n_gpus": world, "config": job_config(args, w, world),
+                          "ms_max_over_ranks": max(float(g[0]) for g in got),
+                          "shards": [[int(g[1]), int(g[2])] for g in got]}), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -660,23 +750,46 @@ def main():
                     help="override the workload's dtype (c2 runs fp64 by default)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     ap.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of CPU baseline sampling")
+    ap.add_argument("--dry-orchestration", action="store_true",
+                    help="test hook: rank launch, shards and the max-over-ranks reduction only (gloo, no GPU)")
     args = ap.parse_args()
+    args.requested_warmup = args.warmup
     if args.warmup < 3:
         args.warmup = 3
+    launched = "WORLD_SIZE" in os.environ
+    if args.impl == "reference":
+        # the reference CPU arm runs on rank 0 only (other torchrun ranks exit 0)
+        world = int(os.environ.get("WORLD_SIZE", "1")) if launched else max(1, args.gpus)
+        run_reference(args, int(os.environ.get("RANK", "0")), world)
+        return
+    if not launched and args.gpus > 1:
+        sys.exit(spawn_ranks(args.gpus))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
-    if args.impl == "reference":
-        run_reference(args, rank, world)
+    if args.dry_orchestration:
+        dry_orchestration(args, rank, world)
         return
+    backend = None
     if world > 1:
         import torch
         import torch.distributed as dist
 
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        ndev = torch.cuda.device_count()
+        dev_index = local_rank % ndev
+        torch.cuda.set_device(dev_index)
+        # one rank per GPU: NCCL carries the barrier and the max-over-ranks
+        # timing reduction (there is no data-path collective). Ranks sharing a
+        # device (a 1-GPU test box) use gloo: NCCL rejects duplicate GPUs.
+        backend = "nccl" if ndev >= int(os.environ.get("LOCAL_WORLD_SIZE", world)) else "gloo"
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev_index))
+        else:
+            dist.init_process_group("gloo")
+    else:
+        dev_index = local_rank
     try:
-        run_ours(args, rank, world, local_rank)
+        run_ours(args, rank, world, dev_index, backend)
     finally:
         if world > 1:
             import torch.distributed as dist

@@ -46,6 +46,7 @@ class Plan2d {
   Orientation orientation_;
   std::vector<std::complex<double>> twiddle_a_, twiddle_b_;
   detail::PlanPtr plan_;
+  bool private_plan_ = false;  // detached from the plan cache by the corrupt hook
 };
 
 RealTensor dct_2d(const RealTensor& x, const Plan2d& plan, const ExecConfig& cfg = {},

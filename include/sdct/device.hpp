@@ -21,6 +21,8 @@ class DevicePlan {
   void run(int kind, const void* d_in, void* d_out, void* stream = nullptr,
            void* d_workspace = nullptr) const;
   std::size_t workspace_bytes() const;
+  /// Device memory the plan owns right now (sdct_plan_device_bytes).
+  std::size_t device_bytes() const;
   bool fast() const;
   sdct_plan_t handle() const { return plan_.get(); }
 

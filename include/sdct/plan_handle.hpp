@@ -21,9 +21,16 @@ struct PlanDeleter {
 };
 using PlanPtr = std::shared_ptr<sdct_plan_s>;
 
-/// Creates a device plan (fp64 unless dtype says otherwise); throws on error.
+/// Device plan for (dims, batch, dtype, orientation) on the current device,
+/// shared through an LRU cache bounded by entries and device bytes
+/// (SDCT_PLAN_CACHE_BYTES); throws on error.
 PlanPtr make_plan(const std::vector<std::int64_t>& dims, std::int64_t batch, int dtype,
                   int orientation);
+/// A fresh plan that no cache shares (fault injection mutates its tables).
+PlanPtr make_plan_uncached(const std::vector<std::int64_t>& dims, std::int64_t batch, int dtype,
+                           int orientation);
+/// Number of plans the cache currently holds.
+std::size_t plan_cache_entries();
 
 }  // namespace detail
 }  // namespace sdct

@@ -93,6 +93,10 @@ int sdct_plan_destroy(sdct_plan_t plan);
 int sdct_plan_orientation(sdct_plan_t plan, int* orientation);
 int sdct_plan_is_fast(sdct_plan_t plan, int* fast);
 int sdct_plan_workspace_size(sdct_plan_t plan, size_t* bytes);
+/* Device memory the plan currently owns (tables, and whatever it allocated on
+ * first use: its own workspace, host staging, pipeline lanes, scratch). Plan
+ * caches (C++ make_plan, Python plan_for) bound their footprint with it. */
+int sdct_plan_device_bytes(sdct_plan_t plan, size_t* bytes);
 
 /* Test-only fault injection: negates axis-1 twiddle b[index] (2D) exactly like
  * sdct::Plan2d::corrupt_twiddle_for_testing (proj/src/dct2d.cpp:312-317);

@@ -92,6 +92,13 @@ def _ref_lib():
                                        ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double),
                                        ctypes.c_uint, ctypes.c_int]
         lib.sdct_ref_force.restype = ctypes.c_int
+        D = ctypes.POINTER(ctypes.c_double)
+        lib.sdct_ref_run_timed.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_size_t), D, D,
+                                           ctypes.c_uint, ctypes.c_int, D]
+        lib.sdct_ref_run_timed.restype = ctypes.c_int
+        lib.sdct_ref_force_timed.argtypes = [ctypes.c_size_t, ctypes.c_size_t, D, D, D, ctypes.c_uint,
+                                             ctypes.c_int, D]
+        lib.sdct_ref_force_timed.restype = ctypes.c_int
         lib.sdct_ref_write_dctb.argtypes = [ctypes.c_char_p, ctypes.c_int, ctypes.POINTER(ctypes.c_size_t),
                                             ctypes.POINTER(ctypes.c_double)]
         lib.sdct_ref_write_dctb.restype = ctypes.c_int
@@ -211,6 +218,32 @@ class _Ref:
             msg = lib.sdct_ref_last_error().decode()
             raise ValueError(msg) if rc == 1 else RuntimeError(msg)
         return out
+
+    def run_timed(self, kind: str, x, threads: int = 0, reps: int = 1):
+        """(output, seconds per call): plan and input tensor built once outside
+        the clock, `reps` calls of the transform timed inside the reference."""
+        lib = _ref_lib()
+        x = _as64(x)
+        dims = (ctypes.c_size_t * x.ndim)(*x.shape)
+        out = np.empty_like(x)
+        sec = ctypes.c_double(0.0)
+        rc = lib.sdct_ref_run_timed(KINDS[kind], x.ndim, dims, _dp(x), _dp(out), threads, reps, ctypes.byref(sec))
+        if rc != 0:
+            msg = lib.sdct_ref_last_error().decode()
+            raise ValueError(msg) if rc == 1 else RuntimeError(msg)
+        return out, sec.value / reps
+
+    def force_timed(self, x, threads: int = 0, reps: int = 1):
+        """((xi1, xi2), seconds per call) of force_demo_fields, input built once."""
+        lib = _ref_lib()
+        x = _as64(x)
+        xi1, xi2 = np.empty_like(x), np.empty_like(x)
+        sec = ctypes.c_double(0.0)
+        rc = lib.sdct_ref_force_timed(x.shape[0], x.shape[1], _dp(x), _dp(xi1), _dp(xi2), threads, reps,
+                                      ctypes.byref(sec))
+        if rc != 0:
+            raise RuntimeError(lib.sdct_ref_last_error().decode())
+        return (xi1, xi2), sec.value / reps
 
     def force_demo_fields(self, x, threads: int = 0, reps: int = 1):
         lib = _ref_lib()

@@ -10,6 +10,7 @@
 // `reps` times so a caller can time the prebuilt-plan path; the output of the
 // last repetition is written to `out`.
 
+#include <chrono>
 #include <cstddef>
 #include <cstring>
 #include <exception>
@@ -144,6 +145,76 @@ int sdct_ref_read_dctb(const char* path, int* rank, std::size_t* dims, double* o
   } catch (const sdct::ShapeError& e) {
     g_err = e.what();
     return 1;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 2;
+  }
+}
+
+}  // extern "C"
+
+extern "C" {
+
+// Timed variants for bench.py's CPU arm: the plan is built once outside the
+// clock (as a prebuilt-plan caller would hold it), the input tensor is built
+// once, and only the `reps` transform calls are timed (steady_clock);
+// *seconds = their total. The output of the last call lands in `out`.
+int sdct_ref_run_timed(int kind, int rank, const std::size_t* dims, const double* in, double* out,
+                       unsigned threads, int reps, double* seconds) {
+  try {
+    sdct::ExecConfig cfg;
+    cfg.parallelism_degree = threads;
+    sdct::Shape shape(dims, dims + rank);
+    sdct::RealTensor x(shape, std::vector<double>(in, in + sdct::numel(shape)));
+    sdct::RealTensor y;
+    std::chrono::steady_clock::time_point t0;
+    if (kind == REF_DCT3 || kind == REF_IDCT3) {
+      if (rank != 3) throw sdct::ShapeError("3D kinds need rank 3");
+      sdct::Plan3d plan(dims[0], dims[1], dims[2]);
+      t0 = std::chrono::steady_clock::now();
+      for (int r = 0; r < reps; ++r)
+        y = kind == REF_DCT3 ? sdct::dct_3d(x, plan, cfg) : sdct::idct_3d(x, plan, cfg);
+    } else {
+      if (rank != 2) throw sdct::ShapeError("2D kinds need rank 2");
+      sdct::Plan2d plan(dims[0], dims[1]);
+      t0 = std::chrono::steady_clock::now();
+      for (int r = 0; r < reps; ++r) {
+        switch (kind) {
+          case REF_DCT2: y = sdct::dct_2d(x, plan, cfg); break;
+          case REF_IDCT2: y = sdct::idct_2d(x, plan, cfg); break;
+          case REF_IDCT_IDXST: y = sdct::idct_idxst_2d(x, plan, cfg); break;
+          case REF_IDXST_IDCT: y = sdct::idxst_idct_2d(x, plan, cfg); break;
+          case REF_DCT2_ROWCOL: y = sdct::dct_2d_rowcol(x, plan, cfg); break;
+          default: throw sdct::ShapeError("unknown kind");
+        }
+      }
+    }
+    *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    std::memcpy(out, y.data(), y.size() * sizeof(double));
+    return 0;
+  } catch (const sdct::ShapeError& e) {
+    g_err = e.what();
+    return 1;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 2;
+  }
+}
+
+// sdct::force_demo_fields timed the same way (input built once, calls timed).
+int sdct_ref_force_timed(std::size_t n1, std::size_t n2, const double* in, double* xi1, double* xi2,
+                         unsigned threads, int reps, double* seconds) {
+  try {
+    sdct::ExecConfig cfg;
+    cfg.parallelism_degree = threads;
+    sdct::RealTensor x(sdct::Shape{n1, n2}, std::vector<double>(in, in + n1 * n2));
+    sdct::ForceFields f;
+    const auto t0 = std::chrono::steady_clock::now();
+    for (int r = 0; r < reps; ++r) f = sdct::force_demo_fields(x, cfg);
+    *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    std::memcpy(xi1, f.xi1.data(), n1 * n2 * sizeof(double));
+    std::memcpy(xi2, f.xi2.data(), n1 * n2 * sizeof(double));
+    return 0;
   } catch (const std::exception& e) {
     g_err = e.what();
     return 2;

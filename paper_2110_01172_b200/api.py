@@ -3,7 +3,9 @@ device path for torch CUDA tensors (cached ``_sdct.Plan`` per shape/dtype/device
 workspace from torch's caching allocator on the current stream)."""
 from __future__ import annotations
 
+import os
 import threading
+from collections import OrderedDict
 
 from . import _sdct
 
@@ -15,12 +17,16 @@ _KIND = {
 }
 _RANK = {"dct_1d": 1, "idct_1d": 1, "idxst_1d": 1, "dct_3d": 3, "idct_3d": 3}
 
-_plans: dict = {}
+_plans: "OrderedDict" = OrderedDict()
 _lock = threading.Lock()
+PLAN_CACHE_MAX = 32
+PLAN_CACHE_BYTES = int(os.environ.get("SDCT_PLAN_CACHE_BYTES", str(2 << 30)))
 
 
 def plan_for(dims, batch: int = 1, dtype: str = "float64", device: int = 0):
-    """Cached device plan for ``batch`` items of shape ``dims``."""
+    """Cached device plan for ``batch`` items of shape ``dims`` (LRU; bounded
+    by PLAN_CACHE_MAX entries and PLAN_CACHE_BYTES of device memory the cached
+    plans own — tables plus whatever they allocated on first use)."""
     key = (tuple(int(d) for d in dims), int(batch), dtype, int(device))
     with _lock:
         p = _plans.get(key)
@@ -30,6 +36,11 @@ def plan_for(dims, batch: int = 1, dtype: str = "float64", device: int = 0):
             with torch.cuda.device(device):
                 p = _sdct.Plan(list(key[0]), key[1], dtype)
             _plans[key] = p
+        _plans.move_to_end(key)
+        total = sum(q.device_bytes for q in _plans.values())
+        while len(_plans) > 1 and (len(_plans) > PLAN_CACHE_MAX or total > PLAN_CACHE_BYTES):
+            _, old = _plans.popitem(last=False)
+            total -= old.device_bytes
         return p
 
 
@@ -47,6 +58,8 @@ def _device_call(name: str, x):
     if x.dtype not in (torch.float32, torch.float64):
         raise ValueError(f"{name}: dtype must be float32 or float64, got {x.dtype}")
     x = x.contiguous()
+    if x.data_ptr() % 16:
+        x = x.clone()  # the kernels move rows with 16-B bulk copies / TMA
     core = tuple(x.shape[x.dim() - rank:])
     batch = 1
     for d in x.shape[: x.dim() - rank]:
@@ -156,6 +169,8 @@ def force_demo_fields(density, threads: int = 0):
     if x.dtype not in (torch.float32, torch.float64):
         raise ValueError(f"force_demo_fields: dtype must be float32 or float64, got {x.dtype}")
     x = x.contiguous()
+    if x.data_ptr() % 16:
+        x = x.clone()
     core = tuple(x.shape[-2:])
     batch = 1
     for d in x.shape[:-2]:
@@ -253,6 +268,8 @@ def compress(x, epsilon: float):
     if t.dtype not in (torch.float32, torch.float64):
         raise ValueError(f"compress: dtype must be float32 or float64, got {t.dtype}")
     t = t.contiguous()
+    if t.data_ptr() % 16:
+        t = t.clone()
     dt = "float32" if t.dtype == torch.float32 else "float64"
     dev = t.device.index if t.device.index is not None else torch.cuda.current_device()
     plan = plan_for(tuple(t.shape), 1, dt, dev)

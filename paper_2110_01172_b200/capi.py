@@ -30,6 +30,7 @@ SIGNATURES = [
     ("sdct_plan_orientation", ctypes.c_int, [_VP, ctypes.POINTER(ctypes.c_int)]),
     ("sdct_plan_is_fast", ctypes.c_int, [_VP, ctypes.POINTER(ctypes.c_int)]),
     ("sdct_plan_workspace_size", ctypes.c_int, [_VP, ctypes.POINTER(ctypes.c_size_t)]),
+    ("sdct_plan_device_bytes", ctypes.c_int, [_VP, ctypes.POINTER(ctypes.c_size_t)]),
     ("sdct_plan_corrupt_twiddle", ctypes.c_int, [_VP, ctypes.c_int64]),
     ("sdct_exec", ctypes.c_int, [_VP, ctypes.c_int, _VP, _VP, _VP, _VP]),
     ("sdct_exec_host", ctypes.c_int, [_VP, ctypes.c_int, _VP, _VP, _VP]),

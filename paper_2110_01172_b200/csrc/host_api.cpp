@@ -3,7 +3,12 @@
 // conditions, proj/src/dct2d.cpp:12-38, transforms_ext.cpp:14-35), then hands
 // the host tensor to sdct_exec_host, which stages it through the plan's device
 // buffers. No arithmetic happens here: there is no CPU fallback.
+#include <cuda_runtime.h>
+
 #include <cmath>
+#include <cstdlib>
+#include <list>
+#include <mutex>
 #include <numbers>
 #include <string>
 
@@ -52,10 +57,92 @@ void check(int status) {
   }
 }
 
-PlanPtr make_plan(const std::vector<std::int64_t>& dims, std::int64_t batch, int dtype, int orientation) {
+PlanPtr make_plan_uncached(const std::vector<std::int64_t>& dims, std::int64_t batch, int dtype,
+                           int orientation) {
   sdct_plan_t p = nullptr;
   check(sdct_plan_create(&p, static_cast<int>(dims.size()), dims.data(), batch, dtype, orientation, -1));
   return PlanPtr(p, PlanDeleter{});
+}
+
+namespace {
+
+// Device-plan cache. The reference rebuilds its plan on every convenience
+// call and every Python call (proj/src/dct2d.cpp:389-393, module.cpp); on the
+// GPU a plan means device tables and lazily allocated buffers, so plans are
+// shared per (shape, batch, dtype, orientation, device). LRU, bounded by
+// entry count and by the device bytes the cached plans own
+// (sdct_plan_device_bytes; SDCT_PLAN_CACHE_BYTES, default 2 GiB). Eviction
+// drops only the cache's reference: plans held by Plan2d/... objects live on.
+struct CacheKey {
+  std::vector<std::int64_t> dims;
+  std::int64_t batch;
+  int dtype, orientation, device;
+  bool operator==(const CacheKey& o) const {
+    return dims == o.dims && batch == o.batch && dtype == o.dtype && orientation == o.orientation &&
+           device == o.device;
+  }
+};
+
+struct PlanCache {
+  std::mutex mu;
+  std::list<std::pair<CacheKey, PlanPtr>> lru;  // front = most recent
+  static constexpr std::size_t kMaxEntries = 32;
+  std::size_t cap_bytes() const {
+    static const std::size_t cap = [] {
+      const char* v = std::getenv("SDCT_PLAN_CACHE_BYTES");
+      return v ? static_cast<std::size_t>(std::strtoull(v, nullptr, 10)) : (std::size_t(2) << 30);
+    }();
+    return cap;
+  }
+  void trim() {  // caller holds mu
+    auto bytes = [](const PlanPtr& p) {
+      std::size_t b = 0;
+      sdct_plan_device_bytes(p.get(), &b);
+      return b;
+    };
+    std::size_t total = 0;
+    for (const auto& e : lru) total += bytes(e.second);
+    while (lru.size() > 1 && (lru.size() > kMaxEntries || total > cap_bytes())) {
+      total -= std::min(total, bytes(lru.back().second));
+      lru.pop_back();
+    }
+  }
+};
+
+PlanCache& plan_cache() {
+  static PlanCache* c = new PlanCache;  // never destroyed: plans may outlive static teardown order
+  return *c;
+}
+
+}  // namespace
+
+PlanPtr make_plan(const std::vector<std::int64_t>& dims, std::int64_t batch, int dtype, int orientation) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  CacheKey key{dims, batch, dtype, orientation, dev};
+  PlanCache& c = plan_cache();
+  {
+    std::lock_guard<std::mutex> lock(c.mu);
+    for (auto it = c.lru.begin(); it != c.lru.end(); ++it) {
+      if (it->first == key) {
+        c.lru.splice(c.lru.begin(), c.lru, it);
+        PlanPtr p = c.lru.front().second;
+        c.trim();
+        return p;
+      }
+    }
+  }
+  PlanPtr p = make_plan_uncached(dims, batch, dtype, orientation);
+  std::lock_guard<std::mutex> lock(c.mu);
+  c.lru.emplace_front(key, p);
+  c.trim();
+  return p;
+}
+
+std::size_t plan_cache_entries() {
+  PlanCache& c = plan_cache();
+  std::lock_guard<std::mutex> lock(c.mu);
+  return c.lru.size();
 }
 
 RealTensor run_host(sdct_plan_t plan, int kind, const RealTensor& x, StageCounters* counters) {
@@ -176,6 +263,13 @@ void Plan2d::corrupt_twiddle_for_testing(std::size_t index) {
   if (index >= twiddle_b_.size())
     throw BoundsError("corrupt_twiddle_for_testing: index " + std::to_string(index) +
                       " out of range for table of size " + std::to_string(twiddle_b_.size()));
+  // the device plan may be shared through the plan cache: corrupt a private copy
+  if (!private_plan_) {
+    plan_ = detail::make_plan_uncached({static_cast<std::int64_t>(n1_), static_cast<std::int64_t>(n2_)}, 1, SDCT_F64,
+                                       orientation_ == Orientation::Direct ? SDCT_ORIENT_DIRECT
+                                                                           : SDCT_ORIENT_TRANSPOSED);
+    private_plan_ = true;  // first corruption: nothing to replay
+  }
   detail::check(sdct_plan_corrupt_twiddle(plan_.get(), static_cast<int64_t>(index)));
   twiddle_b_[index] = -twiddle_b_[index];
 }
@@ -266,6 +360,12 @@ void DevicePlan::run(int kind, const void* d_in, void* d_out, void* stream, void
 std::size_t DevicePlan::workspace_bytes() const {
   std::size_t b = 0;
   detail::check(sdct_plan_workspace_size(plan_.get(), &b));
+  return b;
+}
+
+std::size_t DevicePlan::device_bytes() const {
+  std::size_t b = 0;
+  detail::check(sdct_plan_device_bytes(plan_.get(), &b));
   return b;
 }
 

@@ -97,7 +97,7 @@ struct RowArgs {
   const void* fb;                  // factor tables of tb / tu: e^{-i theta q} = hi[q >> fs] lo[q & (2^fs-1)]
   const void* fu;
   int fs;
-  int bad_q;                       // corrupt_twiddle_for_testing: b(bad_q) negated (-1: none)
+  const unsigned char* badq;       // corrupt_twiddle_for_testing: b(q) negated where badq[q] != 0 (null: none)
   int weight;                      // 2D inverse input: 0 none, 1/2 force-field weight w1/w2, 3 compression threshold
   double thr_eps, thr_scale;       // weight 3: zero |b| < thr_eps, scale the rest
   unsigned long long* thr_count;   // weight 3: zeroed coefficients (device counter, may be null)

@@ -283,8 +283,9 @@ __global__ void __launch_bounds__(Row2Geom<T, M, MODE>::CTA, Row2Geom<T, M, MODE
           // needs none: b(M-q) = e^{-i pi/4} conj b(q), W^{M-q} = -conj W^q
           const V bq = fac_lookup(fb, k2, a.fs), w = fac_lookup(fu, k2, a.fs);
           const V bm = mirror_b(bq);
-          item(k2, Z0a, Z0b, Z1a, Z1b, k2 == a.bad_q ? mk(-bq.x, -bq.y) : bq, w);
-          if (2 * k2 != M) item(M - k2, Z0b, Z0a, Z1b, Z1a, M - k2 == a.bad_q ? mk(-bm.x, -bm.y) : bm, mk(-w.x, w.y));
+          item(k2, Z0a, Z0b, Z1a, Z1b, (a.badq && a.badq[k2]) ? mk(-bq.x, -bq.y) : bq, w);
+          if (2 * k2 != M)
+            item(M - k2, Z0b, Z0a, Z1b, Z1a, (a.badq && a.badq[M - k2]) ? mk(-bm.x, -bm.y) : bm, mk(-w.x, w.y));
         }
       }
     } else {
@@ -398,8 +399,8 @@ __global__ void __launch_bounds__(Row2Geom<T, M, MODE>::CTA, Row2Geom<T, M, MODE
       auto pack_item = [&](int kk, const T* o, int sa, int sb) {
         V A0, A1, B0, B1;  // X'(line, k), X'(line, M-k)
         V bk = fac_lookup(fb, kk, a.fs), bm = mirror_b(bk);
-        if (kk == a.bad_q) bk = mk(-bk.x, -bk.y);
-        if (M - kk == a.bad_q) bm = mk(-bm.x, -bm.y);
+        if (a.badq && a.badq[kk]) bk = mk(-bk.x, -bk.y);
+        if (a.badq && a.badq[M - kk]) bm = mk(-bm.x, -bm.y);
         xp(o, cconj(bk), A0, A1);
         xp(o + 4, cconj(bm), B0, B1);
         // partner line of each row (-k1): swap for pairs, self for P == 0

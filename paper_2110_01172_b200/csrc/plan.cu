@@ -111,7 +111,11 @@ struct sdct_plan_s {
   void* fb = nullptr;    // dtype factor tables of tb and tu over q <= M (see RowArgs::fb)
   void* fu = nullptr;
   int fs = 0;
-  int bad_q = -1;        // corrupt_twiddle_for_testing index (row kernels), -1 = none  // intermediate storage row of frequency k: axis 0, axis 1 (3D)
+  // corrupt_twiddle_for_testing: host toggle map of negated b entries and its
+  // device copy (the 2D row kernels form b(q) from factor tables, so they
+  // negate b(q) where the map is set); null until the hook is first used
+  std::vector<unsigned char> badq_host;
+  unsigned char* badq = nullptr;
   double2* gq[3] = {nullptr, nullptr, nullptr};  // generic fp64 quarter-wave tables
   double2* gc[3] = {nullptr, nullptr, nullptr};  // generic fp64 circle tables
   int bm[3] = {0, 0, 0};                          // Bluestein length per axis (0 = none)
@@ -141,6 +145,7 @@ struct sdct_plan_s {
     return 2 * static_cast<size_t>(batch) * static_cast<size_t>(numel) * sizeof(double2);
   }
   size_t item_bytes() const { return static_cast<size_t>(numel) * elem(); }
+  size_t table_bytes = 0;  // the one table allocation
 };
 
 namespace {
@@ -379,6 +384,7 @@ int build_plan(sdct_plan_s* p) {
   }
   cudaError_t e = cudaMalloc(&p->tables, blob.size());
   if (e != cudaSuccess) return cuda_fail(e, "allocating plan tables");
+  p->table_bytes = blob.size();
   e = cudaMemcpy(p->tables, blob.data(), blob.size(), cudaMemcpyHostToDevice);
   if (e != cudaSuccess) return cuda_fail(e, "uploading plan tables");
   unsigned char* base = static_cast<unsigned char*>(p->tables);
@@ -411,8 +417,8 @@ int build_plan(sdct_plan_s* p) {
     }
   }
   p->b_offset_gen = r >= 2 ? off_gq[1] : off_gq[0];
-  e = cudaMalloc(&p->ws, p->ws_bytes);
-  if (e != cudaSuccess) return cuda_fail(e, "allocating plan workspace");
+  // the plan-owned workspace is allocated on first use with no caller
+  // workspace (ensure_ws): the torch path always passes its own
   return SDCT_OK;
 }
 
@@ -588,7 +594,7 @@ int run_fast(sdct_plan_s* p, int kind, int only_stage, const void* in, void* out
   ra.fb = p->fb;
   ra.fu = p->fu;
   ra.fs = p->fs;
-  ra.bad_q = p->bad_q;
+  ra.badq = p->badq;
   ra.weight = weight;
   if (thr) {
     ra.thr_eps = thr->eps;
@@ -753,8 +759,12 @@ int run(sdct_plan_s* p, int kind, int only_stage, const void* in, void* out, voi
     int rc = SDCT_OK;
     for (long long b0 = 0; b0 < p->batch && rc == SDCT_OK; b0 += chunk) {
       const int bc = static_cast<int>(std::min<long long>(chunk, p->batch - b0));
+      // each chunk's intermediate lives at its own offset of the workspace
+      // (the fast workspace is batch * item_bytes), so a staged call
+      // (only_stage >= 0) never lets chunk c+1 overwrite chunk c's intermediate
       rc = run_fast<T>(p, kind, only_stage, static_cast<const unsigned char*>(in) + b0 * ib,
-                       static_cast<unsigned char*>(out) + b0 * ib, ws, st, nstages, weight, thr, bc);
+                       static_cast<unsigned char*>(out) + b0 * ib, static_cast<unsigned char*>(ws) + b0 * ib, st,
+                       nstages, weight, thr, bc);
     }
     return rc;
   }
@@ -778,10 +788,31 @@ int run(sdct_plan_s* p, int kind, int only_stage, const void* in, void* out, voi
   return SDCT_OK;
 }
 
+// The plan-owned workspace, allocated on first use (callers that pass their
+// own workspace never pay for it).
+int ensure_ws(sdct_plan_s* p) {
+  std::lock_guard<std::mutex> lock(p->gws_mu);
+  if (p->ws) return SDCT_OK;
+  DeviceGuard g(p->device);
+  cudaError_t e = cudaMalloc(&p->ws, p->ws_bytes);
+  if (e != cudaSuccess) return cuda_fail(e, "allocating plan workspace");
+  return SDCT_OK;
+}
+
+bool aligned16(const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15u) == 0; }
+
 int dispatch(sdct_plan_s* p, int kind, int only_stage, const void* in, void* out, void* ws,
              cudaStream_t st, int* nstages, int weight = 0, const Threshold* thr = nullptr) {
   if (!kind_ok(p, kind)) return fail(SDCT_ERR_PLAN, "transform kind does not match the plan rank");
-  if (!ws) ws = p->ws;
+  // the kernels move rows with 16-B bulk copies / TMA and 128-bit accesses:
+  // reject misaligned buffers up front (a fault there would poison the context)
+  if (!aligned16(in) || !aligned16(out) || (ws && !aligned16(ws)))
+    return fail(SDCT_ERR_ARG, "device buffers must be 16-byte aligned");
+  if (!ws) {
+    const int rc = ensure_ws(p);
+    if (rc != SDCT_OK) return rc;
+    ws = p->ws;
+  }
   DeviceGuard g(p->device);
   return p->dtype == SDCT_F32 ? run<float>(p, kind, only_stage, in, out, ws, st, nstages, weight, thr)
                               : run<double>(p, kind, only_stage, in, out, ws, st, nstages, weight, thr);
@@ -949,6 +980,7 @@ int sdct_plan_destroy(sdct_plan_t p) {
   cudaFree(p->d_out);
   cudaFree(p->gws);
   cudaFree(p->aux);
+  cudaFree(p->badq);
   for (int l = 0; l < sdct_plan_s::kLanes; ++l) {
     for (void* b : p->lane_buf[l]) cudaFree(b);
     if (p->lane_st[l]) cudaStreamDestroy(p->lane_st[l]);
@@ -968,6 +1000,17 @@ int sdct_plan_orientation(sdct_plan_t p, int* o) {
 int sdct_plan_is_fast(sdct_plan_t p, int* f) {
   if (!p || !f) return fail(SDCT_ERR_ARG, "null argument");
   *f = p->fast ? 1 : 0;
+  return SDCT_OK;
+}
+
+int sdct_plan_device_bytes(sdct_plan_t p, size_t* bytes) {
+  if (!p || !bytes) return fail(SDCT_ERR_ARG, "null argument");
+  std::lock_guard<std::mutex> lock(p->mu);
+  const size_t item = static_cast<size_t>(p->batch) * p->item_bytes();
+  size_t b = p->table_bytes + (p->ws ? p->ws_bytes : 0) + (p->d_in ? 2 * item : 0) + (p->aux ? 2 * item : 0) +
+             (p->badq ? static_cast<size_t>(p->n[p->rank >= 2 ? 1 : 0]) : 0);
+  if (p->lane_st[0]) b += sdct_plan_s::kLanes * (2 * item + p->ws_bytes);
+  *bytes = b;
   return SDCT_OK;
 }
 
@@ -1006,9 +1049,18 @@ int sdct_plan_corrupt_twiddle(sdct_plan_t p, int64_t index) {
   };
   int rc = flip(p->b_offset_gen, false);
   if (rc == SDCT_OK && p->fast) rc = flip(p->b_offset_fast, p->dtype == SDCT_F32);
-  // the 2D row kernels form b(q) from factor tables: they negate b at the
-  // corrupted index instead (same effect as the negated table entry)
-  if (rc == SDCT_OK) p->bad_q = p->bad_q < 0 ? static_cast<int>(index) : p->bad_q;
+  // the 2D row kernels form b(q) from factor tables: they negate b where the
+  // toggle map is set (same effect as the negated table entry; a second call
+  // on the same index restores it, like the reference's repeated negation)
+  if (rc == SDCT_OK && p->fast) {
+    const size_t n = static_cast<size_t>(p->n[axis]);
+    if (p->badq_host.empty()) p->badq_host.assign(n, 0);
+    p->badq_host[static_cast<size_t>(index)] ^= 1;
+    cudaError_t e = cudaSuccess;
+    if (!p->badq) e = cudaMalloc(&p->badq, n);
+    if (e == cudaSuccess) e = cudaMemcpy(p->badq, p->badq_host.data(), n, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) rc = cuda_fail(e, "uploading corrupt-twiddle map");
+  }
   return rc;
 }
 

@@ -147,6 +147,9 @@ PYBIND11_MODULE(_sdct, m) {
         py::arg("p"), py::arg("s"), "1 / ((1 - p) + p / s)");
 
   // ---- device-memory plans --------------------------------------------------
+  m.def("plan_cache_entries", &sdct::detail::plan_cache_entries,
+        "Device plans held by the C++ plan cache (shared by the numpy entry points)");
+
   py::class_<sdct::DevicePlan>(m, "Plan")
       .def(py::init([](const std::vector<std::int64_t>& dims, std::int64_t batch, const std::string& dtype) {
              sdct::Dtype dt;
@@ -211,6 +214,7 @@ PYBIND11_MODULE(_sdct, m) {
              return n;
            })
       .def_property_readonly("workspace_bytes", &sdct::DevicePlan::workspace_bytes)
+      .def_property_readonly("device_bytes", &sdct::DevicePlan::device_bytes)
       .def_property_readonly("fast", &sdct::DevicePlan::fast);
 
   m.attr("DCT_2D") = py::int_(static_cast<int>(SDCT_DCT_2D));

@@ -108,3 +108,47 @@ def test_gloo_world2_slab_3d_matches_full_transform():
         assert p.exitcode == 0
     assert oracle.rel_l2(y, oracle.port.dct_3d(x)) <= 1e-13
     assert oracle.rel_l2(z / (x.size / 8), x) <= 1e-13
+
+
+# ---- bench.py rank orchestration (what the driver's SCALE run exercises) ---
+def _bench(*argv, env=None, timeout=240):
+    import json
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    e = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "LOCAL_WORLD_SIZE")}
+    e.update(env or {})
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), *argv], capture_output=True, text=True,
+                       timeout=timeout, env=e)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    return json.loads(lines[0])
+
+
+@pytest.mark.parametrize("gpus", [2, 4])
+def test_bench_self_spawns_ranks(gpus):
+    """`bench.py --gpus N` without torchrun launches N ranks itself (gloo
+    control plane here), shards c5 contiguously and reduces max over ranks."""
+    out = _bench("--dry-orchestration", "--gpus", str(gpus), "--workload", "c5")
+    assert out["n_gpus"] == gpus
+    assert out["ms_max_over_ranks"] == 10.0 + gpus - 1
+    covered = [i for s, e in out["shards"] for i in range(s, e)]
+    assert covered == list(range(512))
+
+
+def test_bench_arms_print_identical_config():
+    """Both arms describe the workload with the same config dict and n_gpus
+    (the reference arm runs on rank 0 only)."""
+    ours = _bench("--dry-orchestration", "--gpus", "2", "--workload", "c2")
+    import oracle
+
+    if not oracle.ref_available():
+        pytest.skip("reference library not built")
+    ref = _bench("--impl", "reference", "--gpus", "2", "--workload", "c1", "--steps", "1", "--warmup", "3")
+    ours1 = _bench("--dry-orchestration", "--gpus", "2", "--workload", "c1")
+    assert ref["config"] == ours1["config"]
+    assert ref["n_gpus"] == ours1["n_gpus"] == ours["n_gpus"] == 2
+    assert ref["impl"] == "reference" and ref["cpu_baseline"]["kind"] == "reference"
+    assert "prebuilt plans" in ref["cpu_baseline"]["sample"]

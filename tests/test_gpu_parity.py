@@ -340,6 +340,36 @@ def test_corrupt_twiddle_is_detected(cuda):
             plan.corrupt_twiddle(shape[1])
 
 
+def test_corrupt_twiddle_toggles_like_the_reference(cuda):
+    # the reference negates twiddle_b[i] on every call (dct2d.cpp:312-317):
+    # corrupting one index twice restores it, and every corrupted index counts
+    torch = _torch()
+    from paper_2110_01172_b200 import capi
+
+    for shape in ((64, 64), (16, 32), (7, 9)):
+        x = rnd(shape, 15)
+        xt = torch.tensor(x, device="cuda")
+        want = oracle.port.dct_direct_2d(x)
+
+        def run(plan):
+            out = torch.empty_like(xt)
+            plan.exec("dct_2d", xt.data_ptr(), out.data_ptr())
+            torch.cuda.synchronize()
+            return out.cpu().numpy()
+
+        plan = capi.Plan(shape)
+        plan.corrupt_twiddle(3)
+        plan.corrupt_twiddle(3)
+        assert oracle.max_rel(run(plan), want) <= 1e-12, shape  # restored
+        plan.corrupt_twiddle(2)
+        one = run(plan)
+        plan.corrupt_twiddle(1)
+        two = run(plan)
+        assert oracle.max_rel(one, want) > 1e-6 and oracle.max_rel(two, one) > 1e-6, shape
+        plan.corrupt_twiddle(1)
+        assert np.array_equal(run(plan), one), shape
+
+
 def test_kind_rank_mismatch_is_plan_error(cuda):
     torch = _torch()
     from paper_2110_01172_b200 import capi
