@@ -65,8 +65,14 @@ enum {
   SDCT_DCT_2D_ROWCOL = 6, /* sdct::dct_2d_rowcol proj/include/sdct/dct2d.hpp:111-112 */
   SDCT_DCT_1D = 7,        /* sdct::dct_1d        proj/include/sdct/dct1d.hpp:90-93  (rank-1 plans) */
   SDCT_IDCT_1D = 8,       /* sdct::idct_1d       proj/include/sdct/dct1d.hpp:97-99  (rank-1 plans) */
-  SDCT_IDXST_1D = 9       /* sdct::idxst_1d      proj/include/sdct/transforms_ext.hpp:29-31 */
+  SDCT_IDXST_1D = 9,      /* sdct::idxst_1d      proj/include/sdct/transforms_ext.hpp:29-31 */
+  SDCT_IDCT_IDXST_2D_ROWCOL = 10, /* sdct::idct_idxst_2d_rowcol proj/include/sdct/transforms_ext.hpp:43-44 */
+  SDCT_IDXST_IDCT_2D_ROWCOL = 11  /* sdct::idxst_idct_2d_rowcol proj/include/sdct/transforms_ext.hpp:45-46 */
 };
+/* The three *_ROWCOL kinds are the reference's 8-stage row-column baselines
+ * (proj/src/dct2d.cpp:395-406, transforms_ext.cpp:287-311): per axis one
+ * kernel (parity reorder / embedding, row FFTs and twiddle stage fused) and
+ * one tiled transpose — 4 launches, 4 HBM round trips of the tensor. */
 
 typedef struct sdct_plan_s* sdct_plan_t;
 
@@ -154,6 +160,31 @@ int sdct_compress(sdct_plan_t plan, const void* d_in, void* d_out, double epsilo
  * once per image. */
 int sdct_exec_host_pipelined(sdct_plan_t plan, const int* kinds, int nkinds, const void* h_in, int64_t in_stride,
                              void* h_out, int64_t out_stride, int64_t count, void* stream);
+
+/* Batched transpose of device memory: `batch` items of rows x cols (dtype
+ * SDCT_F32/F64) become cols x rows, out of place, stream-ordered. The axis
+ * regrouping of the reference's rank-4 factorisation (transpose_2d inside
+ * proj/src/transforms_ext.cpp:396-425) and the row-column kinds use it. */
+int sdct_transpose(int dtype, int64_t rows, int64_t cols, int64_t batch, const void* d_in, void* d_out,
+                   void* stream);
+
+/* Stage-level real FFTs with the reference's HalfSpectrum layout — replace
+ * sdct::rfft_nd / irfft_nd (proj/include/sdct/rfft.hpp:66-70, rfft.cpp:182-245):
+ * unnormalised, kernel e^{-2 pi i nk/N}, one-sided (last/2 + 1 complex entries,
+ * interleaved re/im doubles) along the last axis, full along the others.
+ * The plan gives rank (1..3), extents and batch; fp64 plans only (the
+ * reference is fp64). d_workspace: NULL (plan-owned scratch; serialise
+ * concurrent calls on one plan) or sdct_rfft_workspace_size bytes. The
+ * inverse treats the stored half as authoritative and keeps the real part. */
+int sdct_rfft_workspace_size(sdct_plan_t plan, size_t* bytes);
+int sdct_rfft_nd(sdct_plan_t plan, const void* d_x, void* d_half, void* d_workspace, void* stream);
+int sdct_irfft_nd(sdct_plan_t plan, const void* d_half, void* d_x, void* d_workspace, void* stream);
+/* Host-memory versions (copy in, run, copy out, synchronise). */
+int sdct_rfft_nd_host(sdct_plan_t plan, const double* h_x, double* h_half);
+int sdct_irfft_nd_host(sdct_plan_t plan, const double* h_half, double* h_x);
+/* O(n^2) direct DFT of n complex values on the GPU (sdct::dft_naive,
+ * proj/src/rfft.cpp:113-127, the backend's own reference); host buffers. */
+int sdct_dft_naive_host(int64_t n, int inverse, const double* h_in, double* h_out);
 
 /* Stage-level access for timing the individual kernels of a transform:
  * number of kernel launches of `kind`, and a launch of one of them with the

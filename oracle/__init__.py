@@ -36,6 +36,8 @@ KINDS = {
     "dct_3d": 4,
     "idct_3d": 5,
     "dct_2d_rowcol": 6,
+    "idct_idxst_2d_rowcol": 7,
+    "idxst_idct_2d_rowcol": 8,
 }
 
 
@@ -67,6 +69,7 @@ def _port_lib():
         for name in ("dct_direct_1d", "idct_direct_1d", "idxst_direct_1d"):
             getattr(lib, "sdct_oracle_" + name).argtypes = [P, S, P]
         lib.sdct_oracle_dct_direct_2d.argtypes = [P, S, S, P]
+        lib.sdct_oracle_rowcol_2d.argtypes = [P, S, S, ctypes.c_int, P]
         lib.sdct_oracle_force_fields_2d.argtypes = [P, S, S, P, P]
         _port = lib
     return _port
@@ -196,6 +199,22 @@ class _Port:
     def idxst_direct_1d(self, x):
         lib = _port_lib()
         return self._batched(x, 1, lambda a, s, o: lib.sdct_oracle_idxst_direct_1d(_dp(a), s[0], _dp(o)))
+
+    def _rowcol(self, x, kind):
+        lib = _port_lib()
+        return self._batched(x, 2, lambda a, s, o: lib.sdct_oracle_rowcol_2d(_dp(a), s[0], s[1], kind, _dp(o)))
+
+    def dct_2d_rowcol(self, x):
+        """dct_rows + transpose twice (proj/src/dct2d.cpp:395-406)."""
+        return self._rowcol(x, 0)
+
+    def idct_idxst_2d_rowcol(self, x):
+        """composite_2d_rowcol, IdctIdxst (proj/src/transforms_ext.cpp:287-301)."""
+        return self._rowcol(x, 1)
+
+    def idxst_idct_2d_rowcol(self, x):
+        """composite_2d_rowcol, IdxstIdct (proj/src/transforms_ext.cpp:287-301)."""
+        return self._rowcol(x, 2)
 
     def dct_direct_2d(self, x):
         lib = _port_lib()

@@ -35,6 +35,8 @@ enum RefKind {
   REF_DCT3 = 4,
   REF_IDCT3 = 5,
   REF_DCT2_ROWCOL = 6,
+  REF_IDCT_IDXST_ROWCOL = 7,
+  REF_IDXST_IDCT_ROWCOL = 8,
 };
 
 }  // namespace
@@ -67,6 +69,8 @@ int sdct_ref_run(int kind, int rank, const std::size_t* dims, const double* in, 
           case REF_IDCT_IDXST: y = sdct::idct_idxst_2d(x, plan, cfg); break;
           case REF_IDXST_IDCT: y = sdct::idxst_idct_2d(x, plan, cfg); break;
           case REF_DCT2_ROWCOL: y = sdct::dct_2d_rowcol(x, plan, cfg); break;
+          case REF_IDCT_IDXST_ROWCOL: y = sdct::idct_idxst_2d_rowcol(x, plan, cfg); break;
+          case REF_IDXST_IDCT_ROWCOL: y = sdct::idxst_idct_2d_rowcol(x, plan, cfg); break;
           default: throw sdct::ShapeError("unknown kind");
         }
       }
@@ -185,6 +189,8 @@ int sdct_ref_run_timed(int kind, int rank, const std::size_t* dims, const double
           case REF_IDCT_IDXST: y = sdct::idct_idxst_2d(x, plan, cfg); break;
           case REF_IDXST_IDCT: y = sdct::idxst_idct_2d(x, plan, cfg); break;
           case REF_DCT2_ROWCOL: y = sdct::dct_2d_rowcol(x, plan, cfg); break;
+          case REF_IDCT_IDXST_ROWCOL: y = sdct::idct_idxst_2d_rowcol(x, plan, cfg); break;
+          case REF_IDXST_IDCT_ROWCOL: y = sdct::idxst_idct_2d_rowcol(x, plan, cfg); break;
           default: throw sdct::ShapeError("unknown kind");
         }
       }

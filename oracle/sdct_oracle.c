@@ -455,3 +455,65 @@ void sdct_oracle_force_fields_2d(const double* x, size_t n1, size_t n2, double* 
   free(a1);
   free(a2);
 }
+
+/* ---- row-column baselines ------------------------------------------------
+ * dct_rows (dct2d.cpp:248-290): per row, parity reorder, rfft_row, then
+ * y(k) = Re(tw(k) X(k)) with X(k) = conj X(n-k) past the stored half.
+ * inverse_rows (transforms_ext.cpp:40-88): v(k) = (x(k), -x(n-k)) [cosine] or
+ * (x(n-k), -x(k)) [sine, 0 at k = 0] times conj tw(k), irfft_row, then
+ * y(m) = 1/2 t(ps(m)), odd m negated for the sine embedding. */
+static void rows_pass(const double* x, size_t rows, size_t n, int inverse, int sine, double* y) {
+  size_t h = n / 2 + 1;
+  cd* tw = quarter_wave(n);
+  fftws w;
+  ws_init(&w, n);
+  cd* s = (cd*)malloc(sizeof(cd) * n);
+  for (size_t r = 0; r < rows; ++r) {
+    const double* xr = x + r * n;
+    double* yr = y + r * n;
+    if (!inverse) {
+      for (size_t m = 0; m < n; ++m) s[m] = xr[parity_embed(m, n)];
+      ws_transform(&w, s, 0);
+      for (size_t k = 0; k < n; ++k) {
+        cd v = k < h ? s[k] : conj(s[n - k]);
+        yr[k] = creal(tw[k]) * creal(v) - cimag(tw[k]) * cimag(v);
+      }
+    } else {
+      for (size_t k = 0; k < h; ++k) {
+        cd v;
+        if (sine) v = (k == 0) ? 0.0 : xr[n - k] - I * xr[k];
+        else v = xr[k] - I * (k == 0 ? 0.0 : xr[n - k]);
+        s[k] = conj(tw[k]) * v;
+      }
+      for (size_t k = h; k < n; ++k) s[k] = conj(s[n - k]);
+      ws_transform(&w, s, 1);
+      for (size_t m = 0; m < n; ++m) {
+        double v = 0.5 * creal(s[parity_source(m, n)]);
+        yr[m] = (sine && (m & 1u)) ? -v : v;
+      }
+    }
+  }
+  free(s);
+  ws_free(&w);
+  free(tw);
+}
+
+static void transpose_2d(const double* x, size_t r, size_t c, double* y) {
+  for (size_t i = 0; i < r; ++i)
+    for (size_t j = 0; j < c; ++j) y[j * r + i] = x[i * c + j];
+}
+
+/* dct_2d_rowcol (dct2d.cpp:395-406) for kind 0; composite_2d_rowcol
+ * (transforms_ext.cpp:287-301) for kind 1 (IdctIdxst: sine along axis 1) and
+ * kind 2 (IdxstIdct: sine along axis 0). */
+void sdct_oracle_rowcol_2d(const double* x, size_t n1, size_t n2, int kind, double* y) {
+  double* a = (double*)malloc(sizeof(double) * n1 * n2);
+  double* b = (double*)malloc(sizeof(double) * n1 * n2);
+  int inv = kind != 0;
+  rows_pass(x, n1, n2, inv, kind == 1, a);
+  transpose_2d(a, n1, n2, b);
+  rows_pass(b, n2, n1, inv, kind == 2, a);
+  transpose_2d(a, n2, n1, y);
+  free(a);
+  free(b);
+}

@@ -31,8 +31,10 @@ from .api import (
     idct_2d,
     idct_3d,
     idct_idxst_2d,
+    idct_idxst_2d_rowcol,
     idxst_1d,
     idxst_idct_2d,
+    idxst_idct_2d_rowcol,
     plan_for,
     stream_host,
 )
@@ -42,6 +44,7 @@ __all__ = [
     "ShapeError", "FormatError", "DeviceError", "amdahl_speedup",
     "dct_1d", "idct_1d", "idxst_1d",
     "dct_2d", "dct_2d_rowcol", "idct_2d", "idct_idxst_2d", "idxst_idct_2d",
+    "idct_idxst_2d_rowcol", "idxst_idct_2d_rowcol",
     "dct_3d", "dct_4d", "idct_3d", "plan_for", "stream_host", "force_demo_fields",
     "dct_oracle_1d", "dct_oracle_2d", "compress",
     "read_dctb", "write_dctb", "transform_file",

@@ -13,6 +13,7 @@ _KIND = {
     "dct_1d": _sdct.DCT_1D, "idct_1d": _sdct.IDCT_1D, "idxst_1d": _sdct.IDXST_1D,
     "dct_2d": _sdct.DCT_2D, "idct_2d": _sdct.IDCT_2D, "idct_idxst_2d": _sdct.IDCT_IDXST_2D,
     "idxst_idct_2d": _sdct.IDXST_IDCT_2D, "dct_2d_rowcol": _sdct.DCT_2D_ROWCOL,
+    "idct_idxst_2d_rowcol": _sdct.IDCT_IDXST_2D_ROWCOL, "idxst_idct_2d_rowcol": _sdct.IDXST_IDCT_2D_ROWCOL,
     "dct_3d": _sdct.DCT_3D, "idct_3d": _sdct.IDCT_3D,
 }
 _RANK = {"dct_1d": 1, "idct_1d": 1, "idxst_1d": 1, "dct_3d": 3, "idct_3d": 3}
@@ -105,6 +106,8 @@ idct_1d = _make("idct_1d")
 idxst_1d = _make("idxst_1d")
 dct_2d = _make("dct_2d")
 dct_2d_rowcol = _make("dct_2d_rowcol")
+idct_idxst_2d_rowcol = _make("idct_idxst_2d_rowcol")
+idxst_idct_2d_rowcol = _make("idxst_idct_2d_rowcol")
 idct_2d = _make("idct_2d")
 idct_idxst_2d = _make("idct_idxst_2d")
 idxst_idct_2d = _make("idxst_idct_2d")

@@ -96,7 +96,59 @@ def build(verbose: bool = False, jobs: int | None = None) -> str:
     if os.path.exists(src) and (not os.path.exists(exe) or os.path.getmtime(exe) < max(
             os.path.getmtime(src), os.path.getmtime(LIBSO), hdr_time)):
         _run(["g++"] + CXXFLAGS + [src, "-o", exe, "-L", LIB, "-lsdct_b200", "-pthread", "-Wl,-rpath,$ORIGIN"])
+    build_acceptance()
     return LIBSO
+
+
+REFERENCE = "/root/reference/proj"
+ACC_BIN = os.path.join(ROOT, "tests", "cpp", "bin", "acceptance_dropin")
+# headers of the hot path come from this repo (the drop-in); the reference's
+# own headers serve everything off the path (PGM/DCTB I/O, compression app,
+# quadratic oracles, bench helper, Amdahl model)
+DROPIN_HEADERS = ["tensor", "exec", "errors", "dct1d", "dct2d", "transforms_ext", "rfft", "force", "plan_handle",
+                  "device"]
+REFERENCE_HEADERS = ["io", "compress", "oracle", "bench", "amdahl", "verify"]
+REFERENCE_SUPPORT = ["oracle", "bench", "compress", "amdahl", "io"]
+
+
+def build_acceptance() -> str | None:
+    """The reference's own acceptance program (proj/tests/acceptance.cpp),
+    compiled unmodified from where it lies in /root/reference against this
+    repo's include/sdct and linked with libsdct_b200.so: the compatibility
+    check of SURVEY.md §8(b). Its off-path helpers (oracle.cpp, bench.cpp,
+    compress.cpp, amdahl.cpp, io.cpp) are compiled from the reference too and
+    call the drop-in where they call the transforms. Output (git-ignored,
+    travels to the GPU box): tests/cpp/bin/acceptance_dropin. Skipped when the
+    reference tree is absent (the GPU box uses the prebuilt binary)."""
+    if not os.path.isdir(REFERENCE):
+        return None
+    import shutil
+    import tempfile
+
+    srcs = [os.path.join(REFERENCE, "tests", "acceptance.cpp")] + [
+        os.path.join(REFERENCE, "src", f + ".cpp") for f in REFERENCE_SUPPORT]
+    hdrs = [os.path.join(INC, "sdct", h + ".hpp") for h in DROPIN_HEADERS] + [
+        os.path.join(REFERENCE, "include", "sdct", h + ".hpp") for h in REFERENCE_HEADERS]
+    if os.path.exists(ACC_BIN) and os.path.getmtime(ACC_BIN) >= _newest(srcs + hdrs + [LIBSO]):
+        return ACC_BIN
+    os.makedirs(os.path.dirname(ACC_BIN), exist_ok=True)
+    tmp = tempfile.mkdtemp(prefix="sdct_acc_")
+    try:
+        inc = os.path.join(tmp, "inc", "sdct")
+        os.makedirs(inc)
+        for h in hdrs:
+            os.symlink(h, os.path.join(inc, os.path.basename(h)))
+        objs = []
+        for src in srcs:
+            obj = os.path.join(tmp, os.path.basename(src) + ".o")
+            _run(["g++", "-std=c++20", "-O2", "-pthread", "-I", os.path.join(tmp, "inc"), "-I", INC, "-c", src,
+                  "-o", obj])
+            objs.append(obj)
+        _run(["g++", "-o", ACC_BIN] + objs + ["-L", LIB, "-lsdct_b200", "-pthread",
+                                             "-Wl,-rpath,$ORIGIN/../../../paper_2110_01172_b200/lib"])
+    finally:
+        shutil.rmtree(tmp, ignore_errors=True)
+    return ACC_BIN
 
 
 if __name__ == "__main__":

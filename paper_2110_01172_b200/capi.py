@@ -15,8 +15,10 @@ ORIENT_AUTO, ORIENT_DIRECT, ORIENT_TRANSPOSED = -1, 0, 1
 KINDS = {
     "dct_2d": 0, "idct_2d": 1, "idct_idxst_2d": 2, "idxst_idct_2d": 3, "dct_3d": 4,
     "idct_3d": 5, "dct_2d_rowcol": 6, "dct_1d": 7, "idct_1d": 8, "idxst_1d": 9,
+    "idct_idxst_2d_rowcol": 10, "idxst_idct_2d_rowcol": 11,
 }
 RANK_OF = {"dct_2d": 2, "idct_2d": 2, "idct_idxst_2d": 2, "idxst_idct_2d": 2, "dct_2d_rowcol": 2,
+           "idct_idxst_2d_rowcol": 2, "idxst_idct_2d_rowcol": 2,
            "dct_3d": 3, "idct_3d": 3, "dct_1d": 1, "idct_1d": 1, "idxst_1d": 1}
 
 # (name, restype, argtypes) for every function declared in include/sdct_b200.h
@@ -39,6 +41,13 @@ SIGNATURES = [
     ("sdct_compress", ctypes.c_int, [_VP, _VP, _VP, ctypes.c_double, _VP, _VP, _VP]),
     ("sdct_exec_host_pipelined", ctypes.c_int, [_VP, ctypes.POINTER(ctypes.c_int), ctypes.c_int, _VP, ctypes.c_int64,
                                                 _VP, ctypes.c_int64, ctypes.c_int64, _VP]),
+    ("sdct_transpose", ctypes.c_int, [ctypes.c_int, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, _VP, _VP, _VP]),
+    ("sdct_rfft_workspace_size", ctypes.c_int, [_VP, ctypes.POINTER(ctypes.c_size_t)]),
+    ("sdct_rfft_nd", ctypes.c_int, [_VP, _VP, _VP, _VP, _VP]),
+    ("sdct_irfft_nd", ctypes.c_int, [_VP, _VP, _VP, _VP, _VP]),
+    ("sdct_rfft_nd_host", ctypes.c_int, [_VP, _VP, _VP]),
+    ("sdct_irfft_nd_host", ctypes.c_int, [_VP, _VP, _VP]),
+    ("sdct_dft_naive_host", ctypes.c_int, [ctypes.c_int64, ctypes.c_int, _VP, _VP]),
     ("sdct_stage_count", ctypes.c_int, [_VP, ctypes.c_int, ctypes.POINTER(ctypes.c_int)]),
     ("sdct_exec_stage", ctypes.c_int, [_VP, ctypes.c_int, ctypes.c_int, _VP, _VP, _VP, _VP]),
     ("sdct_counters", ctypes.c_int, [_VP, ctypes.c_int, ctypes.POINTER(ctypes.c_uint64)]),

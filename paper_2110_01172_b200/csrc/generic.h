@@ -13,7 +13,7 @@ struct GenericJob {
   int mode = 0;          // inverse composite embedding: 0 none, 1 axis 0, 2 axis 1 (rank 1: 2 = idxst)
   int sign_axis = -1;    // inverse: negate odd k along this axis
   double scale = 1.0;    // inverse gather scale (1/4 in 2D, 1/8 in 3D, 1/2 in 1D)
-  bool legacy = false;   // 2D: one full-tensor pass per stage (the row-column comparator)
+  bool legacy = false;   // 2D: force the one-pass-per-stage pipeline (developer A/B; no kind sets it)
   const double2* quarter[3] = {nullptr, nullptr, nullptr};  // e^{-i pi k/(2 N_a)}
   const double2* circle[3] = {nullptr, nullptr, nullptr};   // e^{-2 pi i t / N_a}
   // Bluestein tables of axes whose largest prime factor is large (2D
@@ -36,6 +36,14 @@ cudaError_t prep_smem_ptr(const void* kernel, size_t smem);
 // Workspace: 2 * numel * batch * sizeof(double2) bytes.
 template <typename T>
 cudaError_t generic_run(const GenericJob& job, const void* in, void* out, void* ws, cudaStream_t st);
+
+// rfft_nd / irfft_nd of the reference (rfft.cpp:182-245), fp64, on the
+// job's rank/dims/batch and circle tables. `half` is the one-sided spectrum
+// [batch][dims..., last/2+1] of interleaved complex; ws = generic scratch.
+cudaError_t generic_rfft(const GenericJob& job, const double* x, double2* half, void* ws, cudaStream_t st);
+cudaError_t generic_irfft(const GenericJob& job, const double2* half, double* x, void* ws, cudaStream_t st);
+// dft_naive (rfft.cpp:113-127): O(n^2) direct DFT of n complex values (device buffers).
+cudaError_t dft_naive_run(const double2* in, double2* out, int n, bool inverse, cudaStream_t st);
 
 // DREAMPlace-style field weighting (proj/src/force.cpp:19-31): aw = a * w_which /
 // (w1^2 + w2^2), w_d = pi k_d / n_d, 0 at DC. dtype float when f32.

@@ -16,6 +16,7 @@
 #include "sdct/dct1d.hpp"
 #include "sdct/dct2d.hpp"
 #include "sdct/force.hpp"
+#include "sdct/rfft.hpp"
 #include "sdct/transforms_ext.hpp"
 #include "sdct_b200.h"
 
@@ -320,6 +321,60 @@ RealTensor composite_2d(const RealTensor& x, const Plan2d& plan, CompositeKind k
   return kind == CompositeKind::IdctIdxst ? idct_idxst_2d(x, plan, cfg, c) : idxst_idct_2d(x, plan, cfg, c);
 }
 
+RealTensor idct_idxst_2d_rowcol(const RealTensor& x, const Plan2d& plan, const ExecConfig&, StageCounters* c) {
+  require_plan2(x, plan, "composite_2d_rowcol");
+  return detail::run_host(plan.handle(), SDCT_IDCT_IDXST_2D_ROWCOL, x, c);
+}
+RealTensor idxst_idct_2d_rowcol(const RealTensor& x, const Plan2d& plan, const ExecConfig&, StageCounters* c) {
+  require_plan2(x, plan, "composite_2d_rowcol");
+  return detail::run_host(plan.handle(), SDCT_IDXST_IDCT_2D_ROWCOL, x, c);
+}
+RealTensor composite_2d_rowcol(const RealTensor& x, const Plan2d& plan, CompositeKind kind, const ExecConfig& cfg,
+                               StageCounters* c) {
+  return kind == CompositeKind::IdctIdxst ? idct_idxst_2d_rowcol(x, plan, cfg, c)
+                                          : idxst_idct_2d_rowcol(x, plan, cfg, c);
+}
+
+// ---- rank 4 -------------------------------------------------------------------
+RealTensor dct_nd_factorized(const RealTensor& x, const ExecConfig&) {
+  if (x.rank() != 4)
+    throw ShapeError("dct_nd_factorized expects a rank-4 tensor, got " + shape_to_string(x.dims()));
+  const std::int64_t d0 = static_cast<std::int64_t>(x.dim(0)), d1 = static_cast<std::int64_t>(x.dim(1));
+  const std::int64_t d2 = static_cast<std::int64_t>(x.dim(2)), d3 = static_cast<std::int64_t>(x.dim(3));
+  const std::size_t bytes = x.size() * sizeof(double);
+  // round one over axes (0,1): [d0 d1][d2 d3] -> [d2 d3][d0][d1] (transpose),
+  // d2*d3 fused 2D transforms, transpose back; round two over (2,3): d0*d1
+  // contiguous 2D transforms (transforms_ext.cpp:402-423)
+  detail::PlanPtr p01 = detail::make_plan({d0, d1}, d2 * d3, SDCT_F64, SDCT_ORIENT_AUTO);
+  detail::PlanPtr p23 = detail::make_plan({d2, d3}, d0 * d1, SDCT_F64, SDCT_ORIENT_AUTO);
+  void* a = nullptr;
+  void* b = nullptr;
+  auto cu = [](cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw DeviceError(std::string(what) + ": " + cudaGetErrorString(e));
+  };
+  cu(cudaMalloc(&a, bytes), "dct_nd_factorized: allocating");
+  if (cudaMalloc(&b, bytes) != cudaSuccess) {
+    cudaFree(a);
+    throw DeviceError("dct_nd_factorized: allocating");
+  }
+  RealTensor y(x.dims());
+  try {
+    cu(cudaMemcpy(a, x.data(), bytes, cudaMemcpyHostToDevice), "dct_nd_factorized: H2D");
+    detail::check(sdct_transpose(SDCT_F64, d0 * d1, d2 * d3, 1, a, b, nullptr));
+    detail::check(sdct_exec(p01.get(), SDCT_DCT_2D, b, a, nullptr, nullptr));
+    detail::check(sdct_transpose(SDCT_F64, d2 * d3, d0 * d1, 1, a, b, nullptr));
+    detail::check(sdct_exec(p23.get(), SDCT_DCT_2D, b, a, nullptr, nullptr));
+    cu(cudaMemcpy(y.data(), a, bytes, cudaMemcpyDeviceToHost), "dct_nd_factorized: D2H");
+  } catch (...) {
+    cudaFree(a);
+    cudaFree(b);
+    throw;
+  }
+  cudaFree(a);
+  cudaFree(b);
+  return y;
+}
+
 // ---- 3D ---------------------------------------------------------------------
 Plan3d::Plan3d(std::size_t n1, std::size_t n2, std::size_t n3)
     : n1_(checked_extent(n1)),
@@ -373,6 +428,94 @@ bool DevicePlan::fast() const {
   int f = 0;
   detail::check(sdct_plan_is_fast(plan_.get(), &f));
   return f != 0;
+}
+
+// ---- stage-level real FFTs (rfft.hpp) ----------------------------------------
+std::vector<std::complex<double>> dft_naive(const std::vector<std::complex<double>>& x, bool inverse) {
+  std::vector<std::complex<double>> out(x.size());
+  if (x.empty()) return out;
+  detail::check(sdct_dft_naive_host(static_cast<std::int64_t>(x.size()), inverse ? 1 : 0,
+                                    reinterpret_cast<const double*>(x.data()), reinterpret_cast<double*>(out.data())));
+  return out;
+}
+
+namespace {
+std::vector<std::int64_t> checked_fft_dims(const Shape& dims) {
+  if (dims.empty() || dims.size() > 3)
+    throw ShapeError("real FFT plans cover rank 1..3 on the GPU, got rank " + std::to_string(dims.size()));
+  std::vector<std::int64_t> d;
+  for (std::size_t n : dims) d.push_back(static_cast<std::int64_t>(checked_extent(n)));
+  return d;
+}
+}  // namespace
+
+FftPlanNd::FftPlanNd(Shape dims)
+    : dims_(std::move(dims)), plan_(detail::make_plan(checked_fft_dims(dims_), 1, SDCT_F64, SDCT_ORIENT_DIRECT)) {}
+
+HalfSpectrum rfft_nd(const RealTensor& x, const FftPlanNd& plan, const ExecConfig&) {
+  if (x.dims() != plan.dims())
+    throw PlanError("rfft_nd: plan built for " + shape_to_string(plan.dims()) + ", input is " +
+                    shape_to_string(x.dims()));
+  HalfSpectrum s(x.dims());
+  detail::check(sdct_rfft_nd_host(plan.handle(), x.data(), reinterpret_cast<double*>(s.data.data())));
+  return s;
+}
+
+RealTensor irfft_nd(const HalfSpectrum& spectrum, const FftPlanNd& plan, const ExecConfig&) {
+  if (spectrum.logical_dims != plan.dims())
+    throw PlanError("irfft_nd: plan built for " + shape_to_string(plan.dims()) + ", spectrum is " +
+                    shape_to_string(spectrum.logical_dims));
+  Shape stored = spectrum.logical_dims;
+  stored.back() = stored.back() / 2 + 1;
+  if (spectrum.data.dims() != stored)
+    throw ShapeError("irfft_nd: stored spectrum " + shape_to_string(spectrum.data.dims()) + " does not match " +
+                     shape_to_string(stored));
+  RealTensor out(spectrum.logical_dims);
+  detail::check(sdct_irfft_nd_host(plan.handle(), reinterpret_cast<const double*>(spectrum.data.data()), out.data()));
+  return out;
+}
+
+namespace {
+HalfSpectrum rfft_rank(const RealTensor& x, std::size_t rank, const ExecConfig& cfg) {
+  if (x.rank() != rank)
+    throw ShapeError("expected a rank-" + std::to_string(rank) + " tensor, got " + shape_to_string(x.dims()));
+  return rfft_nd(x, FftPlanNd(x.dims()), cfg);
+}
+RealTensor irfft_rank(const HalfSpectrum& s, std::size_t rank, const ExecConfig& cfg) {
+  if (s.logical_dims.size() != rank)
+    throw ShapeError("expected a rank-" + std::to_string(rank) + " spectrum, got " +
+                     shape_to_string(s.logical_dims));
+  return irfft_nd(s, FftPlanNd(s.logical_dims), cfg);
+}
+}  // namespace
+
+HalfSpectrum rfft_1d(const RealTensor& x, const ExecConfig& cfg) { return rfft_rank(x, 1, cfg); }
+RealTensor irfft_1d(const HalfSpectrum& s, const ExecConfig& cfg) { return irfft_rank(s, 1, cfg); }
+HalfSpectrum rfft_2d(const RealTensor& x, const ExecConfig& cfg) { return rfft_rank(x, 2, cfg); }
+RealTensor irfft_2d(const HalfSpectrum& s, const ExecConfig& cfg) { return irfft_rank(s, 2, cfg); }
+HalfSpectrum rfft_3d(const RealTensor& x, const ExecConfig& cfg) { return rfft_rank(x, 3, cfg); }
+RealTensor irfft_3d(const HalfSpectrum& s, const ExecConfig& cfg) { return irfft_rank(s, 3, cfg); }
+
+ComplexTensor expand_spectrum(const HalfSpectrum& spectrum) {
+  // a host-side layout conversion (no arithmetic beyond conjugation)
+  const Shape& dims = spectrum.logical_dims;
+  const std::size_t rank = dims.size(), h = spectrum.data.dims().back();
+  ComplexTensor full(dims);
+  std::vector<std::size_t> idx(rank, 0);
+  for (std::size_t flat = 0; flat < full.size(); ++flat) {
+    std::size_t src = 0;
+    bool mirror = idx.back() >= h;
+    for (std::size_t a = 0; a < rank; ++a) {
+      const std::size_t i = mirror ? (dims[a] - idx[a]) % dims[a] : idx[a];
+      src = src * (a + 1 == rank ? h : dims[a]) + i;
+    }
+    full[flat] = mirror ? std::conj(spectrum.data[src]) : spectrum.data[src];
+    for (std::size_t a = rank; a-- > 0;) {
+      if (++idx[a] < dims[a]) break;
+      idx[a] = 0;
+    }
+  }
+  return full;
 }
 
 ForceFields force_demo_fields(const RealTensor& density, const ExecConfig&) {

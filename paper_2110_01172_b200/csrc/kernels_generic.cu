@@ -956,20 +956,12 @@ int bluestein_len(int n) {
   return M <= 8192 ? M : 0;
 }
 
-// ---------------------------------------------------------------------------
-template <typename T>
-cudaError_t generic_run(const GenericJob& job, const void* in, void* out, void* ws, cudaStream_t st) {
-  Dims d;
-  d.rank = job.rank;
-  d.numel = 1;
-  for (int a = 0; a < 3; ++a) d.n[a] = a < job.rank ? job.dims[a] : 1;
-  for (int a = 0; a < job.rank; ++a) d.numel *= job.dims[a];
-  const long long total = d.numel * job.batch;
-  double2* A = static_cast<double2*>(ws);
-  double2* B = A + total;
-  const int g = nblocks(total);
-  auto dft_all = [&](double2*& cur, double2*& nxt, int inverse) {
-    for (int a = 0; a < job.rank; ++a) {
+// Complex DFT along axes [a0, a1) of the [batch][dims...] complex tensor in
+// cur (result in cur; nxt is scratch of the same size). g = grid for the
+// elementwise kernels over the whole tensor.
+static void dft_axes(const GenericJob& job, int a0, int a1, double2*& cur, double2*& nxt, int inverse, int g,
+              cudaStream_t st) {
+    for (int a = a0; a < a1; ++a) {
       long long inner = 1, outer = job.batch;
       for (int t = a + 1; t < job.rank; ++t) inner *= job.dims[t];
       for (int t = 0; t < a; ++t) outer *= job.dims[t];
@@ -1024,6 +1016,22 @@ cudaError_t generic_run(const GenericJob& job, const void* in, void* out, void* 
         nxt = t;
       }
     }
+  }
+
+// ---------------------------------------------------------------------------
+template <typename T>
+cudaError_t generic_run(const GenericJob& job, const void* in, void* out, void* ws, cudaStream_t st) {
+  Dims d;
+  d.rank = job.rank;
+  d.numel = 1;
+  for (int a = 0; a < 3; ++a) d.n[a] = a < job.rank ? job.dims[a] : 1;
+  for (int a = 0; a < job.rank; ++a) d.numel *= job.dims[a];
+  const long long total = d.numel * job.batch;
+  double2* A = static_cast<double2*>(ws);
+  double2* B = A + total;
+  const int g = nblocks(total);
+  auto dft_all = [&](double2*& cur, double2*& nxt, int inverse) {
+    dft_axes(job, 0, job.rank, cur, nxt, inverse, g, st);
   };
   double2* cur = A;
   double2* nxt = B;
@@ -1077,6 +1085,110 @@ cudaError_t generic_run(const GenericJob& job, const void* in, void* out, void* 
     g_gather_inv<T><<<g, kThreads, 0, st>>>(cur, static_cast<T*>(out), d, job.batch, job.scale,
                                              job.sign_axis);
   }
+  return cudaGetLastError();
+}
+
+// ---- rfft_nd / irfft_nd (rfft.cpp:182-245) ---------------------------------
+// Stage-level real FFTs with the reference's layout: full complex DFT of the
+// real input along every axis, one-sided (floor(N/2)+1 entries) along the
+// last axis; the inverse takes the stored half as authoritative, inverts the
+// leading axes on the half-width data, fills each row's upper half by
+// Hermitian symmetry and keeps the real part (unnormalised both ways).
+namespace {
+
+__global__ void g_real_to_complex(const double* __restrict__ x, double2* __restrict__ c, long long n) {
+  for (long long f = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; f < n;
+       f += static_cast<long long>(gridDim.x) * blockDim.x)
+    c[f] = make_double2(x[f], 0.0);
+}
+
+__global__ void g_take_half(const double2* __restrict__ full, double2* __restrict__ half, long long rows, int nl,
+                            int h) {
+  const long long total = rows * h;
+  for (long long f = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; f < total;
+       f += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long r = f / h;
+    half[f] = full[r * nl + (f - r * h)];
+  }
+}
+
+__global__ void g_hermitian_rows(const double2* __restrict__ half, double2* __restrict__ full, long long rows, int nl,
+                                 int h) {
+  const long long total = rows * nl;
+  for (long long f = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; f < total;
+       f += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long r = f / nl;
+    const int k = static_cast<int>(f - r * nl);
+    double2 v = half[r * h + (k < h ? k : nl - k)];
+    if (k >= h) v.y = -v.y;
+    full[f] = v;
+  }
+}
+
+__global__ void g_real_part(const double2* __restrict__ c, double* __restrict__ x, long long n) {
+  for (long long f = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; f < n;
+       f += static_cast<long long>(gridDim.x) * blockDim.x)
+    x[f] = c[f].x;
+}
+
+// dft_naive (rfft.cpp:113-127): direct O(n^2) sums, exact phase reduction
+__global__ void g_dft_naive(const double2* __restrict__ in, double2* __restrict__ out, int n, int inverse) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  double re = 0.0, im = 0.0;
+  long long p = 0;
+  for (int m = 0; m < n; ++m) {
+    double sn, cs;
+    sincospi(2.0 * static_cast<double>(p) / n, &sn, &cs);
+    if (!inverse) sn = -sn;
+    const double2 v = in[m];
+    re += v.x * cs - v.y * sn;
+    im += v.x * sn + v.y * cs;
+    p += k;
+    if (p >= n) p -= n;
+  }
+  out[k] = make_double2(re, im);
+}
+
+}  // namespace
+
+cudaError_t generic_rfft(const GenericJob& job, const double* x, double2* half, void* ws, cudaStream_t st) {
+  long long numel = 1;
+  for (int a = 0; a < job.rank; ++a) numel *= job.dims[a];
+  const long long total = numel * job.batch;
+  const int nl = job.dims[job.rank - 1], h = nl / 2 + 1;
+  double2* cur = static_cast<double2*>(ws);
+  double2* nxt = cur + total;
+  const int g = nblocks(total);
+  g_real_to_complex<<<g, kThreads, 0, st>>>(x, cur, total);
+  dft_axes(job, 0, job.rank, cur, nxt, 0, g, st);
+  g_take_half<<<nblocks(total / nl * h), kThreads, 0, st>>>(cur, half, total / nl, nl, h);
+  return cudaGetLastError();
+}
+
+cudaError_t generic_irfft(const GenericJob& job, const double2* half, double* x, void* ws, cudaStream_t st) {
+  long long numel = 1;
+  for (int a = 0; a < job.rank; ++a) numel *= job.dims[a];
+  const long long total = numel * job.batch;
+  const int nl = job.dims[job.rank - 1], h = nl / 2 + 1;
+  const long long rows = total / nl;
+  double2* cur = static_cast<double2*>(ws);
+  double2* nxt = cur + total;
+  cudaError_t e = cudaMemcpyAsync(cur, half, static_cast<size_t>(rows) * h * sizeof(double2),
+                                  cudaMemcpyDeviceToDevice, st);
+  if (e != cudaSuccess) return e;
+  GenericJob jh = job;  // the leading axes run on the half-width layout
+  jh.dims[job.rank - 1] = h;
+  dft_axes(jh, 0, job.rank - 1, cur, nxt, 1, nblocks(rows * h), st);
+  g_hermitian_rows<<<nblocks(total), kThreads, 0, st>>>(cur, nxt, rows, nl, h);
+  std::swap(cur, nxt);
+  dft_axes(job, job.rank - 1, job.rank, cur, nxt, 1, nblocks(total), st);
+  g_real_part<<<nblocks(total), kThreads, 0, st>>>(cur, x, total);
+  return cudaGetLastError();
+}
+
+cudaError_t dft_naive_run(const double2* in, double2* out, int n, bool inverse, cudaStream_t st) {
+  g_dft_naive<<<(n + 127) / 128, 128, 0, st>>>(in, out, n, inverse ? 1 : 0);
   return cudaGetLastError();
 }
 

@@ -23,6 +23,7 @@
 #include "../../include/sdct_b200.h"
 #include "fast_launch.cuh"
 #include "generic.h"
+#include "kernels_rowcol.cuh"
 
 using namespace sdctb;
 
@@ -138,13 +139,23 @@ struct sdct_plan_s {
   std::mutex mu;
 
   void* aux = nullptr;  // sdct_force_fields scratch (coefficients + weighted copy), lazily allocated
-  std::mutex gws_mu;    // guards the lazy gws allocation
-  void* gws = nullptr;  // generic-path scratch on fast plans (row-column), lazily allocated
+  std::mutex gws_mu;    // guards the lazy workspace allocation (ensure_ws)
+  // row-column kernels (rank 2): per axis a with a pow2 extent in [8, 8192],
+  // stage tables of the n_a/2-point row FFT, quarter-wave and W_{n_a} tables
+  bool rc_ok[2] = {false, false};
+  TwSet rc_tw[2] = {};
+  void* rc_q[2] = {nullptr, nullptr};
+  void* rc_w[2] = {nullptr, nullptr};
+  void* rws = nullptr;  // rfft_nd / irfft_nd scratch (generic size), lazily allocated
   size_t elem() const { return dtype == SDCT_F32 ? 4 : 8; }
   size_t generic_ws_bytes() const {
     return 2 * static_cast<size_t>(batch) * static_cast<size_t>(numel) * sizeof(double2);
   }
   size_t item_bytes() const { return static_cast<size_t>(numel) * elem(); }
+  // coefficient scratch of force fields / compression: two tensor-sized
+  // halves, the second 256-B aligned (every device buffer handed to a kernel
+  // is 16-B aligned)
+  size_t aux_half() const { return (static_cast<size_t>(batch) * item_bytes() + 255) & ~size_t(255); }
   size_t table_bytes = 0;  // the one table allocation
 };
 
@@ -348,7 +359,26 @@ int build_plan(sdct_plan_s* p) {
     if (r == 3) p->nl[1] = pick_nl(static_cast<int>(p->elem()), p->n[1], p->M, static_cast<long long>(p->n[0]) * p->batch);
     p->ws_bytes = static_cast<size_t>(p->batch) * p->item_bytes();
   } else {
-    p->ws_bytes = p->generic_ws_bytes();
+    // generic scratch, plus (rank 2) one real tensor for the row-column passes
+    p->ws_bytes = p->generic_ws_bytes() + (r == 2 ? static_cast<size_t>(p->batch) * p->item_bytes() : 0);
+  }
+  // row-column row-DCT tables (kernels_rowcol.cuh)
+  size_t off_rcst[2][4], off_rcq[2] = {0, 0}, off_rcw[2] = {0, 0};
+  if (r == 2) {
+    for (int a = 0; a < 2; ++a) {
+      const int n = p->n[a];
+      p->rc_ok[a] = is_pow2(n) && n >= 8 && n <= 2 * kMaxFastLen;
+      if (!p->rc_ok[a]) continue;
+      const bool f32 = p->dtype == SDCT_F32;
+      if (f32) stage_tables<float>(blob, n / 2, off_rcst[a]);
+      else stage_tables<double>(blob, n / 2, off_rcst[a]);
+      circle(re, im, n, 1.0L, 4.0L * n);
+      if (f32) fill_table<float>(blob, off_rcq[a], re, im);
+      else fill_table<double>(blob, off_rcq[a], re, im);
+      circle(re, im, n / 2 + 1, 1.0L, n);
+      if (f32) fill_table<float>(blob, off_rcw[a], re, im);
+      else fill_table<double>(blob, off_rcw[a], re, im);
+    }
   }
   // generic-path tables are always present (odd shapes, row-column, 1D)
   size_t off_bc[3] = {0, 0, 0}, off_bh[3] = {0, 0, 0}, off_bm[3] = {0, 0, 0};
@@ -416,6 +446,12 @@ int build_plan(sdct_plan_s* p) {
       p->bcircle[a] = reinterpret_cast<double2*>(base + off_bm[a]);
     }
   }
+  for (int a = 0; a < 2; ++a) {
+    if (!p->rc_ok[a]) continue;
+    for (int k = 0; k < 4; ++k) p->rc_tw[a].st[k] = off_rcst[a][k] == SIZE_MAX ? nullptr : base + off_rcst[a][k];
+    p->rc_q[a] = base + off_rcq[a];
+    p->rc_w[a] = base + off_rcw[a];
+  }
   p->b_offset_gen = r >= 2 ? off_gq[1] : off_gq[0];
   // the plan-owned workspace is allocated on first use with no caller
   // workspace (ensure_ws): the torch path always passes its own
@@ -429,6 +465,8 @@ bool kind_ok(const sdct_plan_s* p, int kind) {
     case SDCT_IDCT_IDXST_2D:
     case SDCT_IDXST_IDCT_2D:
     case SDCT_DCT_2D_ROWCOL:
+    case SDCT_IDCT_IDXST_2D_ROWCOL:
+    case SDCT_IDXST_IDCT_2D_ROWCOL:
       return p->rank == 2;
     case SDCT_DCT_3D:
     case SDCT_IDCT_3D:
@@ -732,7 +770,6 @@ GenericJob make_job(const sdct_plan_s* p, int kind) {
     j.blue_circle[a] = p->bcircle[a];
   }
   j.batch = p->batch;
-  j.legacy = kind == SDCT_DCT_2D_ROWCOL;
   switch (kind) {
     case SDCT_IDCT_2D: j.inverse = true; j.scale = 0.25; break;
     case SDCT_IDXST_IDCT_2D: j.inverse = true; j.scale = 0.25; j.mode = 1; j.sign_axis = 0; break;
@@ -746,12 +783,81 @@ GenericJob make_job(const sdct_plan_s* p, int kind) {
 }
 
 
+bool is_rowcol(int kind) {
+  return kind == SDCT_DCT_2D_ROWCOL || kind == SDCT_IDCT_IDXST_2D_ROWCOL || kind == SDCT_IDXST_IDCT_2D_ROWCOL;
+}
+
+// Row-column transforms (kernels_rowcol.cuh): axis-1 pass, transpose, axis-0
+// pass, transpose — stages 0..3; stage k reads/writes what the full transform
+// would. The intermediate is one real tensor in the workspace (after the
+// generic scratch on generic plans).
+template <typename T>
+int run_rowcol(sdct_plan_s* p, int kind, int only_stage, const void* in, void* out, void* ws, cudaStream_t st,
+               int* nstages) {
+  const int n1 = p->n[0], n2 = p->n[1];
+  const long long B = p->batch;
+  void* gscratch = p->fast ? nullptr : ws;
+  T* tmp = reinterpret_cast<T*>(static_cast<unsigned char*>(ws) + (p->fast ? 0 : p->generic_ws_bytes()));
+  const bool inv = kind != SDCT_DCT_2D_ROWCOL;
+  // IdctIdxst: sine along axis 1 (the rows of the first pass); IdxstIdct: along axis 0
+  const bool sine_rows = kind == SDCT_IDCT_IDXST_2D_ROWCOL, sine_cols = kind == SDCT_IDXST_IDCT_2D_ROWCOL;
+  cudaError_t e = cudaSuccess;
+  auto pass = [&](int axis, long long rows, const void* src, void* dst, bool sine) {
+    const int n = p->n[axis];
+    RcArgs a{};
+    a.src = src;
+    a.dst = dst;
+    a.rows = rows;
+    a.n = n;
+    a.sine = sine ? 1 : 0;
+    if (p->rc_ok[axis]) {
+      a.tq = p->rc_q[axis];
+      a.tw = p->rc_w[axis];
+      return launch_rowdct<T>(n, inv, a, p->rc_tw[axis], st);
+    }
+    if (n <= 64 || !gscratch) return launch_rowdct_direct<T>(inv, a, st);
+    GenericJob j;  // longer non-pow2 rows: the generic 1D path, batched over the rows
+    j.rank = 1;
+    j.dims[0] = n;
+    j.batch = rows;
+    j.quarter[0] = p->gq[axis];
+    j.circle[0] = p->gc[axis];
+    if (inv) {
+      j.inverse = true;
+      j.scale = 0.5;
+      j.mode = sine ? 2 : 0;
+      j.sign_axis = sine ? 0 : -1;
+    }
+    return generic_run<T>(j, src, dst, gscratch, st);
+  };
+  auto transpose = [&](const void* src, void* dst, int R, int C) {
+    const size_t item = static_cast<size_t>(R) * C * sizeof(T);
+    cudaError_t r = cudaSuccess;
+    for (long long b0 = 0; b0 < B && r == cudaSuccess; b0 += 65535)
+      r = launch_transpose<T>(static_cast<const unsigned char*>(src) + b0 * item,
+                              static_cast<unsigned char*>(dst) + b0 * item, R, C, std::min<long long>(65535, B - b0),
+                              st);
+    return r;
+  };
+  for (int stage = 0; stage < 4 && e == cudaSuccess; ++stage) {
+    if (only_stage >= 0 && only_stage != stage) continue;
+    switch (stage) {
+      case 0: e = pass(1, B * n1, in, tmp, sine_rows); break;
+      case 1: e = transpose(tmp, out, n1, n2); break;
+      case 2: e = pass(0, B * n2, out, tmp, sine_cols); break;
+      default: e = transpose(tmp, out, n2, n1); break;
+    }
+  }
+  if (nstages) *nstages = 4;
+  if (e != cudaSuccess) return cuda_fail(e, "launching row-column kernels");
+  return SDCT_OK;
+}
+
 template <typename T>
 int run(sdct_plan_s* p, int kind, int only_stage, const void* in, void* out, void* ws,
         cudaStream_t st, int* nstages, int weight, const Threshold* thr) {
-  // Row-column baseline and the 1D transforms run on the generic path.
-  const bool use_fast = p->fast && kind != SDCT_DCT_2D_ROWCOL;
-  if (use_fast) {
+  if (is_rowcol(kind)) return run_rowcol<T>(p, kind, only_stage, in, out, ws, st, nstages);
+  if (p->fast) {
     // batch items ride on grid.y / grid.z (<= 65535): larger batches run as
     // consecutive launch sets over contiguous chunks (same workspace layout)
     const long long chunk = 65535;
@@ -770,19 +876,6 @@ int run(sdct_plan_s* p, int kind, int only_stage, const void* in, void* out, voi
   }
   if (nstages) *nstages = 1;  // generic path is timed as one unit
   if (only_stage > 0) return SDCT_OK;
-  if (p->fast) {
-    // fast plan running a generic-path transform (row-column, 1D): needs the
-    // larger generic scratch, which the plan owns (a caller's workspace is
-    // sized for the fast path by sdct_plan_workspace_size)
-    {
-      std::lock_guard<std::mutex> lock(p->gws_mu);  // not p->mu: host entry points hold it across dispatch
-      if (!p->gws) {
-        cudaError_t ea = cudaMalloc(&p->gws, p->generic_ws_bytes());
-        if (ea != cudaSuccess) return cuda_fail(ea, "allocating generic scratch");
-      }
-    }
-    ws = p->gws;
-  }
   cudaError_t e = generic_run<T>(make_job(p, kind), in, out, ws, st);
   if (e != cudaSuccess) return cuda_fail(e, "launching generic-path kernels");
   return SDCT_OK;
@@ -978,9 +1071,9 @@ int sdct_plan_destroy(sdct_plan_t p) {
   cudaFree(p->ws);
   cudaFree(p->d_in);
   cudaFree(p->d_out);
-  cudaFree(p->gws);
   cudaFree(p->aux);
   cudaFree(p->badq);
+  cudaFree(p->rws);
   for (int l = 0; l < sdct_plan_s::kLanes; ++l) {
     for (void* b : p->lane_buf[l]) cudaFree(b);
     if (p->lane_st[l]) cudaStreamDestroy(p->lane_st[l]);
@@ -1007,8 +1100,8 @@ int sdct_plan_device_bytes(sdct_plan_t p, size_t* bytes) {
   if (!p || !bytes) return fail(SDCT_ERR_ARG, "null argument");
   std::lock_guard<std::mutex> lock(p->mu);
   const size_t item = static_cast<size_t>(p->batch) * p->item_bytes();
-  size_t b = p->table_bytes + (p->ws ? p->ws_bytes : 0) + (p->d_in ? 2 * item : 0) + (p->aux ? 2 * item : 0) +
-             (p->badq ? static_cast<size_t>(p->n[p->rank >= 2 ? 1 : 0]) : 0);
+  size_t b = p->table_bytes + (p->ws ? p->ws_bytes : 0) + (p->d_in ? 2 * item : 0) + (p->aux ? 2 * p->aux_half() : 0) +
+             (p->badq ? static_cast<size_t>(p->n[p->rank >= 2 ? 1 : 0]) : 0) + (p->rws ? p->generic_ws_bytes() : 0);
   if (p->lane_st[0]) b += sdct_plan_s::kLanes * (2 * item + p->ws_bytes);
   *bytes = b;
   return SDCT_OK;
@@ -1081,12 +1174,12 @@ int sdct_force_fields(sdct_plan_t p, const void* d_density, void* d_xi1, void* d
   {
     std::lock_guard<std::mutex> lock(p->mu);
     if (!p->aux) {
-      cudaError_t e = cudaMalloc(&p->aux, 2 * bytes);
+      cudaError_t e = cudaMalloc(&p->aux, 2 * p->aux_half());
       if (e != cudaSuccess) return cuda_fail(e, "allocating force-field scratch");
     }
   }
   void* a = p->aux;                                     // DCT coefficients of the density
-  void* aw = static_cast<unsigned char*>(p->aux) + bytes;  // generic path: weighted copy
+  void* aw = static_cast<unsigned char*>(p->aux) + p->aux_half();  // generic path: weighted copy
   int rc = dispatch(p, SDCT_DCT_2D, -1, d_density, a, d_ws, st, nullptr);
   if (rc != SDCT_OK) return rc;
   if (p->fast) {
@@ -1117,7 +1210,7 @@ int sdct_compress(sdct_plan_t p, const void* d_in, void* d_out, double epsilon, 
   {
     std::lock_guard<std::mutex> lock(p->mu);
     if (!p->aux) {
-      cudaError_t e = cudaMalloc(&p->aux, 2 * bytes);
+      cudaError_t e = cudaMalloc(&p->aux, 2 * p->aux_half());
       if (e != cudaSuccess) return cuda_fail(e, "allocating coefficient scratch");
     }
   }
@@ -1129,7 +1222,7 @@ int sdct_compress(sdct_plan_t p, const void* d_in, void* d_out, double epsilon, 
   thr.scale = 4.0 / (static_cast<double>(p->n[0]) * static_cast<double>(p->n[1]));
   thr.count = d_zeroed;
   if (p->fast) return dispatch(p, SDCT_IDCT_2D, -1, b, d_out, d_ws, st, nullptr, 3, &thr);
-  void* bw = static_cast<unsigned char*>(p->aux) + bytes;
+  void* bw = static_cast<unsigned char*>(p->aux) + p->aux_half();
   cudaError_t e = compress_threshold(b, bw, static_cast<long long>(p->batch) * p->numel, thr.eps, thr.scale, d_zeroed,
                                      p->dtype == SDCT_F32, st);
   if (e != cudaSuccess) return cuda_fail(e, "launching compression threshold");
@@ -1242,10 +1335,144 @@ int sdct_exec_host(sdct_plan_t p, int kind, const void* h_in, void* h_out, void*
   return SDCT_OK;
 }
 
+int sdct_transpose(int dtype, int64_t rows, int64_t cols, int64_t batch, const void* d_in, void* d_out,
+                   void* stream) {
+  if (!d_in || !d_out || d_in == d_out) return fail(SDCT_ERR_ARG, "sdct_transpose: distinct non-null buffers needed");
+  if (dtype != SDCT_F32 && dtype != SDCT_F64) return fail(SDCT_ERR_ARG, "dtype must be SDCT_F32 or SDCT_F64");
+  if (rows <= 0 || cols <= 0 || batch <= 0 || rows > (1LL << 30) || cols > (1LL << 30))
+    return fail(SDCT_ERR_SHAPE, "sdct_transpose: extents must be positive");
+  const size_t es = dtype == SDCT_F32 ? 4 : 8;
+  const size_t item = static_cast<size_t>(rows) * static_cast<size_t>(cols) * es;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaError_t e = cudaSuccess;
+  for (int64_t b0 = 0; b0 < batch && e == cudaSuccess; b0 += 65535) {
+    const long long bc = std::min<long long>(65535, batch - b0);
+    const void* in = static_cast<const unsigned char*>(d_in) + b0 * item;
+    void* out = static_cast<unsigned char*>(d_out) + b0 * item;
+    e = dtype == SDCT_F32 ? launch_transpose<float>(in, out, static_cast<int>(rows), static_cast<int>(cols), bc, st)
+                          : launch_transpose<double>(in, out, static_cast<int>(rows), static_cast<int>(cols), bc, st);
+  }
+  if (e != cudaSuccess) return cuda_fail(e, "launching transpose");
+  return SDCT_OK;
+}
+
+int sdct_rfft_workspace_size(sdct_plan_t p, size_t* bytes) {
+  if (!p || !bytes) return fail(SDCT_ERR_ARG, "null argument");
+  *bytes = p->generic_ws_bytes();
+  return SDCT_OK;
+}
+
+namespace {
+GenericJob rfft_job(const sdct_plan_s* p) {
+  GenericJob j;
+  j.rank = p->rank;
+  for (int a = 0; a < p->rank; ++a) {
+    j.dims[a] = p->n[a];
+    j.circle[a] = p->gc[a];
+  }
+  j.batch = p->batch;
+  return j;
+}
+
+// plan-owned generic scratch for the rfft kinds (lazily allocated)
+int rfft_scratch(sdct_plan_s* p, void** ws) {
+  if (*ws) return SDCT_OK;
+  std::lock_guard<std::mutex> lock(p->gws_mu);
+  if (!p->rws) {
+    DeviceGuard g(p->device);
+    cudaError_t e = cudaMalloc(&p->rws, p->generic_ws_bytes());
+    if (e != cudaSuccess) return cuda_fail(e, "allocating rfft scratch");
+  }
+  *ws = p->rws;
+  return SDCT_OK;
+}
+
+size_t half_bytes(const sdct_plan_s* p) {
+  const size_t nl = static_cast<size_t>(p->n[p->rank - 1]);
+  return static_cast<size_t>(p->batch) * (static_cast<size_t>(p->numel) / nl) * (nl / 2 + 1) * sizeof(double2);
+}
+}  // namespace
+
+int sdct_rfft_nd(sdct_plan_t p, const void* d_x, void* d_half, void* d_ws, void* stream) {
+  if (!p || !d_x || !d_half) return fail(SDCT_ERR_ARG, "null argument to sdct_rfft_nd");
+  if (p->dtype != SDCT_F64) return fail(SDCT_ERR_ARG, "sdct_rfft_nd: fp64 plans only (the reference is fp64)");
+  int rc = rfft_scratch(p, &d_ws);
+  if (rc != SDCT_OK) return rc;
+  DeviceGuard g(p->device);
+  cudaError_t e = generic_rfft(rfft_job(p), static_cast<const double*>(d_x), static_cast<double2*>(d_half), d_ws,
+                               static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? SDCT_OK : cuda_fail(e, "launching rfft_nd");
+}
+
+int sdct_irfft_nd(sdct_plan_t p, const void* d_half, void* d_x, void* d_ws, void* stream) {
+  if (!p || !d_x || !d_half) return fail(SDCT_ERR_ARG, "null argument to sdct_irfft_nd");
+  if (p->dtype != SDCT_F64) return fail(SDCT_ERR_ARG, "sdct_irfft_nd: fp64 plans only (the reference is fp64)");
+  int rc = rfft_scratch(p, &d_ws);
+  if (rc != SDCT_OK) return rc;
+  DeviceGuard g(p->device);
+  cudaError_t e = generic_irfft(rfft_job(p), static_cast<const double2*>(d_half), static_cast<double*>(d_x), d_ws,
+                                static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? SDCT_OK : cuda_fail(e, "launching irfft_nd");
+}
+
+namespace {
+// host round trip through temporary device buffers (stage-level API, not a hot path)
+int rfft_host(sdct_plan_t p, const void* h_in, size_t in_bytes, void* h_out, size_t out_bytes, bool inverse) {
+  DeviceGuard g(p->device);
+  void* a = nullptr;
+  void* b = nullptr;
+  cudaError_t e = cudaMalloc(&a, in_bytes);
+  if (e == cudaSuccess) e = cudaMalloc(&b, out_bytes);
+  int rc = e == cudaSuccess ? SDCT_OK : cuda_fail(e, "allocating rfft buffers");
+  if (rc == SDCT_OK && (e = cudaMemcpy(a, h_in, in_bytes, cudaMemcpyHostToDevice)) != cudaSuccess)
+    rc = cuda_fail(e, "copying rfft input");
+  if (rc == SDCT_OK) rc = inverse ? sdct_irfft_nd(p, a, b, nullptr, nullptr) : sdct_rfft_nd(p, a, b, nullptr, nullptr);
+  if (rc == SDCT_OK && (e = cudaMemcpy(h_out, b, out_bytes, cudaMemcpyDeviceToHost)) != cudaSuccess)
+    rc = cuda_fail(e, "copying rfft output");
+  cudaFree(a);
+  cudaFree(b);
+  return rc;
+}
+}  // namespace
+
+int sdct_rfft_nd_host(sdct_plan_t p, const double* h_x, double* h_half) {
+  if (!p || !h_x || !h_half) return fail(SDCT_ERR_ARG, "null argument to sdct_rfft_nd_host");
+  return rfft_host(p, h_x, static_cast<size_t>(p->batch) * p->numel * sizeof(double), h_half, half_bytes(p), false);
+}
+
+int sdct_irfft_nd_host(sdct_plan_t p, const double* h_half, double* h_x) {
+  if (!p || !h_x || !h_half) return fail(SDCT_ERR_ARG, "null argument to sdct_irfft_nd_host");
+  return rfft_host(p, h_half, half_bytes(p), h_x, static_cast<size_t>(p->batch) * p->numel * sizeof(double), true);
+}
+
+int sdct_dft_naive_host(int64_t n, int inverse, const double* h_in, double* h_out) {
+  if (!h_in || !h_out) return fail(SDCT_ERR_ARG, "null argument to sdct_dft_naive_host");
+  if (n <= 0 || n > (1LL << 24)) return fail(SDCT_ERR_SHAPE, "dft_naive: length must be in 1..2^24");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    return fail(SDCT_ERR_NODEVICE, "no CUDA device available");
+  }
+  const size_t bytes = static_cast<size_t>(n) * sizeof(double2);
+  void* a = nullptr;
+  void* b = nullptr;
+  cudaError_t e = cudaMalloc(&a, bytes);
+  if (e == cudaSuccess) e = cudaMalloc(&b, bytes);
+  if (e == cudaSuccess) e = cudaMemcpy(a, h_in, bytes, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = dft_naive_run(static_cast<const double2*>(a), static_cast<double2*>(b), static_cast<int>(n),
+                                          inverse != 0, nullptr);
+  if (e == cudaSuccess) e = cudaMemcpy(h_out, b, bytes, cudaMemcpyDeviceToHost);
+  cudaFree(a);
+  cudaFree(b);
+  return e == cudaSuccess ? SDCT_OK : cuda_fail(e, "dft_naive");
+}
+
 int sdct_stage_count(sdct_plan_t p, int kind, int* count) {
   if (!p || !count) return fail(SDCT_ERR_ARG, "null argument");
   if (!kind_ok(p, kind)) return fail(SDCT_ERR_PLAN, "transform kind does not match the plan rank");
-  if (p->fast && kind != SDCT_DCT_2D_ROWCOL) {
+  if (is_rowcol(kind)) {
+    *count = 4;
+  } else if (p->fast) {
     *count = p->rank == 2 ? 2 : 3;
   } else {
     *count = 1;
@@ -1277,7 +1504,9 @@ int sdct_counters(sdct_plan_t p, int kind, uint64_t out[5]) {
     case SDCT_IDCT_IDXST_2D: count_idct2(m1, m2, tr ? 1 : 2, c); break;
     case SDCT_DCT_3D: count_dct3(p->n[0], p->n[1], p->n[2], c); break;
     case SDCT_IDCT_3D: count_idct3(p->n[0], p->n[1], p->n[2], c); break;
-    case SDCT_DCT_2D_ROWCOL: c.stages = 8; break;
+    case SDCT_DCT_2D_ROWCOL:
+    case SDCT_IDCT_IDXST_2D_ROWCOL:
+    case SDCT_IDXST_IDCT_2D_ROWCOL: c.stages = 8; break;  // 3 + 1 + 3 + 1 (dct2d.cpp:398-405)
     default: c.stages = 3; break;
   }
   const unsigned long long b = static_cast<unsigned long long>(p->batch);

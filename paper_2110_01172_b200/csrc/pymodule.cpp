@@ -99,6 +99,22 @@ PYBIND11_MODULE(_sdct, m) {
           });
         },
         py::arg("x"), py::arg("threads") = 0, "Row-column 2D DCT (same output as dct_2d)");
+  m.def("idct_idxst_2d_rowcol",
+        [](const Array& x, unsigned) {
+          return run(x, [](const sdct::RealTensor& t) {
+            if (t.rank() != 2) throw sdct::ShapeError("idct_idxst_2d_rowcol expects a rank-2 array");
+            return sdct::idct_idxst_2d_rowcol(t, sdct::Plan2d(t.dim(0), t.dim(1)));
+          });
+        },
+        py::arg("x"), py::arg("threads") = 0, "Row-column IDCT/IDXST composite (same output as idct_idxst_2d)");
+  m.def("idxst_idct_2d_rowcol",
+        [](const Array& x, unsigned) {
+          return run(x, [](const sdct::RealTensor& t) {
+            if (t.rank() != 2) throw sdct::ShapeError("idxst_idct_2d_rowcol expects a rank-2 array");
+            return sdct::idxst_idct_2d_rowcol(t, sdct::Plan2d(t.dim(0), t.dim(1)));
+          });
+        },
+        py::arg("x"), py::arg("threads") = 0, "Row-column IDXST/IDCT composite (same output as idxst_idct_2d)");
   m.def("idct_2d",
         [](const Array& x, unsigned) { return run(x, [](const sdct::RealTensor& t) { return sdct::idct_2d(t); }); },
         py::arg("x"), py::arg("threads") = 0, "Fused inverse 2D DCT (idct_2d(dct_2d(x)) == N1*N2/4 * x)");
@@ -224,6 +240,8 @@ PYBIND11_MODULE(_sdct, m) {
   m.attr("DCT_3D") = py::int_(static_cast<int>(SDCT_DCT_3D));
   m.attr("IDCT_3D") = py::int_(static_cast<int>(SDCT_IDCT_3D));
   m.attr("DCT_2D_ROWCOL") = py::int_(static_cast<int>(SDCT_DCT_2D_ROWCOL));
+  m.attr("IDCT_IDXST_2D_ROWCOL") = py::int_(static_cast<int>(SDCT_IDCT_IDXST_2D_ROWCOL));
+  m.attr("IDXST_IDCT_2D_ROWCOL") = py::int_(static_cast<int>(SDCT_IDXST_IDCT_2D_ROWCOL));
   m.attr("DCT_1D") = py::int_(static_cast<int>(SDCT_DCT_1D));
   m.attr("IDCT_1D") = py::int_(static_cast<int>(SDCT_IDCT_1D));
   m.attr("IDXST_1D") = py::int_(static_cast<int>(SDCT_IDXST_1D));

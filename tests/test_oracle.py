@@ -124,6 +124,21 @@ def test_reference_library_agrees_when_built():
         assert np.array_equal(getattr(oracle.port, kind)(x), oracle.ref.run(kind, x)), kind
 
 
+@pytest.mark.parametrize("shape", [(1, 1), (1, 5), (3, 1), (2, 8), (7, 9), (8, 8), (16, 12), (31, 17), (64, 48)])
+def test_port_rowcol_bitwise_equals_reference(shape):
+    # dct_rows / inverse_rows + transposes (dct2d.cpp:248-290,395-406,
+    # transforms_ext.cpp:40-88,287-311) restated in C vs the unmodified reference
+    if not oracle.ref_available():
+        pytest.skip("oracle/_ref not built (make -C oracle ref)")
+    x = np.random.default_rng(7).uniform(-1, 1, shape)
+    for kind, fused in (("dct_2d_rowcol", "dct_2d"), ("idct_idxst_2d_rowcol", "idct_idxst_2d"),
+                        ("idxst_idct_2d_rowcol", "idxst_idct_2d")):
+        got = getattr(oracle.port, kind)(x)
+        assert np.array_equal(got, oracle.ref.run(kind, x)), (kind, shape)
+        # and the row-column forms agree with the fused ones (acceptance.cpp:291-321)
+        assert oracle.max_rel(got, getattr(oracle.port, fused)(x)) <= 1e-10, (kind, shape)
+
+
 def test_port_force_fields_match_reference_golden(golden):
     # proj/src/force.cpp:11-37 through the reference's pybind module
     keys = _keys(golden, "force_xi1")
