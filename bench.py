@@ -646,6 +646,29 @@ def run_ours(args, rank: int, world: int, local_rank: int, backend: str | None =
         parity["e2e_round_trip_rel_l2"] = float(((out_pin[0].to(torch.float64) / (numel / 4.0) - x0).norm()
                                                  / x0.norm()).item())
 
+    # ---- second e2e figure: the reference's own Python surface on numpy -------
+    # sdct.dct_2d(numpy) -> sdct.idct_2d(numpy): float64 pageable host arrays in
+    # and out of every call (as the reference module takes and returns them),
+    # device plans from the C++ plan cache. Host-synchronous, so wall clock.
+    e2e_np = None
+    if (w["mode"] == "chain" and w["kinds"] == ["dct_2d", "idct_2d"] and dtype == "float64" and B == 1):
+        import numpy as np
+
+        x_np = xs[0][0].double().cpu().numpy()
+        y_np = sd.idct_2d(sd.dct_2d(x_np))  # warm: plan cache + allocator
+        n_np = 5
+        barrier()
+        t_np = time.perf_counter()
+        for _ in range(n_np):
+            y_np = sd.idct_2d(sd.dct_2d(x_np))
+        np_ms = (time.perf_counter() - t_np) * 1e3 / n_np
+        np_ms = max_over_ranks(np_ms)
+        e2e_np = {"value": round(bytes_step / (np_ms / 1e3) / 1e9, 3), "unit": UNIT, "ms_per_step": round(np_ms, 4),
+                  "h2d_bytes_per_step": 2 * x_np.nbytes, "d2h_bytes_per_step": 2 * x_np.nbytes,
+                  "path": "sdct.dct_2d(numpy) -> sdct.idct_2d(numpy): reference Python surface, float64 pageable "
+                          "host arrays per call, cached device plans, wall clock",
+                  "round_trip_rel_l2": float(np.linalg.norm(y_np / (numel / 4.0) - x_np) / np.linalg.norm(x_np))}
+
     # ---- CPU baseline (rank 0, N = 1 only) -----------------------------------
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -680,6 +703,7 @@ def run_ours(args, rank: int, world: int, local_rank: int, backend: str | None =
                              if w["mode"] == "compress" else
                              f"pinned host -> paper_2110_01172_b200.stream_host({w['kinds']}) "
                              "(sdct_exec_host_pipelined, 3 overlapped lanes) -> pinned host")},
+            "e2e_numpy": e2e_np,
             "gpu_launches": args.steps * sum(plan.stage_count(k) for k in kinds),
             "clocks": clk,
             "cufft": cufft,

@@ -20,8 +20,12 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 INC = os.path.join(ROOT, "include")
-OBJ = os.path.join(ROOT, "build", "obj")
-LIB = os.path.join(PKG, "lib")
+# SDCT_BUILD_TAG / SDCT_EXTRA_NVFLAGS: developer A/B builds of the library
+# into build/obj_<tag> and paper_2110_01172_b200/lib_<tag> (selected at run
+# time with LD_LIBRARY_PATH); the default build uses neither.
+_TAG = os.environ.get("SDCT_BUILD_TAG", "")
+OBJ = os.path.join(ROOT, "build", "obj" + ("_" + _TAG if _TAG else ""))
+LIB = os.path.join(PKG, "lib" + ("_" + _TAG if _TAG else ""))
 LIBSO = os.path.join(LIB, "libsdct_b200.so")
 EXT = sysconfig.get_config_var("EXT_SUFFIX") or ".so"
 PYMOD = os.path.join(PKG, "_sdct" + EXT)
@@ -29,7 +33,7 @@ PYMOD = os.path.join(PKG, "_sdct" + EXT)
 NVCC = os.environ.get("NVCC", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = ["-std=c++17", "--expt-relaxed-constexpr", "-O3", "-lineinfo", "-Xcompiler", "-fPIC",
-           "-Xcompiler", "-O3", "-I", INC, "-I", CSRC]
+           "-Xcompiler", "-O3", "-I", INC, "-I", CSRC] + os.environ.get("SDCT_EXTRA_NVFLAGS", "").split()
 CXXFLAGS = ["-std=c++20", "-O2", "-fPIC", "-I", INC]
 
 
@@ -81,6 +85,8 @@ def build(verbose: bool = False, jobs: int | None = None) -> str:
         objs = list(ex.map(lambda s: _compile(s, hdr_time, verbose), lib_srcs))
     if not os.path.exists(LIBSO) or os.path.getmtime(LIBSO) < _newest(objs):
         _run([NVCC] + ARCH + ["-shared", "-o", LIBSO] + objs + ["-Xlinker", "-soname=libsdct_b200.so"])
+    if _TAG:
+        return LIBSO  # A/B library only: the module and programs link the default one
     # pybind11 module over the C++ API
     import pybind11
 

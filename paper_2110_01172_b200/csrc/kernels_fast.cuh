@@ -132,6 +132,22 @@ template <> struct Vec2<double> { using type = double2; };
 // ============================================================================
 template <typename T>
 constexpr int tile_max_threads() { return 512; }
+// developer A/B knobs (build.py SDCT_EXTRA_NVFLAGS); defaults are the measured best
+#ifndef SDCT_COL_MAXT_F64
+#define SDCT_COL_MAXT_F64 512
+#endif
+#ifndef SDCT_COL_FULLTW
+#define SDCT_COL_FULLTW 0
+#endif
+#ifndef SDCT_ROW_FULLTW
+#define SDCT_ROW_FULLTW 0
+#endif
+#ifndef SDCT_COL_XS
+#define SDCT_COL_XS 1
+#endif
+#ifndef SDCT_COL_XS_INV
+#define SDCT_COL_XS_INV 0
+#endif
 
 template <typename T, int L_, int NL_, bool LF>
 struct Tile {
@@ -145,10 +161,11 @@ struct Tile {
   static constexpr int LGNL = ilog2c(NL);
   static constexpr int TOT = L * NL;
   static constexpr int NT0 = TOT / R0;
-  static constexpr int NT = NT0 > tile_max_threads<T>() ? tile_max_threads<T>() : NT0;
+  static constexpr int MAXT = (LF && sizeof(T) == 8) ? SDCT_COL_MAXT_F64 : tile_max_threads<T>();
+  static constexpr int NT = NT0 > MAXT ? MAXT : NT0;
   static constexpr int E = TOT / NT;
   static constexpr unsigned MASK = NT >= 32 ? 0xffffffffu : ((1u << NT) - 1u);
-  static constexpr bool TWF = false;  // true: load all R-1 stage twiddles (no derived products)
+  static constexpr bool TWF = LF && SDCT_COL_FULLTW;  // true: load all R-1 stage twiddles (no derived products)
   // barrier over the threads sharing this tile (whole CTA here; thread
   // groups with named barriers in the grouped row kernel)
   __device__ __forceinline__ static void sync() { __syncthreads(); }
@@ -416,6 +433,96 @@ __device__ __forceinline__ void dit_down(typename TL::V* v, typename TL::V* sm, 
   }
 }
 
+// ---- half-size exchanges (column kernels of 4096 x 2 tiles) -------------------
+// A stage-to-stage exchange normally needs the whole tile in shared memory.
+// Here it runs in two rounds through a buffer of half the tile: in round
+// `ROUND` every thread writes the 8 of its 16 outputs whose membership bit
+// (raw bit HB xor raw bit LB of the element's unswizzled tile address) equals
+// ROUND, and reads the 8 of its next-stage operands with that bit; so every
+// thread always holds 16 values (no extra registers). HB is dropped from the
+// address (xcpos), which is injective within a round because LB fixes it. The
+// swizzle only touches bits 0..2, so bank behaviour per instruction is that of
+// the full-tile pattern (conflict free). HB = 12, LB = 8: the CTA-wide
+// exchange between the stride-256 and stride-16 stages of a 4096-point
+// column (writers vary bit 12, readers bit 8). HB = 8, LB = 4: the warp-local
+// exchange between the stride-16 and unit-stride stages (each warp owns one
+// 256-row block: 4 KB of the buffer per warp, __syncwarp only).
+template <int HB>
+__device__ __forceinline__ int xcpos(int p) {
+  return ((p >> (HB + 1)) << HB) | (p & ((1 << HB) - 1));
+}
+template <int HB, int LB>
+constexpr int xmember(int p) {
+  return ((p >> HB) ^ (p >> LB)) & 1;
+}
+template <class TL, int s, int HB, int LB, int ROUND>
+__device__ __forceinline__ void xwrite(const typename TL::V* v, typename TL::V* X, int t) {
+  using P = typename TL::P;
+  constexpr int R = P::R(s), NBF = TL::E / R;
+#pragma unroll
+  for (int i = 0; i < NBF; ++i) {
+    const int sb = TL::template base<s>(t + i * TL::NT);
+    if (xmember<HB, LB>(sb) == ROUND) {
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+        if (xmember<HB, LB>(TL::template off<s>(r)) == 0) X[xcpos<HB>(sb ^ TL::template off<s>(r))] = v[i * R + r];
+    } else {
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+        if (xmember<HB, LB>(TL::template off<s>(r)) == 1) X[xcpos<HB>(sb ^ TL::template off<s>(r))] = v[i * R + r];
+    }
+  }
+}
+template <class TL, int s, int HB, int LB, int ROUND>
+__device__ __forceinline__ void xread(typename TL::V* v, const typename TL::V* X, int t) {
+  using P = typename TL::P;
+  constexpr int R = P::R(s), NBF = TL::E / R;
+#pragma unroll
+  for (int i = 0; i < NBF; ++i) {
+    const int sb = TL::template base<s>(t + i * TL::NT);
+    if (xmember<HB, LB>(sb) == ROUND) {
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+        if (xmember<HB, LB>(TL::template off<s>(r)) == 0) v[i * R + r] = X[xcpos<HB>(sb ^ TL::template off<s>(r))];
+    } else {
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+        if (xmember<HB, LB>(TL::template off<s>(r)) == 1) v[i * R + r] = X[xcpos<HB>(sb ^ TL::template off<s>(r))];
+    }
+  }
+}
+// CTA-wide exchange stage sw -> stage sr through X (caller: X free, synced)
+template <class TL, int sw, int sr>
+__device__ __forceinline__ void xchg_cta(typename TL::V* v, typename TL::V* X, int t) {
+  xwrite<TL, sw, 12, 8, 0>(v, X, t);
+  __syncthreads();
+  xread<TL, sr, 12, 8, 0>(v, X, t);
+  __syncthreads();
+  xwrite<TL, sw, 12, 8, 1>(v, X, t);
+  __syncthreads();
+  xread<TL, sr, 12, 8, 1>(v, X, t);
+}
+// warp-local exchange stage sw -> stage sr through X (caller: X free, synced)
+template <class TL, int sw, int sr>
+__device__ __forceinline__ void xchg_warp(typename TL::V* v, typename TL::V* X, int t) {
+  xwrite<TL, sw, 8, 4, 0>(v, X, t);
+  __syncwarp();
+  xread<TL, sr, 8, 4, 0>(v, X, t);
+  __syncwarp();
+  xwrite<TL, sw, 8, 4, 1>(v, X, t);
+  __syncwarp();
+  xread<TL, sr, 8, 4, 1>(v, X, t);
+}
+// tiles that take the early-reissue schedule: 4096-point columns, 2-wide
+// bands, 512 threads of 16 elements, three radix-16 stages
+// (measured on B200, 4096^2: fp64 forward column pass 86 -> 80 us; the fp64
+// inverse and both fp32 passes gain nothing, so they keep the in-tile schedule)
+template <class TL, bool INV>
+constexpr bool col_xs() {
+  return (INV ? SDCT_COL_XS_INV : SDCT_COL_XS) && sizeof(typename TL::Real) == 8 && TL::L == 4096 && TL::NL == 2 && TL::NT == 512 && TL::S == 3 && TL::P::R(0) == 16 &&
+         TL::P::R(1) == 16 && TL::P::R(2) == 16;
+}
+
 // ============================================================================
 // Column kernel
 // ============================================================================
@@ -538,22 +645,45 @@ __global__ void __launch_bounds__(Tile<T, L, NL, true>::NT)
         }
       }
       __syncthreads();  // raw tile consumed; smem becomes the exchange buffer
-      StageTw<TL, SL> wl;
-      if constexpr (S == 1) {
-        wl = w0;
-      } else {
+      if constexpr (col_xs<TL, false>()) {
+        // early reissue: the landing buffer is free now, so the next tile
+        // streams in under this tile's whole FFT; the exchanges run through
+        // the half-tile staging buffer X in balanced rounds
+        if (a.trace && t == 0) tr2 = gtimer();
+        if (t == 0 && tile + static_cast<int>(gridDim.x) < a.ntiles) {
+          fence_async_smem();
+          issue(tile + gridDim.x);
+        }
+        V* X = reinterpret_cast<V*>(stg);
+        StageTw<TL, 1> w1;
+        w1.load(tw.st[1], t);
         stage_compute<TL, 0, false>(v, w0);
-        to_smem<TL, 0>(v, sm, t);
+        if (t == 0) bulk_wait_read();  // the previous tile's stores have left X
         __syncthreads();
-        stages_until_last<TL, false, 1>(v, sm, tw, t, wl);
+        xchg_cta<TL, 0, 1>(v, X, t);
+        stage_compute<TL, 1, false>(v, w1);
+        __syncthreads();  // CTA-wide reads of X done before the warp-local writes
+        xchg_warp<TL, 1, 2>(v, X, t);
+        StageTw<TL, 2> w2;  // inactive (span == radix): no twiddles
+        stage_compute<TL, 2, false>(v, w2);
+      } else {
+        StageTw<TL, SL> wl;
+        if constexpr (S == 1) {
+          wl = w0;
+        } else {
+          stage_compute<TL, 0, false>(v, w0);
+          to_smem<TL, 0>(v, sm, t);
+          __syncthreads();
+          stages_until_last<TL, false, 1>(v, sm, tw, t, wl);
+        }
+        __syncthreads();  // last-stage operands are in registers: smem is free
+        if (a.trace && t == 0) tr2 = gtimer();
+        if (t == 0 && tile + static_cast<int>(gridDim.x) < a.ntiles) {
+          fence_async_smem();
+          issue(tile + gridDim.x);
+        }
+        stage_compute<TL, SL, false>(v, wl);
       }
-      __syncthreads();  // last-stage operands are in registers: smem is free
-      if (a.trace && t == 0) tr2 = gtimer();
-      if (t == 0 && tile + static_cast<int>(gridDim.x) < a.ntiles) {
-        fence_async_smem();
-        issue(tile + gridDim.x);
-      }
-      stage_compute<TL, SL, false>(v, wl);
       // ---- store: slot n = b*RL + r -> row sigma(n) = b + (L/RL)*r ----
       // PL parts of L/PL rows; with four parts the staging holds two
       // quarter buffers, so writing part q overlaps the TMA read of part q-1
@@ -603,17 +733,39 @@ __global__ void __launch_bounds__(Tile<T, L, NL, true>::NT)
         }
       }
       __syncthreads();  // raw tile consumed
-      dit_compute<TL, SL, true>(v, wl);
-      if constexpr (S > 1) {
-        to_smem<TL, SL>(v, sm, t);
+      if constexpr (col_xs<TL, true>()) {
+        // early reissue (see the forward): exchanges through X in rounds
+        if (a.trace && t == 0) tr2 = gtimer();
+        if (t == 0 && tile + static_cast<int>(gridDim.x) < a.ntiles) {
+          fence_async_smem();
+          issue(tile + gridDim.x);
+        }
+        V* X = reinterpret_cast<V*>(stg);
+        StageTw<TL, 1> w1;
+        w1.load(tw.st[1], t);
+        dit_compute<TL, 2, true>(v, wl);
+        if (t == 0) bulk_wait_read();  // the previous tile's stores have left X
         __syncthreads();
-        dit_down<TL, true, SL - 1>(v, sm, tw, t);  // ends with stage 0 in registers
-      }
-      __syncthreads();  // all smem reads done
-      if (a.trace && t == 0) tr2 = gtimer();
-      if (t == 0 && tile + static_cast<int>(gridDim.x) < a.ntiles) {
-        fence_async_smem();
-        issue(tile + gridDim.x);
+        xchg_warp<TL, 2, 1>(v, X, t);
+        dit_compute<TL, 1, true>(v, w1);
+        StageTw<TL, 0> w0;
+        w0.load(tw.st[0], t);
+        __syncthreads();  // warp-local reads of X done before the CTA-wide writes
+        xchg_cta<TL, 1, 0>(v, X, t);
+        dit_compute<TL, 0, true>(v, w0);
+      } else {
+        dit_compute<TL, SL, true>(v, wl);
+        if constexpr (S > 1) {
+          to_smem<TL, SL>(v, sm, t);
+          __syncthreads();
+          dit_down<TL, true, SL - 1>(v, sm, tw, t);  // ends with stage 0 in registers
+        }
+        __syncthreads();  // all smem reads done
+        if (a.trace && t == 0) tr2 = gtimer();
+        if (t == 0 && tile + static_cast<int>(gridDim.x) < a.ntiles) {
+          fence_async_smem();
+          issue(tile + gridDim.x);
+        }
       }
       // outputs: stage-0 butterfly (line, j) holds natural index ii = j + r*Q0
       // PI parts of L/PI rows (two quarter buffers when PI == 4, see the forward)

@@ -81,7 +81,7 @@ struct Row2Geom {
   static constexpr int NBUF = MODE != 0 ? 1
                               : (200u * 1024u) / BUF >= 4 ? 4
                               : ((200u * 1024u) / BUF < 2 ? 2 : static_cast<int>((200u * 1024u) / BUF));
-  using TL = Row2Tile<T, M, false, GROUPS>;
+  using TL = Row2Tile<T, M, SDCT_ROW_FULLTW != 0, GROUPS>;
   static constexpr int NT = TL::NT;  // threads per group
   static constexpr int CTA = NT * GROUPS;
   // fp32: 3 CTAs/SM (inverse row 56 -> 52 us at 4096^2); fp64 spills at 3

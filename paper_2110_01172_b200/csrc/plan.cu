@@ -20,10 +20,31 @@
 #include <unordered_map>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/sdct_b200.h"
 #include "fast_launch.cuh"
 #include "generic.h"
 #include "kernels_rowcol.cuh"
+
+namespace {
+// NVTX ranges (header-only NVTX v3: a no-op unless a profiler injects its
+// library): one range per transform call and one per pass, so nsys / ncu
+// --nvtx timelines show "sdct:<kind>" with its "col" / "row" passes nested.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+const char* kind_name(int kind) {
+  static const char* names[] = {"sdct:dct_2d",         "sdct:idct_2d",          "sdct:idct_idxst_2d",
+                                "sdct:idxst_idct_2d",  "sdct:dct_3d",           "sdct:idct_3d",
+                                "sdct:dct_2d_rowcol",  "sdct:dct_1d",           "sdct:idct_1d",
+                                "sdct:idxst_1d",       "sdct:idct_idxst_2d_rowcol", "sdct:idxst_idct_2d_rowcol"};
+  return kind >= 0 && kind < static_cast<int>(sizeof(names) / sizeof(names[0])) ? names[kind] : "sdct:?";
+}
+}  // namespace
 
 using namespace sdctb;
 
@@ -575,6 +596,7 @@ int run_fast(sdct_plan_s* p, int kind, int only_stage, const void* in, void* out
                  const Side& o) {
     a.trace = g_trace;
     if (want() && e == cudaSuccess && map_ok) {
+      NvtxRange nv("col");
       CUtensorMap mi, mo;
       // the forward source pass loads rows by parity class (5D class map)
       map_ok = variant == CV_FWD_SRC && col_class_load(static_cast<int>(es), L, nl)
@@ -599,6 +621,7 @@ int run_fast(sdct_plan_s* p, int kind, int only_stage, const void* in, void* out
   auto col2 = [&](bool inv, ColArgs a, const Side& in, const Side& o) {
     a.twc = p->tw_comb;
     if (want() && e == cudaSuccess && map_ok) {
+      NvtxRange nv("col2");
       CUtensorMap mi, mo;
       if (!inv) {
         map_ok = make_class_map(&mi, f32, a.src, in.inner, in.rows, in.row_stride * es, in.planes, in.plane_stride * es, B,
@@ -616,7 +639,10 @@ int run_fast(sdct_plan_s* p, int kind, int only_stage, const void* in, void* out
     ++stage;
   };
   auto row = [&](int rk, int groups, const RowArgs& a) {
-    if (want() && e == cudaSuccess) e = launch_row<T>(M, rk, dim3(groups, B), st, a, p->tw_row);
+    if (want() && e == cudaSuccess) {
+      NvtxRange nv("row");
+      e = launch_row<T>(M, rk, dim3(groups, B), st, a, p->tw_row);
+    }
     ++stage;
   };
   RowArgs ra{};
@@ -907,6 +933,7 @@ int dispatch(sdct_plan_s* p, int kind, int only_stage, const void* in, void* out
     ws = p->ws;
   }
   DeviceGuard g(p->device);
+  NvtxRange nv(kind_name(kind));
   return p->dtype == SDCT_F32 ? run<float>(p, kind, only_stage, in, out, ws, st, nstages, weight, thr)
                               : run<double>(p, kind, only_stage, in, out, ws, st, nstages, weight, thr);
 }

@@ -111,5 +111,6 @@ int main() {
   run<1024, 64>("64-B rows, 1024-row tiles (64 KB) [16384x1024]", a, b, 1024, 0);
   run<2048, 32>("32-B rows, 2048-row tiles (64 KB) [4096^2]", a, b, 4096, 0);
   run<2048, 16>("16-B rows, 2048-row tiles (32 KB) [4096^2]", a, b, 4096, 0);
+  run<4096, 16>("quad es=2 halves, 4096-row tiles (64 KB)", a, b, 4096, 1);
   return 0;
 }
