@@ -11,6 +11,7 @@
 #include "kernels_fast.cuh"
 #include "kernels_row2.cuh"
 #include "kernels_col2.cuh"
+#include "kernels_rowp.cuh"
 
 namespace sdctb {
 
@@ -183,6 +184,30 @@ cudaError_t launch_row2(dim3 grid, cudaStream_t st, const RowArgs& a, const TwSe
 template <typename T, int M, int KIND>
 cudaError_t launch_row_one(dim3 grid, cudaStream_t st, const RowArgs& a, const TwSet& tw) {
   if constexpr (KIND == RK_FWD2 || KIND == RK_INV2) {
+    if constexpr (rowp_ok<T, M>()) {
+      // fp64 M = 2048: the mirror-paired ring kernel (kernels_rowp.cuh);
+      // SDCT_ROWP=0 selects the row2 schedules below (A/B)
+      static const bool rowp = [] {
+        const char* f = getenv("SDCT_ROWP");
+        return !(f && atoi(f) == 0);
+      }();
+      if (rowp) {
+        auto k = rowp_kernel<T, M, KIND == RK_INV2>;
+        using Geo = Row2Geom<T, M, 0>;
+        cudaError_t e = prep_smem(k, Geo::SMEM);
+        if (e != cudaSuccess) return e;
+        static const int resident = [&] {
+          int dev = 0, sms = 0, per = 0;
+          cudaGetDevice(&dev);
+          cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, Geo::CTA, Geo::SMEM);
+          return sms * (per > 0 ? per : 1);
+        }();
+        const int nitems = static_cast<int>(grid.x * grid.y);
+        const int want = (nitems + 1) / 2;
+        return launch_pdl(k, dim3(want < resident ? want : resident), dim3(Geo::CTA), Geo::SMEM, st, a, tw, nitems);
+      }
+    }
     // measured on B200 (tools/stage_time.py): the forward kernel gains from
     // the persistent grouped ring; the inverse (heavier register use in its
     // preprocess) runs best as one item per CTA for long rows (M = 2048:

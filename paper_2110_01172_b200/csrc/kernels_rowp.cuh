@@ -1,0 +1,407 @@
+// Mirror-paired row-pair kernel of the 2D pipelines (fp64, M = N2/2 = 2048).
+//
+// Same work item and persistent ring as row2_kernel MODE 0 (kernels_row2.cuh:
+// one row pair (k1, N1-k1) per item, two consumer groups, NBUF landing /
+// exchange buffers refilled by 1D bulk copies), but the butterflies of the
+// radix-8 FFT stage next to the frequency domain are assigned so that a
+// thread and its lane ^ 16 partner own mirror frequency sets:
+//
+//   thread (warp w, lane l < 16):  k0 = 16 w + l,   frequencies k0 + (M/8) r
+//   thread (warp w, lane l >= 16): k0 = M/8 - (16 w + l - 16)
+//                                  (lane 16 of warp 0: k0 = M/16, self-mirror)
+//
+// M - (k0 + (M/8) r) = (M/8 - k0) + (M/8)(7 - r), so the coupling of
+// frequency k with M - k that the merged postprocess (proj/src/dct2d.cpp:
+// 82-115, with the Hermitian unpack of the packed real rows) and the merged
+// inverse preprocess (dct2d.cpp:161-198, with the inverse packing) need is a
+// register exchange with the partner lane (__shfl_xor 16) instead of a pass
+// through shared memory:
+//
+//   forward: ... DIF stages 0, 1 -> stage 2 (radix 8) with the paired
+//            mapping -> postprocess straight from registers to y.
+//   inverse: rows of x -> preprocess + packing straight into the paired
+//            radix-8 DIT input layout -> DIT stages 2, 1, 0 -> natural
+//            order -> pair-interleaved intermediate rows.
+//
+// Per item this drops one 64 KB write + read of shared memory (the natural-
+// order postprocess tile, resp. the packed-spectrum tile) and, in the
+// inverse, the barrier across which the preprocess operands were held, which
+// is what kept the inverse off the ring schedule.
+#pragma once
+
+#include "kernels_row2.cuh"
+
+namespace sdctb {
+
+template <typename T, int M>
+constexpr bool rowp_ok() {
+  using TL = Row2Tile<T, M, false, 2>;
+  using P = typename TL::P;
+  return sizeof(T) == 8 && M == 2048 && TL::S == 3 && P::R(2) == 8 && TL::NT == M / 8 && TL::E == 16 &&
+         Row2Geom<T, M, 0>::NBUF >= 3;
+}
+
+// k0 of group-local thread t (see above)
+template <int M>
+__device__ __forceinline__ int rowp_k0(int t) {
+  constexpr int K0 = M / 8;
+  const int w = t >> 5, l = t & 31;
+  if (l < 16) return 16 * w + l;
+  const int u = 16 * w + l - 16;
+  return u == 0 ? K0 / 2 : K0 - u;
+}
+
+// Steps of the thread's frequency set for N2 = 2M = 4096:
+// b(k0 + 256 r) = b(k0) e^{-i pi r / 32}, W^(k0 + 256 r) = W^k0 e^{-i pi r / 8}
+__device__ __forceinline__ double2 rowp_sb(int r) {
+  constexpr double c[9][2] = {{1.0, -0.0},
+                              {0.9951847266721969, -0.0980171403295606},
+                              {0.9807852804032304, -0.19509032201612828},
+                              {0.9569403357322088, -0.2902846772544624},
+                              {0.9238795325112867, -0.3826834323650898},
+                              {0.881921264348355, -0.47139673682599764},
+                              {0.8314696123025452, -0.5555702330196022},
+                              {0.773010453362737, -0.6343932841636455},
+                              {0.7071067811865476, -0.7071067811865476}};
+  return make_double2(c[r][0], c[r][1]);
+}
+__device__ __forceinline__ double2 rowp_sw(int r) {
+  constexpr double c[9][2] = {{1.0, -0.0},
+                              {0.9238795325112867, -0.3826834323650898},
+                              {0.7071067811865476, -0.7071067811865476},
+                              {0.3826834323650898, -0.9238795325112867},
+                              {0.0, -1.0},
+                              {-0.3826834323650898, -0.9238795325112867},
+                              {-0.7071067811865476, -0.7071067811865476},
+                              {-0.9238795325112867, -0.3826834323650898},
+                              {-1.0, 0.0}};
+  return make_double2(c[r][0], c[r][1]);
+}
+
+template <typename T, int M, bool INV>
+__global__ void __launch_bounds__(Row2Geom<T, M, 0>::CTA, 1) rowp_kernel(RowArgs a, TwSet tw, int nitems) {
+  static_assert(rowp_ok<T, M>(), "mirror-paired row kernel: fp64, M = 2048 geometry only");
+  using G = Row2Geom<T, M, 0>;
+  using TL = typename G::TL;
+  using V = cx_t<T>;
+  constexpr int NT = G::NT, NBUF = G::NBUF, GROUPS = G::GROUPS;
+  constexpr int R0 = TL::R0, Q0 = M / R0, NBF0 = TL::E / R0;
+  constexpr int K0 = M / 8;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + G::BARS);
+  uint64_t* empty = full + NBUF;
+  const int grp = static_cast<int>(threadIdx.x) / NT;
+  const int t = static_cast<int>(threadIdx.x) - grp * NT;
+  const int n1 = a.n1, n2 = a.n2, half = n1 / 2;
+
+  auto issue = [&](int it, int b) {  // thread 0: land item `it` (rows q1, m1) in buffer b
+    const int P = it % half, batch = it / half;
+    const int q1 = P, m1 = P == 0 ? half : n1 - P;
+    unsigned char* dst = smem_raw + b * G::BUF;
+    mbar_expect_tx(full + b, G::BUF);
+    if constexpr (!INV) {
+      const V* src = static_cast<const V*>(a.src) + batch * a.src_batch;
+      bulk_load(dst, src + static_cast<long long>(__ldg(a.s0 + q1)) * M, G::BUF / 2, full + b);
+      bulk_load(dst + G::BUF / 2, src + static_cast<long long>(__ldg(a.s0 + m1)) * M, G::BUF / 2, full + b);
+    } else {
+      const T* src = static_cast<const T*>(a.src) + batch * a.src_batch;
+      bulk_load(dst, src + static_cast<long long>(q1) * n2, G::BUF / 2, full + b);
+      bulk_load(dst + G::BUF / 2, src + static_cast<long long>(m1) * n2, G::BUF / 2, full + b);
+    }
+  };
+
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int b = 0; b < NBUF; ++b) {
+      mbar_init(full + b, 1);
+      mbar_init(empty + b, 1);
+    }
+  }
+  __syncthreads();
+  pdl_trigger();
+  pdl_wait();  // the previous kernel's output is complete before the first load
+  if (threadIdx.x == 0) {
+#pragma unroll 1
+    for (int b = 0; b < NBUF; ++b) {
+      const int it = blockIdx.x + b * gridDim.x;
+      if (it < nitems) issue(it, b);
+    }
+  }
+
+  // the paired radix-8 butterfly of this thread: frequencies k0 + K0 r of
+  // both lines, slot 8 bm + r (bm = digit_pos(k0) / 8)
+  const int k0 = rowp_k0<M>(t);
+  const int bm = digit_pos<M>(k0) >> 3;
+  const int pb0 = TL::swz(8 * bm), pb1 = TL::swz(M + 8 * bm);  // swizzled slot bases, lines 0 / 1
+  const bool self0 = k0 == 0, selfh = k0 == K0 / 2;               // self-mirror threads
+  // shuffle source of the mirror exchange: the lane ^ 16 partner; lane 16 of
+  // warp 0 (k0 = K0/2) is its own mirror and reads itself; lane 0 of warp 0
+  // (k0 = 0, mirror slot (8 - r) mod 8 and the Nyquist term) is fixed up
+  // separately after the uniform loop
+  const int msrc = selfh ? (t & 31) : ((t & 31) ^ 16);
+  const V* fbt = static_cast<const V*>(a.fb);
+  const V* fut = static_cast<const V*>(a.fu);
+
+#pragma unroll 1
+  for (int k = grp;; k += GROUPS) {
+    const int it = static_cast<int>(blockIdx.x) + k * static_cast<int>(gridDim.x);
+    if (it >= nitems) break;
+    const int b = k % NBUF;
+    const uint32_t ph = static_cast<uint32_t>(k / NBUF) & 1u;
+    if (k >= NBUF) mbar_wait(empty + b, ph ^ 1u);  // item k-NBUF released the buffer
+    V* sm = reinterpret_cast<V*>(smem_raw + b * G::BUF);
+    const int P = it % half, batch = it / half;
+    const int q1 = P, m1 = P == 0 ? half : n1 - P;
+    V v[16];
+
+    if constexpr (!INV) {
+      // ===== forward: DIF stages 0, 1 (tile mapping), stage 2 paired =======
+      StageTw<TL, 0> w0;
+      w0.load(tw.st[0], t);
+      mbar_wait(full + b, ph);
+#pragma unroll
+      for (int i = 0; i < NBF0; ++i) {
+        int line, j, bb;
+        TL::template decode<0>(t + i * NT, line, j, bb);
+#pragma unroll
+        for (int r = 0; r < R0; ++r) {
+          const int n = j + r * Q0;
+          const int s = (r < R0 / 2) ? 2 * n : 2 * M - 1 - 2 * n;  // pair-interleaved column of z(n)
+          v[i * R0 + r] = sm[line * M + s];
+        }
+      }
+      TL::sync();  // landing rows consumed: the buffer becomes the exchange buffer
+      stage_compute<TL, 0, false>(v, w0);
+      to_smem<TL, 0>(v, sm, t);
+      TL::sync();
+      {
+        StageTw<TL, 1> w1;
+        w1.load(tw.st[1], t);
+        from_smem<TL, 1>(v, sm, t);
+        stage_compute<TL, 1, false>(v, w1);
+      }
+      to_smem<TL, 1>(v, sm, t);
+      TL::sync();
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        v[r] = sm[pb0 ^ TL::swzc(r)];
+        v[8 + r] = sm[pb1 ^ TL::swzc(r)];
+      }
+      dft_reg<T, 8, false>(v);
+      dft_reg<T, 8, false>(v + 8);
+      // v[r] = Z(k1, k0 + K0 r), v[8 + r] = Z(k1', k0 + K0 r) (k1' = N1 - k1)
+
+      // merged postprocess (dct2d.cpp:93-113) with the Hermitian unpack folded
+      // in (see row2_kernel): 2X = (A + B) + (-i W^q)(A - B), A = Z(k1, q),
+      // B = conj Z(-k1, -q); the factors 1/2 ride on a(k1)/4
+      T* y = static_cast<T*>(a.dst) + batch * a.dst_batch;
+      T* r0 = y + static_cast<long long>(q1) * n2;
+      T* r1 = y + static_cast<long long>(m1) * n2;
+      const V av0 = __ldg(static_cast<const V*>(a.ta) + q1), av1 = __ldg(static_cast<const V*>(a.ta) + m1);
+      const V a40 = mk(av0.x * T(0.25), av0.y * T(0.25)), a41 = mk(av1.x * T(0.25), av1.y * T(0.25));
+      auto unpack2 = [](V A, V Bc, V w) {  // Bc = conj(B) as stored
+        const T sx = A.x + Bc.x, sy = A.y - Bc.y;
+        const T dx = A.x - Bc.x, dy = A.y + Bc.y;
+        return mk(fma(w.y, dx, fma(w.x, dy, sx)), fma(w.y, dy, fma(-w.x, dx, sy)));
+      };
+      auto item = [&](int q, V Z0a, V Z0b, V Z1a, V Z1b, V bq, V w) {
+        const bool deg2k = (q == 0) || (q == M);
+        if (P != 0) {
+          const V X1 = unpack2(Z0a, Z1b, w);  // 2 X(k1, q)
+          const V X2 = unpack2(Z1a, Z0b, w);  // 2 X(-k1, q)
+          const V ax1 = cmul(a40, X1), ax2 = cmulc(X2, a40);
+          const V sp = cadd(ax1, ax2), tp = csub(ax1, ax2);
+          r0[q] = fma(bq.x, sp.x, -bq.y * sp.y);
+          r1[q] = -fma(bq.x, tp.y, bq.y * tp.x);
+          if (!deg2k) {
+            r0[n2 - q] = -fma(bq.x, sp.y, bq.y * sp.x);
+            r1[n2 - q] = fma(-bq.x, tp.x, bq.y * tp.y);
+          }
+        } else {
+          const V X0 = unpack2(Z0a, Z0b, w);
+          const V X1 = unpack2(Z1a, Z1b, w);
+          const T c0 = T(2) * a40.x, c1 = T(2) * a41.x;
+          const V bx0 = cmul(bq, X0), bx1 = cmul(bq, X1);
+          r0[q] = c0 * bx0.x;
+          r1[q] = c1 * bx1.x;
+          if (!deg2k) {
+            r0[n2 - q] = -c0 * bx0.y;
+            r1[n2 - q] = -c1 * bx1.y;
+          }
+        }
+      };
+      // b(q), W^q on q = k0 + K0 r: the thread's base values times
+      // compile-time steps (no table lookup per frequency)
+      const V bk0 = fac_lookup(fbt, k0, a.fs), wk0 = fac_lookup(fut, k0, a.fs);
+      auto bq_of = [&](int r) {  // b(k0 + K0 r), negated where the corrupt hook says so
+        V bq = cmul(bk0, rowp_sb(r));
+        if (a.badq && a.badq[k0 + K0 * r]) bq = mk(-bq.x, -bq.y);
+        return bq;
+      };
+      // mirror frequency M - q: the partner's slot 7 - r (k0 = 0: own slot
+      // (8 - r) mod 8, plus q = M with Z(k1, M) = Z(k1, 0))
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        V m0, m1v;
+        m0.x = __shfl_sync(0xffffffffu, v[7 - r].x, msrc);
+        m0.y = __shfl_sync(0xffffffffu, v[7 - r].y, msrc);
+        m1v.x = __shfl_sync(0xffffffffu, v[15 - r].x, msrc);
+        m1v.y = __shfl_sync(0xffffffffu, v[15 - r].y, msrc);
+        if (self0) {
+          m0 = v[(8 - r) & 7];
+          m1v = v[8 + ((8 - r) & 7)];
+        }
+        item(k0 + K0 * r, v[r], m0, v[8 + r], m1v, bq_of(r), cmul(wk0, rowp_sw(r)));
+      }
+      if (self0) item(M, v[0], v[0], v[8], v[8], bq_of(8), rowp_sw(8));
+    } else {
+      // ===== inverse: preprocess + packing into the paired DIT input =======
+      mbar_wait(full + b, ph);
+      const T* rowA = reinterpret_cast<const T*>(sm);
+      const T* rowB = reinterpret_cast<const T*>(sm) + 2 * M;
+      if (a.weight == 3) {
+        // compression threshold folded into this load (compress.cpp:33-45)
+        T* const rws[2] = {const_cast<T*>(rowA), const_cast<T*>(rowB)};
+        const T eps = static_cast<T>(a.thr_eps), sc = static_cast<T>(a.thr_scale);
+        unsigned cnt = 0;
+        for (int e = t; e < 2 * n2; e += NT) {
+          T* rw = rws[e >= n2] + (e & (n2 - 1));
+          const T vv = *rw;
+          const bool drop = fabs(vv) < eps;
+          cnt += drop ? 1u : 0u;
+          *rw = drop ? T(0) : vv * sc;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+        if ((threadIdx.x & 31) == 0 && cnt && a.thr_count) atomicAdd(a.thr_count, static_cast<unsigned long long>(cnt));
+        TL::sync();
+      } else if (a.weight) {
+        // DREAMPlace field weighting folded into this load (force.cpp:19-31)
+        T* const rws[2] = {const_cast<T*>(rowA), const_cast<T*>(rowB)};
+        const T pi = T(3.14159265358979323846);
+        const T w1a = pi * T(q1) / T(n1), w1b = pi * T(m1) / T(n1), sc2 = pi / T(n2);
+        for (int e = t; e < 2 * n2; e += NT) {
+          const int k2 = e & (n2 - 1);
+          T* rw = rws[e >= n2] + k2;
+          const T w1 = e < n2 ? w1a : w1b, w2 = sc2 * T(k2);
+          const T den = fma(w1, w1, w2 * w2);
+          *rw = den > T(0) ? *rw * (a.weight == 1 ? w1 : w2) / den : T(0);
+        }
+        TL::sync();
+      }
+      if (a.mode == 1 && P != 0) {  // IDXST along axis 0 swaps the rows' roles
+        const T* tmp = rowA;
+        rowA = rowB;
+        rowB = tmp;
+      }
+      const V* ta = static_cast<const V*>(a.ta);
+      const V ca0 = cconj(__ldg(ta + q1)), ca1 = cconj(__ldg(ta + m1));
+      // X'(0, nn), X'(1, nn) (proj/src/dct2d.cpp:182-195) from x(nn), x(N2-nn)
+      // of both rows (x(N2) := 0); mode 2 reads x(N2-nn) for D and x(nn) for R
+      // with x(0) := 0 (dct2d.cpp:169-180)
+      auto xpair = [&](int nn, V bk, V& x0, V& x1) {
+        const bool z = nn == 0;
+        const int pd = a.mode == 2 ? n2 - nn : nn;
+        const int pr = a.mode == 2 ? nn : n2 - nn;
+        const bool zd = a.mode == 2 && z;
+        const T DA = zd ? T(0) : rowA[pd & (n2 - 1)], RA = z ? T(0) : rowA[pr & (n2 - 1)];
+        const T DB = zd ? T(0) : rowB[pd & (n2 - 1)], RB = z ? T(0) : rowB[pr & (n2 - 1)];
+        const V cb = cconj(bk);
+        const V c0 = cmul(ca0, cb), c1 = cmul(ca1, cb);
+        if (P == 0) {
+          // rows 0 and N1/2, each its own mirror: row 0 pairs with the zero
+          // row N1; mode 1 zeroes row 0 entirely
+          const T pa = a.mode == 1 ? T(0) : DA, sa = a.mode == 1 ? T(0) : RA;
+          x0 = cmul(c0, mk(pa, -sa));
+          x1 = cmul(c1, mk(DB - RB, -(DB + RB)));
+          return;
+        }
+        x0 = cmul(c0, mk(DA - RB, -(DB + RA)));
+        x1 = cmul(c1, mk(DB - RA, -(DA + RB)));
+      };
+      const V bk0 = fac_lookup(fbt, k0, a.fs), wk0 = fac_lookup(fut, k0, a.fs);
+      auto bq_of = [&](int r) {  // b(k0 + K0 r), negated where the corrupt hook says so
+        V bq = cmul(bk0, rowp_sb(r));
+        if (a.badq && a.badq[k0 + K0 * r]) bq = mk(-bq.x, -bq.y);
+        return bq;
+      };
+#pragma unroll
+      for (int r = 0; r < 8; ++r) xpair(k0 + K0 * r, bq_of(r), v[r], v[8 + r]);
+      V nyq0, nyq1;  // X'(., M) for the k0 = 0 thread's slot 0
+      if (self0) xpair(M, bq_of(8), nyq0, nyq1);
+      TL::sync();  // landing rows consumed: the buffer becomes the exchange buffer
+      // inverse packing Zh(k) = (X(k) + X(k+M)) + i conj(W^k)(X(k) - X(k+M)),
+      // X(line, k + M) = conj X(partner line, M - k) (own line for P == 0)
+      auto packr = [&](int r, V mir0, V mir1) {
+        const int nn = k0 + K0 * r;
+        const V wk = cmul(wk0, rowp_sw(r));
+        const V h0 = nn == 0 ? nyq0 : cconj(P != 0 ? mir1 : mir0);
+        const V h1 = nn == 0 ? nyq1 : cconj(P != 0 ? mir0 : mir1);
+        v[r] = pack(v[r], h0, wk);
+        v[8 + r] = pack(v[8 + r], h1, wk);
+      };
+      // pairs (r, 7 - r): every lane exchanges (converged warp), then all but
+      // the k0 = 0 thread pack both slots in place
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        V a0, a1, c0v, c1v;  // partner's X' at slots 7 - r (mirror of r) and r (mirror of 7 - r)
+        a0.x = __shfl_sync(0xffffffffu, v[7 - r].x, msrc);
+        a0.y = __shfl_sync(0xffffffffu, v[7 - r].y, msrc);
+        a1.x = __shfl_sync(0xffffffffu, v[15 - r].x, msrc);
+        a1.y = __shfl_sync(0xffffffffu, v[15 - r].y, msrc);
+        c0v.x = __shfl_sync(0xffffffffu, v[r].x, msrc);
+        c0v.y = __shfl_sync(0xffffffffu, v[r].y, msrc);
+        c1v.x = __shfl_sync(0xffffffffu, v[8 + r].x, msrc);
+        c1v.y = __shfl_sync(0xffffffffu, v[8 + r].y, msrc);
+        if (!self0) {
+          packr(r, a0, a1);
+          packr(7 - r, c0v, c1v);
+        }
+      }
+      if (self0) {
+        // k0 = 0: mirror of slot r is slot (8 - r) mod 8; slot 0 uses X'(M)
+#pragma unroll
+        for (int r = 1; r < 4; ++r) {
+          const V a0 = v[8 - r], a1 = v[16 - r], c0v = v[r], c1v = v[8 + r];
+          packr(r, a0, a1);
+          packr(8 - r, c0v, c1v);
+        }
+        packr(0, v[0], v[8]);
+        packr(4, v[4], v[12]);
+      }
+      // DIT: stage 2 (radix 8, paired mapping) -> stages 1, 0 (tile mapping)
+      dft_reg<T, 8, true>(v);
+      dft_reg<T, 8, true>(v + 8);
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        sm[pb0 ^ TL::swzc(r)] = v[r];
+        sm[pb1 ^ TL::swzc(r)] = v[8 + r];
+      }
+      TL::sync();
+      dit_down<TL, true, 1>(v, sm, tw, t);  // ends with stage 0 in registers (natural order)
+      to_smem<TL, 0>(v, sm, t);             // same slots this thread just read
+      TL::sync();
+      // store rows (natural row order) in pair-interleaved column order
+      V* dst = static_cast<V*>(a.dst) + batch * a.dst_batch;
+      constexpr int VPR = M;  // one complex per 16-B vector
+      const int irow[2] = {__ldg(a.s0 + q1), __ldg(a.s0 + m1)};
+      const int swt = TL::swz((t >> 1) ^ ((t & 1) ? M - 1 : 0));
+#pragma unroll
+      for (int i2 = 0; i2 < 2 * VPR / NT; ++i2) {
+        const int line = (i2 * NT) / VPR, off = (i2 * NT) % VPR;
+        dst[static_cast<long long>(irow[line]) * M + t + off] = sm[swt ^ TL::swzc(line * M + off / 2)];
+      }
+    }
+    TL::sync();  // every read of buffer b by this group is done
+    if (t == 0) {
+      mbar_arrive(empty + b);
+      const int nxt0 = it + NBUF * static_cast<int>(gridDim.x);
+      if (nxt0 < nitems) {
+        fence_async_smem();  // generic-proxy smem accesses before the async refill
+        issue(nxt0, b);
+      }
+    }
+  }
+}
+
+}  // namespace sdctb
