@@ -299,15 +299,23 @@ __global__ void __launch_bounds__(Row2Geom<T, M, 0>::CTA, 1) rowp_kernel(RowArgs
       // X'(0, nn), X'(1, nn) (proj/src/dct2d.cpp:182-195) from x(nn), x(N2-nn)
       // of both rows (x(N2) := 0); mode 2 reads x(N2-nn) for D and x(nn) for R
       // with x(0) := 0 (dct2d.cpp:169-180)
-      auto xpair = [&](int nn, V bk, V& x0, V& x1) {
+      // c0 = conj a(q1) conj b(nn), c1 = conj a(m1) conj b(nn) with
+      // b(k0 + K0 r) = b(k0) e^{-i pi r/32}: per-item constants times the step
+      const V bk0 = fac_lookup(fbt, k0, a.fs), wk0 = fac_lookup(fut, k0, a.fs);
+      const V cc0 = cmulc(ca0, bk0), cc1 = cmulc(ca1, bk0);
+      auto xpair = [&](int r, V& x0, V& x1) {
+        const int nn = k0 + K0 * r;
         const bool z = nn == 0;
         const int pd = a.mode == 2 ? n2 - nn : nn;
         const int pr = a.mode == 2 ? nn : n2 - nn;
         const bool zd = a.mode == 2 && z;
         const T DA = zd ? T(0) : rowA[pd & (n2 - 1)], RA = z ? T(0) : rowA[pr & (n2 - 1)];
         const T DB = zd ? T(0) : rowB[pd & (n2 - 1)], RB = z ? T(0) : rowB[pr & (n2 - 1)];
-        const V cb = cconj(bk);
-        const V c0 = cmul(ca0, cb), c1 = cmul(ca1, cb);
+        V c0 = cmulc(cc0, rowp_sb(r)), c1 = cmulc(cc1, rowp_sb(r));
+        if (a.badq && a.badq[nn]) {  // corrupt_twiddle_for_testing negated b(nn)
+          c0 = mk(-c0.x, -c0.y);
+          c1 = mk(-c1.x, -c1.y);
+        }
         if (P == 0) {
           // rows 0 and N1/2, each its own mirror: row 0 pairs with the zero
           // row N1; mode 1 zeroes row 0 entirely
@@ -319,16 +327,10 @@ __global__ void __launch_bounds__(Row2Geom<T, M, 0>::CTA, 1) rowp_kernel(RowArgs
         x0 = cmul(c0, mk(DA - RB, -(DB + RA)));
         x1 = cmul(c1, mk(DB - RA, -(DA + RB)));
       };
-      const V bk0 = fac_lookup(fbt, k0, a.fs), wk0 = fac_lookup(fut, k0, a.fs);
-      auto bq_of = [&](int r) {  // b(k0 + K0 r), negated where the corrupt hook says so
-        V bq = cmul(bk0, rowp_sb(r));
-        if (a.badq && a.badq[k0 + K0 * r]) bq = mk(-bq.x, -bq.y);
-        return bq;
-      };
 #pragma unroll
-      for (int r = 0; r < 8; ++r) xpair(k0 + K0 * r, bq_of(r), v[r], v[8 + r]);
+      for (int r = 0; r < 8; ++r) xpair(r, v[r], v[8 + r]);
       V nyq0, nyq1;  // X'(., M) for the k0 = 0 thread's slot 0
-      if (self0) xpair(M, bq_of(8), nyq0, nyq1);
+      if (self0) xpair(8, nyq0, nyq1);  // nn = M
       TL::sync();  // landing rows consumed: the buffer becomes the exchange buffer
       // inverse packing Zh(k) = (X(k) + X(k+M)) + i conj(W^k)(X(k) - X(k+M)),
       // X(line, k + M) = conj X(partner line, M - k) (own line for P == 0)
@@ -378,18 +380,39 @@ __global__ void __launch_bounds__(Row2Geom<T, M, 0>::CTA, 1) rowp_kernel(RowArgs
         sm[pb1 ^ TL::swzc(r)] = v[8 + r];
       }
       TL::sync();
-      dit_down<TL, true, 1>(v, sm, tw, t);  // ends with stage 0 in registers (natural order)
-      to_smem<TL, 0>(v, sm, t);             // same slots this thread just read
+      {
+        StageTw<TL, 1> w1;
+        w1.load(tw.st[1], t);
+        from_smem<TL, 1>(v, sm, t);
+        dit_compute<TL, 1, true>(v, w1);
+        to_smem<TL, 1>(v, sm, t);
+      }
       TL::sync();
-      // store rows (natural row order) in pair-interleaved column order
-      V* dst = static_cast<V*>(a.dst) + batch * a.dst_batch;
-      constexpr int VPR = M;  // one complex per 16-B vector
-      const int irow[2] = {__ldg(a.s0 + q1), __ldg(a.s0 + m1)};
-      const int swt = TL::swz((t >> 1) ^ ((t & 1) ? M - 1 : 0));
+      // last DIT stage with lanes paired j <-> Q0-1-j in each warp (virtual
+      // tile index tv): output z(j + Q0 r) lands in pair-interleaved column
+      // 2(j + Q0 r) (r < R0/2) or 2M-1-2(j + Q0 r), so at store step r the
+      // lower half-warp's v[r] and the upper half-warp's v[R0-1-r] are the two
+      // 16-B halves of the same 32-B sectors: direct coalesced stores, no
+      // natural-order staging pass
+      const int wq = (t >> 5) & 3, l = t & 31;
+      const int jv = l < 16 ? 16 * wq + l : Q0 - 1 - (16 * wq + l - 16);
+      const int lv = t / (NT / 2);
+      const int tv = lv * Q0 + jv;
+      {
+        StageTw<TL, 0> w0;
+        w0.load(tw.st[0], tv);
+        from_smem<TL, 0>(v, sm, tv);
+        dit_compute<TL, 0, true>(v, w0);
+      }
+      V* drow = static_cast<V*>(a.dst) + batch * a.dst_batch +
+                static_cast<long long>(__ldg(a.s0 + (lv ? m1 : q1))) * M;
+      const bool hi = l >= 16;
 #pragma unroll
-      for (int i2 = 0; i2 < 2 * VPR / NT; ++i2) {
-        const int line = (i2 * NT) / VPR, off = (i2 * NT) % VPR;
-        dst[static_cast<long long>(irow[line]) * M + t + off] = sm[swt ^ TL::swzc(line * M + off / 2)];
+      for (int r = 0; r < R0; ++r) {
+        const int rr = hi ? R0 - 1 - r : r;
+        const int m = jv + Q0 * rr;
+        const int col = rr < R0 / 2 ? 2 * m : 2 * M - 1 - 2 * m;
+        drow[col] = hi ? v[R0 - 1 - r] : v[r];
       }
     }
     TL::sync();  // every read of buffer b by this group is done
