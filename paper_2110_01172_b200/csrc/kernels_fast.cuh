@@ -559,7 +559,18 @@ __global__ void __launch_bounds__(Tile<T, L, NL, true>::NT)
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw + BAR_OFF);
   const int t = threadIdx.x;
 
+  // tile -> (band, plane, batch); power-of-two band / plane counts (every
+  // fast-path shape) decode with shifts instead of integer divisions
+  const bool pow2 = ((a.nbands & (a.nbands - 1)) | (a.nplanes & (a.nplanes - 1))) == 0;
+  const int sb_ = __ffs(a.nbands) - 1, sp_ = __ffs(a.nplanes) - 1;
   auto coords = [&](int tile, int& band, int& plane, int& batch) {
+    if (pow2) {
+      band = tile & (a.nbands - 1);
+      const int rest = tile >> sb_;
+      plane = rest & (a.nplanes - 1);
+      batch = rest >> sp_;
+      return;
+    }
     band = tile % a.nbands;
     const int rest = tile / a.nbands;
     plane = rest % a.nplanes;

@@ -93,9 +93,10 @@ __global__ void __launch_bounds__(Row2Geom<T, M, 0>::CTA, 1) rowp_kernel(RowArgs
   const int grp = static_cast<int>(threadIdx.x) / NT;
   const int t = static_cast<int>(threadIdx.x) - grp * NT;
   const int n1 = a.n1, n2 = a.n2, half = n1 / 2;
+  const int lgh = __ffs(half) - 1;  // fast-path extents are powers of two
 
   auto issue = [&](int it, int b) {  // thread 0: land item `it` (rows q1, m1) in buffer b
-    const int P = it % half, batch = it / half;
+    const int P = it & (half - 1), batch = it >> lgh;
     const int q1 = P, m1 = P == 0 ? half : n1 - P;
     unsigned char* dst = smem_raw + b * G::BUF;
     mbar_expect_tx(full + b, G::BUF);
@@ -150,7 +151,7 @@ __global__ void __launch_bounds__(Row2Geom<T, M, 0>::CTA, 1) rowp_kernel(RowArgs
     const uint32_t ph = static_cast<uint32_t>(k / NBUF) & 1u;
     if (k >= NBUF) mbar_wait(empty + b, ph ^ 1u);  // item k-NBUF released the buffer
     V* sm = reinterpret_cast<V*>(smem_raw + b * G::BUF);
-    const int P = it % half, batch = it / half;
+    const int P = it & (half - 1), batch = it >> lgh;
     const int q1 = P, m1 = P == 0 ? half : n1 - P;
     V v[16];
 
