@@ -564,16 +564,22 @@ def test_cluster_split_8192_round_trip(cuda, dtype):
 @pytest.mark.parametrize("dtype", ["float64", "float32"])
 def test_slab_3d_single_rank_matches_fused(cuda, dtype):
     # slab pipeline (batched 2D + contiguous 1D transforms around the two
-    # exchanges) vs the fused 3D kernels; one rank, so the exchanges are copies
+    # exchanges) vs the CPU oracle and the fused 3D kernels; one rank, so the
+    # exchanges are copies
     torch = _torch()
     import paper_2110_01172_b200 as sd
     from paper_2110_01172_b200 import slab3d
 
     tdt = torch.float64 if dtype == "float64" else torch.float32
     for shape in [(64, 32, 48), (16, 16, 16), (12, 10, 9)]:
-        x = torch.tensor(rnd(shape, 77, dtype), dtype=tdt, device="cuda")
+        xn = rnd(shape, 77, dtype)
+        x = torch.tensor(xn, dtype=tdt, device="cuda")
         y = slab3d.dct_3d_slab(x, shape[0])
+        # against the CPU oracle (reference transforms_ext.cpp:322-350) and the fused kernels
+        assert oracle.rel_l2(y.double().cpu().numpy(), oracle.port.dct_3d(xn)) <= TOL[dtype]
         assert oracle.rel_l2(y.double().cpu().numpy(), sd.dct_3d(x).double().cpu().numpy()) <= TOL[dtype]
+        assert oracle.rel_l2(slab3d.idct_3d_slab(x, shape[0]).double().cpu().numpy(),
+                             oracle.port.idct_3d(xn)) <= TOL[dtype]
         z = slab3d.idct_3d_slab(y, shape[0])
         assert oracle.rel_l2(z.double().cpu().numpy() / (x.numel() / 8), x.double().cpu().numpy()) <= TOL[dtype] * 10
 
