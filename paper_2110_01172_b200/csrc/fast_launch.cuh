@@ -193,7 +193,7 @@ cudaError_t launch_row_one(dim3 grid, cudaStream_t st, const RowArgs& a, const T
       }();
       if (rowp) {
         auto k = rowp_kernel<T, M, KIND == RK_INV2>;
-        using Geo = Row2Geom<T, M, 0>;
+        using Geo = RowpGeom<T, M>;
         cudaError_t e = prep_smem(k, Geo::SMEM);
         if (e != cudaSuccess) return e;
         static const int resident = [&] {

@@ -1,20 +1,18 @@
-// Mirror-paired row-pair kernel of the 2D pipelines (fp64, M = N2/2 = 2048).
+// Mirror-paired row-pair kernel of the 2D pipelines (fp64, M = N2/2 = 1024, 2048).
 //
 // Same work item and persistent ring as row2_kernel MODE 0 (kernels_row2.cuh:
 // one row pair (k1, N1-k1) per item, two consumer groups, NBUF landing /
 // exchange buffers refilled by 1D bulk copies), but the butterflies of the
 // radix-8 FFT stage next to the frequency domain are assigned so that a
-// thread and its lane ^ 16 partner own mirror frequency sets:
-//
-//   thread (warp w, lane l < 16):  k0 = 16 w + l,   frequencies k0 + (M/8) r
-//   thread (warp w, lane l >= 16): k0 = M/8 - (16 w + l - 16)
-//                                  (lane 16 of warp 0: k0 = M/16, self-mirror)
+// thread and its lane ^ 16 partner own mirror frequency sets: the thread owns
+// frequencies k0 + (M/8) r (r = 0..7) of both rows, its partner k0' = M/8 - k0
+// (rowp_k0 below; k0 = 0 and M/16 are their own mirrors), and
 //
 // M - (k0 + (M/8) r) = (M/8 - k0) + (M/8)(7 - r), so the coupling of
 // frequency k with M - k that the merged postprocess (proj/src/dct2d.cpp:
 // 82-115, with the Hermitian unpack of the packed real rows) and the merged
 // inverse preprocess (dct2d.cpp:161-198, with the inverse packing) need is a
-// register exchange with the partner lane (__shfl_xor 16) instead of a pass
+// register exchange with the partner lane (a shuffle with lane ^ 16) instead of a pass
 // through shared memory:
 //
 //   forward: ... DIF stages 0, 1 -> stage 2 (radix 8) with the paired
@@ -33,15 +31,34 @@
 
 namespace sdctb {
 
+// Ring geometry: two consumer groups (the row2 tile), NBUF = 3 item buffers;
+// M = 2048 fp64 (64 KB items) runs one CTA per SM, M = 1024 (32 KB) two.
+template <typename T, int M>
+struct RowpGeom {
+  using TL = Row2Tile<T, M, false, 2>;
+  static constexpr unsigned BUF = 2u * M * sizeof(cx_t<T>);
+  static constexpr int GROUPS = 2, NBUF = 3;
+  static constexpr int NT = TL::NT, CTA = 2 * TL::NT;
+  static constexpr int MINB = BUF >= 64u * 1024u ? 1 : 2;
+  static constexpr size_t BARS = static_cast<size_t>(NBUF) * BUF;
+  static constexpr size_t SMEM = BARS + 16 * NBUF;
+};
+
 template <typename T, int M>
 constexpr bool rowp_ok() {
   using TL = Row2Tile<T, M, false, 2>;
   using P = typename TL::P;
-  return sizeof(T) == 8 && M == 2048 && TL::S == 3 && P::R(2) == 8 && TL::NT == M / 8 && TL::E == 16 &&
-         Row2Geom<T, M, 0>::NBUF >= 3;
+  return sizeof(T) == 8 && (M == 2048 || M == 1024) && TL::S == 3 && P::R(2) == 8 && TL::NT == M / 8 && TL::E == 16 &&
+         RowpGeom<T, M>::MINB * RowpGeom<T, M>::SMEM <= 220u * 1024u;
 }
 
-// k0 of group-local thread t (see above)
+// k0 of group-local thread t (see above): lanes l < 16 of warp w take
+// k0 = 16 w + l, lanes l >= 16 the mirrors M/8 - (16 w + l - 16) (lane 16 of
+// warp 0: M/16). Consecutive lanes thus own consecutive frequencies, which
+// keeps the postprocess's y stores and the inverse's operand reads coalesced
+// and conflict free; the paired radix-8 stage's shared-memory accesses are
+// conflict free at M = 2048 except in the phases holding k0 = 0 / the mirrors
+// of 16 w (2-way), and 2-way at M = 1024 (tests/test_host.py).
 template <int M>
 __device__ __forceinline__ int rowp_k0(int t) {
   constexpr int K0 = M / 8;
@@ -79,9 +96,10 @@ __device__ __forceinline__ double2 rowp_sw(int r) {
 }
 
 template <typename T, int M, bool INV>
-__global__ void __launch_bounds__(Row2Geom<T, M, 0>::CTA, 1) rowp_kernel(RowArgs a, TwSet tw, int nitems) {
-  static_assert(rowp_ok<T, M>(), "mirror-paired row kernel: fp64, M = 2048 geometry only");
-  using G = Row2Geom<T, M, 0>;
+__global__ void __launch_bounds__(RowpGeom<T, M>::CTA, RowpGeom<T, M>::MINB)
+    rowp_kernel(RowArgs a, TwSet tw, int nitems) {
+  static_assert(rowp_ok<T, M>(), "mirror-paired row kernel: fp64, M = 1024 / 2048 geometry only");
+  using G = RowpGeom<T, M>;
   using TL = typename G::TL;
   using V = cx_t<T>;
   constexpr int NT = G::NT, NBUF = G::NBUF, GROUPS = G::GROUPS;
@@ -395,7 +413,7 @@ __global__ void __launch_bounds__(Row2Geom<T, M, 0>::CTA, 1) rowp_kernel(RowArgs
       // lower half-warp's v[r] and the upper half-warp's v[R0-1-r] are the two
       // 16-B halves of the same 32-B sectors: direct coalesced stores, no
       // natural-order staging pass
-      const int wq = (t >> 5) & 3, l = t & 31;
+      const int wq = (t >> 5) & (Q0 / 32 - 1), l = t & 31;
       const int jv = l < 16 ? 16 * wq + l : Q0 - 1 - (16 * wq + l - 16);
       const int lv = t / (NT / 2);
       const int tv = lv * Q0 + jv;

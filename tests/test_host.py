@@ -142,3 +142,30 @@ def test_fastdiv_formula():
         for x in xs.tolist():
             q = ((((x * m) >> 32) + x) & 0xFFFFFFFF) >> s
             assert q == x // d, (d, x)
+
+
+def _rowp_k0(t: int, M: int) -> int:
+    # mirror of rowp_k0 (paper_2110_01172_b200/csrc/kernels_rowp.cuh)
+    K0, w, l = M // 8, t >> 5, t & 31
+    if l < 16:
+        return 16 * w + l
+    u = 16 * w + l - 16
+    return K0 // 2 if u == 0 else K0 - u
+
+
+@pytest.mark.parametrize("M", [1024, 2048])
+def test_rowp_mirror_pairing_and_banks(M):
+    # mirror-paired row kernel: every k0 once, lane ^ 16 holds the mirror set
+    # (k0 + k0' = M/8, or both self-mirrors), and the paired radix-8 stage's
+    # shared-memory accesses are at most 2-way conflicted (fp64 row swizzle)
+    K0 = NT = M // 8
+    ks = [_rowp_k0(t, M) for t in range(NT)]
+    assert sorted(ks) == list(range(K0))
+    for t in range(NT):
+        a, b = ks[t], ks[t ^ 16]
+        assert (a + b) % K0 == 0 or {a, b} <= {0, K0 // 2}
+    for line in (0, 1):
+        for t0 in range(0, NT, 32):
+            for r in range(8):
+                addrs = [sm.row_at(line, 8 * (sm.digit_pos(M, ks[t]) >> 3) + r, M, 16) for t in range(t0, t0 + 32)]
+                assert sm.conflict_degree(addrs, 16) <= 2
