@@ -1,4 +1,4 @@
-// Mirror-paired row-pair kernel of the 2D pipelines (fp64, M = N2/2 = 1024, 2048).
+// Mirror-paired row-pair kernel of the 2D pipelines (M = N2/2 = 1024, 2048; fp64 and fp32).
 //
 // Same work item and persistent ring as row2_kernel MODE 0 (kernels_row2.cuh:
 // one row pair (k1, N1-k1) per item, two consumer groups, NBUF landing /
@@ -31,15 +31,17 @@
 
 namespace sdctb {
 
-// Ring geometry: two consumer groups (the row2 tile), NBUF = 3 item buffers;
-// M = 2048 fp64 (64 KB items) runs one CTA per SM, M = 1024 (32 KB) two.
+// Ring geometry: two consumer groups (the row2 tile) and 3-4 item buffers
+// (fp64 M = 2048: 3 x 64 KB, one CTA per SM; fp64 M = 1024: 3 x 32 KB, two).
 template <typename T, int M>
 struct RowpGeom {
   using TL = Row2Tile<T, M, false, 2>;
   static constexpr unsigned BUF = 2u * M * sizeof(cx_t<T>);
-  static constexpr int GROUPS = 2, NBUF = 3;
-  static constexpr int NT = TL::NT, CTA = 2 * TL::NT;
-  static constexpr int MINB = BUF >= 64u * 1024u ? 1 : 2;
+  static constexpr int NT = TL::NT, CTA = 2 * TL::NT, GROUPS = 2;
+  // 512-thread CTAs (M = 2048) keep 128 registers per thread with one CTA per
+  // SM; 256-thread CTAs (M = 1024) run two per SM
+  static constexpr int MINB = CTA >= 512 ? 1 : 2;
+  static constexpr int NBUF = (200u * 1024u) / (BUF * MINB) >= 4 ? 4 : 3;
   static constexpr size_t BARS = static_cast<size_t>(NBUF) * BUF;
   static constexpr size_t SMEM = BARS + 16 * NBUF;
 };
@@ -48,7 +50,7 @@ template <typename T, int M>
 constexpr bool rowp_ok() {
   using TL = Row2Tile<T, M, false, 2>;
   using P = typename TL::P;
-  return sizeof(T) == 8 && (M == 2048 || M == 1024) && TL::S == 3 && P::R(2) == 8 && TL::NT == M / 8 && TL::E == 16 &&
+  return (M == 2048 || M == 1024) && TL::S == 3 && P::R(2) == 8 && TL::NT == M / 8 && TL::E == 16 &&
          RowpGeom<T, M>::MINB * RowpGeom<T, M>::SMEM <= 220u * 1024u;
 }
 
@@ -70,7 +72,8 @@ __device__ __forceinline__ int rowp_k0(int t) {
 
 // Steps of the thread's frequency set for N2 = 2M = 4096:
 // b(k0 + 256 r) = b(k0) e^{-i pi r / 32}, W^(k0 + 256 r) = W^k0 e^{-i pi r / 8}
-__device__ __forceinline__ double2 rowp_sb(int r) {
+template <typename T>
+__device__ __forceinline__ cx_t<T> rowp_sb(int r) {
   constexpr double c[9][2] = {{1.0, -0.0},
                               {0.9951847266721969, -0.0980171403295606},
                               {0.9807852804032304, -0.19509032201612828},
@@ -80,9 +83,10 @@ __device__ __forceinline__ double2 rowp_sb(int r) {
                               {0.8314696123025452, -0.5555702330196022},
                               {0.773010453362737, -0.6343932841636455},
                               {0.7071067811865476, -0.7071067811865476}};
-  return make_double2(c[r][0], c[r][1]);
+  return mk(static_cast<T>(c[r][0]), static_cast<T>(c[r][1]));
 }
-__device__ __forceinline__ double2 rowp_sw(int r) {
+template <typename T>
+__device__ __forceinline__ cx_t<T> rowp_sw(int r) {
   constexpr double c[9][2] = {{1.0, -0.0},
                               {0.9238795325112867, -0.3826834323650898},
                               {0.7071067811865476, -0.7071067811865476},
@@ -92,13 +96,13 @@ __device__ __forceinline__ double2 rowp_sw(int r) {
                               {-0.7071067811865476, -0.7071067811865476},
                               {-0.9238795325112867, -0.3826834323650898},
                               {-1.0, 0.0}};
-  return make_double2(c[r][0], c[r][1]);
+  return mk(static_cast<T>(c[r][0]), static_cast<T>(c[r][1]));
 }
 
 template <typename T, int M, bool INV>
 __global__ void __launch_bounds__(RowpGeom<T, M>::CTA, RowpGeom<T, M>::MINB)
     rowp_kernel(RowArgs a, TwSet tw, int nitems) {
-  static_assert(rowp_ok<T, M>(), "mirror-paired row kernel: fp64, M = 1024 / 2048 geometry only");
+  static_assert(rowp_ok<T, M>(), "mirror-paired row kernel: M = 1024 / 2048 geometry only");
   using G = RowpGeom<T, M>;
   using TL = typename G::TL;
   using V = cx_t<T>;
@@ -253,7 +257,7 @@ __global__ void __launch_bounds__(RowpGeom<T, M>::CTA, RowpGeom<T, M>::MINB)
       // compile-time steps (no table lookup per frequency)
       const V bk0 = fac_lookup(fbt, k0, a.fs), wk0 = fac_lookup(fut, k0, a.fs);
       auto bq_of = [&](int r) {  // b(k0 + K0 r), negated where the corrupt hook says so
-        V bq = cmul(bk0, rowp_sb(r));
+        V bq = cmul(bk0, rowp_sb<T>(r));
         if (a.badq && a.badq[k0 + K0 * r]) bq = mk(-bq.x, -bq.y);
         return bq;
       };
@@ -270,9 +274,9 @@ __global__ void __launch_bounds__(RowpGeom<T, M>::CTA, RowpGeom<T, M>::MINB)
           m0 = v[(8 - r) & 7];
           m1v = v[8 + ((8 - r) & 7)];
         }
-        item(k0 + K0 * r, v[r], m0, v[8 + r], m1v, bq_of(r), cmul(wk0, rowp_sw(r)));
+        item(k0 + K0 * r, v[r], m0, v[8 + r], m1v, bq_of(r), cmul(wk0, rowp_sw<T>(r)));
       }
-      if (self0) item(M, v[0], v[0], v[8], v[8], bq_of(8), rowp_sw(8));
+      if (self0) item(M, v[0], v[0], v[8], v[8], bq_of(8), rowp_sw<T>(8));
     } else {
       // ===== inverse: preprocess + packing into the paired DIT input =======
       mbar_wait(full + b, ph);
@@ -330,7 +334,7 @@ __global__ void __launch_bounds__(RowpGeom<T, M>::CTA, RowpGeom<T, M>::MINB)
         const bool zd = a.mode == 2 && z;
         const T DA = zd ? T(0) : rowA[pd & (n2 - 1)], RA = z ? T(0) : rowA[pr & (n2 - 1)];
         const T DB = zd ? T(0) : rowB[pd & (n2 - 1)], RB = z ? T(0) : rowB[pr & (n2 - 1)];
-        V c0 = cmulc(cc0, rowp_sb(r)), c1 = cmulc(cc1, rowp_sb(r));
+        V c0 = cmulc(cc0, rowp_sb<T>(r)), c1 = cmulc(cc1, rowp_sb<T>(r));
         if (a.badq && a.badq[nn]) {  // corrupt_twiddle_for_testing negated b(nn)
           c0 = mk(-c0.x, -c0.y);
           c1 = mk(-c1.x, -c1.y);
@@ -355,7 +359,7 @@ __global__ void __launch_bounds__(RowpGeom<T, M>::CTA, RowpGeom<T, M>::MINB)
       // X(line, k + M) = conj X(partner line, M - k) (own line for P == 0)
       auto packr = [&](int r, V mir0, V mir1) {
         const int nn = k0 + K0 * r;
-        const V wk = cmul(wk0, rowp_sw(r));
+        const V wk = cmul(wk0, rowp_sw<T>(r));
         const V h0 = nn == 0 ? nyq0 : cconj(P != 0 ? mir1 : mir0);
         const V h1 = nn == 0 ? nyq1 : cconj(P != 0 ? mir0 : mir1);
         v[r] = pack(v[r], h0, wk);
