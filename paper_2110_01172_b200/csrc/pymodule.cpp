@@ -17,6 +17,7 @@
 #include "sdct/device.hpp"
 #include "sdct/errors.hpp"
 #include "sdct/transforms_ext.hpp"
+#include "sdct/plan_handle.hpp"
 #include "sdct_b200.h"
 
 namespace py = pybind11;
@@ -56,6 +57,36 @@ Array run(const Array& x, F&& f) {
   return to_array(y);
 }
 
+// Fused 2D/3D transforms straight between the numpy buffers: the input
+// array (already float64 C-contiguous after forcecast) goes to the device
+// plan's host entry point and the result lands in the freshly allocated
+// output array, with no RealTensor copies in between. Same plan (cache key
+// and orientation) the C++ API's Plan2d / Plan3d would use; any other rank
+// takes the C++ API path, which raises the reference's ShapeError.
+template <typename F>
+Array run_fused(const Array& x, int rank, int kind, F&& fallback) {
+  const py::buffer_info info = x.request();
+  bool ok = info.ndim == rank;
+  for (py::ssize_t d : info.shape) ok = ok && d > 0;
+  if (!ok) return run(x, fallback);
+  std::vector<std::int64_t> dims(info.shape.begin(), info.shape.end());
+  const int orient = rank == 2 ? (sdct::maybe_transpose_strategy(static_cast<std::size_t>(dims[0]),
+                                                                 static_cast<std::size_t>(dims[1])) ==
+                                          sdct::Orientation::Direct
+                                      ? SDCT_ORIENT_DIRECT
+                                      : SDCT_ORIENT_TRANSPOSED)
+                               : SDCT_ORIENT_DIRECT;
+  Array out(std::vector<py::ssize_t>(info.shape.begin(), info.shape.end()));
+  double* po = static_cast<double*>(out.request().ptr);
+  const double* pi = static_cast<const double*>(info.ptr);
+  {
+    py::gil_scoped_release nogil;
+    sdct::detail::PlanPtr plan = sdct::detail::make_plan(dims, 1, SDCT_F64, orient);
+    sdct::detail::check(sdct_exec_host(plan.get(), kind, pi, po, nullptr));
+  }
+  return out;
+}
+
 sdct::Dct1dVariant variant_from_name(const std::string& name) {
   if (name == "4n") return sdct::Dct1dVariant::FourN;
   if (name == "2n-mirrored") return sdct::Dct1dVariant::MirroredTwoN;
@@ -89,7 +120,9 @@ PYBIND11_MODULE(_sdct, m) {
         py::arg("x"), py::arg("threads") = 0, "y(k) = sum_{n>=1} x(n) sin(pi/N n (k+1/2))");
 
   m.def("dct_2d",
-        [](const Array& x, unsigned) { return run(x, [](const sdct::RealTensor& t) { return sdct::dct_2d(t); }); },
+        [](const Array& x, unsigned) {
+          return run_fused(x, 2, SDCT_DCT_2D, [](const sdct::RealTensor& t) { return sdct::dct_2d(t); });
+        },
         py::arg("x"), py::arg("threads") = 0, "Fused forward 2D DCT on the B200");
   m.def("dct_2d_rowcol",
         [](const Array& x, unsigned) {
@@ -116,11 +149,13 @@ PYBIND11_MODULE(_sdct, m) {
         },
         py::arg("x"), py::arg("threads") = 0, "Row-column IDXST/IDCT composite (same output as idxst_idct_2d)");
   m.def("idct_2d",
-        [](const Array& x, unsigned) { return run(x, [](const sdct::RealTensor& t) { return sdct::idct_2d(t); }); },
+        [](const Array& x, unsigned) {
+          return run_fused(x, 2, SDCT_IDCT_2D, [](const sdct::RealTensor& t) { return sdct::idct_2d(t); });
+        },
         py::arg("x"), py::arg("threads") = 0, "Fused inverse 2D DCT (idct_2d(dct_2d(x)) == N1*N2/4 * x)");
   m.def("idct_idxst_2d",
         [](const Array& x, unsigned) {
-          return run(x, [](const sdct::RealTensor& t) {
+          return run_fused(x, 2, SDCT_IDCT_IDXST_2D, [](const sdct::RealTensor& t) {
             if (t.rank() != 2) throw sdct::ShapeError("idct_idxst_2d expects a rank-2 array");
             return sdct::idct_idxst_2d(t, sdct::Plan2d(t.dim(0), t.dim(1)));
           });
@@ -128,17 +163,21 @@ PYBIND11_MODULE(_sdct, m) {
         py::arg("x"), py::arg("threads") = 0, "IDCT along axis 0, IDXST along axis 1 (fused)");
   m.def("idxst_idct_2d",
         [](const Array& x, unsigned) {
-          return run(x, [](const sdct::RealTensor& t) {
+          return run_fused(x, 2, SDCT_IDXST_IDCT_2D, [](const sdct::RealTensor& t) {
             if (t.rank() != 2) throw sdct::ShapeError("idxst_idct_2d expects a rank-2 array");
             return sdct::idxst_idct_2d(t, sdct::Plan2d(t.dim(0), t.dim(1)));
           });
         },
         py::arg("x"), py::arg("threads") = 0, "IDXST along axis 0, IDCT along axis 1 (fused)");
   m.def("dct_3d",
-        [](const Array& x, unsigned) { return run(x, [](const sdct::RealTensor& t) { return sdct::dct_3d(t); }); },
+        [](const Array& x, unsigned) {
+          return run_fused(x, 3, SDCT_DCT_3D, [](const sdct::RealTensor& t) { return sdct::dct_3d(t); });
+        },
         py::arg("x"), py::arg("threads") = 0, "Fused forward 3D DCT on the B200");
   m.def("idct_3d",
-        [](const Array& x, unsigned) { return run(x, [](const sdct::RealTensor& t) { return sdct::idct_3d(t); }); },
+        [](const Array& x, unsigned) {
+          return run_fused(x, 3, SDCT_IDCT_3D, [](const sdct::RealTensor& t) { return sdct::idct_3d(t); });
+        },
         py::arg("x"), py::arg("threads") = 0, "Fused inverse 3D DCT (idct_3d(dct_3d(x)) == N1*N2*N3/8 * x)");
 
   m.def("force_demo_fields",
