@@ -405,6 +405,14 @@ def run_ours(args, rank: int, world: int, local_rank: int, backend: str | None =
     if w["mode"] == "chain" and w["kinds"] == ["dct_2d", "idct_2d"]:
         scale = numel / 4.0
         parity["round_trip_rel_l2"] = float(((outs[0][1] / scale - xs[0]).norm() / xs[0].norm()).item())
+        if rank == 0:
+            # the forward transform of the timed loop's input against the C
+            # oracle (oracle/sdct_oracle.c, a few s at 4096^2 on one host core)
+            import oracle
+
+            x0 = xs[0][0].double().cpu().numpy()
+            parity["dct_2d_rel_l2_vs_oracle"] = float(
+                oracle.rel_l2(outs[0][0][0].double().cpu().numpy(), oracle.port.dct_2d(x0)))
     elif w["mode"] == "compress":
         zeroed.zero_()
         step(0)

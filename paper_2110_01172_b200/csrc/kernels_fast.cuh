@@ -614,7 +614,7 @@ __global__ void __launch_bounds__(Tile<T, L, NL, true>::NT)
     int band, plane, batch;
     coords(tile, band, plane, batch);
     V v[TL::E];
-    unsigned long long tr0 = 0, tr1 = 0, tr2 = 0;
+    unsigned long long tr0 = 0, tr1 = 0, tr2 = 0, tr3 = 0, tr4 = 0, tr5 = 0;
     if (a.trace && t == 0) tr0 = gtimer();
 
     if constexpr (!INV) {
@@ -672,11 +672,14 @@ __global__ void __launch_bounds__(Tile<T, L, NL, true>::NT)
         if (t == 0) bulk_wait_read();  // the previous tile's stores have left X
         __syncthreads();
         xchg_cta<TL, 0, 1>(v, X, t);
+        if (a.trace && t == 0) tr3 = gtimer();
         stage_compute<TL, 1, false>(v, w1);
         __syncthreads();  // CTA-wide reads of X done before the warp-local writes
         xchg_warp<TL, 1, 2>(v, X, t);
+        if (a.trace && t == 0) tr4 = gtimer();
         StageTw<TL, 2> w2;  // inactive (span == radix): no twiddles
         stage_compute<TL, 2, false>(v, w2);
+        if (a.trace && t == 0) tr5 = gtimer();
       } else {
         StageTw<TL, SL> wl;
         if constexpr (S == 1) {
@@ -858,12 +861,18 @@ __global__ void __launch_bounds__(Tile<T, L, NL, true>::NT)
       }
     }
     if (a.trace && t == 0) {
-      unsigned long long* o = a.trace + 5 * static_cast<long long>(tile);
+      // 8 values per tile: loop start, tile landed, next load issued, [early-
+      // reissue schedule: CTA-wide exchange done, warp exchange done, last stage
+      // done], stores issued, CTA id
+      unsigned long long* o = a.trace + 8 * static_cast<long long>(tile);
       o[0] = tr0;
       o[1] = tr1;
       o[2] = tr2;
-      o[3] = gtimer();
-      o[4] = blockIdx.x;
+      o[3] = tr3;
+      o[4] = tr4;
+      o[5] = tr5;
+      o[6] = gtimer();
+      o[7] = blockIdx.x;
     }
   }
   if (t == 0) bulk_wait_all();  // stores complete before the CTA retires

@@ -1,7 +1,8 @@
 """Phase trace of the persistent column kernel (developer tool).
 
-Uses the debug hook sdct_debug_set_trace (5 u64 per tile: loop start, tile
-landed, last-stage operands read, stores issued, CTA id)."""
+Uses the debug hook sdct_debug_set_trace (8 u64 per tile: loop start, tile
+landed, next load issued, [early-reissue schedule: CTA-wide exchange done,
+warp exchange done, last stage done], stores issued, CTA id)."""
 import ctypes
 import os
 import sys
@@ -21,7 +22,7 @@ plan = sd.plan_for((n, n), 1, dt, 0)
 ws = torch.empty(plan.workspace_bytes, dtype=torch.uint8, device="cuda")
 y = torch.empty_like(x)
 s = torch.cuda.current_stream().cuda_stream
-tr = torch.zeros(5 * 65536, dtype=torch.int64, device="cuda")
+tr = torch.zeros(8 * 65536, dtype=torch.int64, device="cuda")
 lib = capi.lib()
 lib.sdct_debug_set_trace.argtypes = [ctypes.c_void_p]
 for kind, st in ((_sdct.DCT_2D, 0), (_sdct.IDCT_2D, 1)):
@@ -31,19 +32,18 @@ for kind, st in ((_sdct.DCT_2D, 0), (_sdct.IDCT_2D, 1)):
         plan.run_stage(kind, st, x.data_ptr(), y.data_ptr(), s, ws.data_ptr())
         torch.cuda.synchronize()
     lib.sdct_debug_set_trace(None)
-    a = tr.view(-1, 5).cpu().numpy()
+    a = tr.view(-1, 8).cpu().numpy()
     a = a[a[:, 0] > 0]
     t0 = a[:, 0].min()
-    wait = (a[:, 1] - a[:, 0]) / 1e3
-    comp = (a[:, 2] - a[:, 1]) / 1e3
-    last = (a[:, 3] - a[:, 2]) / 1e3
-    tot = (a[:, 3].max() - t0) / 1e3
-    ctas = sorted(set(a[:, 4].tolist()))
+    tot = (a[:, 6].max() - t0) / 1e3
+    ctas = sorted(set(a[:, 7].tolist()))
     print(f"{dt} kind {kind}: tiles {len(a)}  span {tot:.1f} us  ctas {len(ctas)}")
-    print(f"  wait for tile   mean {wait.mean():.2f} us  p50 {np.median(wait):.2f}  max {wait.max():.2f}")
-    print(f"  stages..S-2     mean {comp.mean():.2f} us")
-    print(f"  last + stores   mean {last.mean():.2f} us")
-    first = a[a[:, 4] == 0]
-    first = first[np.argsort(first[:, 0])]
-    print("  cta0 (start, landed, lastread, stored) us:",
-          [tuple(round((v - t0) / 1e3, 1) for v in r[:4]) for r in first])
+    print(f"  wait for tile        mean {((a[:, 1] - a[:, 0]) / 1e3).mean():.2f} us")
+    print(f"  landed -> next issued mean {((a[:, 2] - a[:, 1]) / 1e3).mean():.2f} us")
+    if (a[:, 3] > 0).all():
+        print(f"  -> CTA exchange done  mean {((a[:, 3] - a[:, 2]) / 1e3).mean():.2f} us")
+        print(f"  -> warp exchange done mean {((a[:, 4] - a[:, 3]) / 1e3).mean():.2f} us")
+        print(f"  -> last stage done    mean {((a[:, 5] - a[:, 4]) / 1e3).mean():.2f} us")
+        print(f"  -> stores issued      mean {((a[:, 6] - a[:, 5]) / 1e3).mean():.2f} us")
+    else:
+        print(f"  -> stores issued      mean {((a[:, 6] - a[:, 2]) / 1e3).mean():.2f} us")
