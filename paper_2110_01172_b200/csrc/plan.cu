@@ -122,6 +122,7 @@ struct sdct_plan_s {
   TwSet tw_row = {};     // row FFT (length M)
   TwSet tw_col2 = {};    // cluster-split column pass: H-point stage tables (H = n1 / 2)
   bool col2 = false;     // 2D column passes run cluster-split (col2_used)
+  bool colc = false;     // 2D fp64 L = 4096 column passes run as persistent cluster pairs (kernels_colc.cuh)
   void* tw_comb = nullptr;  // cluster-split column pass: W_L^k, k < L/2
   // device tables (one allocation)
   void* tables = nullptr;
@@ -329,7 +330,15 @@ int build_plan(sdct_plan_s* p) {
     }();
     p->col2 = r == 2 && col2_used(static_cast<int>(p->elem()), p->n[0], 1, p->nl[0]) &&
               (p->n[0] > kMaxFastLen || col2_opt);
-    if (p->col2) {
+    // fp64 4096-row columns: the persistent cluster-pair pass is an opt-in
+    // experiment (SDCT_COLC=1): parity-green, but 87-93 us vs 78-82 us for the
+    // single-CTA early-reissue pass
+    static const bool colc_env = [] {
+      const char* f = getenv("SDCT_COLC");
+      return f && atoi(f) == 1;
+    }();
+    p->colc = r == 2 && !p->col2 && colc_env && p->dtype == SDCT_F64 && p->n[0] == 4096 && p->nl[0] == 2;
+    if (p->col2 || p->colc) {
       stages(p->n[0] / 2, st_c2);
       circle(re, im, p->n[0] / 2, 1.0L, p->n[0]);  // W_L^k, k < L/2
       put(off_comb);
@@ -372,8 +381,16 @@ int build_plan(sdct_plan_s* p) {
       blob.resize(off_srow[ax] + p->n[ax] * sizeof(int));
       int* q = reinterpret_cast<int*>(blob.data() + off_srow[ax]);
       const int L = p->n[ax], H = L / 2;
-      for (int k = 0; k < L; ++k)  // cluster-split passes: k = 2k' + c at row cH + sigma_H(k')
-        q[k] = (ax == 0 && p->col2) ? (k & 1) * H + rt_srow(k >> 1, H) : rt_srow(k, L);
+      for (int k = 0; k < L; ++k) {  // cluster-split passes: k = 2k' + c at row cH + sigma_H(k')
+        if (ax == 0 && p->colc) {
+          // cluster-pair pass: k = k' + hf H, slot n = digit_pos_H(k') = 8b + r ->
+          // row hf H + (b / (H/16)) H/2 + r H/16 + b mod H/16 (kernels_colc.cuh)
+          const int kp = k % H, hf = k / H, n = rt_digit_pos(kp, H), b = n >> 3, rr = n & 7, nb2 = H / 16;
+          q[k] = hf * H + (b / nb2) * (H / 2) + rr * nb2 + b % nb2;
+        } else {
+          q[k] = (ax == 0 && p->col2) ? (k & 1) * H + rt_srow(k >> 1, H) : rt_srow(k, L);
+        }
+      }
     }
     const long long pb0 = (r == 2 ? 1 : p->n[1]) * p->batch;
     p->nl[0] = pick_nl(static_cast<int>(p->elem()), p->n[0], p->M, pb0);
@@ -446,7 +463,7 @@ int build_plan(sdct_plan_s* p) {
     tws(st_c0, p->tw_col[0]);
     if (r == 3) tws(st_c1, p->tw_col[1]);
     tws(st_r, p->tw_row);
-    if (p->col2) tws(st_c2, p->tw_col2);
+    if (p->col2 || p->colc) tws(st_c2, p->tw_col2);
     p->tw_comb = off_comb == SIZE_MAX ? nullptr : base + off_comb;
     p->ta = base + off_ta;
     p->tb = base + off_tb;
@@ -564,6 +581,29 @@ bool make_class_map(CUtensorMap* map, bool f32, const void* base, long long inne
   return r == CUDA_SUCCESS;
 }
 
+// 5D map over x (forward source) or y (inverse destination) of the
+// cluster-pair column pass: {inner reals, row mod 4 (stride = row stride),
+// row / 4 (stride = 4 rows), planes, batch}; box {2*nl, 1, min(rows/4, 256), 1, 1}.
+bool make_class4_map(CUtensorMap* map, bool f32, const void* base, long long inner, long long rows,
+                     long long row_stride_b, long long planes, long long plane_stride_b, long long batch,
+                     long long batch_stride_b, int nl) {
+  auto enc = tmap_encoder();
+  if (!enc || rows % 4) return false;
+  const long long quads = rows / 4;
+  const cuuint64_t dims[5] = {static_cast<cuuint64_t>(inner), 4, static_cast<cuuint64_t>(quads),
+                              static_cast<cuuint64_t>(planes), static_cast<cuuint64_t>(batch)};
+  const cuuint64_t strides[4] = {static_cast<cuuint64_t>(row_stride_b), static_cast<cuuint64_t>(4 * row_stride_b),
+                                 static_cast<cuuint64_t>(plane_stride_b), static_cast<cuuint64_t>(batch_stride_b)};
+  const cuuint32_t box[5] = {static_cast<cuuint32_t>(2 * nl), 1, static_cast<cuuint32_t>(quads < 256 ? quads : 256), 1,
+                             1};
+  const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+  const CUresult r = enc(map, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5,
+                         const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                         CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 // Compression threshold carried by the 2D inverse row kernels (weight 3).
 struct Threshold {
   double eps = 0.0, scale = 1.0;
@@ -638,6 +678,28 @@ int run_fast(sdct_plan_s* p, int kind, int only_stage, const void* in, void* out
     }
     ++stage;
   };
+  // persistent cluster-pair 2D column pass (kernels_colc.cuh): forward reads
+  // the source through the 4-class map, the inverse writes y through it
+  auto colc = [&](bool inv, ColArgs a, const Side& in, const Side& o) {
+    a.twc = p->tw_comb;
+    if (want() && e == cudaSuccess && map_ok) {
+      NvtxRange nv("colc");
+      CUtensorMap mi, mo;
+      if (!inv) {
+        map_ok = make_class4_map(&mi, f32, a.src, in.inner, in.rows, in.row_stride * es, in.planes, in.plane_stride * es,
+                                 B, in.batch_stride * es, p->nl[0]) &&
+                 make_col_map(&mo, f32, a.dst, o.inner, o.rows, o.row_stride * es, o.planes, o.plane_stride * es, B,
+                              o.batch_stride * es, p->nl[0], 256);
+      } else {
+        map_ok = make_col_map(&mi, f32, a.src, in.inner, in.rows, in.row_stride * es, in.planes, in.plane_stride * es, B,
+                              in.batch_stride * es, p->nl[0], 256) &&
+                 make_class4_map(&mo, f32, a.dst, o.inner, o.rows, o.row_stride * es, o.planes, o.plane_stride * es, B,
+                                 o.batch_stride * es, p->nl[0]);
+      }
+      if (map_ok) e = launch_colc(inv, M / p->nl[0], B, st, mi, mo, a, p->tw_col2);
+    }
+    ++stage;
+  };
   auto row = [&](int rk, int groups, const RowArgs& a) {
     if (want() && e == cudaSuccess) {
       NvtxRange nv("row");
@@ -677,6 +739,8 @@ int run_fast(sdct_plan_s* p, int kind, int only_stage, const void* in, void* out
       c.out_batch = inter;
       if (p->col2)
         col2(false, c, Side{n2, n1, n2, 1, item, item}, Side{2LL * M, n1, 2LL * M, 1, 2 * inter, 2 * inter});
+      else if (p->colc)
+        colc(false, c, Side{n2, n1, n2, 1, item, item}, Side{2LL * M, n1, 2LL * M, 1, 2 * inter, 2 * inter});
       else
         col(CV_FWD_SRC, n1, p->nl[0], 1, c, p->tw_col[0], Side{n2, n1, n2, 1, item, item},
             Side{2LL * M, n1, 2LL * M, 1, 2 * inter, 2 * inter});
@@ -705,6 +769,8 @@ int run_fast(sdct_plan_s* p, int kind, int only_stage, const void* in, void* out
       c.sign_col = mode == 2;
       if (p->col2)
         col2(true, c, Side{2LL * M, n1, 2LL * M, 1, 2 * inter, 2 * inter}, Side{n2, n1, n2, 1, item, item});
+      else if (p->colc)
+        colc(true, c, Side{2LL * M, n1, 2LL * M, 1, 2 * inter, 2 * inter}, Side{n2, n1, n2, 1, item, item});
       else
         col(CV_INV_DST, n1, p->nl[0], 1, c, p->tw_col[0], Side{2LL * M, n1, 2LL * M, 1, 2 * inter, 2 * inter},
             Side{n2, n1, n2, 1, item, item});

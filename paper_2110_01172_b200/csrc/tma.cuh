@@ -113,6 +113,38 @@ __device__ __forceinline__ float2 ld_dsmem(uint32_t addr, float2*) {
   return v;
 }
 
+// Asynchronous 16-B store into a peer CTA's shared memory (shared::cluster
+// address from mapa) that counts its bytes on the peer's mbarrier (also a
+// shared::cluster address): the peer waits on its own barrier, no cluster
+// barrier needed.
+__device__ __forceinline__ void st_async(uint32_t addr, double2 v, uint32_t bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" ::"r"(addr),
+               "d"(v.x), "d"(v.y), "r"(bar)
+               : "memory");
+}
+__device__ __forceinline__ void st_async(uint32_t addr, float2 v, uint32_t bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f32 [%0], {%1, %2}, [%3];" ::"r"(addr),
+               "f"(v.x), "f"(v.y), "r"(bar)
+               : "memory");
+}
+// arrive (release, cluster scope) on an mbarrier of a peer CTA
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t bar) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+// wait with acquire at cluster scope (the phase was completed by peer-CTA
+// operations whose shared-memory effects must be visible)
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n\t"
+      ".reg .pred p;\n\t"
+      "WAITC_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAITC_%=;\n\t"
+      "}" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+
 // ---- TMA stores (shared -> global), bulk-group completion ------------------
 __device__ __forceinline__ void tma_store_4d(const CUtensorMap* map, int c0, int c1, int c2, int c3, const void* src) {
   asm volatile(
