@@ -4,6 +4,7 @@ to the reference in tests/test_oracle.py) and against the reference's golden
 vectors. Tolerances (BASELINE.json north_star): rel-L2 <= 1e-12 fp64,
 <= 1e-5 fp32 (fp32 inputs are the fp64 draw rounded to fp32, fed identically
 to the fp64 oracle)."""
+import os
 import numpy as np
 import pytest
 import scipy.fft as sf
@@ -842,3 +843,28 @@ def test_orientation_and_threads_do_not_change_results(cuda):
         assert np.array_equal(sd.dct_2d(xh, threads=1), sd.dct_2d(xh, threads=8))
         # counters follow the oriented extents like the reference (dct2d.cpp:371-374)
         assert capi.Plan(shape, orientation=capi.ORIENT_TRANSPOSED).counters("dct_2d")[0] == 3
+
+
+def test_cluster_pair_column_pass_opt_in(cuda):
+    # the opt-in persistent cluster-pair column pass (SDCT_COLC=1, read once per
+    # process, hence the subprocess): fp64 4096-row bands, all four 2D kinds
+    # and a batch, against the C oracle
+    import subprocess
+    import sys
+
+    code = (
+        "import numpy as np, torch, oracle, paper_2110_01172_b200 as sd\n"
+        "rng = np.random.default_rng(9)\n"
+        "x = rng.uniform(-1, 1, (2, 4096, 64))\n"
+        "xt = torch.tensor(x, device='cuda')\n"
+        "err = 0.0\n"
+        "for k in ('dct_2d', 'idct_2d', 'idct_idxst_2d', 'idxst_idct_2d'):\n"
+        "    y = getattr(sd, k)(xt).cpu().numpy()\n"
+        "    for i in range(2):\n"
+        "        err = max(err, oracle.rel_l2(y[i], getattr(oracle.port, k)(x[i])))\n"
+        "print(err)\n")
+    env = dict(os.environ, SDCT_COLC="1")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert float(r.stdout.strip().splitlines()[-1]) <= 1e-12

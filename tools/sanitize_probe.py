@@ -6,12 +6,15 @@ import paper_2110_01172_b200 as sd
 
 torch.manual_seed(0)
 for dt in (torch.float64, torch.float32):
-    for shape in [(64, 128), (2048, 2048), (16, 4096)]:
+    # (4096, 64): early-reissue fp64 column pass; (64, 4096) / (32, 2048) / batched:
+    # the mirror-paired row kernels (M = 2048 / 1024)
+    for shape in [(64, 128), (2048, 2048), (16, 4096), (4096, 64), (64, 4096), (32, 2048), (2, 64, 4096)]:
         x = torch.rand(shape, dtype=dt, device="cuda")
         for f in (sd.dct_2d, sd.idct_2d, sd.idct_idxst_2d, sd.idxst_idct_2d):
             f(x)
         sd.force_demo_fields(x)
-        sd.compress(x, 0.5)
+        if x.dim() == 2:
+            sd.compress(x, 0.5)
     x3 = torch.rand((16, 8, 32), dtype=dt, device="cuda")
     sd.dct_3d(x3)
     sd.idct_3d(x3)
