@@ -187,7 +187,7 @@ cudaError_t launch_row2(dim3 grid, cudaStream_t st, const RowArgs& a, const TwSe
 template <typename T, int M, int KIND>
 cudaError_t launch_row_one(dim3 grid, cudaStream_t st, const RowArgs& a, const TwSet& tw) {
   if constexpr (KIND == RK_FWD2 || KIND == RK_INV2) {
-    if constexpr (rowp_ok<T, M>()) {
+    if constexpr (rowp_ok<T, M, KIND == RK_INV2>()) {
       // fp64 M = 2048: the mirror-paired ring kernel (kernels_rowp.cuh);
       // SDCT_ROWP=0 selects the row2 schedules below (A/B)
       static const bool rowp = [] {

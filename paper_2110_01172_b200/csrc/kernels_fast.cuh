@@ -149,7 +149,7 @@ constexpr int tile_max_threads() { return 512; }
 #define SDCT_COL_XS_INV 0
 #endif
 
-template <typename T, int L_, int NL_, bool LF>
+template <typename T, int L_, int NL_, bool LF, int MAXT_ = 0>
 struct Tile {
   static constexpr int L = L_;
   static constexpr int NL = NL_;
@@ -161,7 +161,8 @@ struct Tile {
   static constexpr int LGNL = ilog2c(NL);
   static constexpr int TOT = L * NL;
   static constexpr int NT0 = TOT / R0;
-  static constexpr int MAXT = (LF && sizeof(T) == 8) ? SDCT_COL_MAXT_F64 : tile_max_threads<T>();
+  // MAXT_ > 0: cap on the thread count (more elements per thread)
+  static constexpr int MAXT = MAXT_ > 0 ? MAXT_ : (LF && sizeof(T) == 8) ? SDCT_COL_MAXT_F64 : tile_max_threads<T>();
   static constexpr int NT = NT0 > MAXT ? MAXT : NT0;
   static constexpr int E = TOT / NT;
   static constexpr unsigned MASK = NT >= 32 ? 0xffffffffu : ((1u << NT) - 1u);

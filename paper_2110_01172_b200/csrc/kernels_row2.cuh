@@ -36,9 +36,9 @@ namespace sdctb {
 // Row tile of the pair kernel. GROUPS > 1: the tile's threads are one of
 // several groups in the CTA; exchanges synchronise on the group's named
 // barrier (id 1 + group).
-template <typename T, int M, bool FULLTW, int GROUPS>
-struct Row2Tile : Tile<T, M, 2, false> {
-  using Base = Tile<T, M, 2, false>;
+template <typename T, int M, bool FULLTW, int GROUPS, int MAXT_ = 0>
+struct Row2Tile : Tile<T, M, 2, false, MAXT_> {
+  using Base = Tile<T, M, 2, false, MAXT_>;
   static constexpr bool TWF = FULLTW;
   __device__ __forceinline__ static void sync() {
     if constexpr (GROUPS == 1) {

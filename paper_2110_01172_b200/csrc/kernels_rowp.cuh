@@ -35,23 +35,32 @@ namespace sdctb {
 // (fp64 M = 2048: 3 x 64 KB, one CTA per SM; fp64 M = 1024: 3 x 32 KB, two).
 template <typename T, int M>
 struct RowpGeom {
-  using TL = Row2Tile<T, M, false, 2>;
+  // M = 512 (radices 8, 8, 8): cap the tile at 64 threads so that every
+  // thread holds 16 elements, the radix-8 last stage's two butterflies being
+  // the two rows (as for M = 1024, 2048)
+  using TL = Row2Tile<T, M, false, 2, M == 512 ? 64 : 0>;
   static constexpr unsigned BUF = 2u * M * sizeof(cx_t<T>);
   static constexpr int NT = TL::NT, CTA = 2 * TL::NT, GROUPS = 2;
   // 512-thread CTAs (M = 2048) keep 128 registers per thread with one CTA per
-  // SM; 256-thread CTAs (M = 1024) run two per SM
-  static constexpr int MINB = CTA >= 512 ? 1 : 2;
+  // SM; 256-thread CTAs (M = 1024) run two per SM, 128-thread CTAs three
+  static constexpr int MINB = CTA >= 512 ? 1 : CTA >= 256 ? 2 : 3;
   static constexpr int NBUF = (200u * 1024u) / (BUF * MINB) >= 4 ? 4 : 3;
   static constexpr size_t BARS = static_cast<size_t>(NBUF) * BUF;
   static constexpr size_t SMEM = BARS + 16 * NBUF;
 };
 
-template <typename T, int M>
+// M = 1024, 2048 both directions; M = 512 forward only (the inverse's paired
+// last DIT stage assumes one stage-0 butterfly per thread)
+template <typename T, int M, bool INV = false>
 constexpr bool rowp_ok() {
-  using TL = Row2Tile<T, M, false, 2>;
-  using P = typename TL::P;
-  return (M == 2048 || M == 1024) && TL::S == 3 && P::R(2) == 8 && TL::NT == M / 8 && TL::E == 16 &&
-         RowpGeom<T, M>::MINB * RowpGeom<T, M>::SMEM <= 220u * 1024u;
+  if constexpr (M != 512 && M != 1024 && M != 2048) {
+    return false;
+  } else {
+    using TL = typename RowpGeom<T, M>::TL;
+    using P = typename TL::P;
+    return (!INV || M != 512) && TL::S == 3 && P::R(2) == 8 && TL::NT == M / 8 && TL::E == 16 &&
+           RowpGeom<T, M>::MINB * RowpGeom<T, M>::SMEM <= 220u * 1024u;
+  }
 }
 
 // k0 of group-local thread t (see above): lanes l < 16 of warp w take
@@ -102,7 +111,7 @@ __device__ __forceinline__ cx_t<T> rowp_sw(int r) {
 template <typename T, int M, bool INV>
 __global__ void __launch_bounds__(RowpGeom<T, M>::CTA, RowpGeom<T, M>::MINB)
     rowp_kernel(RowArgs a, TwSet tw, int nitems) {
-  static_assert(rowp_ok<T, M>(), "mirror-paired row kernel: M = 1024 / 2048 geometry only");
+  static_assert(rowp_ok<T, M, INV>(), "mirror-paired row kernel: M = 512 (forward), 1024, 2048 only");
   using G = RowpGeom<T, M>;
   using TL = typename G::TL;
   using V = cx_t<T>;
