@@ -8,9 +8,13 @@
 // This replaces the reference's scalar radix-2 FftWorkspace::pow2_fft
 // (proj/src/rfft.cpp:65-89) for the power-of-two extents of the hot path.
 //
-// Shared-memory layouts are XOR-swizzled so that every stage's access pattern
-// is bank-conflict free (tests/test_host.py replays the exact index math below
-// through tests/swizzle_model.py).
+// Shared-memory layouts are XOR-swizzled so that every FFT stage's exchange
+// pattern is bank-conflict free (tests/test_host.py replays the exact index
+// math below through tests/swizzle_model.py). Accesses outside the stage
+// exchanges are not covered by that claim: the forward row kernels' stage-0
+// reads of bulk-landed pair-interleaved rows (stride-2 columns, 2-way) and
+// the mirror-paired radix-8 stage at M = 1024 (2-way; also modelled in
+// tests/test_host.py) — see DESIGN.md §6b for what removing them cost.
 #pragma once
 
 #include "sdct_common.cuh"
