@@ -213,6 +213,9 @@ __global__ void __launch_bounds__(RowpGeom<T, M>::CTA, RowpGeom<T, M>::MINB)
         stage_compute<TL, 1, false>(v, w1);
       }
       to_smem<TL, 1>(v, sm, t);
+      // the postprocess's table values, issued ahead of the last stage they follow
+      const V av0 = __ldg(static_cast<const V*>(a.ta) + q1), av1 = __ldg(static_cast<const V*>(a.ta) + m1);
+      const V bk0 = fac_lookup(fbt, k0, a.fs), wk0 = fac_lookup(fut, k0, a.fs);
       TL::sync();
 #pragma unroll
       for (int r = 0; r < 8; ++r) {
@@ -229,7 +232,6 @@ __global__ void __launch_bounds__(RowpGeom<T, M>::CTA, RowpGeom<T, M>::MINB)
       T* y = static_cast<T*>(a.dst) + batch * a.dst_batch;
       T* r0 = y + static_cast<long long>(q1) * n2;
       T* r1 = y + static_cast<long long>(m1) * n2;
-      const V av0 = __ldg(static_cast<const V*>(a.ta) + q1), av1 = __ldg(static_cast<const V*>(a.ta) + m1);
       const V a40 = mk(av0.x * T(0.25), av0.y * T(0.25)), a41 = mk(av1.x * T(0.25), av1.y * T(0.25));
       auto unpack2 = [](V A, V Bc, V w) {  // Bc = conj(B) as stored
         const T sx = A.x + Bc.x, sy = A.y - Bc.y;
@@ -264,7 +266,6 @@ __global__ void __launch_bounds__(RowpGeom<T, M>::CTA, RowpGeom<T, M>::MINB)
       };
       // b(q), W^q on q = k0 + K0 r: the thread's base values times
       // compile-time steps (no table lookup per frequency)
-      const V bk0 = fac_lookup(fbt, k0, a.fs), wk0 = fac_lookup(fut, k0, a.fs);
       auto bq_of = [&](int r) {  // b(k0 + K0 r), negated where the corrupt hook says so
         V bq = cmul(bk0, rowp_sb<T>(r));
         if (a.badq && a.badq[k0 + K0 * r]) bq = mk(-bq.x, -bq.y);
@@ -288,6 +289,9 @@ __global__ void __launch_bounds__(RowpGeom<T, M>::CTA, RowpGeom<T, M>::MINB)
       if (self0) item(M, v[0], v[0], v[8], v[8], bq_of(8), rowp_sw<T>(8));
     } else {
       // ===== inverse: preprocess + packing into the paired DIT input =======
+      // table values of this item, issued before the landing wait they overlap
+      const V ca0 = cconj(__ldg(static_cast<const V*>(a.ta) + q1)), ca1 = cconj(__ldg(static_cast<const V*>(a.ta) + m1));
+      const V bk0 = fac_lookup(fbt, k0, a.fs), wk0 = fac_lookup(fut, k0, a.fs);
       mbar_wait(full + b, ph);
       const T* rowA = reinterpret_cast<const T*>(sm);
       const T* rowB = reinterpret_cast<const T*>(sm) + 2 * M;
@@ -326,14 +330,12 @@ __global__ void __launch_bounds__(RowpGeom<T, M>::CTA, RowpGeom<T, M>::MINB)
         rowA = rowB;
         rowB = tmp;
       }
-      const V* ta = static_cast<const V*>(a.ta);
-      const V ca0 = cconj(__ldg(ta + q1)), ca1 = cconj(__ldg(ta + m1));
+
       // X'(0, nn), X'(1, nn) (proj/src/dct2d.cpp:182-195) from x(nn), x(N2-nn)
       // of both rows (x(N2) := 0); mode 2 reads x(N2-nn) for D and x(nn) for R
       // with x(0) := 0 (dct2d.cpp:169-180)
       // c0 = conj a(q1) conj b(nn), c1 = conj a(m1) conj b(nn) with
       // b(k0 + K0 r) = b(k0) e^{-i pi r/32}: per-item constants times the step
-      const V bk0 = fac_lookup(fbt, k0, a.fs), wk0 = fac_lookup(fut, k0, a.fs);
       const V cc0 = cmulc(ca0, bk0), cc1 = cmulc(ca1, bk0);
       auto xpair = [&](int r, V& x0, V& x1) {
         const int nn = k0 + K0 * r;
