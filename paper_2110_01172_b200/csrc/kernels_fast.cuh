@@ -1028,6 +1028,13 @@ __global__ void __launch_bounds__(row_threads<T, M, KIND>())
   }
 
   V v[TL::E];
+  // 3D forward: the postprocess's a(k1) b(k2) table values, issued before the
+  // row landing they overlap
+  V av3{}, bv3{};
+  if constexpr (KIND == RK_FWD3) {
+    av3 = __ldg(static_cast<const V*>(a.ta) + q1);
+    bv3 = __ldg(static_cast<const V*>(a.tb) + q2);
+  }
   if constexpr (!INV) {
     // ---- forward: the G rows land in smem by 1D bulk copies ----------------
     StageTw<TL, 0> w0;
@@ -1306,9 +1313,7 @@ __global__ void __launch_bounds__(row_threads<T, M, KIND>())
     T* y = static_cast<T*>(a.dst) + batch * a.dst_batch;
     const int n3 = a.n3;
     const V* tu = static_cast<const V*>(a.tu);
-    const V av = __ldg(static_cast<const V*>(a.ta) + q1);
-    const V bv = __ldg(static_cast<const V*>(a.tb) + q2);
-    const V ab = cmul(av, bv), cb = cmulc(bv, av);  // a b, conj(a) b
+    const V ab = cmul(av3, bv3), cb = cmulc(bv3, av3);  // a b, conj(a) b
     auto put = [&](int i, int j, int k, T val) { y[(static_cast<long long>(i) * n2 + j) * n3 + k] = val; };
     auto item = [&](int k3, const V* Za, const V* Zb) {
       // Za[l] = Z(line l, k3), Zb[l] = Z(line l, -k3)
