@@ -67,8 +67,13 @@ enum {
   SDCT_IDCT_1D = 8,       /* sdct::idct_1d       proj/include/sdct/dct1d.hpp:97-99  (rank-1 plans) */
   SDCT_IDXST_1D = 9,      /* sdct::idxst_1d      proj/include/sdct/transforms_ext.hpp:29-31 */
   SDCT_IDCT_IDXST_2D_ROWCOL = 10, /* sdct::idct_idxst_2d_rowcol proj/include/sdct/transforms_ext.hpp:43-44 */
-  SDCT_IDXST_IDCT_2D_ROWCOL = 11  /* sdct::idxst_idct_2d_rowcol proj/include/sdct/transforms_ext.hpp:45-46 */
+  SDCT_IDXST_IDCT_2D_ROWCOL = 11, /* sdct::idxst_idct_2d_rowcol proj/include/sdct/transforms_ext.hpp:45-46 */
+  SDCT_DCT_AXIS0 = 12,    /* sdct::dct_1d (N-point, proj/src/dct1d.cpp) of every column of a rank-2 plan */
+  SDCT_IDCT_AXIS0 = 13    /* sdct::idct_1d of every column of a rank-2 plan */
 };
+/* The two *_AXIS0 kinds are the axis-0 leg of the slab-decomposed 3D transform
+ * (SURVEY.md §8e): one persistent column pass over an (n1 x n2) matrix, n1 a
+ * power of two in [8, 4096], n2 a multiple of 32 bytes' worth of elements. */
 /* The three *_ROWCOL kinds are the reference's 8-stage row-column baselines
  * (proj/src/dct2d.cpp:395-406, transforms_ext.cpp:287-311): per axis one
  * kernel (parity reorder / embedding, row FFTs and twiddle stage fused) and

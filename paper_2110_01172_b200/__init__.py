@@ -24,12 +24,14 @@ from .api import (
     dct_2d_rowcol,
     dct_3d,
     dct_4d,
+    dct_axis0,
     dct_oracle_1d,
     dct_oracle_2d,
     force_demo_fields,
     idct_1d,
     idct_2d,
     idct_3d,
+    idct_axis0,
     idct_idxst_2d,
     idct_idxst_2d_rowcol,
     idxst_1d,
@@ -46,7 +48,7 @@ __all__ = [
     "dct_2d", "dct_2d_rowcol", "idct_2d", "idct_idxst_2d", "idxst_idct_2d",
     "idct_idxst_2d_rowcol", "idxst_idct_2d_rowcol",
     "dct_3d", "dct_4d", "idct_3d", "plan_for", "stream_host", "force_demo_fields",
-    "dct_oracle_1d", "dct_oracle_2d", "compress",
+    "dct_oracle_1d", "dct_oracle_2d", "compress", "dct_axis0", "idct_axis0",
     "read_dctb", "write_dctb", "transform_file",
 ]
 

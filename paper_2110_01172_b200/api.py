@@ -15,6 +15,7 @@ _KIND = {
     "idxst_idct_2d": _sdct.IDXST_IDCT_2D, "dct_2d_rowcol": _sdct.DCT_2D_ROWCOL,
     "idct_idxst_2d_rowcol": _sdct.IDCT_IDXST_2D_ROWCOL, "idxst_idct_2d_rowcol": _sdct.IDXST_IDCT_2D_ROWCOL,
     "dct_3d": _sdct.DCT_3D, "idct_3d": _sdct.IDCT_3D,
+    "dct_axis0": _sdct.DCT_AXIS0, "idct_axis0": _sdct.IDCT_AXIS0,
 }
 _RANK = {"dct_1d": 1, "idct_1d": 1, "idxst_1d": 1, "dct_3d": 3, "idct_3d": 3}
 
@@ -79,6 +80,38 @@ def _device_call(name: str, x):
 
 
 ShapeError = _sdct.ShapeError
+
+
+def dct_axis0(x):
+    """The reference's N-point ``dct_1d`` (proj/src/dct1d.cpp) applied to every
+    column of a rank-2 torch CUDA tensor (n1 x m, optional leading batch dims;
+    n1 a power of two in [8, 4096], m a multiple of 32 bytes' worth of
+    elements): one persistent column pass (kernels_col1d.cuh). The axis-0 leg
+    of the slab-decomposed 3D transform (slab3d.py)."""
+    if not _is_torch_cuda(x):
+        raise TypeError("dct_axis0 takes a torch CUDA tensor")
+    return _device_call("dct_axis0", x) if _axis0_ok(x) else _axis0_by_transpose(dct_1d, x)
+
+
+def idct_axis0(x):
+    """The reference's ``idct_1d`` (idct_1d(dct_1d(x)) == n1/2 x) along axis 0
+    of every column; same shapes as :func:`dct_axis0`."""
+    if not _is_torch_cuda(x):
+        raise TypeError("idct_axis0 takes a torch CUDA tensor")
+    return _device_call("idct_axis0", x) if _axis0_ok(x) else _axis0_by_transpose(idct_1d, x)
+
+
+def _axis0_ok(x) -> bool:
+    """Shapes the axis-0 column pass takes (else: transpose, contiguous 1D
+    transform on the generic GPU path, transpose back)."""
+    if x.dim() < 2:
+        raise ShapeError(f"axis-0 transforms expect a rank-2 tensor (plus optional batch dims), got {tuple(x.shape)}")
+    n1, m = int(x.shape[-2]), int(x.shape[-1])
+    return 8 <= n1 <= 4096 and (n1 & (n1 - 1)) == 0 and (m * x.element_size()) % 32 == 0
+
+
+def _axis0_by_transpose(f, x):
+    return f(x.transpose(-1, -2).contiguous()).transpose(-1, -2).contiguous()
 
 
 def _make(name: str, with_variant: bool = False):

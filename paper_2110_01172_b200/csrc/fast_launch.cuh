@@ -78,6 +78,10 @@ cudaError_t launch_col(int variant, int L, int nl, dim3 grid, cudaStream_t st, c
                        const CUtensorMap& omap, const ColArgs& a, const TwSet& tw);
 template <typename T>
 cudaError_t launch_row(int M, int kind, dim3 grid, cudaStream_t st, const RowArgs& a, const TwSet& tw);
+// axis-0 1D DCT-II / DCT-III column pass (kernels_col1d.cuh), L in [8, 4096]
+template <typename T>
+cudaError_t launch_col1d(bool inv, int L, int bands, int batch, cudaStream_t st, const CUtensorMap& map,
+                         const CUtensorMap& omap, const ColArgs& a, const TwSet& tw);
 // persistent cluster-pair column pass (kernels_colc.cuh): fp64, L = 4096
 cudaError_t launch_colc(bool inv, int bands, int batch, cudaStream_t st, const CUtensorMap& map,
                         const CUtensorMap& omap, const ColArgs& a, const TwSet& tw);

@@ -41,7 +41,8 @@ const char* kind_name(int kind) {
   static const char* names[] = {"sdct:dct_2d",         "sdct:idct_2d",          "sdct:idct_idxst_2d",
                                 "sdct:idxst_idct_2d",  "sdct:dct_3d",           "sdct:idct_3d",
                                 "sdct:dct_2d_rowcol",  "sdct:dct_1d",           "sdct:idct_1d",
-                                "sdct:idxst_1d",       "sdct:idct_idxst_2d_rowcol", "sdct:idxst_idct_2d_rowcol"};
+                                "sdct:idxst_1d",       "sdct:idct_idxst_2d_rowcol", "sdct:idxst_idct_2d_rowcol",
+                                "sdct:dct_axis0",      "sdct:idct_axis0"};
   return kind >= 0 && kind < static_cast<int>(sizeof(names) / sizeof(names[0])) ? names[kind] : "sdct:?";
 }
 }  // namespace
@@ -122,6 +123,9 @@ struct sdct_plan_s {
   TwSet tw_row = {};     // row FFT (length M)
   TwSet tw_col2 = {};    // cluster-split column pass: H-point stage tables (H = n1 / 2)
   bool col2 = false;     // 2D column passes run cluster-split (col2_used)
+  bool ax0_ok = false;   // rank 2, pow2 n1 in [8, 4096]: the axis-0 1D kinds (kernels_col1d.cuh)
+  TwSet tw_ax0 = {};     // n1-point stage tables of the axis-0 pass
+  void* axq = nullptr;   // a(k) = e^{-i pi k / (2 n1)}, k < n1
   bool colc = false;     // 2D fp64 L = 4096 column passes run as persistent cluster pairs (kernels_colc.cuh)
   void* tw_comb = nullptr;  // cluster-split column pass: W_L^k, k < L/2
   // device tables (one allocation)
@@ -400,6 +404,17 @@ int build_plan(sdct_plan_s* p) {
     // generic scratch, plus (rank 2) one real tensor for the row-column passes
     p->ws_bytes = p->generic_ws_bytes() + (r == 2 ? static_cast<size_t>(p->batch) * p->item_bytes() : 0);
   }
+  // axis-0 1D transforms (kernels_col1d.cuh): n1-point stage tables + a(k)
+  size_t off_ax0[4] = {SIZE_MAX, SIZE_MAX, SIZE_MAX, SIZE_MAX}, off_axq = SIZE_MAX;
+  if (r == 2 && is_pow2(p->n[0]) && p->n[0] >= 8 && p->n[0] <= kMaxFastLen) {
+    const bool f32 = p->dtype == SDCT_F32;
+    if (f32) stage_tables<float>(blob, p->n[0], off_ax0);
+    else stage_tables<double>(blob, p->n[0], off_ax0);
+    circle(re, im, p->n[0], 1.0L, 4.0L * p->n[0]);
+    if (f32) fill_table<float>(blob, off_axq, re, im);
+    else fill_table<double>(blob, off_axq, re, im);
+    p->ax0_ok = true;
+  }
   // row-column row-DCT tables (kernels_rowcol.cuh)
   size_t off_rcst[2][4], off_rcq[2] = {0, 0}, off_rcw[2] = {0, 0};
   if (r == 2) {
@@ -490,6 +505,10 @@ int build_plan(sdct_plan_s* p) {
     p->rc_q[a] = base + off_rcq[a];
     p->rc_w[a] = base + off_rcw[a];
   }
+  if (p->ax0_ok) {
+    for (int k = 0; k < 4; ++k) p->tw_ax0.st[k] = off_ax0[k] == SIZE_MAX ? nullptr : base + off_ax0[k];
+    p->axq = base + off_axq;
+  }
   p->b_offset_gen = r >= 2 ? off_gq[1] : off_gq[0];
   // the plan-owned workspace is allocated on first use with no caller
   // workspace (ensure_ws): the torch path always passes its own
@@ -505,6 +524,8 @@ bool kind_ok(const sdct_plan_s* p, int kind) {
     case SDCT_DCT_2D_ROWCOL:
     case SDCT_IDCT_IDXST_2D_ROWCOL:
     case SDCT_IDXST_IDCT_2D_ROWCOL:
+    case SDCT_DCT_AXIS0:
+    case SDCT_IDCT_AXIS0:
       return p->rank == 2;
     case SDCT_DCT_3D:
     case SDCT_IDCT_3D:
@@ -945,10 +966,49 @@ int run_rowcol(sdct_plan_s* p, int kind, int only_stage, const void* in, void* o
   return SDCT_OK;
 }
 
+bool is_axis0(int kind) { return kind == SDCT_DCT_AXIS0 || kind == SDCT_IDCT_AXIS0; }
+
+// Axis-0 1D DCT-II / DCT-III of every column (kernels_col1d.cuh): one
+// persistent column pass, band rows of 32 B, all batch items as tiles.
+template <typename T>
+int run_axis0(sdct_plan_s* p, int kind, const void* in, void* out, cudaStream_t st, int* nstages) {
+  if (nstages) *nstages = 1;
+  const int n1 = p->n[0], n2 = p->n[1];
+  const long long es = sizeof(T);
+  const int nl = static_cast<int>(16 / es);
+  // (the plan's 2D orientation does not apply: p->n are the caller's extents)
+  if (!p->ax0_ok || n2 % (2 * nl) != 0)
+    return fail(SDCT_ERR_PLAN, "axis-0 transforms need a power-of-two n1 in [8, 4096] and n2 a multiple of " +
+                                   std::to_string(2 * nl));
+  const bool inv = kind == SDCT_IDCT_AXIS0;
+  const bool f32 = sizeof(T) == 4;
+  const long long item = static_cast<long long>(n1) * n2;
+  const long long B = p->batch;
+  CUtensorMap mi, mo;
+  bool ok;
+  if (!inv)
+    ok = make_class_map(&mi, f32, in, n2, n1, n2 * es, 1, item * es, B, item * es, nl) &&
+         make_col_map(&mo, f32, out, n2, n1, n2 * es, 1, item * es, B, item * es, nl, n1 / 2);
+  else
+    ok = make_col_map(&mi, f32, in, n2, n1, n2 * es, 1, item * es, B, item * es, nl, n1 / 2) &&
+         make_class_map(&mo, f32, out, n2, n1, n2 * es, 1, item * es, B, item * es, nl);
+  if (!ok) return fail(SDCT_ERR_CUDA, "cuTensorMapEncodeTiled failed (axis-0 pass)");
+  ColArgs a{};
+  a.src = in;
+  a.dst = out;
+  a.twc = p->axq;  // a(k) = e^{-i pi k / (2 n1)}
+  a.scale = 0.5;  // idct_1d: y(pe(n)) = z(n) / 2
+  NvtxRange nv("col1d");
+  const cudaError_t e = launch_col1d<T>(inv, n1, n2 / (2 * nl), static_cast<int>(B), st, mi, mo, a, p->tw_ax0);
+  if (e != cudaSuccess) return cuda_fail(e, "launching the axis-0 column pass");
+  return SDCT_OK;
+}
+
 template <typename T>
 int run(sdct_plan_s* p, int kind, int only_stage, const void* in, void* out, void* ws,
         cudaStream_t st, int* nstages, int weight, const Threshold* thr) {
   if (is_rowcol(kind)) return run_rowcol<T>(p, kind, only_stage, in, out, ws, st, nstages);
+  if (is_axis0(kind)) return only_stage > 0 ? SDCT_OK : run_axis0<T>(p, kind, in, out, st, nstages);
   if (p->fast) {
     // batch items ride on grid.y / grid.z (<= 65535): larger batches run as
     // consecutive launch sets over contiguous chunks (same workspace layout)
@@ -1565,6 +1625,8 @@ int sdct_stage_count(sdct_plan_t p, int kind, int* count) {
   if (!kind_ok(p, kind)) return fail(SDCT_ERR_PLAN, "transform kind does not match the plan rank");
   if (is_rowcol(kind)) {
     *count = 4;
+  } else if (kind == SDCT_DCT_AXIS0 || kind == SDCT_IDCT_AXIS0) {
+    *count = 1;
   } else if (p->fast) {
     *count = p->rank == 2 ? 2 : 3;
   } else {
@@ -1600,6 +1662,9 @@ int sdct_counters(sdct_plan_t p, int kind, uint64_t out[5]) {
     case SDCT_DCT_2D_ROWCOL:
     case SDCT_IDCT_IDXST_2D_ROWCOL:
     case SDCT_IDXST_IDCT_2D_ROWCOL: c.stages = 8; break;  // 3 + 1 + 3 + 1 (dct2d.cpp:398-405)
+    case SDCT_DCT_AXIS0:
+    case SDCT_IDCT_AXIS0:
+      return fail(SDCT_ERR_PLAN, "no reference stage counters for the axis-0 transforms");
     default: c.stages = 3; break;
   }
   const unsigned long long b = static_cast<unsigned long long>(p->batch);

@@ -281,6 +281,8 @@ PYBIND11_MODULE(_sdct, m) {
   m.attr("DCT_2D_ROWCOL") = py::int_(static_cast<int>(SDCT_DCT_2D_ROWCOL));
   m.attr("IDCT_IDXST_2D_ROWCOL") = py::int_(static_cast<int>(SDCT_IDCT_IDXST_2D_ROWCOL));
   m.attr("IDXST_IDCT_2D_ROWCOL") = py::int_(static_cast<int>(SDCT_IDXST_IDCT_2D_ROWCOL));
+  m.attr("DCT_AXIS0") = py::int_(static_cast<int>(SDCT_DCT_AXIS0));
+  m.attr("IDCT_AXIS0") = py::int_(static_cast<int>(SDCT_IDCT_AXIS0));
   m.attr("DCT_1D") = py::int_(static_cast<int>(SDCT_DCT_1D));
   m.attr("IDCT_1D") = py::int_(static_cast<int>(SDCT_IDCT_1D));
   m.attr("IDXST_1D") = py::int_(static_cast<int>(SDCT_IDXST_1D));

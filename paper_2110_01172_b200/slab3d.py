@@ -13,14 +13,24 @@ and the slab pipeline is:
 
   1. local : batched 2D transform of this rank's planes (the fused fast path);
   2. all-to-all #1 (NCCL over NVLink): every rank sends rank t the columns
-     j in t's axis-1 slab, receives all n1 planes of its own axis-1 slab,
-     laid out [j][k][i] so axis 0 is contiguous;
-  3. local : batched 1D transform along that contiguous axis;
-  4. all-to-all #2: back to axis-0 slabs.
+     j in t's axis-1 slab. Received as [src][i_loc][j_loc][k], which IS the
+     (n1 x s2 n3) matrix with rows i = src s1 + i_loc in order — the axis-0
+     placement falls out of the exchange, no reorder copy;
+  3. local : the 1D transform along axis 0 of that matrix, taken in place by
+     one persistent column pass (``dct_axis0`` / ``idct_axis0``,
+     kernels_col1d.cuh: the axis-0 parity reorder rides on the tile load,
+     the postprocess on the store) instead of transpose, contiguous 1D
+     transform, transpose back;
+  4. all-to-all #2: its output is already blocked by destination rank
+     (rows t s1 .. t s1 + s1 - 1 are rank t's planes), so it is sent as is;
+     the receiver's [src][i_loc][j_loc][k] becomes [i_loc][j][k] with one
+     reorder copy.
 
-The exchanges are the only collectives (the transposes are the "standard
-communication operations" PAPER.md:649-660 mentions). The local transforms are
-injectable so the exchange logic runs under gloo on CPU in tests/.
+Two full-tensor reorder copies per transform (the send blocks of #1 and the
+final placement of #2) instead of the four of a transpose-based 1D leg. The
+exchanges are the only collectives (the transposes are the "standard
+communication operations" PAPER.md:649-660 mentions). The local transforms
+are injectable so the exchange logic runs under gloo on CPU in tests/.
 """
 from __future__ import annotations
 
@@ -38,7 +48,7 @@ def _all_to_all(send: torch.Tensor, group) -> torch.Tensor:
     return recv
 
 
-def _slab_pipeline(x_local: torch.Tensor, n1: int, two_d, one_d, group) -> torch.Tensor:
+def _slab_pipeline(x_local: torch.Tensor, n1: int, two_d, axis0, group) -> torch.Tensor:
     G = dist.get_world_size(group) if dist.is_initialized() else 1
     s1, n2, n3 = x_local.shape
     if s1 * G != n1 or n2 % G:
@@ -48,32 +58,33 @@ def _slab_pipeline(x_local: torch.Tensor, n1: int, two_d, one_d, group) -> torch
     a = two_d(x_local.contiguous())                                   # [s1][n2][n3]
     # 2. block t = columns j of rank t's axis-1 slab: [G][s1][s2][n3]
     send = a.reshape(s1, G, s2, n3).permute(1, 0, 2, 3).contiguous()
-    recv = _all_to_all(send, group)                                   # [G src][s1][s2][n3]: i = src*s1 + i_loc
-    b = recv.permute(2, 3, 0, 1).reshape(s2, n3, n1).contiguous()    # [j][k][i], axis 0 contiguous
-    # 3. 1D transform along axis 0 for every (j, k) of this slab
-    c = one_d(b)                                                      # [s2][n3][n1]
-    # 4. back to axis-0 slabs: block t = planes i of rank t: [G][s2][n3][s1]
-    send2 = c.reshape(s2, n3, G, s1).permute(2, 0, 1, 3).contiguous()
-    recv2 = _all_to_all(send2, group)                                 # [G src][s2][n3][s1]: j = src*s2 + j_loc
-    return recv2.permute(3, 0, 1, 2).reshape(s1, n2, n3).contiguous()
+    recv = _all_to_all(send, group)                                   # [G src][s1][s2][n3] = (n1 x s2 n3)
+    # 3. 1D transform along axis 0 of the (n1 x s2 n3) matrix, in place of
+    #    transpose + 1D + transpose
+    c = axis0(recv.view(n1, s2 * n3))
+    # 4. rows t*s1 .. t*s1+s1-1 are rank t's planes: already blocked by destination
+    recv2 = _all_to_all(c.view(G, s1, s2, n3).contiguous(), group)   # [G src][s1][s2][n3]: j = src*s2 + j_loc
+    return recv2.permute(1, 0, 2, 3).reshape(s1, n2, n3).contiguous()
 
 
-def dct_3d_slab(x_local: torch.Tensor, n1: int, group=None, two_d=None, one_d=None) -> torch.Tensor:
+def dct_3d_slab(x_local: torch.Tensor, n1: int, group=None, two_d=None, axis0=None) -> torch.Tensor:
     """This rank's axis-0 slab of dct_3d(x), given its slab of x (CUDA tensor,
-    fp32/fp64). n1 is the global axis-0 extent."""
-    if two_d is None or one_d is None:
+    fp32/fp64). n1 is the global axis-0 extent (a power of two in [8, 4096]
+    for the GPU axis-0 pass, with s2 n3 a multiple of 32 bytes' worth of
+    elements). ``two_d`` / ``axis0`` replace the local transforms (tests)."""
+    if two_d is None or axis0 is None:
         import paper_2110_01172_b200 as sd
 
         two_d = two_d or sd.dct_2d
-        one_d = one_d or sd.dct_1d
-    return _slab_pipeline(x_local, n1, two_d, one_d, group)
+        axis0 = axis0 or sd.dct_axis0
+    return _slab_pipeline(x_local, n1, two_d, axis0, group)
 
 
-def idct_3d_slab(x_local: torch.Tensor, n1: int, group=None, two_d=None, one_d=None) -> torch.Tensor:
+def idct_3d_slab(x_local: torch.Tensor, n1: int, group=None, two_d=None, axis0=None) -> torch.Tensor:
     """This rank's axis-0 slab of idct_3d(x) (idct_3d(dct_3d(x)) = n1 n2 n3 / 8 x)."""
-    if two_d is None or one_d is None:
+    if two_d is None or axis0 is None:
         import paper_2110_01172_b200 as sd
 
         two_d = two_d or sd.idct_2d
-        one_d = one_d or sd.idct_1d
-    return _slab_pipeline(x_local, n1, two_d, one_d, group)
+        axis0 = axis0 or sd.idct_axis0
+    return _slab_pipeline(x_local, n1, two_d, axis0, group)

@@ -80,8 +80,10 @@ def _slab_worker(rank, world, port, q):
     # local transforms on CPU from the C restatement (the GPU kernels need a
     # device); the exchange logic under test is the same code the GPUs run
     wrap = lambda f: (lambda t: torch.tensor(f(t.numpy())))  # noqa: E731
-    y = slab3d.dct_3d_slab(xl, n1, two_d=wrap(oracle.port.dct_2d), one_d=wrap(oracle.port.dct_direct_1d))
-    z = slab3d.idct_3d_slab(y, n1, two_d=wrap(oracle.port.idct_2d), one_d=wrap(oracle.port.idct_direct_1d))
+    # the axis-0 leg: the 1D transform of every column of an (n1 x m) matrix
+    ax0 = lambda f: (lambda t: torch.tensor(np.ascontiguousarray(f(np.ascontiguousarray(t.numpy().T)).T)))  # noqa: E731
+    y = slab3d.dct_3d_slab(xl, n1, two_d=wrap(oracle.port.dct_2d), axis0=ax0(oracle.port.dct_direct_1d))
+    z = slab3d.idct_3d_slab(y, n1, two_d=wrap(oracle.port.idct_2d), axis0=ax0(oracle.port.idct_direct_1d))
     ys = [torch.zeros_like(y) for _ in range(world)]
     zs = [torch.zeros_like(z) for _ in range(world)]
     dist.all_gather(ys, y)

@@ -868,3 +868,28 @@ def test_cluster_pair_column_pass_opt_in(cuda):
     r = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stderr[-2000:]
     assert float(r.stdout.strip().splitlines()[-1]) <= 1e-12
+
+
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+def test_axis0_transforms_vs_oracle(cuda, dtype):
+    # dct_1d / idct_1d of every column (the slab pipeline's axis-0 leg): the
+    # persistent column pass for power-of-two n1 in [8, 4096], the transpose
+    # route otherwise, against the C oracle (direct sums) and scipy at n1 = 4096
+    torch = _torch()
+    import paper_2110_01172_b200 as sd
+
+    tdt = torch.float64 if dtype == "float64" else torch.float32
+    for shape in [(8, 16), (16, 32), (256, 64), (1024, 24), (2, 64, 16), (4096, 8), (12, 10), (64, 6)]:
+        x = rnd(shape, 31, dtype)
+        xt = torch.tensor(x, dtype=tdt, device="cuda")
+        y = sd.dct_axis0(xt).double().cpu().numpy()
+        z = sd.idct_axis0(xt).double().cpu().numpy()
+        if shape[-2] >= 4096:
+            ry, rz = sf.dct(x, type=2, axis=-2) / 2, sf.dct(x, type=3, axis=-2) / 2
+        else:
+            xs = np.ascontiguousarray(np.swapaxes(x, -1, -2))
+            ry = np.swapaxes(oracle.port.dct_direct_1d(xs), -1, -2)
+            rz = np.swapaxes(oracle.port.idct_direct_1d(xs), -1, -2)
+        tol = 1e-12 if dtype == "float64" else 1e-5
+        assert oracle.rel_l2(y, ry) <= tol, (shape, oracle.rel_l2(y, ry))
+        assert oracle.rel_l2(z, rz) <= tol, (shape, oracle.rel_l2(z, rz))
