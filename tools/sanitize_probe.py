@@ -25,5 +25,9 @@ for dt in (torch.float64, torch.float32):
         for f in (sd.dct_2d, sd.idct_2d, sd.idct_idxst_2d, sd.idxst_idct_2d):
             f(xg)
     sd.dct_2d(torch.rand((8192, 16), dtype=dt, device="cuda"))
+    # axis-0 column pass (slab3d's axis-0 leg)
+    xa = torch.rand((2, 256, 64), dtype=dt, device="cuda")
+    sd.dct_axis0(xa)
+    sd.idct_axis0(xa)
 torch.cuda.synchronize()
 print("probe done")
