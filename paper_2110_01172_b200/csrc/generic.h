@@ -23,17 +23,32 @@ struct GenericJob {
   const double2* blue_chirp[3] = {nullptr, nullptr, nullptr};
   const double2* blue_hat[3] = {nullptr, nullptr, nullptr};
   const double2* blue_circle[3] = {nullptr, nullptr, nullptr};
+  // the plan's generic workspace carries the global Bluestein scratch
+  // (bluestein_scratch_elems); generic_run points blue_ws at it
+  bool blue_scratch = false;
+  double2* blue_ws = nullptr;
 };
 
 // Bluestein length for an axis of extent n (0 = mixed radix is used): the
-// pow2 M >= 2n - 1 when n's largest prime factor exceeds 64 and M <= 8192.
+// pow2 M >= 2n - 1 when n's largest prime factor exceeds 64 (n <= 2^23).
 int bluestein_len(int n);
+
+// The two-pass 2D pipeline (g2_kernel) holds lines of up to kG2MaxN points
+// (Bluestein convolution lengths included); other shapes run one pass per
+// stage, with long Bluestein axes as global M-point line FFTs.
+constexpr int kG2MaxN = 8192;
+bool generic_two_pass(int rank, const int* dims, const int* blue_m);
+
+// Lines per chunk of the global Bluestein pass (bounds its scratch) and the
+// scratch it needs, in double2 elements (0 when no axis uses it).
+long long bluestein_chunk_lines(int M, long long lines);
+long long bluestein_scratch_elems(int rank, const int* dims, const int* blue_m, long long batch);
 
 // Opt a kernel in to `smem` bytes of dynamic shared memory on the current
 // device (cached per device and kernel; plan.cu).
 cudaError_t prep_smem_ptr(const void* kernel, size_t smem);
 
-// Workspace: 2 * numel * batch * sizeof(double2) bytes.
+// Workspace: (2 * numel * batch + bluestein_scratch_elems) * sizeof(double2) bytes.
 template <typename T>
 cudaError_t generic_run(const GenericJob& job, const void* in, void* out, void* ws, cudaStream_t st);
 

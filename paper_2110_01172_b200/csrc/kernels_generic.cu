@@ -940,25 +940,189 @@ cudaError_t g2_launch(G2Args a, cudaStream_t st) {
   return n <= G2Cfg<8>::CAP ? g2_launch_cfg<T, KIND, 8>(a, st) : g2_launch_cfg<T, KIND, 16>(a, st);
 }
 
+// ---- Bluestein along one axis, one pass per stage ---------------------------
+// rfft.cpp:26,43-62 runs Bluestein for lengths its radix-2 FFT cannot take;
+// here it serves the axes whose largest prime factor exceeds 64 and that the
+// two-pass pipeline does not take (1D, 3D, long 2D axes):
+//   X(k) = c_k sum_j (x_j c_j) conj(c_{k-j}),  c_j = e^{-i pi j^2 / n},
+// a circular convolution of power-of-two length M >= 2n - 1 (bhat = FFT_M of
+// the wrapped conjugate chirp, plan tables). The inverse DFT is
+// conj(DFT(conj(x))). M = fa fb (fa = min(M, 4096)) runs as a four-step FFT
+// whose every pass reads and writes contiguous rows: with m = m1 + fa m2 and
+// k = k2 + fb k1,
+//   pre : u[k2][m1] = W_M^{m1 k2} sum_{m2} xc(m1 + fa m2) W_fb^{m2 k2}
+//         (xc = chirped, zero-padded input, read straight from the tensor)
+//   fa-point line FFTs over the rows k2 -> X(k2 + fb k1) at [k2][k1]
+//   x bhat in that order, inverse line FFTs, then
+//   post: v(m1 + fa m2) = sum_{k2} W_fb^{-m2 k2} W_M^{-m1 k2} z[k2][m1],
+//         out = op(c_m v(m) / M) written back into the tensor.
+// Lines l = o * inner + i of the [outer][n][inner] tensor run in chunks.
+__global__ void g_blue_pre(const double2* __restrict__ in, double2* __restrict__ u, long long l0, long long lines,
+                           int n, long long inner, int lgM, int lgfa, const double2* __restrict__ chirp,
+                           const double2* __restrict__ circ, int inverse) {
+  const int M = 1 << lgM, fa = 1 << lgfa, fb = M >> lgfa;
+  const long long total = lines << lgfa;  // one thread per (line, m1)
+  for (long long f = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; f < total;
+       f += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long ll = f >> lgfa;
+    const int m1 = static_cast<int>(f & (fa - 1));
+    const long long l = l0 + ll;
+    const long long o = inner == 1 ? l : l / inner, i = l - o * inner;
+    const double2* line = in + o * n * inner + i;
+    double2* dst = u + (ll << lgM) + m1;
+    for (int k2 = 0; k2 < fb; ++k2) {
+      double re = 0.0, im = 0.0;
+      for (int m2 = 0; m2 < fb; ++m2) {
+        const int m = m1 + fa * m2;
+        if (m >= n) break;
+        double2 v = line[static_cast<long long>(m) * inner];
+        if (inverse) v.y = -v.y;
+        v = cm(v, chirp[m]);
+        const double2 w = circ[((m2 * k2) & (fb - 1)) << lgfa];  // W_fb^{m2 k2}
+        re = fma(v.x, w.x, fma(-v.y, w.y, re));
+        im = fma(v.x, w.y, fma(v.y, w.x, im));
+      }
+      dst[static_cast<long long>(k2) << lgfa] = cm(make_double2(re, im), circ[(m1 * k2) & (M - 1)]);
+    }
+  }
+}
+
+// spectrum row k2, column k1 holds X(k2 + fb k1)
+__global__ void g_blue_mul(double2* __restrict__ u, long long total, int lgM, int lgfa,
+                           const double2* __restrict__ hat) {
+  const int M = 1 << lgM, fa = 1 << lgfa, fb = M >> lgfa;
+  for (long long f = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; f < total;
+       f += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int q = static_cast<int>(f & (M - 1));
+    u[f] = cm(u[f], hat[(q >> lgfa) + fb * (q & (fa - 1))]);
+  }
+}
+
+__global__ void g_blue_post(const double2* __restrict__ z, double2* __restrict__ out, long long l0, long long lines,
+                            int n, long long inner, int lgM, int lgfa, const double2* __restrict__ chirp,
+                            const double2* __restrict__ circ, int inverse) {
+  const int M = 1 << lgM, fa = 1 << lgfa, fb = M >> lgfa;
+  const double inv_m = 1.0 / static_cast<double>(M);
+  const long long total = lines << lgfa;
+  for (long long f = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; f < total;
+       f += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long ll = f >> lgfa;
+    const int m1 = static_cast<int>(f & (fa - 1));
+    const long long l = l0 + ll;
+    const long long o = inner == 1 ? l : l / inner, i = l - o * inner;
+    double2* line = out + o * n * inner + i;
+    const double2* src = z + (ll << lgM) + m1;
+    for (int m2 = 0; m2 < fb; ++m2) {
+      const int m = m1 + fa * m2;
+      if (m >= n) break;
+      double re = 0.0, im = 0.0;
+      for (int k2 = 0; k2 < fb; ++k2) {
+        double2 w = cm(circ[((m2 * k2) & (fb - 1)) << lgfa], circ[(m1 * k2) & (M - 1)]);  // conj below
+        w.y = -w.y;
+        const double2 v = src[static_cast<long long>(k2) << lgfa];
+        re = fma(v.x, w.x, fma(-v.y, w.y, re));
+        im = fma(v.x, w.y, fma(v.y, w.x, im));
+      }
+      double2 r = cm(make_double2(re, im), chirp[m]);
+      r.x *= inv_m;
+      r.y *= inverse ? -inv_m : inv_m;
+      line[static_cast<long long>(m) * inner] = r;
+    }
+  }
+}
+
 }  // namespace
 
-int bluestein_len(int n) {
+static int largest_prime(int n) {
   int m = n, p = 1;
   for (int d = 2; d * d <= m; ++d)
     while (m % d == 0) {
       p = std::max(p, d);
       m /= d;
     }
-  if (m > 1) p = std::max(p, m);
-  if (p <= 64) return 0;
+  return m > 1 ? std::max(p, m) : p;
+}
+
+int bluestein_len(int n) {
+  if (n < 2 || n > (1 << 23)) return 0;  // M / 4096 must fit one split cofactor
+  if (largest_prime(n) <= 64) return 0;
   int M = 1;
   while (M < 2 * n - 1) M <<= 1;
-  return M <= 8192 ? M : 0;
+  return M;
+}
+
+// Two-pass pipeline: both extents <= kG2MaxN, and an axis whose Bluestein
+// length exceeds the line capacity (4096 < n <= 8192) stays on the mixed
+// radix inside it only while its largest prime factor is moderate (a prime
+// radix p costs p MACs per element: 4097 = 17 x 241 runs there as fast as the
+// global Bluestein pass; 8191 took 20 ms that way and 0.23 ms through it)
+bool generic_two_pass(int rank, const int* dims, const int* blue_m) {
+  if (rank != 2) return false;
+  for (int a = 0; a < 2; ++a) {
+    if (dims[a] > kG2MaxN) return false;
+    if (blue_m[a] > kG2MaxN && largest_prime(dims[a]) > 256) return false;
+  }
+  return true;
+}
+
+long long bluestein_chunk_lines(int M, long long lines) {
+  const long long cap = std::max<long long>(1, (8LL << 20) / M);  // <= 8 Mi complex per buffer
+  return std::min(lines, cap);
+}
+
+long long bluestein_scratch_elems(int rank, const int* dims, const int* blue_m, long long batch) {
+  if (generic_two_pass(rank, dims, blue_m)) return 0;
+  long long numel = 1, best = 0;
+  for (int a = 0; a < rank; ++a) numel *= dims[a];
+  for (int a = 0; a < rank; ++a)
+    if (blue_m[a]) best = std::max(best, 2 * bluestein_chunk_lines(blue_m[a], batch * (numel / dims[a])) * blue_m[a]);
+  return best;
 }
 
 // Complex DFT along axes [a0, a1) of the [batch][dims...] complex tensor in
 // cur (result in cur; nxt is scratch of the same size). g = grid for the
 // elementwise kernels over the whole tensor.
+// shared-memory line FFT of length len over lines (outer', inner'); tab is a
+// circle table e^{-2 pi i t / (len ts)} read with stride ts
+static void line_fft_run(const double2* src, double2* dst, long long outer_, int len, long long inner_,
+                         const double2* tab, int ts, int inverse, cudaStream_t st) {
+  // threads per CTA: the fewest (>= 128) that hold a whole line at
+  // kFftPerThread outputs each (small CTAs: the passes are latency bound)
+  const int nt = len <= 1024 ? 128 : len <= 2048 ? 256 : 512;
+  int lpc = 1;
+  while (lpc < 16 && 2 * lpc * len <= kFftPerThread * nt &&
+         (inner_ == 1 ? lpc * 2 <= outer_ : inner_ % (lpc * 2) == 0))
+    lpc *= 2;
+  const size_t smem = (static_cast<size_t>(lpc) * len + len) * sizeof(double2);
+  if (smem > 48 * 1024) prep_smem_ptr(reinterpret_cast<const void*>(g_fft_axis_smem), 140 * 1024);
+  const long long tiles = inner_ > 1 ? outer_ * (inner_ / lpc) : (outer_ + lpc - 1) / lpc;
+  g_fft_axis_smem<<<static_cast<unsigned>(tiles), nt, smem, st>>>(src, dst, outer_, len, inner_, tab, ts, inverse,
+                                                                      factorise(len), lpc);
+}
+
+// axis a of cur ([outer][n][inner]) -> nxt through the global Bluestein pass
+static void blue_axis(const GenericJob& job, int a, const double2* cur, double2* nxt, long long outer,
+                      long long inner, int inverse, cudaStream_t st) {
+  const int n = job.dims[a], M = job.blue_m[a];
+  int lgM = 0;
+  while ((1 << lgM) < M) ++lgM;
+  const int lgfa = lgM < 12 ? lgM : 12, fa = 1 << lgfa, fb = M >> lgfa;
+  const long long L = outer * inner, chunk = bluestein_chunk_lines(M, L);
+  double2* U = job.blue_ws;
+  double2* V = U + chunk * M;
+  const double2* circ = job.blue_circle[a];
+  for (long long l0 = 0; l0 < L; l0 += chunk) {
+    const long long cnt = std::min(chunk, L - l0);
+    g_blue_pre<<<nblocks(cnt * fa), kThreads, 0, st>>>(cur, U, l0, cnt, n, inner, lgM, lgfa, job.blue_chirp[a], circ,
+                                                       inverse);
+    line_fft_run(U, V, cnt * fb, fa, 1, circ, fb, 0, st);
+    g_blue_mul<<<nblocks(cnt * M), kThreads, 0, st>>>(V, cnt * M, lgM, lgfa, job.blue_hat[a]);
+    line_fft_run(V, U, cnt * fb, fa, 1, circ, fb, 1, st);
+    g_blue_post<<<nblocks(cnt * fa), kThreads, 0, st>>>(U, nxt, l0, cnt, n, inner, lgM, lgfa, job.blue_chirp[a], circ,
+                                                        inverse);
+  }
+}
+
 static void dft_axes(const GenericJob& job, int a0, int a1, double2*& cur, double2*& nxt, int inverse, int g,
               cudaStream_t st) {
     for (int a = a0; a < a1; ++a) {
@@ -966,21 +1130,19 @@ static void dft_axes(const GenericJob& job, int a0, int a1, double2*& cur, doubl
       for (int t = a + 1; t < job.rank; ++t) inner *= job.dims[t];
       for (int t = 0; t < a; ++t) outer *= job.dims[t];
       const int n = job.dims[a];
-      // shared-memory line FFT of length len over lines (outer', inner'), table stride ts
+      if (job.blue_m[a] && job.blue_ws) {
+        if (inner > 1) {  // strided axis: rows first, so every Bluestein pass is coalesced
+          g_transpose(cur, nxt, outer, n, inner, st);  // [o][n][inner] -> [o][inner][n]
+          blue_axis(job, a, nxt, cur, outer * inner, 1, inverse, st);
+          g_transpose(cur, nxt, outer, inner, n, st);  // back
+        } else {
+          blue_axis(job, a, cur, nxt, outer, 1, inverse, st);
+        }
+        std::swap(cur, nxt);
+        continue;
+      }
       auto line_fft = [&](const double2* src, double2* dst, long long outer_, int len, long long inner_, int ts) {
-        // threads per CTA: the fewest (>= 128) that hold a whole line at
-        // kFftPerThread outputs each (small CTAs: the passes are latency bound)
-        const int nt = len <= 1024 ? 128 : len <= 2048 ? 256 : 512;
-        int lpc = 1;
-        while (lpc < 16 && 2 * lpc * len <= kFftPerThread * nt &&
-               (inner_ == 1 ? lpc * 2 <= outer_ : inner_ % (lpc * 2) == 0))
-          lpc *= 2;
-        const size_t smem = (static_cast<size_t>(lpc) * len + len) * sizeof(double2);
-        if (smem > 48 * 1024) prep_smem_ptr(reinterpret_cast<const void*>(g_fft_axis_smem), 140 * 1024);
-        const long long tiles = inner_ > 1 ? outer_ * (inner_ / lpc) : (outer_ + lpc - 1) / lpc;
-        g_fft_axis_smem<<<static_cast<unsigned>(tiles), nt, smem, st>>>(src, dst, outer_, len, inner_,
-                                                                            job.circle[a], ts, inverse,
-                                                                            factorise(len), lpc);
+        line_fft_run(src, dst, outer_, len, inner_, job.circle[a], ts, inverse, st);
       };
       int fa = 0, fb = 0;
       if (n > kFftMaxN) split_factors(n, fa, fb);
@@ -1030,12 +1192,15 @@ cudaError_t generic_run(const GenericJob& job, const void* in, void* out, void* 
   double2* A = static_cast<double2*>(ws);
   double2* B = A + total;
   const int g = nblocks(total);
+  GenericJob jb = job;  // global Bluestein scratch after the two tensor buffers
+  jb.blue_ws = job.blue_scratch ? B + total : nullptr;
   auto dft_all = [&](double2*& cur, double2*& nxt, int inverse) {
-    dft_axes(job, 0, job.rank, cur, nxt, inverse, g, st);
+    dft_axes(jb, 0, job.rank, cur, nxt, inverse, g, st);
   };
   double2* cur = A;
   double2* nxt = B;
-  if (job.rank == 2 && !job.legacy && job.dims[0] <= G2Cfg<16>::CAP && job.dims[1] <= G2Cfg<16>::CAP) {
+  static_assert(G2Cfg<16>::CAP == kG2MaxN, "two-pass line capacity");
+  if (!job.legacy && generic_two_pass(job.rank, job.dims, job.blue_m)) {
     // two-pass pipeline (gathers / pre / post fused into the line FFTs)
     G2Args a{};
     a.n1 = job.dims[0];
@@ -1049,7 +1214,7 @@ cudaError_t generic_run(const GenericJob& job, const void* in, void* out, void* 
     cudaError_t e;
     auto axis = [&](int ax) {  // FFT-axis tables (mixed radix or Bluestein)
       a.circle = job.circle[ax];
-      a.bm = job.blue_m[ax];
+      a.bm = job.blue_m[ax] <= kG2MaxN ? job.blue_m[ax] : 0;  // longer: mixed radix (generic_two_pass)
       a.bchirp = job.blue_chirp[ax];
       a.bhat = job.blue_hat[ax];
       a.bcircle = job.blue_circle[ax];

@@ -174,8 +174,10 @@ struct sdct_plan_s {
   void* rc_w[2] = {nullptr, nullptr};
   void* rws = nullptr;  // rfft_nd / irfft_nd scratch (generic size), lazily allocated
   size_t elem() const { return dtype == SDCT_F32 ? 4 : 8; }
+  long long blue_elems = 0;  // global Bluestein scratch (bluestein_scratch_elems)
   size_t generic_ws_bytes() const {
-    return 2 * static_cast<size_t>(batch) * static_cast<size_t>(numel) * sizeof(double2);
+    return (2 * static_cast<size_t>(batch) * static_cast<size_t>(numel) + static_cast<size_t>(blue_elems)) *
+           sizeof(double2);
   }
   size_t item_bytes() const { return static_cast<size_t>(numel) * elem(); }
   // coefficient scratch of force fields / compression: two tensor-sized
@@ -401,6 +403,10 @@ int build_plan(sdct_plan_s* p) {
     if (r == 3) p->nl[1] = pick_nl(static_cast<int>(p->elem()), p->n[1], p->M, static_cast<long long>(p->n[0]) * p->batch);
     p->ws_bytes = static_cast<size_t>(p->batch) * p->item_bytes();
   } else {
+    // Bluestein lengths of axes with a large prime factor (two-pass 2D
+    // pipeline when it holds them, else the global pass), their scratch
+    for (int a = 0; a < r; ++a) p->bm[a] = bluestein_len(p->n[a]);
+    p->blue_elems = bluestein_scratch_elems(r, p->n, p->bm, p->batch);
     // generic scratch, plus (rank 2) one real tensor for the row-column passes
     p->ws_bytes = p->generic_ws_bytes() + (r == 2 ? static_cast<size_t>(p->batch) * p->item_bytes() : 0);
   }
@@ -440,8 +446,7 @@ int build_plan(sdct_plan_s* p) {
     fill_table<double>(blob, off_gq[a], re, im);
     circle(re, im, p->n[a], 1.0L, p->n[a]);
     fill_table<double>(blob, off_gc[a], re, im);
-    // Bluestein (2D generic pipeline, axes with a large prime factor)
-    p->bm[a] = (!fast && r == 2) ? bluestein_len(p->n[a]) : 0;
+    // Bluestein tables (generic plans, axes with a large prime factor)
     if (p->bm[a]) {
       const int n = p->n[a], M = p->bm[a];
       const long double pi = 3.141592653589793238462643383279502884L;
@@ -882,6 +887,7 @@ GenericJob make_job(const sdct_plan_s* p, int kind) {
     j.blue_hat[a] = p->bhat[a];
     j.blue_circle[a] = p->bcircle[a];
   }
+  j.blue_scratch = p->blue_elems > 0;
   j.batch = p->batch;
   switch (kind) {
     case SDCT_IDCT_2D: j.inverse = true; j.scale = 0.25; break;

@@ -170,6 +170,36 @@ def test_generic_2d_round_trip_large(cuda, dtype):
     assert err <= (1e-13 if dtype == "float64" else 1e-5), err
 
 
+# axes with a large prime factor that the two-pass 2D pipeline cannot hold
+# (Bluestein length > 8192), and 1D / 3D extents: the one-pass-per-stage path
+# runs them as global Bluestein convolutions (rfft.cpp:26,43-62), chunked
+SHAPES_BLUE = [(4097, 24), (24, 4097), (8191, 10), (8209, 6), (6, 8209), (67, 5, 8), (3, 131, 4), (2, 3, 4099)]
+
+
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+def test_generic_global_bluestein_vs_oracle(cuda, dtype):
+    for i, shape in enumerate(SHAPES_BLUE):
+        kinds = KINDS_2D if len(shape) == 2 else ["dct_3d", "idct_3d"]
+        x = rnd(shape, 900 + i, dtype)
+        for kind in kinds:
+            got = run_capi(kind, x, dtype, poison=True)
+            err = oracle.rel_l2(got, getattr(oracle.port, kind)(x))
+            assert err <= TOL[dtype], (kind, shape, dtype, err)
+    for j, n in enumerate((4099, 8191, 10007)):
+        x = rnd((n,), 950 + j, dtype)
+        # scipy's unnormalised DCT-II / DCT-III / DST-III in the reference's
+        # scaling (proj/src/dct1d.cpp; dct_1d = DCT-II / 2, idxst_1d drops x_0)
+        want = {"dct_1d": sf.dct(x, type=2) / 2.0, "idct_1d": sf.dct(x, type=3) / 2.0,
+                "idxst_1d": sf.dst(np.concatenate([x[1:], [0.0]]), type=3) / 2.0}
+        for kind, ref in want.items():
+            err = oracle.rel_l2(run_capi(kind, x, dtype, poison=True), ref)
+            assert err <= TOL[dtype], (kind, n, dtype, err)
+    x = rnd((3, 4097, 6), 960, dtype)
+    got = run_capi("idct_2d", x, dtype, batch_shape=(3,), poison=True)
+    want = np.stack([oracle.port.idct_2d(x[b]) for b in range(3)])
+    assert oracle.rel_l2(got, want) <= TOL[dtype]
+
+
 # every output element written, no workspace read before it is written: the
 # column passes store through TMA (cp.async.bulk.tensor global<-shared), which
 # compute-sanitizer's initcheck cannot see, so coverage is proven by poisoning
