@@ -32,13 +32,16 @@ def plan_for(dims, batch: int = 1, dtype: str = "float64", device: int = 0):
     key = (tuple(int(d) for d in dims), int(batch), dtype, int(device))
     with _lock:
         p = _plans.get(key)
-        if p is None:
-            import torch
+        if p is not None:  # hit: no per-call walk over the cache
+            _plans.move_to_end(key)
+            return p
+        import torch
 
-            with torch.cuda.device(device):
-                p = _sdct.Plan(list(key[0]), key[1], dtype)
-            _plans[key] = p
-        _plans.move_to_end(key)
+        with torch.cuda.device(device):
+            p = _sdct.Plan(list(key[0]), key[1], dtype)
+        _plans[key] = p
+        # bounds checked on insertion (plans grow lazily after their first use,
+        # so the byte total is re-read from every cached plan here)
         total = sum(q.device_bytes for q in _plans.values())
         while len(_plans) > 1 and (len(_plans) > PLAN_CACHE_MAX or total > PLAN_CACHE_BYTES):
             _, old = _plans.popitem(last=False)

@@ -30,8 +30,10 @@ struct GenericJob {
 };
 
 // Bluestein length for an axis of extent n (0 = mixed radix is used): the
-// pow2 M >= 2n - 1 when n's largest prime factor exceeds 64 (n <= 2^23).
-int bluestein_len(int n);
+// pow2 M >= 2n - 1 when n's largest prime factor exceeds 64 (n <= 2^23), or,
+// for an axis of a two-pass tile (tile = true, M <= kG2MaxN), when its prime
+// factors above 7 sum to more than 20 M / n.
+int bluestein_len(int n, bool tile);
 
 // The two-pass 2D pipeline (g2_kernel) holds lines of up to kG2MaxN points
 // (Bluestein convolution lengths included); other shapes run one pass per

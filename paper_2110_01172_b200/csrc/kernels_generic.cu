@@ -1043,12 +1043,25 @@ static int largest_prime(int n) {
   return m > 1 ? std::max(p, m) : p;
 }
 
-int bluestein_len(int n) {
+int bluestein_len(int n, bool tile) {
   if (n < 2 || n > (1 << 23)) return 0;  // M / 4096 must fit one split cofactor
-  if (largest_prime(n) <= 64) return 0;
   int M = 1;
   while (M < 2 * n - 1) M <<= 1;
-  return M;
+  if (largest_prime(n) > 64) return M;
+  if (!tile || M > kG2MaxN) return 0;
+  // inside a two-pass tile, Bluestein also beats the mixed radix when the
+  // thread-per-output prime passes (factors > 7, p MACs per element each) cost
+  // more than ~20 x the convolution's growth M / n (measured on 989..2023:
+  // 1023 = 3.11.31 151 -> 121 us, 1849 = 43^2 540 -> 416 us; 2023 = 7.17^2 and
+  // 1147 = 31.37 stay mixed radix, 340 / 168 us vs 428 / 209 us)
+  int m = n, big = 0;
+  for (int d = 2; d * d <= m; ++d)
+    while (m % d == 0) {
+      if (d > 7) big += d;
+      m /= d;
+    }
+  if (m > 7) big += m;
+  return static_cast<double>(big) > 20.0 * M / n ? M : 0;
 }
 
 // Two-pass pipeline: both extents <= kG2MaxN, and an axis whose Bluestein

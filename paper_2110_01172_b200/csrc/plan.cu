@@ -405,7 +405,8 @@ int build_plan(sdct_plan_s* p) {
   } else {
     // Bluestein lengths of axes with a large prime factor (two-pass 2D
     // pipeline when it holds them, else the global pass), their scratch
-    for (int a = 0; a < r; ++a) p->bm[a] = bluestein_len(p->n[a]);
+    const bool tile = r == 2 && p->n[0] <= kG2MaxN && p->n[1] <= kG2MaxN;  // two-pass candidate
+    for (int a = 0; a < r; ++a) p->bm[a] = bluestein_len(p->n[a], tile);
     p->blue_elems = bluestein_scratch_elems(r, p->n, p->bm, p->batch);
     // generic scratch, plus (rank 2) one real tensor for the row-column passes
     p->ws_bytes = p->generic_ws_bytes() + (r == 2 ? static_cast<size_t>(p->batch) * p->item_bytes() : 0);
