@@ -165,6 +165,9 @@ struct sdct_plan_s {
   std::mutex mu;
 
   void* aux = nullptr;  // sdct_force_fields scratch (coefficients + weighted copy), lazily allocated
+  // force fields: side stream for the second composite and its fork / join events
+  cudaStream_t side_st = nullptr;
+  cudaEvent_t side_fork = nullptr, side_join = nullptr;
   std::mutex gws_mu;    // guards the lazy workspace allocation (ensure_ws)
   // row-column kernels (rank 2): per axis a with a pow2 extent in [8, 8192],
   // stage tables of the n_a/2-point row FFT, quarter-wave and W_{n_a} tables
@@ -1240,6 +1243,9 @@ int sdct_plan_destroy(sdct_plan_t p) {
     if (p->lane_ev[l]) cudaEventDestroy(p->lane_ev[l]);
   }
   if (p->fork_ev) cudaEventDestroy(p->fork_ev);
+  if (p->side_st) cudaStreamDestroy(p->side_st);
+  if (p->side_fork) cudaEventDestroy(p->side_fork);
+  if (p->side_join) cudaEventDestroy(p->side_join);
   delete p;
   return SDCT_OK;
 }
@@ -1337,15 +1343,31 @@ int sdct_force_fields(sdct_plan_t p, const void* d_density, void* d_xi1, void* d
       cudaError_t e = cudaMalloc(&p->aux, 2 * p->aux_half());
       if (e != cudaSuccess) return cuda_fail(e, "allocating force-field scratch");
     }
+    if (p->fast && !p->side_st) {
+      cudaError_t e = cudaStreamCreateWithFlags(&p->side_st, cudaStreamNonBlocking);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->side_fork, cudaEventDisableTiming);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->side_join, cudaEventDisableTiming);
+      if (e != cudaSuccess) return cuda_fail(e, "creating force-field side stream");
+    }
   }
   void* a = p->aux;                                     // DCT coefficients of the density
   void* aw = static_cast<unsigned char*>(p->aux) + p->aux_half();  // generic path: weighted copy
   int rc = dispatch(p, SDCT_DCT_2D, -1, d_density, a, d_ws, st, nullptr);
   if (rc != SDCT_OK) return rc;
   if (p->fast) {
-    // fast path: the weighting rides on the inverse row kernels' loads
+    // fast path: the weighting rides on the inverse row kernels' loads. The
+    // two composites only share the coefficients, so the second runs on the
+    // plan's side stream (its intermediate in the aux half the generic path
+    // uses for the weighted copy) and fills the first one's partial waves
+    // (fork / join keep the call stream-ordered and graph-capturable)
+    cudaError_t e = cudaEventRecord(p->side_fork, st);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(p->side_st, p->side_fork, 0);
+    if (e != cudaSuccess) return cuda_fail(e, "forking the force-field side stream");
     rc = dispatch(p, SDCT_IDCT_IDXST_2D, -1, a, d_xi1, d_ws, st, nullptr, 1);
-    if (rc == SDCT_OK) rc = dispatch(p, SDCT_IDXST_IDCT_2D, -1, a, d_xi2, d_ws, st, nullptr, 2);
+    if (rc == SDCT_OK) rc = dispatch(p, SDCT_IDXST_IDCT_2D, -1, a, d_xi2, aw, p->side_st, nullptr, 2);
+    e = cudaEventRecord(p->side_join, p->side_st);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(st, p->side_join, 0);
+    if (e != cudaSuccess) return cuda_fail(e, "joining the force-field side stream");
     return rc;
   }
   for (int which = 1; which <= 2; ++which) {
