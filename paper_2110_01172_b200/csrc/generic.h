@@ -23,6 +23,7 @@ struct GenericJob {
   const double2* blue_chirp[3] = {nullptr, nullptr, nullptr};
   const double2* blue_hat[3] = {nullptr, nullptr, nullptr};
   const double2* blue_circle[3] = {nullptr, nullptr, nullptr};
+  const double2* blue_fa[3] = {nullptr, nullptr, nullptr};  // circle of min(M, 4096) (global pass line FFTs)
   // the plan's generic workspace carries the global Bluestein scratch
   // (bluestein_scratch_elems); generic_run points blue_ws at it
   bool blue_scratch = false;

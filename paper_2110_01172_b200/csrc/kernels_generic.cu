@@ -317,20 +317,27 @@ __device__ __forceinline__ void line_passes(double2* x, const double2* tw, int n
   }
 }
 
-__global__ void __launch_bounds__(512) g_fft_axis_smem(const double2* __restrict__ in, double2* __restrict__ out,
-                                                       long long outer, int n, long long inner,
-                                                       const double2* __restrict__ tab, int tab_stride, int inverse,
-                                                       Radices rad, int lpc) {
-  // shared memory: twiddle table (n) + the lines (lpc * n); each pass computes
-  // its outputs into registers, synchronises, and writes them back in place
+// GTW (long lines, 2048..4096 points): 16 outputs per thread and the twiddles
+// read from the global circle table through L1 (tab_stride 1), so the line
+// alone fills shared memory and two CTAs share an SM (one 512-thread CTA with
+// a 128 KB table + line per SM left the load latency exposed: ~1 TB/s)
+template <int FPT, bool GTW>
+__global__ void __launch_bounds__(GTW ? 256 : 512, GTW ? 2 : 1)
+    g_fft_axis_smem(const double2* __restrict__ in, double2* __restrict__ out, long long outer, int n,
+                    long long inner, const double2* __restrict__ tab, int tab_stride, int inverse, Radices rad,
+                    int lpc) {
+  // shared memory: twiddle table (n, !GTW) + the lines (lpc * n); each pass
+  // computes its outputs into registers, synchronises, and writes them back in place
   extern __shared__ __align__(16) double2 fsm[];
-  double2* tw = fsm;
-  double2* x = fsm + n;
+  const double2* tw = GTW ? tab : fsm;
+  double2* x = GTW ? fsm : fsm + n;
   const int t = threadIdx.x, nt = blockDim.x;
-  for (int e = t; e < n; e += nt) {
-    double2 w = tab[static_cast<long long>(e) * tab_stride];  // e^{-2 pi i e / n} from a longer circle table
-    if (inverse) w.y = -w.y;
-    tw[e] = w;
+  if constexpr (!GTW) {
+    for (int e = t; e < n; e += nt) {
+      double2 w = tab[static_cast<long long>(e) * tab_stride];  // e^{-2 pi i e / n} from a longer circle table
+      if (inverse) w.y = -w.y;
+      fsm[e] = w;
+    }
   }
   // tile of lines: (o, i0..i0+lpc) for inner > 1, rows o0..o0+lpc for inner == 1
   const long long tiles_per_o = inner > 1 ? inner / lpc : 1;
@@ -361,9 +368,9 @@ __global__ void __launch_bounds__(512) g_fft_axis_smem(const double2* __restrict
   }
   __syncthreads();
   if (inverse)
-    line_passes<kFftPerThread, true>(x, tw, n, rad, total, t, nt, n);
+    line_passes<FPT, true, GTW>(x, tw, n, rad, total, t, nt, n);
   else
-    line_passes<kFftPerThread, false>(x, tw, n, rad, total, t, nt, n);
+    line_passes<FPT, false, GTW>(x, tw, n, rad, total, t, nt, n);
   for (int e = t; e < total; e += nt) {
     long long dst;
     int l, m;
@@ -1099,6 +1106,15 @@ long long bluestein_scratch_elems(int rank, const int* dims, const int* blue_m, 
 // circle table e^{-2 pi i t / (len ts)} read with stride ts
 static void line_fft_run(const double2* src, double2* dst, long long outer_, int len, long long inner_,
                          const double2* tab, int ts, int inverse, cudaStream_t st) {
+  if (ts == 1 && len >= 2048 && len <= kFftMaxN) {  // long lines: GTW variant, one line per CTA
+    const size_t smem = static_cast<size_t>(len) * sizeof(double2);
+    prep_smem_ptr(reinterpret_cast<const void*>(g_fft_axis_smem<16, true>), 64 * 1024);
+    const long long tiles = inner_ > 1 ? outer_ * inner_ : outer_;
+    const int nt = ((len + 15) / 16 + 31) & ~31;  // 16 outputs per thread, whole warps
+    g_fft_axis_smem<16, true><<<static_cast<unsigned>(tiles), nt, smem, st>>>(src, dst, outer_, len, inner_, tab, 1,
+                                                                              inverse, factorise(len), 1);
+    return;
+  }
   // threads per CTA: the fewest (>= 128) that hold a whole line at
   // kFftPerThread outputs each (small CTAs: the passes are latency bound)
   const int nt = len <= 1024 ? 128 : len <= 2048 ? 256 : 512;
@@ -1107,10 +1123,10 @@ static void line_fft_run(const double2* src, double2* dst, long long outer_, int
          (inner_ == 1 ? lpc * 2 <= outer_ : inner_ % (lpc * 2) == 0))
     lpc *= 2;
   const size_t smem = (static_cast<size_t>(lpc) * len + len) * sizeof(double2);
-  if (smem > 48 * 1024) prep_smem_ptr(reinterpret_cast<const void*>(g_fft_axis_smem), 140 * 1024);
+  if (smem > 48 * 1024) prep_smem_ptr(reinterpret_cast<const void*>(g_fft_axis_smem<kFftPerThread, false>), 140 * 1024);
   const long long tiles = inner_ > 1 ? outer_ * (inner_ / lpc) : (outer_ + lpc - 1) / lpc;
-  g_fft_axis_smem<<<static_cast<unsigned>(tiles), nt, smem, st>>>(src, dst, outer_, len, inner_, tab, ts, inverse,
-                                                                      factorise(len), lpc);
+  g_fft_axis_smem<kFftPerThread, false><<<static_cast<unsigned>(tiles), nt, smem, st>>>(
+      src, dst, outer_, len, inner_, tab, ts, inverse, factorise(len), lpc);
 }
 
 // axis a of cur ([outer][n][inner]) -> nxt through the global Bluestein pass
@@ -1128,9 +1144,9 @@ static void blue_axis(const GenericJob& job, int a, const double2* cur, double2*
     const long long cnt = std::min(chunk, L - l0);
     g_blue_pre<<<nblocks(cnt * fa), kThreads, 0, st>>>(cur, U, l0, cnt, n, inner, lgM, lgfa, job.blue_chirp[a], circ,
                                                        inverse);
-    line_fft_run(U, V, cnt * fb, fa, 1, circ, fb, 0, st);
+    line_fft_run(U, V, cnt * fb, fa, 1, job.blue_fa[a], 1, 0, st);
     g_blue_mul<<<nblocks(cnt * M), kThreads, 0, st>>>(V, cnt * M, lgM, lgfa, job.blue_hat[a]);
-    line_fft_run(V, U, cnt * fb, fa, 1, circ, fb, 1, st);
+    line_fft_run(V, U, cnt * fb, fa, 1, job.blue_fa[a], 1, 1, st);
     g_blue_post<<<nblocks(cnt * fa), kThreads, 0, st>>>(U, nxt, l0, cnt, n, inner, lgM, lgfa, job.blue_chirp[a], circ,
                                                         inverse);
   }

@@ -149,6 +149,7 @@ struct sdct_plan_s {
   double2* bchirp[3] = {nullptr, nullptr, nullptr};
   double2* bhat[3] = {nullptr, nullptr, nullptr};
   double2* bcircle[3] = {nullptr, nullptr, nullptr};
+  double2* bfa[3] = {nullptr, nullptr, nullptr};  // e^{-2 pi i t / 4096} when M > 4096, else bcircle
   size_t b_offset_fast = 0, b_offset_gen = 0;    // element offsets of table b (corrupt hook)
   // workspace + host staging
   void* ws = nullptr;
@@ -444,7 +445,7 @@ int build_plan(sdct_plan_s* p) {
     }
   }
   // generic-path tables are always present (odd shapes, row-column, 1D)
-  size_t off_bc[3] = {0, 0, 0}, off_bh[3] = {0, 0, 0}, off_bm[3] = {0, 0, 0};
+  size_t off_bc[3] = {0, 0, 0}, off_bh[3] = {0, 0, 0}, off_bm[3] = {0, 0, 0}, off_bf[3] = {0, 0, 0};
   for (int a = 0; a < r; ++a) {
     circle(re, im, p->n[a], 1.0L, 4.0L * p->n[a]);
     fill_table<double>(blob, off_gq[a], re, im);
@@ -472,6 +473,10 @@ int build_plan(sdct_plan_s* p) {
       fill_table<double>(blob, off_bh[a], hr, hi);
       circle(re, im, M, 1.0L, M);
       fill_table<double>(blob, off_bm[a], re, im);
+      if (M > 4096) {
+        circle(re, im, 4096, 1.0L, 4096);
+        fill_table<double>(blob, off_bf[a], re, im);
+      }
     }
   }
   cudaError_t e = cudaMalloc(&p->tables, blob.size());
@@ -506,6 +511,7 @@ int build_plan(sdct_plan_s* p) {
       p->bchirp[a] = reinterpret_cast<double2*>(base + off_bc[a]);
       p->bhat[a] = reinterpret_cast<double2*>(base + off_bh[a]);
       p->bcircle[a] = reinterpret_cast<double2*>(base + off_bm[a]);
+      p->bfa[a] = p->bm[a] > 4096 ? reinterpret_cast<double2*>(base + off_bf[a]) : p->bcircle[a];
     }
   }
   for (int a = 0; a < 2; ++a) {
@@ -890,6 +896,7 @@ GenericJob make_job(const sdct_plan_s* p, int kind) {
     j.blue_chirp[a] = p->bchirp[a];
     j.blue_hat[a] = p->bhat[a];
     j.blue_circle[a] = p->bcircle[a];
+    j.blue_fa[a] = p->bfa[a];
   }
   j.blue_scratch = p->blue_elems > 0;
   j.batch = p->batch;
