@@ -24,6 +24,7 @@
 
 #include "../../include/sdct_b200.h"
 #include "fast_launch.cuh"
+#include "host_stage.hpp"
 #include "generic.h"
 #include "kernels_rowcol.cuh"
 
@@ -165,6 +166,10 @@ struct sdct_plan_s {
   void* lane_buf[kLanes][3] = {};
   std::mutex mu;
 
+  // sdct_exec_host: pinned staging chunks for pageable host buffers (host_stage.hpp)
+  static constexpr size_t kStageChunk = 32u << 20;
+  void* h_stage[2] = {nullptr, nullptr};
+  cudaEvent_t stage_ev[2] = {nullptr, nullptr};
   void* aux = nullptr;  // sdct_force_fields scratch (coefficients + weighted copy), lazily allocated
   // force fields: side stream for the second composite and its fork / join events
   cudaStream_t side_st = nullptr;
@@ -1250,6 +1255,10 @@ int sdct_plan_destroy(sdct_plan_t p) {
     if (p->lane_ev[l]) cudaEventDestroy(p->lane_ev[l]);
   }
   if (p->fork_ev) cudaEventDestroy(p->fork_ev);
+  for (int b = 0; b < 2; ++b) {
+    if (p->h_stage[b]) cudaFreeHost(p->h_stage[b]);
+    if (p->stage_ev[b]) cudaEventDestroy(p->stage_ev[b]);
+  }
   if (p->side_st) cudaStreamDestroy(p->side_st);
   if (p->side_fork) cudaEventDestroy(p->side_fork);
   if (p->side_join) cudaEventDestroy(p->side_join);
@@ -1514,12 +1523,64 @@ int sdct_exec_host(sdct_plan_t p, int kind, const void* h_in, void* h_out, void*
     if ((e = cudaMalloc(&p->d_in, bytes)) != cudaSuccess) return cuda_fail(e, "allocating staging");
     if ((e = cudaMalloc(&p->d_out, bytes)) != cudaSuccess) return cuda_fail(e, "allocating staging");
   }
-  if ((e = cudaMemcpyAsync(p->d_in, h_in, bytes, cudaMemcpyHostToDevice, st)) != cudaSuccess)
-    return cuda_fail(e, "copying input to device");
+  // pinned (or registered) host buffers go straight to the copy engine;
+  // pageable ones through the chunked staging of host_stage.hpp
+  auto pinned = [](const void* h) {
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, h) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    return at.type == cudaMemoryTypeHost;
+  };
+  const bool stage_in = !pinned(h_in), stage_out = !pinned(h_out);
+  if ((stage_in || stage_out) && !p->h_stage[0]) {
+    for (int b = 0; b < 2; ++b) {
+      if ((e = cudaMallocHost(&p->h_stage[b], sdct_plan_s::kStageChunk)) != cudaSuccess)
+        return cuda_fail(e, "allocating pinned staging");
+      if ((e = cudaEventCreateWithFlags(&p->stage_ev[b], cudaEventDisableTiming)) != cudaSuccess)
+        return cuda_fail(e, "creating staging event");
+    }
+  }
+  const size_t CH = sdct_plan_s::kStageChunk;
+  const long long nch = static_cast<long long>((bytes + CH - 1) / CH);
+  auto len_of = [&](long long c) { return std::min(CH, bytes - static_cast<size_t>(c) * CH); };
+  CopyPool& pool = CopyPool::get();
+  if (!stage_in) {
+    if ((e = cudaMemcpyAsync(p->d_in, h_in, bytes, cudaMemcpyHostToDevice, st)) != cudaSuccess)
+      return cuda_fail(e, "copying input to device");
+  } else {
+    for (long long c = 0; c < nch; ++c) {
+      const int b = static_cast<int>(c & 1);
+      if (c >= 2 && (e = cudaEventSynchronize(p->stage_ev[b])) != cudaSuccess) return cuda_fail(e, "staging wait");
+      pool.copy(p->h_stage[b], static_cast<const unsigned char*>(h_in) + c * CH, len_of(c));
+      if ((e = cudaMemcpyAsync(static_cast<unsigned char*>(p->d_in) + c * CH, p->h_stage[b], len_of(c),
+                               cudaMemcpyHostToDevice, st)) != cudaSuccess)
+        return cuda_fail(e, "copying input to device");
+      if ((e = cudaEventRecord(p->stage_ev[b], st)) != cudaSuccess) return cuda_fail(e, "staging event");
+    }
+  }
   const int rc = dispatch(p, kind, -1, p->d_in, p->d_out, nullptr, st, nullptr);
   if (rc != SDCT_OK) return rc;
-  if ((e = cudaMemcpyAsync(h_out, p->d_out, bytes, cudaMemcpyDeviceToHost, st)) != cudaSuccess)
-    return cuda_fail(e, "copying output to host");
+  if (!stage_out) {
+    if ((e = cudaMemcpyAsync(h_out, p->d_out, bytes, cudaMemcpyDeviceToHost, st)) != cudaSuccess)
+      return cuda_fail(e, "copying output to host");
+  } else {
+    auto issue = [&](long long c) {
+      const int b = static_cast<int>(c & 1);
+      cudaError_t r = cudaMemcpyAsync(p->h_stage[b], static_cast<const unsigned char*>(p->d_out) + c * CH, len_of(c),
+                                      cudaMemcpyDeviceToHost, st);
+      return r == cudaSuccess ? cudaEventRecord(p->stage_ev[b], st) : r;
+    };
+    for (long long c = 0; c < std::min<long long>(2, nch); ++c)
+      if ((e = issue(c)) != cudaSuccess) return cuda_fail(e, "copying output to host");
+    for (long long c = 0; c < nch; ++c) {
+      const int b = static_cast<int>(c & 1);
+      if ((e = cudaEventSynchronize(p->stage_ev[b])) != cudaSuccess) return cuda_fail(e, "staging wait");
+      pool.copy(static_cast<unsigned char*>(h_out) + c * CH, p->h_stage[b], len_of(c));
+      if (c + 2 < nch && (e = issue(c + 2)) != cudaSuccess) return cuda_fail(e, "copying output to host");
+    }
+  }
   if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return cuda_fail(e, "synchronising");
   return SDCT_OK;
 }

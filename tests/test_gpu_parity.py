@@ -200,6 +200,28 @@ def test_generic_global_bluestein_vs_oracle(cuda, dtype):
     assert oracle.rel_l2(got, want) <= TOL[dtype]
 
 
+def test_host_buffers_staged_and_pinned(cuda):
+    # sdct_exec_host (numpy / RealTensor surface): pageable buffers larger than
+    # two 32 MB staging chunks with a short tail chunk go through the chunked
+    # parallel staging (host_stage.hpp); pinned buffers take the direct copy
+    torch = _torch()
+    import paper_2110_01172_b200 as sd
+    from paper_2110_01172_b200 import capi
+
+    x = rnd((2048, 2600), 43)  # 42.6 MB: chunks of 32 + 10.6 MB
+    want = oracle.port.dct_2d(x)
+    assert oracle.rel_l2(sd.dct_2d(x), want) <= TOL["float64"]
+    plan = capi.Plan((2048, 2600))
+    xp = torch.from_numpy(x).pin_memory()
+    yp = torch.empty_like(xp).pin_memory()
+    plan.exec_host("dct_2d", xp.data_ptr(), yp.data_ptr())
+    assert oracle.rel_l2(yp.numpy(), want) <= TOL["float64"]
+    yq = np.empty_like(x)  # pinned input, pageable output
+    plan.exec_host("dct_2d", xp.data_ptr(), yq.ctypes.data)
+    assert np.array_equal(yq, yp.numpy())
+    plan.close()
+
+
 # every output element written, no workspace read before it is written: the
 # column passes store through TMA (cp.async.bulk.tensor global<-shared), which
 # compute-sanitizer's initcheck cannot see, so coverage is proven by poisoning
