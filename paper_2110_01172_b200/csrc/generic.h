@@ -23,7 +23,11 @@ struct GenericJob {
   const double2* blue_chirp[3] = {nullptr, nullptr, nullptr};
   const double2* blue_hat[3] = {nullptr, nullptr, nullptr};
   const double2* blue_circle[3] = {nullptr, nullptr, nullptr};
-  const double2* blue_fa[3] = {nullptr, nullptr, nullptr};  // circle of min(M, 4096) (global pass line FFTs)
+  const double2* blue_fa[3] = {nullptr, nullptr, nullptr};  // circle of min(M, 4096)
+  // global pass: stage tables of the min(M, 4096)-point column FFT, bhat in its
+  // [plane k2][storage row rt_srow(k1)] order
+  const void* blue_st[3][4] = {};
+  const double2* blue_hatp[3] = {nullptr, nullptr, nullptr};
   // the plan's generic workspace carries the global Bluestein scratch
   // (bluestein_scratch_elems); generic_run points blue_ws at it
   bool blue_scratch = false;
@@ -50,6 +54,12 @@ long long bluestein_scratch_elems(int rank, const int* dims, const int* blue_m, 
 // Opt a kernel in to `smem` bytes of dynamic shared memory on the current
 // device (cached per device and kernel; plan.cu).
 cudaError_t prep_smem_ptr(const void* kernel, size_t smem);
+
+// Batched complex FFT of `planes` x L rows x W lines (lines innermost, W even)
+// through the fast column kernel (plan.cu): forward rows natural -> rt_srow
+// order (DIF), inverse the reverse (DIT), unnormalised; st = its stage tables.
+cudaError_t bluestein_line_fft(const double2* src, double2* dst, int L, int W, int planes, bool inverse,
+                               const void* const st_tables[4], cudaStream_t st);
 
 // Workspace: (2 * numel * batch + bluestein_scratch_elems) * sizeof(double2) bytes.
 template <typename T>

@@ -954,86 +954,78 @@ cudaError_t g2_launch(G2Args a, cudaStream_t st) {
 //   X(k) = c_k sum_j (x_j c_j) conj(c_{k-j}),  c_j = e^{-i pi j^2 / n},
 // a circular convolution of power-of-two length M >= 2n - 1 (bhat = FFT_M of
 // the wrapped conjugate chirp, plan tables). The inverse DFT is
-// conj(DFT(conj(x))). M = fa fb (fa = min(M, 4096)) runs as a four-step FFT
-// whose every pass reads and writes contiguous rows: with m = m1 + fa m2 and
-// k = k2 + fb k1,
-//   pre : u[k2][m1] = W_M^{m1 k2} sum_{m2} xc(m1 + fa m2) W_fb^{m2 k2}
-//         (xc = chirped, zero-padded input, read straight from the tensor)
-//   fa-point line FFTs over the rows k2 -> X(k2 + fb k1) at [k2][k1]
-//   x bhat in that order, inverse line FFTs, then
-//   post: v(m1 + fa m2) = sum_{k2} W_fb^{-m2 k2} W_M^{-m1 k2} z[k2][m1],
-//         out = op(c_m v(m) / M) written back into the tensor.
-// Lines l = o * inner + i of the [outer][n][inner] tensor run in chunks.
-__global__ void g_blue_pre(const double2* __restrict__ in, double2* __restrict__ u, long long l0, long long lines,
-                           int n, long long inner, int lgM, int lgfa, const double2* __restrict__ chirp,
+// conj(DFT(conj(x))). The axis is brought to the front ([n][lines], lines
+// innermost) and processed in chunks of W lines; M = fa fb (fa = min(M, 4096))
+// runs as a four-step FFT with m = m1 + fa m2 and k = k2 + fb k1:
+//   pre : u[k2][m1][w] = W_M^{m1 k2} sum_{m2} xc(m1 + fa m2) W_fb^{m2 k2}
+//         (xc = chirped, zero-padded input)
+//   the fast path's column kernel: fa-point DIF FFTs down the rows of each
+//   plane k2, spectrum rows in rt_srow order; x bhat permuted to that order
+//   (plan table); the inverse column kernel (DIT) back to natural rows; then
+//   post: v(m1 + fa m2) = sum_{k2} W_fb^{-m2 k2} W_M^{-m1 k2} z[k2][m1][w],
+//         out = op(c_m v(m) / M).
+// Every pass reads and writes whole rows of W lines (coalesced).
+__global__ void g_blue_pre(const double2* __restrict__ in, double2* __restrict__ u, long long i0, int cnt, int W,
+                           int n, long long L, int lgM, int lgfa, const double2* __restrict__ chirp,
                            const double2* __restrict__ circ, int inverse) {
   const int M = 1 << lgM, fa = 1 << lgfa, fb = M >> lgfa;
-  const long long total = lines << lgfa;  // one thread per (line, m1)
+  const long long total = static_cast<long long>(fa) * W;  // one thread per (m1, w)
   for (long long f = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; f < total;
        f += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const long long ll = f >> lgfa;
-    const int m1 = static_cast<int>(f & (fa - 1));
-    const long long l = l0 + ll;
-    const long long o = inner == 1 ? l : l / inner, i = l - o * inner;
-    const double2* line = in + o * n * inner + i;
-    double2* dst = u + (ll << lgM) + m1;
+    const int m1 = static_cast<int>(f / W), w = static_cast<int>(f - static_cast<long long>(m1) * W);
+    const double2* col = in + i0 + w;
     for (int k2 = 0; k2 < fb; ++k2) {
       double re = 0.0, im = 0.0;
-      for (int m2 = 0; m2 < fb; ++m2) {
-        const int m = m1 + fa * m2;
-        if (m >= n) break;
-        double2 v = line[static_cast<long long>(m) * inner];
-        if (inverse) v.y = -v.y;
-        v = cm(v, chirp[m]);
-        const double2 w = circ[((m2 * k2) & (fb - 1)) << lgfa];  // W_fb^{m2 k2}
-        re = fma(v.x, w.x, fma(-v.y, w.y, re));
-        im = fma(v.x, w.y, fma(v.y, w.x, im));
+      if (w < cnt) {
+        for (int m2 = 0; m2 < fb; ++m2) {
+          const int m = m1 + fa * m2;
+          if (m >= n) break;
+          double2 v = col[static_cast<long long>(m) * L];
+          if (inverse) v.y = -v.y;
+          v = cm(v, chirp[m]);
+          const double2 t = circ[((m2 * k2) & (fb - 1)) << lgfa];  // W_fb^{m2 k2}
+          re = fma(v.x, t.x, fma(-v.y, t.y, re));
+          im = fma(v.x, t.y, fma(v.y, t.x, im));
+        }
       }
-      dst[static_cast<long long>(k2) << lgfa] = cm(make_double2(re, im), circ[(m1 * k2) & (M - 1)]);
+      u[(static_cast<long long>(k2) * fa + m1) * W + w] = cm(make_double2(re, im), circ[(m1 * k2) & (M - 1)]);
     }
   }
 }
 
-// spectrum row k2, column k1 holds X(k2 + fb k1)
-__global__ void g_blue_mul(double2* __restrict__ u, long long total, int lgM, int lgfa,
-                           const double2* __restrict__ hat) {
-  const int M = 1 << lgM, fa = 1 << lgfa, fb = M >> lgfa;
+// plane p, storage row s (rt_srow order) holds X(p + fb k1(s)); hatp is that order
+__global__ void g_blue_mul(double2* __restrict__ u, long long total, int W, const double2* __restrict__ hatp) {
   for (long long f = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; f < total;
-       f += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const int q = static_cast<int>(f & (M - 1));
-    u[f] = cm(u[f], hat[(q >> lgfa) + fb * (q & (fa - 1))]);
-  }
+       f += static_cast<long long>(gridDim.x) * blockDim.x)
+    u[f] = cm(u[f], hatp[f / W]);
 }
 
-__global__ void g_blue_post(const double2* __restrict__ z, double2* __restrict__ out, long long l0, long long lines,
-                            int n, long long inner, int lgM, int lgfa, const double2* __restrict__ chirp,
+__global__ void g_blue_post(const double2* __restrict__ z, double2* __restrict__ out, long long i0, int cnt, int W,
+                            int n, long long L, int lgM, int lgfa, const double2* __restrict__ chirp,
                             const double2* __restrict__ circ, int inverse) {
   const int M = 1 << lgM, fa = 1 << lgfa, fb = M >> lgfa;
   const double inv_m = 1.0 / static_cast<double>(M);
-  const long long total = lines << lgfa;
+  const long long total = static_cast<long long>(fa) * cnt;
   for (long long f = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; f < total;
        f += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const long long ll = f >> lgfa;
-    const int m1 = static_cast<int>(f & (fa - 1));
-    const long long l = l0 + ll;
-    const long long o = inner == 1 ? l : l / inner, i = l - o * inner;
-    double2* line = out + o * n * inner + i;
-    const double2* src = z + (ll << lgM) + m1;
+    const int m1 = static_cast<int>(f / cnt), w = static_cast<int>(f - static_cast<long long>(m1) * cnt);
+    double2* col = out + i0 + w;
+    const double2* src = z + static_cast<long long>(m1) * W + w;
     for (int m2 = 0; m2 < fb; ++m2) {
       const int m = m1 + fa * m2;
       if (m >= n) break;
       double re = 0.0, im = 0.0;
       for (int k2 = 0; k2 < fb; ++k2) {
-        double2 w = cm(circ[((m2 * k2) & (fb - 1)) << lgfa], circ[(m1 * k2) & (M - 1)]);  // conj below
-        w.y = -w.y;
-        const double2 v = src[static_cast<long long>(k2) << lgfa];
-        re = fma(v.x, w.x, fma(-v.y, w.y, re));
-        im = fma(v.x, w.y, fma(v.y, w.x, im));
+        double2 t = cm(circ[((m2 * k2) & (fb - 1)) << lgfa], circ[(m1 * k2) & (M - 1)]);
+        t.y = -t.y;  // W_fb^{-m2 k2} W_M^{-m1 k2}
+        const double2 v = src[static_cast<long long>(k2) * fa * W];
+        re = fma(v.x, t.x, fma(-v.y, t.y, re));
+        im = fma(v.x, t.y, fma(v.y, t.x, im));
       }
       double2 r = cm(make_double2(re, im), chirp[m]);
       r.x *= inv_m;
       r.y *= inverse ? -inv_m : inv_m;
-      line[static_cast<long long>(m) * inner] = r;
+      col[static_cast<long long>(m) * L] = r;
     }
   }
 }
@@ -1071,23 +1063,20 @@ int bluestein_len(int n, bool tile) {
   return static_cast<double>(big) > 20.0 * M / n ? M : 0;
 }
 
-// Two-pass pipeline: both extents <= kG2MaxN, and an axis whose Bluestein
-// length exceeds the line capacity (4096 < n <= 8192) stays on the mixed
-// radix inside it only while its largest prime factor is moderate (a prime
-// radix p costs p MACs per element: 4097 = 17 x 241 runs there as fast as the
-// global Bluestein pass; 8191 took 20 ms that way and 0.23 ms through it)
+// Two-pass pipeline: both extents <= kG2MaxN and every Bluestein length
+// within the tile; an axis with a large prime factor and 4096 < n <= 8192
+// runs the global pass instead (4097 = 17 x 241: 8.2 ms on the tile's mixed
+// radix, where a prime radix p costs p MACs per element; 8191 took 20 ms there)
 bool generic_two_pass(int rank, const int* dims, const int* blue_m) {
   if (rank != 2) return false;
-  for (int a = 0; a < 2; ++a) {
-    if (dims[a] > kG2MaxN) return false;
-    if (blue_m[a] > kG2MaxN && largest_prime(dims[a]) > 256) return false;
-  }
+  for (int a = 0; a < 2; ++a)
+    if (dims[a] > kG2MaxN || blue_m[a] > kG2MaxN) return false;
   return true;
 }
 
 long long bluestein_chunk_lines(int M, long long lines) {
-  const long long cap = std::max<long long>(1, (8LL << 20) / M);  // <= 8 Mi complex per buffer
-  return std::min(lines, cap);
+  const long long cap = std::max<long long>(2, ((8LL << 20) / M) & ~1LL);  // <= 8 Mi complex per buffer
+  return std::min(lines + (lines & 1), cap);  // even: whole 2-line bands of the column kernel
 }
 
 long long bluestein_scratch_elems(int rank, const int* dims, const int* blue_m, long long batch) {
@@ -1129,26 +1118,29 @@ static void line_fft_run(const double2* src, double2* dst, long long outer_, int
       src, dst, outer_, len, inner_, tab, ts, inverse, factorise(len), lpc);
 }
 
-// axis a of cur ([outer][n][inner]) -> nxt through the global Bluestein pass
-static void blue_axis(const GenericJob& job, int a, const double2* cur, double2* nxt, long long outer,
-                      long long inner, int inverse, cudaStream_t st) {
+// axis a of the [n][L] matrix X (lines innermost) -> Y through the global
+// Bluestein pass, in chunks of W lines
+static void blue_axis(const GenericJob& job, int a, const double2* X, double2* Y, long long L, int inverse,
+                      cudaStream_t st) {
   const int n = job.dims[a], M = job.blue_m[a];
   int lgM = 0;
   while ((1 << lgM) < M) ++lgM;
   const int lgfa = lgM < 12 ? lgM : 12, fa = 1 << lgfa, fb = M >> lgfa;
-  const long long L = outer * inner, chunk = bluestein_chunk_lines(M, L);
+  const int W = static_cast<int>(bluestein_chunk_lines(M, L));
   double2* U = job.blue_ws;
-  double2* V = U + chunk * M;
+  double2* V = U + static_cast<long long>(W) * M;
   const double2* circ = job.blue_circle[a];
-  for (long long l0 = 0; l0 < L; l0 += chunk) {
-    const long long cnt = std::min(chunk, L - l0);
-    g_blue_pre<<<nblocks(cnt * fa), kThreads, 0, st>>>(cur, U, l0, cnt, n, inner, lgM, lgfa, job.blue_chirp[a], circ,
-                                                       inverse);
-    line_fft_run(U, V, cnt * fb, fa, 1, job.blue_fa[a], 1, 0, st);
-    g_blue_mul<<<nblocks(cnt * M), kThreads, 0, st>>>(V, cnt * M, lgM, lgfa, job.blue_hat[a]);
-    line_fft_run(V, U, cnt * fb, fa, 1, job.blue_fa[a], 1, 1, st);
-    g_blue_post<<<nblocks(cnt * fa), kThreads, 0, st>>>(U, nxt, l0, cnt, n, inner, lgM, lgfa, job.blue_chirp[a], circ,
-                                                        inverse);
+  for (long long i0 = 0; i0 < L; i0 += W) {
+    const int cnt = static_cast<int>(std::min<long long>(W, L - i0));
+    const int Wc = cnt + (cnt & 1);  // column-kernel bands are 2 lines wide
+    g_blue_pre<<<nblocks(static_cast<long long>(fa) * Wc), kThreads, 0, st>>>(X, U, i0, cnt, Wc, n, L, lgM, lgfa,
+                                                                            job.blue_chirp[a], circ, inverse);
+    bluestein_line_fft(U, V, fa, Wc, fb, false, job.blue_st[a], st);
+    g_blue_mul<<<nblocks(static_cast<long long>(M) * Wc), kThreads, 0, st>>>(V, static_cast<long long>(M) * Wc, Wc,
+                                                                           job.blue_hatp[a]);
+    bluestein_line_fft(V, U, fa, Wc, fb, true, job.blue_st[a], st);
+    g_blue_post<<<nblocks(static_cast<long long>(fa) * cnt), kThreads, 0, st>>>(U, Y, i0, cnt, Wc, n, L, lgM, lgfa,
+                                                                              job.blue_chirp[a], circ, inverse);
   }
 }
 
@@ -1160,12 +1152,15 @@ static void dft_axes(const GenericJob& job, int a0, int a1, double2*& cur, doubl
       for (int t = 0; t < a; ++t) outer *= job.dims[t];
       const int n = job.dims[a];
       if (job.blue_m[a] && job.blue_ws) {
-        if (inner > 1) {  // strided axis: rows first, so every Bluestein pass is coalesced
-          g_transpose(cur, nxt, outer, n, inner, st);  // [o][n][inner] -> [o][inner][n]
-          blue_axis(job, a, nxt, cur, outer * inner, 1, inverse, st);
-          g_transpose(cur, nxt, outer, inner, n, st);  // back
+        // the axis in front, lines innermost: [o][n][inner] -> [n][inner][o]
+        // (lines in (i, o) order; none needed when outer == 1)
+        const long long L = outer * inner;
+        if (outer > 1) {
+          g_transpose(cur, nxt, 1, outer, static_cast<long long>(n) * inner, st);
+          blue_axis(job, a, nxt, cur, L, inverse, st);
+          g_transpose(cur, nxt, 1, static_cast<long long>(n) * inner, outer, st);  // back
         } else {
-          blue_axis(job, a, cur, nxt, outer, 1, inverse, st);
+          blue_axis(job, a, cur, nxt, L, inverse, st);
         }
         std::swap(cur, nxt);
         continue;
@@ -1243,7 +1238,7 @@ cudaError_t generic_run(const GenericJob& job, const void* in, void* out, void* 
     cudaError_t e;
     auto axis = [&](int ax) {  // FFT-axis tables (mixed radix or Bluestein)
       a.circle = job.circle[ax];
-      a.bm = job.blue_m[ax] <= kG2MaxN ? job.blue_m[ax] : 0;  // longer: mixed radix (generic_two_pass)
+      a.bm = job.blue_m[ax];
       a.bchirp = job.blue_chirp[ax];
       a.bhat = job.blue_hat[ax];
       a.bcircle = job.blue_circle[ax];

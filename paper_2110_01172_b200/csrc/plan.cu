@@ -151,6 +151,8 @@ struct sdct_plan_s {
   double2* bhat[3] = {nullptr, nullptr, nullptr};
   double2* bcircle[3] = {nullptr, nullptr, nullptr};
   double2* bfa[3] = {nullptr, nullptr, nullptr};  // e^{-2 pi i t / 4096} when M > 4096, else bcircle
+  TwSet bst[3] = {};                               // global Bluestein: min(M, 4096)-point column FFT tables
+  double2* bhatp[3] = {nullptr, nullptr, nullptr}; // global Bluestein: bhat in [k2][rt_srow(k1)] order
   size_t b_offset_fast = 0, b_offset_gen = 0;    // element offsets of table b (corrupt hook)
   // workspace + host staging
   void* ws = nullptr;
@@ -451,6 +453,9 @@ int build_plan(sdct_plan_s* p) {
   }
   // generic-path tables are always present (odd shapes, row-column, 1D)
   size_t off_bc[3] = {0, 0, 0}, off_bh[3] = {0, 0, 0}, off_bm[3] = {0, 0, 0}, off_bf[3] = {0, 0, 0};
+  size_t off_bst[3][4], off_bhp[3] = {0, 0, 0};
+  for (auto& o : off_bst)
+    for (size_t& v : o) v = SIZE_MAX;
   for (int a = 0; a < r; ++a) {
     circle(re, im, p->n[a], 1.0L, 4.0L * p->n[a]);
     fill_table<double>(blob, off_gq[a], re, im);
@@ -481,6 +486,19 @@ int build_plan(sdct_plan_s* p) {
       if (M > 4096) {
         circle(re, im, 4096, 1.0L, 4096);
         fill_table<double>(blob, off_bf[a], re, im);
+      }
+      if (p->blue_elems) {  // the global pass: column-kernel FFTs of fa points, fb planes
+        const int fa = M < 4096 ? M : 4096, fb = M / fa;
+        stage_tables<double>(blob, fa, off_bst[a]);
+        std::vector<long double> pr(M), pi2(M);
+        for (int k1 = 0; k1 < fa; ++k1) {
+          const int srow = rt_srow(k1, fa);
+          for (int k2 = 0; k2 < fb; ++k2) {
+            pr[static_cast<size_t>(k2) * fa + srow] = hr[k2 + static_cast<size_t>(fb) * k1];
+            pi2[static_cast<size_t>(k2) * fa + srow] = hi[k2 + static_cast<size_t>(fb) * k1];
+          }
+        }
+        fill_table<double>(blob, off_bhp[a], pr, pi2);
       }
     }
   }
@@ -517,6 +535,10 @@ int build_plan(sdct_plan_s* p) {
       p->bhat[a] = reinterpret_cast<double2*>(base + off_bh[a]);
       p->bcircle[a] = reinterpret_cast<double2*>(base + off_bm[a]);
       p->bfa[a] = p->bm[a] > 4096 ? reinterpret_cast<double2*>(base + off_bf[a]) : p->bcircle[a];
+      if (p->blue_elems) {
+        for (int k = 0; k < 4; ++k) p->bst[a].st[k] = off_bst[a][k] == SIZE_MAX ? nullptr : base + off_bst[a][k];
+        p->bhatp[a] = reinterpret_cast<double2*>(base + off_bhp[a]);
+      }
     }
   }
   for (int a = 0; a < 2; ++a) {
@@ -644,6 +666,32 @@ bool make_class4_map(CUtensorMap* map, bool f32, const void* base, long long inn
                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
+
+}  // namespace
+
+// Batched complex line FFT for the generic path's global Bluestein pass
+// (generic.h): the fast column kernel on a [planes][L][W] complex tensor.
+cudaError_t sdctb::bluestein_line_fft(const double2* src, double2* dst, int L, int W, int planes, bool inverse,
+                               const void* const st_tables[4], cudaStream_t st) {
+  const int nld = nl_default(8, L);
+  const int nl = (W % nld == 0 && static_cast<long long>(W / nld) * planes >= 148) ? nld : 2;
+  const long long row_b = 16LL * W, plane_b = row_b * L, batch_b = plane_b * planes;
+  CUtensorMap mi, mo;
+  if (!make_col_map(&mi, false, src, 2LL * W, L, row_b, planes, plane_b, 1, batch_b, nl, L) ||
+      !make_col_map(&mo, false, dst, 2LL * W, L, row_b, planes, plane_b, 1, batch_b, nl, L / 2))
+    return cudaErrorInvalidValue;
+  ColArgs c{};
+  c.src = src;
+  c.dst = dst;
+  c.in_row = c.out_row = W;
+  c.in_plane = c.out_plane = static_cast<long long>(L) * W;
+  c.in_batch = c.out_batch = c.in_plane * planes;
+  TwSet tw{};
+  for (int k = 0; k < 4; ++k) tw.st[k] = st_tables[k];
+  return launch_col<double>(inverse ? CV_INV_INTER : CV_FWD_INTER, L, nl, dim3(W / nl, planes, 1), st, mi, mo, c, tw);
+}
+
+namespace {
 
 // Compression threshold carried by the 2D inverse row kernels (weight 3).
 struct Threshold {
@@ -902,6 +950,8 @@ GenericJob make_job(const sdct_plan_s* p, int kind) {
     j.blue_hat[a] = p->bhat[a];
     j.blue_circle[a] = p->bcircle[a];
     j.blue_fa[a] = p->bfa[a];
+    for (int k = 0; k < 4; ++k) j.blue_st[a][k] = p->bst[a].st[k];
+    j.blue_hatp[a] = p->bhatp[a];
   }
   j.blue_scratch = p->blue_elems > 0;
   j.batch = p->batch;
