@@ -1,3 +1,4 @@
+#include <cstdlib>
 #include <algorithm>
 // Generic path: any extents (odd, non-power-of-two, tiny), ranks 1..3, fp64
 // arithmetic throughout (inputs/outputs may be fp32). It restates the
@@ -1106,7 +1107,11 @@ static void line_fft_run(const double2* src, double2* dst, long long outer_, int
   }
   // threads per CTA: the fewest (>= 128) that hold a whole line at
   // kFftPerThread outputs each (small CTAs: the passes are latency bound)
-  const int nt = len <= 1024 ? 128 : len <= 2048 ? 256 : 512;
+  static const int nt_short = [] {
+    const char* f = getenv("SDCT_G_NT");  // developer A/B knob
+    return f ? atoi(f) : 128;
+  }();
+  const int nt = len <= 1024 ? nt_short : len <= 2048 ? 256 : 512;
   int lpc = 1;
   while (lpc < 16 && 2 * lpc * len <= kFftPerThread * nt &&
          (inner_ == 1 ? lpc * 2 <= outer_ : inner_ % (lpc * 2) == 0))
@@ -1173,8 +1178,14 @@ static void dft_axes(const GenericJob& job, int a0, int a1, double2*& cur, doubl
       if ((n > 1 && n <= kFftMaxN) || fa > 0) {
         // strided axes (inner > 1) whose lines would be read with little
         // coalescing are transposed to rows first: [o][n][inner] -> [o][inner][n]
-        const bool tr = inner > 1 && (static_cast<long long>(16) * (fa > 0 ? fa : n) > kFftPerThread * kThreads ||
-                                      inner % 16 != 0);
+        // (>= 4 lines per CTA keep 64-B row segments: 3D 200^3 fp64 DCT 802 -> 672 us,
+        // 250^3 1480 -> 1334 us against a rule of 16 lines)
+        static const int lmin = [] {
+          const char* f = getenv("SDCT_G_LMIN");  // developer A/B knob
+          return f ? atoi(f) : 4;
+        }();
+        const bool tr = inner > 1 && (static_cast<long long>(lmin) * (fa > 0 ? fa : n) > kFftPerThread * kThreads ||
+                                      inner % lmin != 0);
         long long o2 = outer, in2 = inner;
         if (tr) {
           g_transpose(cur, nxt, outer, n, inner, st);
