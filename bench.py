@@ -237,7 +237,59 @@ def cpu_reference_rate(w, budget_s: float, max_steps: int | None = None):
 
 
 # ---------------------------------------------------------------------------
-def cufft_times(x, dims, batch, stream, reps):
+def graph_time(fn, reps, stream, eager=False):
+    """Average ms of fn() over `reps` back-to-back calls on `stream`, the calls
+    captured once into a CUDA graph and replayed (so host launch latency, which
+    exceeds the device time of the small configs, is not what gets timed).
+    fn(sh) must launch on the raw stream handle sh. Falls back to eager launches
+    (returned flag False) if capture fails or eager is requested."""
+    import torch
+
+    def eager_run():
+        for _ in range(3):
+            fn(stream.cuda_stream)
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(reps):
+            fn(stream.cuda_stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / reps
+
+    if eager:
+        return eager_run(), False
+    try:
+        g = capture_graph(lambda sh: [fn(sh) for _ in range(reps)], stream)
+    except Exception:
+        return eager_run(), False
+    g.replay()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    g.replay()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps, True
+
+
+def capture_graph(body, stream):
+    """Capture body(sh) (launches on raw stream handle sh) into a CUDA graph."""
+    import torch
+
+    cs = torch.cuda.Stream(stream.device)
+    cs.wait_stream(stream)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=cs, capture_error_mode="thread_local"):
+        body(cs.cuda_stream)
+    torch.cuda.synchronize()
+    return g
+
+
+def cufft_times(x, dims, batch, stream, reps, eager=False):
     """cuFFT R2C and C2R (D2Z / Z2D for fp64) of the same shape and batch,
     called directly through libcufft (ctypes; cufftPlanMany) so no framework
     copies or plan-cache effects are timed. Library baseline only (north_star:
@@ -275,14 +327,13 @@ def cufft_times(x, dims, batch, stream, reps):
         for _ in range(3):
             if ex(pl, a_, b_) != 0:
                 raise RuntimeError("cufftExec failed")
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(reps):
+
+        def call(sh, ex=ex, pl=pl, a_=a_, b_=b_):
+            lib.cufftSetStream(pl, ctypes.c_void_p(sh))
             ex(pl, a_, b_)
-        e1.record(stream)
-        torch.cuda.synchronize()
-        res.append(e0.elapsed_time(e1) / reps)
+
+        res.append(graph_time(call, reps, stream, eager)[0])
+        lib.cufftSetStream(pl, ctypes.c_void_p(stream.cuda_stream))
     lib.cufftDestroy(pf)
     lib.cufftDestroy(pi)
     return res[0], res[1]
@@ -372,18 +423,19 @@ def run_ours(args, rank: int, world: int, local_rank: int, backend: str | None =
         eps_c = float(b0.abs().median().item())
         del b0
 
-    def step(i):
+    def step(i, sh=None):
+        sh = s if sh is None else sh
         r = i % rot
         src = xs[r]
         if w["mode"] == "force":
-            plan.force_fields(src.data_ptr(), outs[r][0].data_ptr(), outs[r][1].data_ptr(), s, ws.data_ptr())
+            plan.force_fields(src.data_ptr(), outs[r][0].data_ptr(), outs[r][1].data_ptr(), sh, ws.data_ptr())
             return
         if w["mode"] == "compress":
-            plan.compress(src.data_ptr(), outs[r][0].data_ptr(), eps_c, zeroed.data_ptr(), s, ws.data_ptr())
+            plan.compress(src.data_ptr(), outs[r][0].data_ptr(), eps_c, zeroed.data_ptr(), sh, ws.data_ptr())
             return
         for j, k in enumerate(kinds):
             dst = outs[r][j]
-            plan.run(k, src.data_ptr(), dst.data_ptr(), s, ws.data_ptr())
+            plan.run(k, src.data_ptr(), dst.data_ptr(), sh, ws.data_ptr())
             if w["mode"] == "chain":
                 src = dst
 
@@ -448,11 +500,28 @@ def run_ours(args, rank: int, world: int, local_rank: int, backend: str | None =
             if ref is not None:
                 parity[f"{k}_rel_l2_vs_oracle"] = float(oracle.rel_l2(outs[0][j][0].double().cpu().numpy(), ref))
 
+    # the K timed steps are captured once into a CUDA graph (the same plan.run
+    # launches, programmatic dependent launch edges kept) and replayed: the
+    # small configs' kernels run shorter than Python + driver launch latency,
+    # so eager launching would time the host, not the device
+    graph, graph_note = None, "eager launches (--eager)"
+    if not args.eager:
+        try:
+            graph = capture_graph(lambda sh: [step(j, sh) for j in range(args.steps)], stream)
+            graph_note = f"CUDA graph of the {args.steps} steps, replayed (captured once before warm-up)"
+        except Exception as e:  # pragma: no cover - reported, falls back to eager
+            graph_note = f"eager launches (graph capture failed: {str(e)[:120]})"
+
     clocks = ClockSampler(local_rank)
     clocks.start()
     t_w = time.perf_counter()
     i = 0
     while i < args.warmup or time.perf_counter() - t_w < 1.0:  # >= W steps and >= 1 s soak
+        if graph is not None:
+            graph.replay()
+            i += args.steps
+            torch.cuda.synchronize()
+            continue
         step(i)
         i += 1
         if i % 20 == 0:
@@ -463,8 +532,11 @@ def run_ours(args, rank: int, world: int, local_rank: int, backend: str | None =
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    for j in range(args.steps):
-        step(j)
+    if graph is not None:
+        graph.replay()
+    else:
+        for j in range(args.steps):
+            step(j)
     e1.record(stream)
     torch.cuda.synchronize()
     barrier()
@@ -475,33 +547,49 @@ def run_ours(args, rank: int, world: int, local_rank: int, backend: str | None =
     value = job_bytes_step * args.steps / (ms / 1e3) / 1e9
 
     # ---- per-kernel timing (roofline of the dominant kernel) ----------------
-    # live: the timed loop's steps again, with an event between every kernel
-    # launch on the launching stream (steady state: each kernel meets the L2
-    # its predecessor left behind, as inside the timed region)
+    # graph mode: for each kernel of the step, n_inst back-to-back launches of
+    # that kernel alone on the timed loop's rotating buffers (inputs cold as in
+    # the step; the workspace intermediate as its producer leaves it), captured
+    # into a CUDA graph and timed with events around the replay. Eager mode:
+    # the timed loop's steps again with an event between every kernel launch.
     peak, peak_kind = _peaks()
     stage_list = [(kn, k, st) for kn, k in zip(w["kinds"], kinds) for st in range(plan.stage_count(k))]
     n_inst = max(10, min(args.steps, 50))
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(len(stage_list) + 1)] for _ in range(n_inst)]
-    torch.cuda.synchronize()
-    for j in range(n_inst):
-        r = j % rot
-        src = xs[r]
-        evs[j][0].record(stream)
-        e_i = 1
-        for kn, k in zip(w["kinds"], kinds):
-            dst = outs[r][w["kinds"].index(kn)]
-            for st in range(plan.stage_count(k)):
-                plan.run_stage(k, st, src.data_ptr(), dst.data_ptr(), s, ws.data_ptr())
-                evs[j][e_i].record(stream)
-                e_i += 1
-            if w["mode"] == "chain":
-                src = dst
     torch.cuda.synchronize()
     kernels = []
-    for i, (kn, k, st) in enumerate(stage_list):
-        ts = [evs[j][i].elapsed_time(evs[j][i + 1]) for j in range(n_inst)]
-        avg = sum(ts) / len(ts)
-        kernels.append({"kernel": f"{kn}.stage{st}", "ms": avg, "gbs": bytes_transform / (avg / 1e3) / 1e9})
+    kt_graph = graph is not None
+    if kt_graph:
+        for ki, (kn, k) in enumerate(zip(w["kinds"], kinds)):
+            for st in range(plan.stage_count(k)):
+                def one(sh, j=[0], ki=ki, k=k, st=st):
+                    r = j[0] % rot
+                    j[0] += 1
+                    src = outs[r][ki - 1] if (w["mode"] == "chain" and ki > 0) else xs[r]
+                    plan.run_stage(k, st, src.data_ptr(), outs[r][ki].data_ptr(), sh, ws.data_ptr())
+
+                avg, ok = graph_time(one, n_inst, stream)
+                kt_graph = kt_graph and ok
+                kernels.append({"kernel": f"{kn}.stage{st}", "ms": avg, "gbs": bytes_transform / (avg / 1e3) / 1e9})
+    else:
+        evs = [[torch.cuda.Event(enable_timing=True) for _ in range(len(stage_list) + 1)] for _ in range(n_inst)]
+        for j in range(n_inst):
+            r = j % rot
+            src = xs[r]
+            evs[j][0].record(stream)
+            e_i = 1
+            for kn, k in zip(w["kinds"], kinds):
+                dst = outs[r][w["kinds"].index(kn)]
+                for st in range(plan.stage_count(k)):
+                    plan.run_stage(k, st, src.data_ptr(), dst.data_ptr(), s, ws.data_ptr())
+                    evs[j][e_i].record(stream)
+                    e_i += 1
+                if w["mode"] == "chain":
+                    src = dst
+        torch.cuda.synchronize()
+        for i, (kn, k, st) in enumerate(stage_list):
+            ts = [evs[j][i].elapsed_time(evs[j][i + 1]) for j in range(n_inst)]
+            avg = sum(ts) / len(ts)
+            kernels.append({"kernel": f"{kn}.stage{st}", "ms": avg, "gbs": bytes_transform / (avg / 1e3) / 1e9})
     # cold: each kernel alone after an L2 flush (ncu-like conditions), for reference
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
     cold = []
@@ -536,7 +624,11 @@ def run_ours(args, rank: int, world: int, local_rank: int, backend: str | None =
     roofline = {"bound": "hbm", "achieved": round(dom["gbs"], 2), "peak": peak, "unit": "GB/s",
                 "frac": round(dom["gbs"] / peak, 4), "traffic": traffic, "kernel": dom["kernel"],
                 "peak_kind": peak_kind, "per_launch_bytes": bytes_transform,
-                "timing": (f"live: {n_inst} steps of the timed loop with an event between kernels (the events "
+                "timing": (f"live, CUDA graph: {n_inst} back-to-back launches of each kernel alone on the timed "
+                           "loop's rotating buffers, events around the graph replay (programmatic dependent launch "
+                           "overlaps each launch's prologue with its predecessor's tail, as in the step)"
+                           if kt_graph else
+                           f"live: {n_inst} steps of the timed loop with an event between kernels (the events "
                            "stop programmatic dependent launch from overlapping kernel tails, so the per-kernel "
                            "times sum to more than ms_per_step)"),
                 "all_kernels": [{k2: (round(v, 4) if isinstance(v, float) else v) for k2, v in k_.items()}
@@ -551,19 +643,18 @@ def run_ours(args, rank: int, world: int, local_rank: int, backend: str | None =
     cufft = {}
     try:
         reps = 10 if B > 1 else 20
-        r2c, c2r = cufft_times(xs[0], list(dims), B, stream, reps)
+        # both sides timed the same way: reps calls on one input, captured
+        # into a CUDA graph and replayed (eager with --eager)
+        r2c, c2r = cufft_times(xs[0], list(dims), B, stream, reps, args.eager)
         a = torch.cuda.Event(enable_timing=True)
         b = torch.cuda.Event(enable_timing=True)
         ours = {}
         src = xs[0]
         for kn, k in zip(w["kinds"], kinds):
-            a.record(stream)
-            for _ in range(reps):
-                plan.run(k, src.data_ptr(), outs[0][0].data_ptr(), s, ws.data_ptr())
-            b.record(stream)
-            torch.cuda.synchronize()
-            ours[kn] = a.elapsed_time(b) / reps
+            ours[kn] = graph_time(lambda sh, k=k: plan.run(k, src.data_ptr(), outs[0][0].data_ptr(), sh,
+                                                          ws.data_ptr()), reps, stream, args.eager)[0]
         cufft = {"api": "libcufft cufftPlanMany + cufftExec{D2Z,Z2D|R2C,C2R}, plan built outside timing",
+                 "timing": "eager launches" if args.eager else "CUDA graph replay of the repeated calls (both sides)",
                  "r2c_ms": round(r2c, 4), "c2r_ms": round(c2r, 4)}
         if len(dims) == 2 and "dct_2d" in w["kinds"]:
             # row-column DCT on the same shape (north_star: "reported alongside"):
@@ -572,12 +663,9 @@ def run_ours(args, rank: int, world: int, local_rank: int, backend: str | None =
             k_rc = _sdct.DCT_2D_ROWCOL
             plan.run(k_rc, xs[0].data_ptr(), outs[0][0].data_ptr(), s, 0)
             torch.cuda.synchronize()
-            a.record(stream)
-            for _ in range(3):
-                plan.run(k_rc, xs[0].data_ptr(), outs[0][0].data_ptr(), s, 0)
-            b.record(stream)
-            torch.cuda.synchronize()
-            cufft["rowcol_dct_2d_ms"] = round(a.elapsed_time(b) / 3, 4)
+            rc_ms = graph_time(lambda sh: plan.run(k_rc, xs[0].data_ptr(), outs[0][0].data_ptr(), sh, 0), 3,
+                               stream, args.eager)[0]
+            cufft["rowcol_dct_2d_ms"] = round(rc_ms, 4)
         for kn, v in ours.items():
             cufft[f"{kn}_ms"] = round(v, 4)
             base = r2c if kn.startswith("dct") else c2r
@@ -693,7 +781,7 @@ def run_ours(args, rank: int, world: int, local_rank: int, backend: str | None =
             "dtype": "f64" if dt == torch.float64 else "f32",
             "data": "synthetic uniform(-1,1), device-resident",
             "config": job_config(args, w, world),
-            "measurement": {"l2": ("working set per step > 2x the 126 MB L2 (no flush needed)" if rot == 1 else
+            "measurement": {"launch": graph_note, "l2": ("working set per step > 2x the 126 MB L2 (no flush needed)" if rot == 1 else
                                    f"inputs/outputs rotate over {rot} sets ({rot * set_bytes / 2**20:.0f} MB > 2x L2)"),
                             "bytes_per_step_per_gpu": bytes_step, "warmup_steps_run": warm_done,
                             "warmup_rule": f">= {args.warmup} untimed steps and >= 1 s of soak before timing",
@@ -781,6 +869,7 @@ def main():
     ap.add_argument("--dtype", choices=["float64", "float32"], default=None,
                     help="override the workload's dtype (c2 runs fp64 by default)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    ap.add_argument("--eager", action="store_true", help="launch the timed steps eagerly (no CUDA graph)")
     ap.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of CPU baseline sampling")
     ap.add_argument("--dry-orchestration", action="store_true",
                     help="test hook: rank launch, shards and the max-over-ranks reduction only (gloo, no GPU)")

@@ -69,6 +69,7 @@ struct ColArgs {
   int out_plane_map;                        // ST_DST: 0 plane, 1 pe(plane), 2 pe(digit_rev(plane))
   int out_plane_n;                          // extent used by out_plane_map
   int sign_row, sign_col;                   // final gather: negate odd k along axis
+  int pair_b, sign_row2, sign_col2;         // paired inverse launch: batch items >= pair_b use the *2 signs
   double scale;                             // final gather scale
   int tma_plane_par;                        // TMA plane coordinate = parity_embed(plane, n) when > 0
   const void* twc;                          // cluster-split pass: W_L^k, k < L/2
@@ -101,7 +102,18 @@ struct RowArgs {
   int weight;                      // 2D inverse input: 0 none, 1/2 force-field weight w1/w2, 3 compression threshold
   double thr_eps, thr_scale;       // weight 3: zero |b| < thr_eps, scale the rest
   unsigned long long* thr_count;   // weight 3: zeroed coefficients (device counter, may be null)
+  // paired inverse launch (force fields: both composites in one launch): batch
+  // items b >= pair_b read source item b - pair_b and use mode2 / weight2
+  int pair_b, mode2, weight2;
 };
+
+// inverse row kernels: (source item, composite mode, input weighting) of batch item b
+__device__ __forceinline__ void inv_item(const RowArgs& a, int b, int& img, int& mode, int& weight) {
+  const bool h2 = a.pair_b > 0 && b >= a.pair_b;
+  img = h2 ? b - a.pair_b : b;
+  mode = h2 ? a.mode2 : a.mode;
+  weight = h2 ? a.weight2 : a.weight;
+}
 
 // ---- small helpers ----------------------------------------------------------
 __device__ __forceinline__ int s_to_m(int s, int M) { return (s & 1) ? M - 1 - (s >> 1) : (s >> 1); }
@@ -817,6 +829,8 @@ __global__ void __launch_bounds__(Tile<T, L, NL, true>::NT)
         // 2L-1-2ii (ii >= L/2), staged per class and stored through a 5D map
         // {reals, row class, row pair, planes, batch}
         const T sc = static_cast<T>(a.scale);
+        const bool h2_ = a.pair_b > 0 && batch >= a.pair_b;
+        const int srow_ = h2_ ? a.sign_row2 : a.sign_row, scol_ = h2_ ? a.sign_col2 : a.sign_col;
         int pl = plane;
         if (a.out_plane_map == 1) pl = parity_embed(plane, a.out_plane_n);
         // part q holds ii in [q L/PI, (q+1) L/PI): class q / (PI/2) (even rows
@@ -844,8 +858,8 @@ __global__ void __launch_bounds__(Tile<T, L, NL, true>::NT)
               const int srow = (half == 0 ? ii : L - 1 - ii) - pbase;   // pair index within the part
               const V z = v[i * R0 + r];
               const T recv = __shfl_xor_sync(TL::MASK, z.y, 1);
-              const T s0 = (a.sign_row && (k1 & 1)) ? -sc : sc;
-              const T s1 = a.sign_col ? -s0 : s0;
+              const T s0 = (srow_ && (k1 & 1)) ? -sc : sc;
+              const T s1 = scol_ ? -s0 : s0;
               // h=0: (Re z(u), Im z(M-1-u)) = y(4u, 4u+1); h=1: (Im z(u), Re z(M-1-u)) = y(4u+2, 4u+3)
               sv[srow * NL + line] = h ? V2{recv * s0, z.x * s1} : V2{z.x * s0, recv * s1};
             }

@@ -125,7 +125,9 @@ __global__ void __launch_bounds__(Row2Geom<T, M, MODE>::CTA, Row2Geom<T, M, MODE
       const V* src = static_cast<const V*>(a.src) + batch * a.src_batch;
       bulk_load(dst, src + static_cast<long long>(__ldg(a.s0 + row)) * M, G::BUF / 2, bar);
     } else {
-      const T* src = static_cast<const T*>(a.src) + batch * a.src_batch;
+      int img, md_, wt_;
+      inv_item(a, batch, img, md_, wt_);
+      const T* src = static_cast<const T*>(a.src) + img * a.src_batch;
       bulk_load(dst, src + static_cast<long long>(row) * n2, G::BUF / 2, bar);
     }
   };
@@ -190,6 +192,8 @@ __global__ void __launch_bounds__(Row2Geom<T, M, MODE>::CTA, Row2Geom<T, M, MODE
     int q1, m1;
     rows_of(P, q1, m1);
     V v[TL::E];
+    int img_, imode, iweight;  // inverse: source item, composite mode, weighting (paired launches)
+    inv_item(a, batch, img_, imode, iweight);
 
     if constexpr (!INV) {
       // ================= forward: FFT + unpack + merged postprocess ==========
@@ -296,7 +300,7 @@ __global__ void __launch_bounds__(Row2Geom<T, M, MODE>::CTA, Row2Geom<T, M, MODE
       // (the weighting below runs on the landed rows in their own order)
       mbar_wait(full + b, ph);
       if constexpr (MODE == 2) mbar_wait(empty, ph);
-      if (a.weight == 3) {
+      if (iweight == 3) {
         // compression (proj/src/compress.cpp:33-45) folded into this load:
         // zero every coefficient with |b| < eps (counted), scale the rest by
         // the 4/(N1 N2) reconstruction normalisation (linear, so it commutes
@@ -316,7 +320,7 @@ __global__ void __launch_bounds__(Row2Geom<T, M, MODE>::CTA, Row2Geom<T, M, MODE
         for (int o = W / 2; o > 0; o >>= 1) cnt += __shfl_xor_sync(TL::MASK, cnt, o);
         if ((threadIdx.x & 31) == 0 && cnt && a.thr_count) atomicAdd(a.thr_count, static_cast<unsigned long long>(cnt));
         TL::sync();
-      } else if (a.weight) {
+      } else if (iweight) {
         // DREAMPlace-style field weighting of the input coefficients
         // (proj/src/force.cpp:19-31), folded into this load: a1 = a w1/(w1^2+w2^2)
         // (weight 1) or a2 = a w2/(w1^2+w2^2) (weight 2), w_d = pi k_d / n_d, 0 at DC
@@ -328,7 +332,7 @@ __global__ void __launch_bounds__(Row2Geom<T, M, MODE>::CTA, Row2Geom<T, M, MODE
           T* rw = rws[e >= n2] + k2;
           const T w1 = e < n2 ? w1a : w1b, w2 = sc2 * T(k2);
           const T den = fma(w1, w1, w2 * w2);
-          *rw = den > T(0) ? *rw * (a.weight == 1 ? w1 : w2) / den : T(0);
+          *rw = den > T(0) ? *rw * (iweight == 1 ? w1 : w2) / den : T(0);
         }
         TL::sync();
       }
@@ -336,7 +340,7 @@ __global__ void __launch_bounds__(Row2Geom<T, M, MODE>::CTA, Row2Geom<T, M, MODE
       // both rows; mode 2 (IDXST along axis 1) reads x(N2-n2) for D and x(n2)
       // for R with x(0) := 0 (proj/src/dct2d.cpp:169-180)
       // IDXST along axis 0 (mode 1) swaps the two rows' roles for pairs
-      if (a.mode == 1 && P != 0) {
+      if (imode == 1 && P != 0) {
         const T* tmp = rowA;
         rowA = rowB;
         rowB = tmp;
@@ -347,9 +351,9 @@ __global__ void __launch_bounds__(Row2Geom<T, M, MODE>::CTA, Row2Geom<T, M, MODE
         for (int u = 0; u < 2; ++u) {
           const int nn = u ? M - kk : kk;
           const bool z = nn == 0;
-          const int pd = a.mode == 2 ? n2 - nn : nn;
-          const int pr = a.mode == 2 ? nn : n2 - nn;
-          const bool zd = a.mode == 2 && z;
+          const int pd = imode == 2 ? n2 - nn : nn;
+          const int pr = imode == 2 ? nn : n2 - nn;
+          const bool zd = imode == 2 && z;
           o[4 * u + 0] = zd ? T(0) : rowA[pd & (n2 - 1)];
           o[4 * u + 1] = z ? T(0) : rowA[pr & (n2 - 1)];
           o[4 * u + 2] = zd ? T(0) : rowB[pd & (n2 - 1)];
@@ -386,7 +390,7 @@ __global__ void __launch_bounds__(Row2Geom<T, M, MODE>::CTA, Row2Geom<T, M, MODE
         if (P == 0) {
           // rows 0 and N1/2, each its own mirror: row 0 pairs with the zero
           // row N1; mode 1 zeroes row 0 entirely
-          const T pa = a.mode == 1 ? T(0) : o[0], sa = a.mode == 1 ? T(0) : o[1];
+          const T pa = imode == 1 ? T(0) : o[0], sa = imode == 1 ? T(0) : o[1];
           x0 = cmul(c0, mk(pa, -sa));
           x1 = cmul(c1, mk(o[2] - o[3], -(o[2] + o[3])));
           return;

@@ -108,6 +108,13 @@ __device__ __forceinline__ cx_t<T> rowp_sw(int r) {
   return mk(static_cast<T>(c[r][0]), static_cast<T>(c[r][1]));
 }
 
+// force-field weighting inside the inverse preprocess reads (1) or as a
+// separate pass over the landed rows (0, A/B)
+#ifndef SDCT_ROWP_WPRE
+#define SDCT_ROWP_WPRE 1
+#endif
+constexpr bool kWeightInPre = SDCT_ROWP_WPRE != 0;
+
 template <typename T, int M, bool INV>
 __global__ void __launch_bounds__(RowpGeom<T, M>::CTA, RowpGeom<T, M>::MINB)
     rowp_kernel(RowArgs a, TwSet tw, int nitems) {
@@ -136,7 +143,9 @@ __global__ void __launch_bounds__(RowpGeom<T, M>::CTA, RowpGeom<T, M>::MINB)
       bulk_load(dst, src + static_cast<long long>(__ldg(a.s0 + q1)) * M, G::BUF / 2, full + b);
       bulk_load(dst + G::BUF / 2, src + static_cast<long long>(__ldg(a.s0 + m1)) * M, G::BUF / 2, full + b);
     } else {
-      const T* src = static_cast<const T*>(a.src) + batch * a.src_batch;
+      int img, md_, wt_;
+      inv_item(a, batch, img, md_, wt_);
+      const T* src = static_cast<const T*>(a.src) + img * a.src_batch;
       bulk_load(dst, src + static_cast<long long>(q1) * n2, G::BUF / 2, full + b);
       bulk_load(dst + G::BUF / 2, src + static_cast<long long>(m1) * n2, G::BUF / 2, full + b);
     }
@@ -185,6 +194,8 @@ __global__ void __launch_bounds__(RowpGeom<T, M>::CTA, RowpGeom<T, M>::MINB)
     const int P = it & (half - 1), batch = it >> lgh;
     const int q1 = P, m1 = P == 0 ? half : n1 - P;
     V v[16];
+    int img_, imode, iweight;  // inverse: source item, composite mode, weighting (paired launches)
+    inv_item(a, batch, img_, imode, iweight);
 
     if constexpr (!INV) {
       // ===== forward: DIF stages 0, 1 (tile mapping), stage 2 paired =======
@@ -295,7 +306,7 @@ __global__ void __launch_bounds__(RowpGeom<T, M>::CTA, RowpGeom<T, M>::MINB)
       mbar_wait(full + b, ph);
       const T* rowA = reinterpret_cast<const T*>(sm);
       const T* rowB = reinterpret_cast<const T*>(sm) + 2 * M;
-      if (a.weight == 3) {
+      if (iweight == 3) {
         // compression threshold folded into this load (compress.cpp:33-45)
         T* const rws[2] = {const_cast<T*>(rowA), const_cast<T*>(rowB)};
         const T eps = static_cast<T>(a.thr_eps), sc = static_cast<T>(a.thr_scale);
@@ -311,7 +322,7 @@ __global__ void __launch_bounds__(RowpGeom<T, M>::CTA, RowpGeom<T, M>::MINB)
         for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
         if ((threadIdx.x & 31) == 0 && cnt && a.thr_count) atomicAdd(a.thr_count, static_cast<unsigned long long>(cnt));
         TL::sync();
-      } else if (a.weight) {
+      } else if (iweight && !kWeightInPre) {
         // DREAMPlace field weighting folded into this load (force.cpp:19-31)
         T* const rws[2] = {const_cast<T*>(rowA), const_cast<T*>(rowB)};
         const T pi = T(3.14159265358979323846);
@@ -321,15 +332,39 @@ __global__ void __launch_bounds__(RowpGeom<T, M>::CTA, RowpGeom<T, M>::MINB)
           T* rw = rws[e >= n2] + k2;
           const T w1 = e < n2 ? w1a : w1b, w2 = sc2 * T(k2);
           const T den = fma(w1, w1, w2 * w2);
-          *rw = den > T(0) ? *rw * (a.weight == 1 ? w1 : w2) / den : T(0);
+          *rw = den > T(0) ? *rw * (iweight == 1 ? w1 : w2) / den : T(0);
         }
         TL::sync();
       }
-      if (a.mode == 1 && P != 0) {  // IDXST along axis 0 swaps the rows' roles
+      const bool swp = imode == 1 && P != 0;
+      if (swp) {  // IDXST along axis 0 swaps the rows' roles
         const T* tmp = rowA;
         rowA = rowB;
         rowB = tmp;
       }
+      // field weighting (force.cpp:19-31) applied to the four values each
+      // xpair reads: x(k1, k2) *= w_j / (w1^2 + w2^2), w1 = pi k1/N1,
+      // w2 = pi k2/N2; the four denominators share one division (batched
+      // reciprocal). den = 0 only at (0, 0), where the numerator is 0 too.
+      const T pi_ = T(3.14159265358979323846);
+      const T wA = pi_ * T(swp ? m1 : q1) / T(n1), wB = pi_ * T(swp ? q1 : m1) / T(n1);
+      const T wA2 = wA * wA, wB2 = wB * wB, sc2 = pi_ / T(n2);
+      auto weigh = [&](int pd, int pr, T& DA, T& RA, T& DB, T& RB) {
+        const T wd = sc2 * T(pd), wr = sc2 * T(pr);
+        T dAd = fma(wd, wd, wA2), dAr = fma(wr, wr, wA2), dBd = fma(wd, wd, wB2), dBr = fma(wr, wr, wB2);
+        dAd = dAd > T(0) ? dAd : T(1);
+        dBd = dBd > T(0) ? dBd : T(1);
+        dAr = dAr > T(0) ? dAr : T(1);
+        dBr = dBr > T(0) ? dBr : T(1);
+        const T pA = dAd * dAr, pB = dBd * dBr;
+        const T inv = T(1) / (pA * pB);
+        const T iA = inv * pB, iB = inv * pA;
+        const bool w1 = iweight == 1;
+        DA *= (w1 ? wA : wd) * (iA * dAr);
+        RA *= (w1 ? wA : wr) * (iA * dAd);
+        DB *= (w1 ? wB : wd) * (iB * dBr);
+        RB *= (w1 ? wB : wr) * (iB * dBd);
+      };
 
       // X'(0, nn), X'(1, nn) (proj/src/dct2d.cpp:182-195) from x(nn), x(N2-nn)
       // of both rows (x(N2) := 0); mode 2 reads x(N2-nn) for D and x(nn) for R
@@ -340,11 +375,12 @@ __global__ void __launch_bounds__(RowpGeom<T, M>::CTA, RowpGeom<T, M>::MINB)
       auto xpair = [&](int r, V& x0, V& x1) {
         const int nn = k0 + K0 * r;
         const bool z = nn == 0;
-        const int pd = a.mode == 2 ? n2 - nn : nn;
-        const int pr = a.mode == 2 ? nn : n2 - nn;
-        const bool zd = a.mode == 2 && z;
-        const T DA = zd ? T(0) : rowA[pd & (n2 - 1)], RA = z ? T(0) : rowA[pr & (n2 - 1)];
-        const T DB = zd ? T(0) : rowB[pd & (n2 - 1)], RB = z ? T(0) : rowB[pr & (n2 - 1)];
+        const int pd = imode == 2 ? n2 - nn : nn;
+        const int pr = imode == 2 ? nn : n2 - nn;
+        const bool zd = imode == 2 && z;
+        T DA = zd ? T(0) : rowA[pd & (n2 - 1)], RA = z ? T(0) : rowA[pr & (n2 - 1)];
+        T DB = zd ? T(0) : rowB[pd & (n2 - 1)], RB = z ? T(0) : rowB[pr & (n2 - 1)];
+        if (kWeightInPre && (iweight == 1 || iweight == 2)) weigh(pd, pr, DA, RA, DB, RB);
         V c0 = cmulc(cc0, rowp_sb<T>(r)), c1 = cmulc(cc1, rowp_sb<T>(r));
         if (a.badq && a.badq[nn]) {  // corrupt_twiddle_for_testing negated b(nn)
           c0 = mk(-c0.x, -c0.y);
@@ -353,7 +389,7 @@ __global__ void __launch_bounds__(RowpGeom<T, M>::CTA, RowpGeom<T, M>::MINB)
         if (P == 0) {
           // rows 0 and N1/2, each its own mirror: row 0 pairs with the zero
           // row N1; mode 1 zeroes row 0 entirely
-          const T pa = a.mode == 1 ? T(0) : DA, sa = a.mode == 1 ? T(0) : RA;
+          const T pa = imode == 1 ? T(0) : DA, sa = imode == 1 ? T(0) : RA;
           x0 = cmul(c0, mk(pa, -sa));
           x1 = cmul(c1, mk(DB - RB, -(DB + RB)));
           return;

@@ -65,6 +65,10 @@ int cuda_fail(cudaError_t e, const char* what) {
               std::string(what) + ": " + cudaGetErrorString(e));
 }
 
+bool getenv_flag(const char* name) {  // developer A/B switches (tools/)
+  const char* f = getenv(name);
+  return f && atoi(f) == 1;
+}
 bool is_pow2(long long n) { return n > 0 && (n & (n - 1)) == 0; }
 int ilog2i(long long n) {
   int l = 0;
@@ -173,6 +177,7 @@ struct sdct_plan_s {
   void* h_stage[2] = {nullptr, nullptr};
   cudaEvent_t stage_ev[2] = {nullptr, nullptr};
   void* aux = nullptr;  // sdct_force_fields scratch (coefficients + weighted copy), lazily allocated
+  int aux_n = 2;        // aux halves: 3 on fast single-image plans (two paired intermediates)
   // force fields: side stream for the second composite and its fork / join events
   cudaStream_t side_st = nullptr;
   cudaEvent_t side_fork = nullptr, side_join = nullptr;
@@ -699,6 +704,16 @@ struct Threshold {
   unsigned long long* count = nullptr;
 };
 
+// Paired inverse launch (sdct_force_fields): both field composites of one
+// image as batch items 0 and 1 of a single row launch and a single column
+// launch. Item 1 takes mode2 / weight2 / the *2 signs; both read the same
+// coefficients; the intermediates and outputs sit at byte strides of their own.
+struct PairSpec {
+  int mode1, weight1, mode2, weight2;
+  long long ws_stride;   // bytes between the two intermediates
+  long long out_stride;  // bytes between the two outputs (out = the first)
+};
+
 // Geometry of one side (input or output) of a column pass, in reals.
 struct Side {
   long long inner, rows, row_stride, planes, plane_stride, batch_stride;
@@ -706,11 +721,12 @@ struct Side {
 
 template <typename T>
 int run_fast(sdct_plan_s* p, int kind, int only_stage, const void* in, void* out, void* ws,
-             cudaStream_t st, int* nstages, int weight, const Threshold* thr, int bcount) {
+             cudaStream_t st, int* nstages, int weight, const Threshold* thr, int bcount,
+             const PairSpec* pair = nullptr) {
   const int n1 = p->n[0], n2 = p->n[1], n3 = p->n[2];
   const int M = p->M;
   const long long item = p->numel;
-  const int B = bcount;  // items of this launch set (<= 65535, see run())
+  const int B = pair ? 2 : bcount;  // items of this launch set (<= 65535, see run())
   int stage = 0;
   cudaError_t e = cudaSuccess;
   auto want = [&](void) { return only_stage < 0 || only_stage == stage; };
@@ -839,30 +855,44 @@ int run_fast(sdct_plan_s* p, int kind, int only_stage, const void* in, void* out
       ra.dst_batch = item;
       row(RK_FWD2, n1 / 2, ra);
     } else {
-      const int mode = kind == SDCT_IDXST_IDCT_2D ? 1 : kind == SDCT_IDCT_IDXST_2D ? 2 : 0;
+      const int mode = pair ? pair->mode1 : kind == SDCT_IDXST_IDCT_2D ? 1 : kind == SDCT_IDCT_IDXST_2D ? 2 : 0;
+      // batch strides (complex elements of the intermediate, reals of y)
+      const long long wsb = pair ? pair->ws_stride / (2 * es) : inter;
+      const long long outb = pair ? pair->out_stride / es : item;
       ra.src = in;
       ra.src_batch = item;
       ra.dst = ws;
-      ra.dst_batch = inter;
+      ra.dst_batch = wsb;
       ra.mode = mode;
+      if (pair) {
+        ra.weight = pair->weight1;
+        ra.pair_b = 1;
+        ra.mode2 = pair->mode2;
+        ra.weight2 = pair->weight2;
+      }
       row(RK_INV2, n1 / 2, ra);
       ColArgs c{};
       c.src = ws;
       c.dst = out;
       c.in_row = M;
-      c.in_batch = inter;
+      c.in_batch = wsb;
       c.out_row = n2;
-      c.out_batch = item;
+      c.out_batch = outb;
       c.scale = 0.25;
       c.sign_row = mode == 1;
       c.sign_col = mode == 2;
+      if (pair) {
+        c.pair_b = 1;
+        c.sign_row2 = pair->mode2 == 1;
+        c.sign_col2 = pair->mode2 == 2;
+      }
       if (p->col2)
-        col2(true, c, Side{2LL * M, n1, 2LL * M, 1, 2 * inter, 2 * inter}, Side{n2, n1, n2, 1, item, item});
+        col2(true, c, Side{2LL * M, n1, 2LL * M, 1, 2 * wsb, 2 * wsb}, Side{n2, n1, n2, 1, outb, outb});
       else if (p->colc)
-        colc(true, c, Side{2LL * M, n1, 2LL * M, 1, 2 * inter, 2 * inter}, Side{n2, n1, n2, 1, item, item});
+        colc(true, c, Side{2LL * M, n1, 2LL * M, 1, 2 * wsb, 2 * wsb}, Side{n2, n1, n2, 1, outb, outb});
       else
-        col(CV_INV_DST, n1, p->nl[0], 1, c, p->tw_col[0], Side{2LL * M, n1, 2LL * M, 1, 2 * inter, 2 * inter},
-            Side{n2, n1, n2, 1, item, item});
+        col(CV_INV_DST, n1, p->nl[0], 1, c, p->tw_col[0], Side{2LL * M, n1, 2LL * M, 1, 2 * wsb, 2 * wsb},
+            Side{n2, n1, n2, 1, outb, outb});
     }
   } else {
     const long long inter = static_cast<long long>(n1) * n2 * M;
@@ -1332,7 +1362,7 @@ int sdct_plan_device_bytes(sdct_plan_t p, size_t* bytes) {
   if (!p || !bytes) return fail(SDCT_ERR_ARG, "null argument");
   std::lock_guard<std::mutex> lock(p->mu);
   const size_t item = static_cast<size_t>(p->batch) * p->item_bytes();
-  size_t b = p->table_bytes + (p->ws ? p->ws_bytes : 0) + (p->d_in ? 2 * item : 0) + (p->aux ? 2 * p->aux_half() : 0) +
+  size_t b = p->table_bytes + (p->ws ? p->ws_bytes : 0) + (p->d_in ? 2 * item : 0) + (p->aux ? p->aux_n * p->aux_half() : 0) +
              (p->badq ? static_cast<size_t>(p->n[p->rank >= 2 ? 1 : 0]) : 0) + (p->rws ? p->generic_ws_bytes() : 0);
   if (p->lane_st[0]) b += sdct_plan_s::kLanes * (2 * item + p->ws_bytes);
   *bytes = b;
@@ -1403,10 +1433,18 @@ int sdct_force_fields(sdct_plan_t p, const void* d_density, void* d_xi1, void* d
   DeviceGuard g(p->device);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const size_t bytes = static_cast<size_t>(p->batch) * p->item_bytes();
+  // fast single-image plans with the plain column pass: both composites as
+  // the two batch items of one paired row launch and one paired column launch
+  // (their intermediates in aux halves 1 and 2, the outputs at their own stride)
+  const long long ostride = static_cast<const unsigned char*>(d_xi2) - static_cast<const unsigned char*>(d_xi1);
+  const bool paired = p->fast && p->batch == 1 && !p->col2 && !p->colc && !getenv_flag("SDCT_FORCE_UNPAIRED") &&
+                      ((reinterpret_cast<uintptr_t>(d_xi1) | reinterpret_cast<uintptr_t>(d_xi2)) & 15u) == 0 &&
+                      (ostride < 0 ? -ostride : ostride) < (1LL << 39);
   {
     std::lock_guard<std::mutex> lock(p->mu);
     if (!p->aux) {
-      cudaError_t e = cudaMalloc(&p->aux, 2 * p->aux_half());
+      p->aux_n = p->fast && p->batch == 1 ? 3 : 2;
+      cudaError_t e = cudaMalloc(&p->aux, p->aux_n * p->aux_half());
       if (e != cudaSuccess) return cuda_fail(e, "allocating force-field scratch");
     }
     if (p->fast && !p->side_st) {
@@ -1420,6 +1458,23 @@ int sdct_force_fields(sdct_plan_t p, const void* d_density, void* d_xi1, void* d
   void* aw = static_cast<unsigned char*>(p->aux) + p->aux_half();  // generic path: weighted copy
   int rc = dispatch(p, SDCT_DCT_2D, -1, d_density, a, d_ws, st, nullptr);
   if (rc != SDCT_OK) return rc;
+  if (paired && p->aux_n == 3) {
+    // item 0 = the field at the lower address (TMA batch strides are unsigned)
+    const bool first1 = ostride >= 0;
+    PairSpec ps{};
+    ps.mode1 = first1 ? 2 : 1;  // xi1 = idct_idxst (mode 2, weight 1), xi2 = idxst_idct (mode 1, weight 2)
+    ps.weight1 = first1 ? 1 : 2;
+    ps.mode2 = first1 ? 1 : 2;
+    ps.weight2 = first1 ? 2 : 1;
+    ps.ws_stride = static_cast<long long>(p->aux_half());
+    ps.out_stride = first1 ? ostride : -ostride;
+    void* lo = first1 ? d_xi1 : d_xi2;
+    DeviceGuard g2(p->device);
+    NvtxRange nv("force_pair");
+    return p->dtype == SDCT_F32
+               ? run_fast<float>(p, SDCT_IDCT_IDXST_2D, -1, a, lo, aw, st, nullptr, 0, nullptr, 1, &ps)
+               : run_fast<double>(p, SDCT_IDCT_IDXST_2D, -1, a, lo, aw, st, nullptr, 0, nullptr, 1, &ps);
+  }
   if (p->fast) {
     // fast path: the weighting rides on the inverse row kernels' loads. The
     // two composites only share the coefficients, so the second runs on the
@@ -1458,7 +1513,8 @@ int sdct_compress(sdct_plan_t p, const void* d_in, void* d_out, double epsilon, 
   {
     std::lock_guard<std::mutex> lock(p->mu);
     if (!p->aux) {
-      cudaError_t e = cudaMalloc(&p->aux, 2 * p->aux_half());
+      p->aux_n = p->fast && p->batch == 1 ? 3 : 2;
+      cudaError_t e = cudaMalloc(&p->aux, p->aux_n * p->aux_half());
       if (e != cudaSuccess) return cuda_fail(e, "allocating coefficient scratch");
     }
   }

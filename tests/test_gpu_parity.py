@@ -597,6 +597,40 @@ def test_force_fields_vs_oracle(cuda, dtype):
 
 
 @pytest.mark.parametrize("dtype", ["float64", "float32"])
+def test_force_fields_paired_launch(cuda, dtype, monkeypatch):
+    # single-image fast plans run both field composites as the two batch items
+    # of one row launch and one column launch; the outputs may sit in either
+    # address order (TMA batch strides are unsigned) and must match the
+    # unpaired launches bit for bit and the oracle
+    torch = _torch()
+    import paper_2110_01172_b200 as sd
+
+    tdt = torch.float64 if dtype == "float64" else torch.float32
+    for i, shape in enumerate([(64, 128), (512, 256), (1024, 1024)]):
+        x = rnd(shape, 700 + i, dtype)
+        xd = torch.tensor(x, dtype=tdt, device="cuda")
+        plan = sd.plan_for(shape, 1, dtype, 0)
+        ws = torch.empty(plan.workspace_bytes, dtype=torch.uint8, device="cuda")
+        s = torch.cuda.current_stream().cuda_stream
+        w1, w2 = oracle.port.force_demo_fields(x)
+        got = {}
+        for order in ("lo_hi", "hi_lo", "unpaired"):
+            buf = torch.full((3,) + shape, float("nan"), dtype=tdt, device="cuda")
+            o1, o2 = (buf[0], buf[2]) if order != "hi_lo" else (buf[2], buf[0])
+            if order == "unpaired":
+                monkeypatch.setenv("SDCT_FORCE_UNPAIRED", "1")
+            plan.force_fields(xd.data_ptr(), o1.data_ptr(), o2.data_ptr(), s, ws.data_ptr())
+            torch.cuda.synchronize()
+            monkeypatch.delenv("SDCT_FORCE_UNPAIRED", raising=False)
+            assert torch.isnan(buf[1]).all(), (shape, order)  # nothing written between the outputs
+            got[order] = (o1.clone(), o2.clone())
+            assert oracle.rel_l2(o1.double().cpu().numpy(), w1) <= TOL[dtype], (shape, order)
+            assert oracle.rel_l2(o2.double().cpu().numpy(), w2) <= TOL[dtype], (shape, order)
+        for order in ("lo_hi", "hi_lo"):
+            assert torch.equal(got[order][0], got["unpaired"][0]) and torch.equal(got[order][1], got["unpaired"][1])
+
+
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
 def test_cluster_split_8192_round_trip(cuda, dtype):
     # n1 = 8192 columns run as cluster-split halves (kernels_col2.cuh): round
     # trip at full size, plus an oracle spot check of one forward transform
