@@ -550,10 +550,11 @@ constexpr bool col_xs() {
 //   inverse (DIT): input rows in sigma order; output natural rows (ST_INTER)
 //                  or the final gather to y (ST_DST: rows pe(i), 1/4 or 1/8,
 //                  signs), stored as even / odd y-row classes.
+// The body takes the CTA's rank and the CTA count so that a fused kernel
+// (kernels_fused.cuh) can run it as its first phase.
 template <typename T, int L, int NL, bool INV, int LOAD, int STORE>
-__global__ void __launch_bounds__(Tile<T, L, NL, true>::NT)
-    col_kernel(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUtensorMap tout, ColArgs a,
-               TwSet tw) {
+__device__ __forceinline__ void col_body(const CUtensorMap& tin, const CUtensorMap& tout, const ColArgs& a,
+                                         const TwSet& tw, const int cta, const int ncta) {
   using TL = Tile<T, L, NL, true>;
   using P = typename TL::P;
   using V = cx_t<T>;
@@ -620,10 +621,10 @@ __global__ void __launch_bounds__(Tile<T, L, NL, true>::NT)
   __syncthreads();
   pdl_trigger();
   pdl_wait();  // the previous kernel's output is complete before the first load
-  if (t == 0 && static_cast<int>(blockIdx.x) < a.ntiles) issue(blockIdx.x);
+  if (t == 0 && static_cast<int>(cta) < a.ntiles) issue(cta);
 
   uint32_t phase = 0;
-  for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
+  for (int tile = cta; tile < a.ntiles; tile += ncta) {
     int band, plane, batch;
     coords(tile, band, plane, batch);
     V v[TL::E];
@@ -674,9 +675,9 @@ __global__ void __launch_bounds__(Tile<T, L, NL, true>::NT)
         // streams in under this tile's whole FFT; the exchanges run through
         // the half-tile staging buffer X in balanced rounds
         if (a.trace && t == 0) tr2 = gtimer();
-        if (t == 0 && tile + static_cast<int>(gridDim.x) < a.ntiles) {
+        if (t == 0 && tile + static_cast<int>(ncta) < a.ntiles) {
           fence_async_smem();
-          issue(tile + gridDim.x);
+          issue(tile + ncta);
         }
         V* X = reinterpret_cast<V*>(stg);
         StageTw<TL, 1> w1;
@@ -705,9 +706,9 @@ __global__ void __launch_bounds__(Tile<T, L, NL, true>::NT)
         }
         __syncthreads();  // last-stage operands are in registers: smem is free
         if (a.trace && t == 0) tr2 = gtimer();
-        if (t == 0 && tile + static_cast<int>(gridDim.x) < a.ntiles) {
+        if (t == 0 && tile + static_cast<int>(ncta) < a.ntiles) {
           fence_async_smem();
-          issue(tile + gridDim.x);
+          issue(tile + ncta);
         }
         stage_compute<TL, SL, false>(v, wl);
       }
@@ -763,9 +764,9 @@ __global__ void __launch_bounds__(Tile<T, L, NL, true>::NT)
       if constexpr (col_xs<TL, true>()) {
         // early reissue (see the forward): exchanges through X in rounds
         if (a.trace && t == 0) tr2 = gtimer();
-        if (t == 0 && tile + static_cast<int>(gridDim.x) < a.ntiles) {
+        if (t == 0 && tile + static_cast<int>(ncta) < a.ntiles) {
           fence_async_smem();
-          issue(tile + gridDim.x);
+          issue(tile + ncta);
         }
         V* X = reinterpret_cast<V*>(stg);
         StageTw<TL, 1> w1;
@@ -789,9 +790,9 @@ __global__ void __launch_bounds__(Tile<T, L, NL, true>::NT)
         }
         __syncthreads();  // all smem reads done
         if (a.trace && t == 0) tr2 = gtimer();
-        if (t == 0 && tile + static_cast<int>(gridDim.x) < a.ntiles) {
+        if (t == 0 && tile + static_cast<int>(ncta) < a.ntiles) {
           fence_async_smem();
-          issue(tile + gridDim.x);
+          issue(tile + ncta);
         }
       }
       // outputs: stage-0 butterfly (line, j) holds natural index ii = j + r*Q0
@@ -887,10 +888,17 @@ __global__ void __launch_bounds__(Tile<T, L, NL, true>::NT)
       o[4] = tr4;
       o[5] = tr5;
       o[6] = gtimer();
-      o[7] = blockIdx.x;
+      o[7] = cta;
     }
   }
   if (t == 0) bulk_wait_all();  // stores complete before the CTA retires
+}
+
+template <typename T, int L, int NL, bool INV, int LOAD, int STORE>
+__global__ void __launch_bounds__(Tile<T, L, NL, true>::NT)
+    col_kernel(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUtensorMap tout, ColArgs a,
+               TwSet tw) {
+  col_body<T, L, NL, INV, LOAD, STORE>(tin, tout, a, tw, static_cast<int>(blockIdx.x), static_cast<int>(gridDim.x));
 }
 
 // ============================================================================

@@ -116,8 +116,8 @@ __device__ __forceinline__ cx_t<T> rowp_sw(int r) {
 constexpr bool kWeightInPre = SDCT_ROWP_WPRE != 0;
 
 template <typename T, int M, bool INV>
-__global__ void __launch_bounds__(RowpGeom<T, M>::CTA, RowpGeom<T, M>::MINB)
-    rowp_kernel(RowArgs a, TwSet tw, int nitems) {
+__device__ __forceinline__ void rowp_body(const RowArgs& a, const TwSet& tw, const int nitems, const int cta,
+                                          const int ncta) {
   static_assert(rowp_ok<T, M, INV>(), "mirror-paired row kernel: M = 512 (forward), 1024, 2048 only");
   using G = RowpGeom<T, M>;
   using TL = typename G::TL;
@@ -164,7 +164,7 @@ __global__ void __launch_bounds__(RowpGeom<T, M>::CTA, RowpGeom<T, M>::MINB)
   if (threadIdx.x == 0) {
 #pragma unroll 1
     for (int b = 0; b < NBUF; ++b) {
-      const int it = blockIdx.x + b * gridDim.x;
+      const int it = cta + b * ncta;
       if (it < nitems) issue(it, b);
     }
   }
@@ -185,7 +185,7 @@ __global__ void __launch_bounds__(RowpGeom<T, M>::CTA, RowpGeom<T, M>::MINB)
 
 #pragma unroll 1
   for (int k = grp;; k += GROUPS) {
-    const int it = static_cast<int>(blockIdx.x) + k * static_cast<int>(gridDim.x);
+    const int it = static_cast<int>(cta) + k * static_cast<int>(ncta);
     if (it >= nitems) break;
     const int b = k % NBUF;
     const uint32_t ph = static_cast<uint32_t>(k / NBUF) & 1u;
@@ -488,13 +488,19 @@ __global__ void __launch_bounds__(RowpGeom<T, M>::CTA, RowpGeom<T, M>::MINB)
     TL::sync();  // every read of buffer b by this group is done
     if (t == 0) {
       mbar_arrive(empty + b);
-      const int nxt0 = it + NBUF * static_cast<int>(gridDim.x);
+      const int nxt0 = it + NBUF * static_cast<int>(ncta);
       if (nxt0 < nitems) {
         fence_async_smem();  // generic-proxy smem accesses before the async refill
         issue(nxt0, b);
       }
     }
   }
+}
+
+template <typename T, int M, bool INV>
+__global__ void __launch_bounds__(RowpGeom<T, M>::CTA, RowpGeom<T, M>::MINB)
+    rowp_kernel(RowArgs a, TwSet tw, int nitems) {
+  rowp_body<T, M, INV>(a, tw, nitems, static_cast<int>(blockIdx.x), static_cast<int>(gridDim.x));
 }
 
 }  // namespace sdctb

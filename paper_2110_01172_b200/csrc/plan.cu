@@ -842,6 +842,10 @@ int run_fast(sdct_plan_s* p, int kind, int only_stage, const void* in, void* out
       c.in_batch = item;
       c.out_row = M;
       c.out_batch = inter;
+      ra.src = ws;
+      ra.src_batch = inter;
+      ra.dst = out;
+      ra.dst_batch = item;
       if (p->col2)
         col2(false, c, Side{n2, n1, n2, 1, item, item}, Side{2LL * M, n1, 2LL * M, 1, 2 * inter, 2 * inter});
       else if (p->colc)
