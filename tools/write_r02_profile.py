@@ -20,7 +20,7 @@ txt += f"""
 ## Round 2: live per-kernel roofline (bench.py c2, `profiles/r02/bench_c2.json`)
 
 Algorithmic bytes per launch = 2 * 4096^2 * 8 = 268,435,456 B; peak = MEASURED_PEAKS.json
-hbm_gbs = {peak} GB/s. Live times: the timed loop with an event between kernels.
+hbm_gbs = {peak} GB/s. Live times: per-kernel CUDA graphs (50 back-to-back launches of each kernel on the timed loop's rotating buffers, events around the replay).
 
 | kernel | r01 us | r02 us | GB/s | frac |
 |---|---|---|---|---|
