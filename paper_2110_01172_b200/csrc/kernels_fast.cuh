@@ -1336,7 +1336,12 @@ __global__ void __launch_bounds__(row_threads<T, M, KIND>())
     const int n3 = a.n3;
     const V* tu = static_cast<const V*>(a.tu);
     const V ab = cmul(av3, bv3), cb = cmulc(bv3, av3);  // a b, conj(a) b
-    auto put = [&](int i, int j, int k, T val) { y[(static_cast<long long>(i) * n2 + j) * n3 + k] = val; };
+    // the four output rows (k1, k2) of this group: base pointers once per CTA
+    T* const yqq = y + (static_cast<long long>(q1) * n2 + q2) * n3;
+    T* const yqm = y + (static_cast<long long>(q1) * n2 + m2) * n3;
+    T* const ymq = y + (static_cast<long long>(m1) * n2 + q2) * n3;
+    T* const ymm = y + (static_cast<long long>(m1) * n2 + m2) * n3;
+
     auto item = [&](int k3, const V* Za, const V* Zb) {
       // Za[l] = Z(line l, k3), Zb[l] = Z(line l, -k3)
       const V w = __ldg(tu + k3);
@@ -1349,36 +1354,41 @@ __global__ void __launch_bounds__(row_threads<T, M, KIND>())
       const V f2 = deg1 ? f1 : X[1];
       const V f3 = deg2 ? f1 : X[2];
       const V f4 = deg1 ? f3 : (deg2 ? f2 : X[3]);
-      const V c = __ldg(static_cast<const V*>(a.tc) + k3);
+      V c = __ldg(static_cast<const V*>(a.tc) + k3);  // times the 1/4 of the outputs
+      c = mk(T(0.25) * c.x, T(0.25) * c.y);
       const V t1 = cmul(ab, f1), t2 = cmul(cb, f2), t3 = cmul(cconj(cb), f3), t4 = cmul(cconj(ab), f4);
       const V s12 = cadd(t1, t2), s34 = cadd(t3, t4);
       const V u00 = cmul(c, cadd(s12, s34));
-      put(q1, q2, k3, T(0.25) * u00.x);
-      if (!deg3) put(q1, q2, m3, T(-0.25) * u00.y);
+      yqq[k3] = u00.x;
+      if (!deg3) yqq[m3] = -u00.y;
       if (!deg2) {
         const V u01 = cmul(c, csub(s12, s34));
-        put(q1, m2, k3, T(-0.25) * u01.y);
-        if (!deg3) put(q1, m2, m3, T(-0.25) * u01.x);
+        yqm[k3] = -u01.y;
+        if (!deg3) yqm[m3] = -u01.x;
       }
       if (!deg1) {
         const V d12 = csub(t1, t2), d34 = csub(t3, t4);
         const V u10 = cmul(c, cadd(d12, d34));
-        put(m1, q2, k3, T(-0.25) * u10.y);
-        if (!deg3) put(m1, q2, m3, T(-0.25) * u10.x);
+        ymq[k3] = -u10.y;
+        if (!deg3) ymq[m3] = -u10.x;
         if (!deg2) {
           const V u11 = cmul(c, csub(d12, d34));
-          put(m1, m2, k3, T(-0.25) * u11.x);
-          if (!deg3) put(m1, m2, m3, T(0.25) * u11.y);
+          ymm[k3] = -u11.x;
+          if (!deg3) ymm[m3] = u11.y;
         }
       }
     };
     for (int k3 = t; k3 <= M / 2; k3 += NT) {
       const int kb = (M - k3) & (M - 1);
+      // row_nat(l, k) = f(l M) ^ f(k): the swizzle is GF(2)-linear and l M, k
+      // have disjoint bits, so f(l M) is a compile-time constant
+      const int fk = SwzRow<T>::f(k3), fb = SwzRow<T>::f(kb);  // k3 <= M/2 < M
       V Za[4], Zb[4];
 #pragma unroll
       for (int l = 0; l < 4; ++l) {
-        Za[l] = sm[row_nat<T, M>(l, k3)];
-        Zb[l] = sm[row_nat<T, M>(l, kb)];
+        const int fl = SwzRow<T>::fc(l * M);
+        Za[l] = sm[fl ^ fk];
+        Zb[l] = sm[fl ^ fb];
       }
       item(k3, Za, Zb);
       if (2 * k3 != M) item(M - k3, Zb, Za);
