@@ -137,6 +137,15 @@ int sdct_exec_host(sdct_plan_t plan, int kind, const void* h_in, void* h_out, vo
  * concurrent calls on one plan must be ordered by the caller (one stream). */
 int sdct_force_fields(sdct_plan_t plan, const void* d_density, void* d_xi1, void* d_xi2, void* d_workspace,
                       void* stream);
+/* Bytes of the caller-provided coefficient scratch that sdct_force_fields_scratch
+ * and sdct_compress_scratch take (0 for plans of rank != 2). */
+int sdct_scratch_size(sdct_plan_t plan, size_t* bytes);
+/* sdct_force_fields with the coefficient / intermediate scratch in d_scratch
+ * (256-byte aligned, sdct_scratch_size bytes; NULL = the plan-owned buffer):
+ * with a scratch per call, concurrent calls on one plan from different streams
+ * are safe. */
+int sdct_force_fields_scratch(sdct_plan_t plan, const void* d_density, void* d_xi1, void* d_xi2, void* d_workspace,
+                              void* d_scratch, void* stream);
 /* Same on host memory (H2D, the fused device pipeline, D2H, synchronised). */
 int sdct_force_fields_host(sdct_plan_t plan, const void* h_density, void* h_xi1, void* h_xi2, void* stream);
 
@@ -151,6 +160,9 @@ int sdct_force_fields_host(sdct_plan_t plan, const void* h_density, void* h_xi1,
  * concurrent calls on one plan). */
 int sdct_compress(sdct_plan_t plan, const void* d_in, void* d_out, double epsilon, unsigned long long* d_zeroed,
                   void* d_workspace, void* stream);
+/* sdct_compress with a caller-provided scratch (as sdct_force_fields_scratch). */
+int sdct_compress_scratch(sdct_plan_t plan, const void* d_in, void* d_out, double epsilon,
+                          unsigned long long* d_zeroed, void* d_workspace, void* d_scratch, void* stream);
 
 /* Host streaming: `count` independent items (each one plan-sized batch) go
  * host -> device -> kinds[0] -> ... -> kinds[nkinds-1] -> host. Item i's input

@@ -221,7 +221,11 @@ def force_demo_fields(density, threads: int = 0):
     with torch.cuda.device(dev):
         stream = torch.cuda.current_stream(dev)
         ws = torch.empty(plan.workspace_bytes, dtype=torch.uint8, device=x.device)
-        plan.force_fields(x.data_ptr(), xi1.data_ptr(), xi2.data_ptr(), stream.cuda_stream, ws.data_ptr())
+        # per-call coefficient scratch from the caching allocator: concurrent
+        # calls on the shared cached plan from other streams stay independent
+        scratch = torch.empty(plan.scratch_bytes, dtype=torch.uint8, device=x.device)
+        plan.force_fields(x.data_ptr(), xi1.data_ptr(), xi2.data_ptr(), stream.cuda_stream, ws.data_ptr(),
+                          scratch.data_ptr())
     return xi1, xi2
 
 
@@ -317,8 +321,9 @@ def compress(x, epsilon: float):
     with torch.cuda.device(dev):
         stream = torch.cuda.current_stream(dev)
         ws = torch.empty(plan.workspace_bytes, dtype=torch.uint8, device=t.device)
+        scratch = torch.empty(plan.scratch_bytes, dtype=torch.uint8, device=t.device)  # per call (see force)
         plan.compress(t.data_ptr(), out.data_ptr(), float(epsilon), zeroed.data_ptr(), stream.cuda_stream,
-                      ws.data_ptr())
+                      ws.data_ptr(), scratch.data_ptr())
     total = t.numel()
     nz = int(zeroed.item())
     stats = {"total_coefficients": total, "zeroed_coefficients": nz, "zeroed_fraction": nz / total}

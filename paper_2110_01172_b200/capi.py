@@ -39,6 +39,9 @@ SIGNATURES = [
     ("sdct_force_fields", ctypes.c_int, [_VP, _VP, _VP, _VP, _VP, _VP]),
     ("sdct_force_fields_host", ctypes.c_int, [_VP, _VP, _VP, _VP, _VP]),
     ("sdct_compress", ctypes.c_int, [_VP, _VP, _VP, ctypes.c_double, _VP, _VP, _VP]),
+    ("sdct_scratch_size", ctypes.c_int, [_VP, ctypes.POINTER(ctypes.c_size_t)]),
+    ("sdct_force_fields_scratch", ctypes.c_int, [_VP, _VP, _VP, _VP, _VP, _VP, _VP]),
+    ("sdct_compress_scratch", ctypes.c_int, [_VP, _VP, _VP, ctypes.c_double, _VP, _VP, _VP, _VP]),
     ("sdct_exec_host_pipelined", ctypes.c_int, [_VP, ctypes.POINTER(ctypes.c_int), ctypes.c_int, _VP, ctypes.c_int64,
                                                 _VP, ctypes.c_int64, ctypes.c_int64, _VP]),
     ("sdct_transpose", ctypes.c_int, [ctypes.c_int, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, _VP, _VP, _VP]),

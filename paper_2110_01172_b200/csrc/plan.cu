@@ -1429,7 +1429,42 @@ int sdct_exec(sdct_plan_t p, int kind, const void* d_in, void* d_out, void* d_ws
   return dispatch(p, kind, -1, d_in, d_out, d_ws, static_cast<cudaStream_t>(stream), nullptr);
 }
 
+// Coefficient / intermediate scratch of sdct_force_fields and sdct_compress:
+// aux_count halves of aux_half bytes (three on fast single-image plans: the
+// coefficients and the two paired intermediates). A caller-provided scratch
+// makes concurrent calls on one plan safe; otherwise the plan's own buffer is
+// allocated on first use (and calls on one plan must be ordered).
+static int aux_count(const sdct_plan_s* p) { return p->fast && p->batch == 1 ? 3 : 2; }
+
+static int aux_scratch(sdct_plan_s* p, void* scratch, void** base) {
+  if (scratch) {
+    if ((reinterpret_cast<uintptr_t>(scratch) & 255u) != 0)
+      return fail(SDCT_ERR_ARG, "scratch buffers must be 256-byte aligned");
+    *base = scratch;
+    return SDCT_OK;
+  }
+  std::lock_guard<std::mutex> lock(p->mu);
+  if (!p->aux) {
+    p->aux_n = aux_count(p);
+    cudaError_t e = cudaMalloc(&p->aux, p->aux_n * p->aux_half());
+    if (e != cudaSuccess) return cuda_fail(e, "allocating coefficient scratch");
+  }
+  *base = p->aux;
+  return SDCT_OK;
+}
+
+int sdct_scratch_size(sdct_plan_t p, size_t* bytes) {
+  if (!p || !bytes) return fail(SDCT_ERR_ARG, "null argument to sdct_scratch_size");
+  *bytes = p->rank == 2 ? static_cast<size_t>(aux_count(p)) * p->aux_half() : 0;
+  return SDCT_OK;
+}
+
 int sdct_force_fields(sdct_plan_t p, const void* d_density, void* d_xi1, void* d_xi2, void* d_ws, void* stream) {
+  return sdct_force_fields_scratch(p, d_density, d_xi1, d_xi2, d_ws, nullptr, stream);
+}
+
+int sdct_force_fields_scratch(sdct_plan_t p, const void* d_density, void* d_xi1, void* d_xi2, void* d_ws,
+                              void* d_scratch, void* stream) {
   if (!p || !d_density || !d_xi1 || !d_xi2) return fail(SDCT_ERR_ARG, "null argument to sdct_force_fields");
   if (p->rank != 2) return fail(SDCT_ERR_PLAN, "force fields need a rank-2 plan");
   if (d_density == d_xi1 || d_density == d_xi2 || d_xi1 == d_xi2)
@@ -1444,13 +1479,13 @@ int sdct_force_fields(sdct_plan_t p, const void* d_density, void* d_xi1, void* d
   const bool paired = p->fast && p->batch == 1 && !p->col2 && !p->colc && !getenv_flag("SDCT_FORCE_UNPAIRED") &&
                       ((reinterpret_cast<uintptr_t>(d_xi1) | reinterpret_cast<uintptr_t>(d_xi2)) & 15u) == 0 &&
                       (ostride < 0 ? -ostride : ostride) < (1LL << 39);
+  void* aux = nullptr;
+  {
+    const int rc0 = aux_scratch(p, d_scratch, &aux);
+    if (rc0 != SDCT_OK) return rc0;
+  }
   {
     std::lock_guard<std::mutex> lock(p->mu);
-    if (!p->aux) {
-      p->aux_n = p->fast && p->batch == 1 ? 3 : 2;
-      cudaError_t e = cudaMalloc(&p->aux, p->aux_n * p->aux_half());
-      if (e != cudaSuccess) return cuda_fail(e, "allocating force-field scratch");
-    }
     if (p->fast && !p->side_st) {
       cudaError_t e = cudaStreamCreateWithFlags(&p->side_st, cudaStreamNonBlocking);
       if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->side_fork, cudaEventDisableTiming);
@@ -1458,11 +1493,11 @@ int sdct_force_fields(sdct_plan_t p, const void* d_density, void* d_xi1, void* d
       if (e != cudaSuccess) return cuda_fail(e, "creating force-field side stream");
     }
   }
-  void* a = p->aux;                                     // DCT coefficients of the density
-  void* aw = static_cast<unsigned char*>(p->aux) + p->aux_half();  // generic path: weighted copy
+  void* a = aux;                                              // DCT coefficients of the density
+  void* aw = static_cast<unsigned char*>(aux) + p->aux_half();  // generic path: weighted copy
   int rc = dispatch(p, SDCT_DCT_2D, -1, d_density, a, d_ws, st, nullptr);
   if (rc != SDCT_OK) return rc;
-  if (paired && p->aux_n == 3) {
+  if (paired && aux_count(p) == 3) {
     // item 0 = the field at the lower address (TMA batch strides are unsigned)
     const bool first1 = ostride >= 0;
     PairSpec ps{};
@@ -1507,6 +1542,11 @@ int sdct_force_fields(sdct_plan_t p, const void* d_density, void* d_xi1, void* d
 
 int sdct_compress(sdct_plan_t p, const void* d_in, void* d_out, double epsilon, unsigned long long* d_zeroed,
                   void* d_ws, void* stream) {
+  return sdct_compress_scratch(p, d_in, d_out, epsilon, d_zeroed, d_ws, nullptr, stream);
+}
+
+int sdct_compress_scratch(sdct_plan_t p, const void* d_in, void* d_out, double epsilon, unsigned long long* d_zeroed,
+                          void* d_ws, void* d_scratch, void* stream) {
   if (!p || !d_in || !d_out) return fail(SDCT_ERR_ARG, "null argument to sdct_compress");
   if (p->rank != 2) return fail(SDCT_ERR_PLAN, "compression needs a rank-2 plan");
   if (std::isnan(epsilon) || epsilon < 0.0) return fail(SDCT_ERR_ARG, "compress: epsilon must be >= 0");
@@ -1514,15 +1554,12 @@ int sdct_compress(sdct_plan_t p, const void* d_in, void* d_out, double epsilon, 
   DeviceGuard g(p->device);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const size_t bytes = static_cast<size_t>(p->batch) * p->item_bytes();
+  void* aux = nullptr;
   {
-    std::lock_guard<std::mutex> lock(p->mu);
-    if (!p->aux) {
-      p->aux_n = p->fast && p->batch == 1 ? 3 : 2;
-      cudaError_t e = cudaMalloc(&p->aux, p->aux_n * p->aux_half());
-      if (e != cudaSuccess) return cuda_fail(e, "allocating coefficient scratch");
-    }
+    const int rc0 = aux_scratch(p, d_scratch, &aux);
+    if (rc0 != SDCT_OK) return rc0;
   }
-  void* b = p->aux;
+  void* b = aux;
   int rc = dispatch(p, SDCT_DCT_2D, -1, d_in, b, d_ws, st, nullptr);
   if (rc != SDCT_OK) return rc;
   Threshold thr;
@@ -1530,7 +1567,7 @@ int sdct_compress(sdct_plan_t p, const void* d_in, void* d_out, double epsilon, 
   thr.scale = 4.0 / (static_cast<double>(p->n[0]) * static_cast<double>(p->n[1]));
   thr.count = d_zeroed;
   if (p->fast) return dispatch(p, SDCT_IDCT_2D, -1, b, d_out, d_ws, st, nullptr, 3, &thr);
-  void* bw = static_cast<unsigned char*>(p->aux) + p->aux_half();
+  void* bw = static_cast<unsigned char*>(aux) + p->aux_half();
   cudaError_t e = compress_threshold(b, bw, static_cast<long long>(p->batch) * p->numel, thr.eps, thr.scale, d_zeroed,
                                      p->dtype == SDCT_F32, st);
   if (e != cudaSuccess) return cuda_fail(e, "launching compression threshold");

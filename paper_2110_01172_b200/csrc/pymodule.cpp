@@ -244,24 +244,27 @@ PYBIND11_MODULE(_sdct, m) {
            py::arg("count"), py::arg("stream") = 0)
       .def("force_fields",
            [](const sdct::DevicePlan& p, std::uintptr_t d_density, std::uintptr_t d_xi1, std::uintptr_t d_xi2,
-              std::uintptr_t stream, std::uintptr_t ws) {
+              std::uintptr_t stream, std::uintptr_t ws, std::uintptr_t scratch) {
              py::gil_scoped_release nogil;
-             sdct::detail::check(sdct_force_fields(p.handle(), reinterpret_cast<const void*>(d_density),
-                                                   reinterpret_cast<void*>(d_xi1), reinterpret_cast<void*>(d_xi2),
-                                                   reinterpret_cast<void*>(ws), reinterpret_cast<void*>(stream)));
+             sdct::detail::check(sdct_force_fields_scratch(
+                 p.handle(), reinterpret_cast<const void*>(d_density), reinterpret_cast<void*>(d_xi1),
+                 reinterpret_cast<void*>(d_xi2), reinterpret_cast<void*>(ws), reinterpret_cast<void*>(scratch),
+                 reinterpret_cast<void*>(stream)));
            },
-           py::arg("d_density"), py::arg("d_xi1"), py::arg("d_xi2"), py::arg("stream") = 0, py::arg("workspace") = 0)
+           py::arg("d_density"), py::arg("d_xi1"), py::arg("d_xi2"), py::arg("stream") = 0, py::arg("workspace") = 0,
+           py::arg("scratch") = 0)
       .def("compress",
            [](const sdct::DevicePlan& p, std::uintptr_t d_in, std::uintptr_t d_out, double eps, std::uintptr_t d_zeroed,
-              std::uintptr_t stream, std::uintptr_t ws) {
+              std::uintptr_t stream, std::uintptr_t ws, std::uintptr_t scratch) {
              py::gil_scoped_release nogil;
-             sdct::detail::check(sdct_compress(p.handle(), reinterpret_cast<const void*>(d_in),
-                                               reinterpret_cast<void*>(d_out), eps,
-                                               reinterpret_cast<unsigned long long*>(d_zeroed),
-                                               reinterpret_cast<void*>(ws), reinterpret_cast<void*>(stream)));
+             sdct::detail::check(sdct_compress_scratch(p.handle(), reinterpret_cast<const void*>(d_in),
+                                                       reinterpret_cast<void*>(d_out), eps,
+                                                       reinterpret_cast<unsigned long long*>(d_zeroed),
+                                                       reinterpret_cast<void*>(ws), reinterpret_cast<void*>(scratch),
+                                                       reinterpret_cast<void*>(stream)));
            },
            py::arg("d_in"), py::arg("d_out"), py::arg("epsilon"), py::arg("d_zeroed") = 0, py::arg("stream") = 0,
-           py::arg("workspace") = 0)
+           py::arg("workspace") = 0, py::arg("scratch") = 0)
       .def("stage_count",
            [](const sdct::DevicePlan& p, int kind) {
              int n = 0;
@@ -270,7 +273,12 @@ PYBIND11_MODULE(_sdct, m) {
            })
       .def_property_readonly("workspace_bytes", &sdct::DevicePlan::workspace_bytes)
       .def_property_readonly("device_bytes", &sdct::DevicePlan::device_bytes)
-      .def_property_readonly("fast", &sdct::DevicePlan::fast);
+      .def_property_readonly("fast", &sdct::DevicePlan::fast)
+      .def_property_readonly("scratch_bytes", [](const sdct::DevicePlan& p) {
+        size_t b = 0;
+        sdct::detail::check(sdct_scratch_size(p.handle(), &b));
+        return b;
+      });
 
   m.attr("DCT_2D") = py::int_(static_cast<int>(SDCT_DCT_2D));
   m.attr("IDCT_2D") = py::int_(static_cast<int>(SDCT_IDCT_2D));

@@ -596,6 +596,43 @@ def test_force_fields_vs_oracle(cuda, dtype):
         sd.force_demo_fields(torch.zeros(8, device="cuda", dtype=tdt))
 
 
+def test_force_and_compress_concurrent_streams(cuda):
+    # the torch entry points give every call its own coefficient scratch, so
+    # calls on the one cached plan from two streams in flight at once stay
+    # independent (each compared with the oracle)
+    torch = _torch()
+    import paper_2110_01172_b200 as sd
+
+    shape = (512, 512)
+    xs = [rnd(shape, 1200 + i) for i in range(4)]
+    want = [oracle.port.force_demo_fields(x) for x in xs]
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    xd = [torch.tensor(x, device="cuda") for x in xs]
+    torch.cuda.synchronize()
+    got = []
+    for rep in range(3):
+        for i, x in enumerate(xd):
+            with torch.cuda.stream(s1 if i % 2 == 0 else s2):
+                got.append((i, sd.force_demo_fields(x)))
+    torch.cuda.synchronize()
+    for i, (f1, f2) in got:
+        assert oracle.rel_l2(f1.cpu().numpy(), want[i][0]) <= 1e-12
+        assert oracle.rel_l2(f2.cpu().numpy(), want[i][1]) <= 1e-12
+    # the C ABI with an explicit scratch and the plan-owned buffer agree bit for bit
+    plan = sd.plan_for(shape, 1, "float64", 0)
+    assert plan.scratch_bytes >= 3 * 512 * 512 * 8
+    ws = torch.empty(plan.workspace_bytes, dtype=torch.uint8, device="cuda")
+    sc = torch.empty(plan.scratch_bytes, dtype=torch.uint8, device="cuda")
+    o = [torch.empty(shape, dtype=torch.float64, device="cuda") for _ in range(4)]
+    s = torch.cuda.current_stream().cuda_stream
+    plan.force_fields(xd[0].data_ptr(), o[0].data_ptr(), o[1].data_ptr(), s, ws.data_ptr())
+    plan.force_fields(xd[0].data_ptr(), o[2].data_ptr(), o[3].data_ptr(), s, ws.data_ptr(), sc.data_ptr())
+    torch.cuda.synchronize()
+    assert torch.equal(o[0], o[2]) and torch.equal(o[1], o[3])
+    with pytest.raises(ValueError):  # misaligned scratch
+        plan.force_fields(xd[0].data_ptr(), o[0].data_ptr(), o[1].data_ptr(), s, ws.data_ptr(), sc.data_ptr() + 16)
+
+
 @pytest.mark.parametrize("dtype", ["float64", "float32"])
 def test_force_fields_paired_launch(cuda, dtype, monkeypatch):
     # single-image fast plans run both field composites as the two batch items
