@@ -105,6 +105,10 @@ struct RowArgs {
   // paired inverse launch (force fields: both composites in one launch): batch
   // items b >= pair_b read source item b - pair_b and use mode2 / weight2
   int pair_b, mode2, weight2;
+  // inverse row passes: walk the items last to first (rev = 1), so that a pass
+  // reading the previous row pass's output meets the most recently written
+  // rows, the ones still in L2, first
+  int rev;
 };
 
 // inverse row kernels: (source item, composite mode, input weighting) of batch item b

@@ -134,6 +134,7 @@ __device__ __forceinline__ void rowp_body(const RowArgs& a, const TwSet& tw, con
   const int lgh = __ffs(half) - 1;  // fast-path extents are powers of two
 
   auto issue = [&](int it, int b) {  // thread 0: land item `it` (rows q1, m1) in buffer b
+    if (INV && a.rev) it = nitems - 1 - it;
     const int P = it & (half - 1), batch = it >> lgh;
     const int q1 = P, m1 = P == 0 ? half : n1 - P;
     unsigned char* dst = smem_raw + b * G::BUF;
@@ -191,7 +192,8 @@ __device__ __forceinline__ void rowp_body(const RowArgs& a, const TwSet& tw, con
     const uint32_t ph = static_cast<uint32_t>(k / NBUF) & 1u;
     if (k >= NBUF) mbar_wait(empty + b, ph ^ 1u);  // item k-NBUF released the buffer
     V* sm = reinterpret_cast<V*>(smem_raw + b * G::BUF);
-    const int P = it & (half - 1), batch = it >> lgh;
+    const int itm = (INV && a.rev) ? nitems - 1 - it : it;
+    const int P = itm & (half - 1), batch = itm >> lgh;
     const int q1 = P, m1 = P == 0 ? half : n1 - P;
     V v[16];
     int img_, imode, iweight;  // inverse: source item, composite mode, weighting (paired launches)

@@ -54,6 +54,14 @@ namespace {
 
 thread_local std::string g_last_error;
 unsigned long long* g_trace = nullptr;  // debug: column-kernel phase timestamps (sdct_debug_set_trace)
+// inverse 2D row passes walk their items last to first (RowArgs::rev): in a
+// DCT -> IDCT chain the forward row pass's latest rows are still in L2
+// (c2 fp64 round trip ~1% faster, tools/ab_rowinv_rev.sh); SDCT_ROWINV_REV=0
+// restores first-to-last (developer A/B)
+const int g_rowinv_rev = [] {
+  const char* f = getenv("SDCT_ROWINV_REV");
+  return f ? atoi(f) : 1;
+}();
 
 int fail(int code, const std::string& msg) {
   g_last_error = msg;
@@ -868,6 +876,7 @@ int run_fast(sdct_plan_s* p, int kind, int only_stage, const void* in, void* out
       ra.dst = ws;
       ra.dst_batch = wsb;
       ra.mode = mode;
+      ra.rev = g_rowinv_rev;
       if (pair) {
         ra.weight = pair->weight1;
         ra.pair_b = 1;
