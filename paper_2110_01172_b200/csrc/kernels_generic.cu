@@ -942,10 +942,29 @@ cudaError_t g2_launch_cfg(G2Args a, cudaStream_t st) {
   return cudaLaunchKernelEx(&cfg, g2_kernel<T, KIND, FPT>, a);
 }
 
+// Column passes of columns in [W, 2048) points take the wide tile (512
+// threads, up to 8192 elements: >= 4 columns, so every row segment is >= 64 B
+// of fp64 complex and the outputs' row segments are >= 32 B) instead of one
+// column per 256-thread tile. Measured on B200 (tools/ab_g2wide.sh, graph-timed
+// calls): fp64 2000^2 DCT 124 -> 116 us, IDCT 138 -> 124 us, 1800^2 104 -> 99 /
+// 121 -> 111 us, 1700x900 81 -> 70 / 91 -> 73 us; 1536^2 slower (75 -> 92 us),
+// so W = 1700; fp32 only the forward column pass gains (2000^2 134 -> 129 us,
+// its inverse 146 -> 152 us). SDCT_G2_WIDE_MIN overrides W (developer A/B).
+int g2_wide_min() {
+  static const int v = [] {
+    const char* f = getenv("SDCT_G2_WIDE_MIN");
+    return f ? atoi(f) : 1700;
+  }();
+  return v;
+}
+
 template <typename T, int KIND>
 cudaError_t g2_launch(G2Args a, cudaStream_t st) {
-  const int n = a.bm ? a.bm : (KIND == G2_FWD_ROWS || KIND == G2_INV_ROWS) ? a.n2 : a.n1;
-  return n <= G2Cfg<8>::CAP ? g2_launch_cfg<T, KIND, 8>(a, st) : g2_launch_cfg<T, KIND, 16>(a, st);
+  constexpr bool ROWS = KIND == G2_FWD_ROWS || KIND == G2_INV_ROWS;
+  const int n = a.bm ? a.bm : ROWS ? a.n2 : a.n1;
+  const bool wide = !ROWS && !a.bm && n >= g2_wide_min() && n < 2048 &&
+                    (sizeof(T) == 8 || KIND == G2_FWD_COLS);
+  return n <= G2Cfg<8>::CAP && !wide ? g2_launch_cfg<T, KIND, 8>(a, st) : g2_launch_cfg<T, KIND, 16>(a, st);
 }
 
 // ---- Bluestein along one axis, one pass per stage ---------------------------
