@@ -1517,7 +1517,6 @@ int sdct_force_fields_scratch(sdct_plan_t p, const void* d_density, void* d_xi1,
     ps.ws_stride = static_cast<long long>(p->aux_half());
     ps.out_stride = first1 ? ostride : -ostride;
     void* lo = first1 ? d_xi1 : d_xi2;
-    DeviceGuard g2(p->device);
     NvtxRange nv("force_pair");
     return p->dtype == SDCT_F32
                ? run_fast<float>(p, SDCT_IDCT_IDXST_2D, -1, a, lo, aw, st, nullptr, 0, nullptr, 1, &ps)
