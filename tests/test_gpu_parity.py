@@ -596,6 +596,44 @@ def test_force_fields_vs_oracle(cuda, dtype):
         sd.force_demo_fields(torch.zeros(8, device="cuda", dtype=tdt))
 
 
+def test_cuda_graph_capture_of_plan_calls(cuda):
+    # bench.py times its steps as a replayed CUDA graph: every public device
+    # entry point must be capturable (no host syncs, no allocation inside) and
+    # the replay must reproduce the eager results bit for bit
+    torch = _torch()
+    import paper_2110_01172_b200 as sd
+    from paper_2110_01172_b200 import _sdct
+
+    for shape, dt in (((1024, 1024), torch.float64), ((512, 256), torch.float32), ((100, 60), torch.float64)):
+        x = torch.rand(shape, dtype=dt, device="cuda")
+        plan = sd.plan_for(shape, 1, "float64" if dt == torch.float64 else "float32", 0)
+        ws = torch.empty(plan.workspace_bytes, dtype=torch.uint8, device="cuda")
+        sc = torch.empty(max(plan.scratch_bytes, 256), dtype=torch.uint8, device="cuda")
+        zer = torch.zeros(1, dtype=torch.int64, device="cuda")
+        outs = [torch.empty_like(x) for _ in range(5)]
+
+        def body(sh):
+            plan.run(_sdct.DCT_2D, x.data_ptr(), outs[0].data_ptr(), sh, ws.data_ptr())
+            plan.run(_sdct.IDCT_2D, outs[0].data_ptr(), outs[1].data_ptr(), sh, ws.data_ptr())
+            plan.force_fields(x.data_ptr(), outs[2].data_ptr(), outs[3].data_ptr(), sh, ws.data_ptr(), sc.data_ptr())
+            plan.compress(x.data_ptr(), outs[4].data_ptr(), 0.25, zer.data_ptr(), sh, ws.data_ptr(), sc.data_ptr())
+
+        body(torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+        want = [o.clone() for o in outs]
+        for o in outs:
+            o.fill_(float("nan"))
+        cs = torch.cuda.Stream()
+        cs.wait_stream(torch.cuda.current_stream())
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=cs, capture_error_mode="thread_local"):
+            body(cs.cuda_stream)
+        g.replay()
+        torch.cuda.synchronize()
+        for o, w in zip(outs, want):
+            assert torch.equal(o, w), shape
+
+
 def test_force_and_compress_concurrent_streams(cuda):
     # the torch entry points give every call its own coefficient scratch, so
     # calls on the one cached plan from two streams in flight at once stay
